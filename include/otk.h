@@ -1,0 +1,203 @@
+/*
+ * otk.h -- C ABI of the B200 (sm_100a) log-domain Sinkhorn library
+ *          (libotk_sm100.so, built from paper_2201_12324_b200/csrc).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (`otkit`, /root/reference/pkg/src/otkit) is pure Python; its seam is the
+ * Geometry plugin API (geometry.py:100-168) driven by the solver loop
+ * sinkhorn.py:151-200.  Each entry point below names the reference function
+ * it replaces.  Conventions:
+ *   - every array argument is a DEVICE pointer to caller-owned, contiguous,
+ *     row-major memory (float32 unless stated; fp16 planes as uint16_t);
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream);
+ *   - the library never allocates persistent device memory: scratch space is
+ *     passed in (sizes from the *_workspace_bytes queries);
+ *   - return value: OTK_OK (0) or a negative error; otk_last_error() gives
+ *     the message (thread-local).  Solver entries may also return the
+ *     positive OTK_DIVERGED / OTK_BAD_POTENTIAL outcomes.
+ * Potentials use the reference convention: -inf allowed (zero-weight
+ * locations), NaN / +inf are invalid (geometry.py:65-72).
+ */
+#ifndef OTK_H
+#define OTK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OTK_ABI_VERSION 1
+
+enum otk_status {
+  OTK_OK = 0,
+  OTK_EINVAL = -1,      /* invalid argument                -> ValueError   */
+  OTK_ECUDA = -2,       /* CUDA runtime / launch failure   -> RuntimeError */
+  OTK_ENOTSUP = -3,     /* unsupported on this device/shape                */
+  OTK_ENCCL = -4,       /* NCCL failure (multi-GPU)                        */
+  OTK_DIVERGED = 1,     /* NaN at a check: errors.py:10-20 DivergedError   */
+  OTK_BAD_POTENTIAL = 2 /* NaN/+inf potential fed to a half-step:
+                           geometry.py:65-72 ValueError                    */
+};
+
+/* flags for otk_lse_partial / otk_cost_partial */
+#define OTK_SAME_POINTS 0x1 /* x and y are the same set: exact-zero diagonal (geometry.py:259-261) */
+#define OTK_CLAMP 0x2       /* clamp C >= 0 (geometry.py:273)                                      */
+#define OTK_IMPL_SIMT 0x10  /* force the FP32 FMA kernel                                           */
+#define OTK_IMPL_TC 0x20    /* force the tcgen05 split-fp16 kernel                                 */
+
+/* finalize modes */
+#define OTK_FIN_SOLVER 0 /* out = eps*logw + |p|^2 - eps*ln2*L   (sinkhorn.py:173-174)            */
+#define OTK_FIN_APPLY 1  /* out = f - |p|^2 + eps*ln2*L           (geometry.py:336-354, axis=rows) */
+
+int otk_abi_version(void);
+const char *otk_last_error(void);
+int otk_device_query(int device, int *sm_count, int *cc_major, int *cc_minor);
+
+/* K0 -- per-point preparation.  Replaces the norm einsums of _cost_block
+ * (geometry.py:269-270).  sqnorm[i] = |p_i|^2 (float64 accumulate).  If hi/lo
+ * are non-NULL also writes the split-fp16 operand planes used by the
+ * tcgen05 kernel: hi = fp16(s*p), lo = fp16(s*p - hi), row pitch dpad >= d
+ * (zero padded), s = split_scale (a power of two). */
+int otk_prep_points(const float *pts, int64_t n, int32_t d, float *sqnorm,
+                    uint16_t *hi, uint16_t *lo, int32_t dpad, float split_scale,
+                    void *stream);
+
+/* max |p_ik| over the array (for choosing split_scale); out is one float. */
+int otk_absmax(const float *pts, int64_t count, float *out, void *stream);
+
+/* Bias of the reduced side for the next half-step: bias_j = kappa*(pot_j - sq_j)
+ * (sq may be NULL -> 0).  NaN/+inf in pot -> atomicMin(first_bad, step). */
+int otk_make_bias(const float *pot, const float *sq, int64_t m, float kappa,
+                  float *bias, int32_t *first_bad, int32_t step, void *stream);
+
+/* K1/K2 -- online half-step partials.  Replaces PointCloudGeometry.apply_lse_kernel
+ * (geometry.py:336-354) and its _cost_rows/_cost_cols blocks (263-292), never
+ * materialising C.  With kappa = log2(e)/eps and
+ *     u_ij = 2*kappa*<p_i, q_j> + q_bias_j,
+ * writes partial[s*np + i] = log2 sum_{j in split s} 2^(u_ij)   (-inf if empty).
+ * Columns are split into `nsplit` equal contiguous ranges (fixed order).
+ * OTK_CLAMP / OTK_SAME_POINTS reproduce max(C,0) and the zero diagonal;
+ * they need p_sq / q_sq.  The TC path needs the hi/lo planes (dpad % 64 == 0);
+ * split_inv = 1/(s_p*s_q) undoes the operand scaling. */
+int otk_lse_partial(const float *p, const float *p_sq, const uint16_t *p_hi,
+                    const uint16_t *p_lo, int64_t np, const float *q,
+                    const float *q_sq, const uint16_t *q_hi, const uint16_t *q_lo,
+                    int64_t nq, int32_t d, int32_t dpad, float split_inv,
+                    const float *q_bias, float kappa, int32_t flags,
+                    int32_t nsplit, float *partial, void *stream);
+
+/* Suggested split count for otk_lse_partial on this device. */
+int otk_lse_suggest_nsplit(int64_t np, int64_t nq, int32_t d, int32_t flags);
+
+/* Combine partials (fixed split order) and produce the potential:
+ *   SOLVER: out_i = eps*base_i + p_sq_i - eps*ln2*L_i      (base = log w)
+ *   APPLY:  out_i = base_i - p_sq_i + eps*ln2*L_i          (base = f)
+ * p_sq may be NULL (0).  If out_bias != NULL also writes the bias of this
+ * side for the next half-step: (out_i - p_sq_i)*kappa_next.  NaN/+inf in
+ * out -> atomicMin(first_bad, step) (first_bad may be NULL). */
+int otk_lse_finalize(const float *partial, int32_t nsplit, int64_t np,
+                     const float *p_sq, const float *base, int32_t mode,
+                     float eps, float kappa_next, float *out_pot,
+                     float *out_bias, int32_t *first_bad, int32_t step,
+                     void *stream);
+
+/* K5 -- fused convergence check (sinkhorn.py:175-189 + _dual_objective 115-119).
+ * From f_prev = f_t, f_next = f_{t+1} (the next rows half-step) and g = g_t:
+ *   r_i = a_i*exp((f_prev_i - f_next_i)/eps)  (= exp(apply_lse_kernel(f,g,rows)/eps))
+ * out[0]=sum|r-a|, [1]=sum r, [2]=sum_{a>0} a f_prev, [3]=sum_{b>0} b g,
+ * [4]=#NaN(f_prev), [5]=#NaN(g), [6]=#(+inf)(f_prev), [7]=#(+inf)(g).
+ * f_next may be NULL (only [2..7] computed).  Deterministic float64
+ * reduction; ws = otk_check_workspace_bytes() bytes of scratch. */
+size_t otk_check_workspace_bytes(void);
+int otk_check(const float *f_prev, const float *f_next, const float *a,
+              int64_t n, const float *g, const float *b, int64_t m, double eps,
+              double *out, void *ws, void *stream);
+
+/* K6 -- online reg_ot_cost (sinkhorn.py:210-216, never materialised):
+ * out[0] = sum_ij C_ij P_ij, out[1] = sum_ij P_ij with P = exp((f_i+g_j-C_ij)/eps).
+ * ws: otk_cost_workspace_bytes(np) bytes. */
+size_t otk_cost_workspace_bytes(int64_t np, int64_t nq);
+int otk_cost_partial(const float *p, const float *p_sq, int64_t np,
+                     const float *q, const float *q_sq, int64_t nq, int32_t d,
+                     const float *f, const float *g, double eps, int32_t flags,
+                     double *out, void *ws, void *stream);
+
+/* transport_matrix (sinkhorn.py:203-207): P[i*m+j] = exp((f_i+g_j-C_ij)/eps). */
+int otk_transport_matrix(const float *p, const float *p_sq, int64_t np,
+                         const float *q, const float *q_sq, int64_t nq,
+                         int32_t d, const float *f, const float *g, double eps,
+                         int32_t flags, float *plan, void *stream);
+
+/* ---------------- materialised / batched path (DenseGeometry) ---------------- */
+
+/* K4 -- C[b,i,j] = sum_k (x_bik - y_bjk)^2 (PointCloudGeometry.cost_matrix,
+ * geometry.py:314-316; exact-zero diagonal with OTK_SAME_POINTS). */
+int otk_dense_cost(const float *x, const float *y, int64_t batch, int64_t n,
+                   int64_t m, int32_t d, int32_t flags, float *cost,
+                   void *stream);
+
+/* K3 -- DenseGeometry.apply_lse_kernel (geometry.py:204-211), batched, fused
+ * with the finalize step.  axis 0 ("rows"): out[b,i] from reduction over j;
+ * axis 1 ("cols"): out[b,j] from reduction over i.  For problem b with
+ * kappa_b = log2(e)/eps_b and u = in_bias[b,*] - kappa_b*C:
+ *   SOLVER: out = eps_b*base - eps_b*ln2*L;   APPLY: out = base + eps_b*ln2*L
+ * and out_bias = out*kappa_next_b (next half-step's bias) when non-NULL.
+ * active[b] == 0 skips problem b (NULL = all active). */
+int otk_dense_lse(const float *cost, int64_t batch, int64_t n, int64_t m,
+                  int32_t axis, const float *in_bias, const float *base,
+                  int32_t mode, const float *eps, const float *kappa_next,
+                  const int32_t *active, float *out_pot, float *out_bias,
+                  int32_t *first_bad, int32_t step, void *stream);
+
+/* Batched fused check: out[b*8 + k] as in otk_check, per problem. */
+int otk_check_batched(const float *f_prev, const float *f_next, const float *a,
+                      int64_t n, const float *g, const float *b, int64_t m,
+                      int64_t batch, const float *eps, const int32_t *active,
+                      double *out, void *stream);
+
+/* Batched dense reg_ot_cost: out[b*2+0] = sum C P, out[b*2+1] = sum P. */
+int otk_dense_cost_reduce(const float *cost, int64_t batch, int64_t n,
+                          int64_t m, const float *f, const float *g,
+                          const float *eps, double *out, void *stream);
+
+/* ---------------- native solver loop ---------------- */
+
+typedef struct otk_solve_args {
+  /* problem (device pointers) */
+  const float *x, *y;        /* [n,d], [m,d]                                  */
+  int64_t n, m;
+  int32_t d;
+  const float *a, *b;        /* weights [n], [m]                              */
+  const float *log_a, *log_b;/* log weights (-inf where weight is 0)          */
+  int32_t same_points;
+  /* epsilon schedule (geometry.py:75-97): eps_t = max(target, target*init*decay^t) */
+  double eps_target, eps_init_scale, eps_decay;
+  double threshold;
+  int32_t max_iters, inner_iters;
+  const float *g_init;       /* nullable warm start (sinkhorn.py:166)         */
+  int32_t flags;             /* OTK_IMPL_* / OTK_CLAMP                        */
+  int32_t use_graphs;        /* capture constant-eps check periods            */
+  /* outputs */
+  float *f_out, *g_out;      /* device [n], [m]                               */
+  double *errors, *duals;    /* host arrays, capacity max_checks              */
+  int32_t max_checks;
+  int32_t n_checks, iterations, converged, fail_iter;
+  /* workspace (device) */
+  void *workspace;
+  size_t workspace_bytes;
+  void *stream;
+} otk_solve_args;
+
+/* Bytes of device workspace otk_solve_pointcloud needs for these args. */
+size_t otk_solve_workspace_bytes(const otk_solve_args *args);
+
+/* Whole solve_sinkhorn (sinkhorn.py:122-200) on device.  Returns OTK_OK,
+ * OTK_DIVERGED (fail_iter = t) or OTK_BAD_POTENTIAL (fail_iter = t). */
+int otk_solve_pointcloud(otk_solve_args *args);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OTK_H */
