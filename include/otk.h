@@ -144,7 +144,8 @@ int otk_dense_cost(const float *x, const float *y, int64_t batch, int64_t n,
  * kappa_b = log2(e)/eps_b and u = in_bias[b,*] - kappa_b*C:
  *   SOLVER: out = eps_b*base - eps_b*ln2*L;   APPLY: out = base + eps_b*ln2*L
  * and out_bias = out*kappa_next_b (next half-step's bias) when non-NULL.
- * active[b] == 0 skips problem b (NULL = all active). */
+ * active[b] == 0 skips problem b (NULL = all active).  first_bad is per
+ * problem: NaN/+inf in out -> atomicMin(first_bad + b, step). */
 int otk_dense_lse(const float *cost, int64_t batch, int64_t n, int64_t m,
                   int32_t axis, const float *in_bias, const float *base,
                   int32_t mode, const float *eps, const float *kappa_next,
@@ -156,6 +157,10 @@ int otk_check_batched(const float *f_prev, const float *f_next, const float *a,
                       int64_t n, const float *g, const float *b, int64_t m,
                       int64_t batch, const float *eps, const int32_t *active,
                       double *out, void *stream);
+
+/* transport_matrix for a stored cost (sinkhorn.py:203-207), one problem. */
+int otk_dense_plan(const float *cost, int64_t n, int64_t m, const float *f,
+                   const float *g, double eps, float *plan, void *stream);
 
 /* Batched dense reg_ot_cost: out[b*2+0] = sum C P, out[b*2+1] = sum P. */
 int otk_dense_cost_reduce(const float *cost, int64_t batch, int64_t n,
@@ -184,6 +189,7 @@ typedef struct otk_solve_args {
   double *errors, *duals;    /* host arrays, capacity max_checks              */
   int32_t max_checks;
   int32_t n_checks, iterations, converged, fail_iter;
+  int32_t launches;          /* kernels launched (graph nodes included)       */
   /* workspace (device) */
   void *workspace;
   size_t workspace_bytes;
@@ -192,6 +198,10 @@ typedef struct otk_solve_args {
 
 /* Bytes of device workspace otk_solve_pointcloud needs for these args. */
 size_t otk_solve_workspace_bytes(const otk_solve_args *args);
+
+/* Pipe throughput microbenchmarks (roofline denominators measured on the box):
+ * MUFU ex2 results/s and FP32 FFMA/s (full chip, best of 3). */
+int otk_bench_pipes(double *ex2_per_s, double *ffma_per_s, void *stream);
 
 /* Whole solve_sinkhorn (sinkhorn.py:122-200) on device.  Returns OTK_OK,
  * OTK_DIVERGED (fail_iter = t) or OTK_BAD_POTENTIAL (fail_iter = t). */

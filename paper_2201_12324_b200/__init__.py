@@ -1,0 +1,53 @@
+"""B200-native (sm_100a) log-domain Sinkhorn for point clouds.
+
+Drop-in for the hot path of the reference package ``otkit`` (OTT paper,
+arXiv 2201.12324): same public names for the linear entropic problem.
+Every computation runs in libotk_sm100.so (hand-written CUDA for sm_100a,
+C ABI in include/otk.h); there is no CPU fallback.
+"""
+
+from .errors import DivergedError, OtkitError
+from .geometry import (
+    COST_FNS,
+    DEFAULT_EPSILON_SCALE,
+    DenseGeometry,
+    EpsilonSchedule,
+    Geometry,
+    PointCloudGeometry,
+)
+from .sinkhorn import (
+    Coupling,
+    LinearProblem,
+    RegOTCost,
+    SinkhornOutput,
+    grad_points,
+    grad_weights,
+    reg_ot_cost,
+    solve_sinkhorn,
+    solve_sinkhorn_batched,
+    transport_matrix,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "__version__",
+    "OtkitError",
+    "DivergedError",
+    "Geometry",
+    "DenseGeometry",
+    "PointCloudGeometry",
+    "EpsilonSchedule",
+    "COST_FNS",
+    "DEFAULT_EPSILON_SCALE",
+    "LinearProblem",
+    "SinkhornOutput",
+    "Coupling",
+    "RegOTCost",
+    "solve_sinkhorn",
+    "solve_sinkhorn_batched",
+    "transport_matrix",
+    "reg_ot_cost",
+    "grad_weights",
+    "grad_points",
+]

@@ -1,0 +1,256 @@
+// Entry points of libotk_sm100.so that are not a half-step kernel:
+// error plumbing, device query, K0 prep, bias, finalize (K7 local combine),
+// and the K5 fused convergence check.
+#include <cuda_fp16.h>
+
+#include <cstdarg>
+#include <cstring>
+
+#include "otk_common.cuh"
+
+namespace otk {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char *what) {
+  set_error("CUDA error %s (%d) in %s", cudaGetErrorString(e), (int)e, what);
+  return OTK_ECUDA;
+}
+
+int num_sms() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  }
+  return cached;
+}
+
+// ---------------------------------------------------------------- K0 prep
+// One warp per point: |p|^2 in float64, optional split-fp16 planes.
+__global__ void prep_kernel(const float *__restrict__ pts, int64_t n, int d,
+                            float *__restrict__ sq, __half *__restrict__ hi,
+                            __half *__restrict__ lo, int dpad, float scale) {
+  int64_t warp = (int64_t)(blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32);
+  int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const float *row = pts + warp * d;
+  double acc = 0.0;
+  for (int k = lane; k < d; k += 32) {
+    double v = row[k];
+    acc = fma(v, v, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) sq[warp] = (float)acc;
+  if (hi != nullptr) {
+    __half *hrow = hi + warp * dpad;
+    __half *lrow = lo + warp * dpad;
+    for (int k = lane; k < dpad; k += 32) {
+      float v = (k < d) ? row[k] * scale : 0.f;
+      __half h = __float2half_rn(v);
+      hrow[k] = h;
+      lrow[k] = __float2half_rn(v - __half2float(h));
+    }
+  }
+}
+
+__global__ void absmax_kernel(const float *__restrict__ p, int64_t count, unsigned *__restrict__ out) {
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(p[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
+}
+
+__global__ void bias_kernel(const float *__restrict__ pot, const float *__restrict__ sq, int64_t m,
+                            float kappa, float *__restrict__ bias, int *__restrict__ first_bad,
+                            int step) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  float v = pot[j];
+  if (first_bad != nullptr && bad_potential(v)) atomicMin(first_bad, step);
+  bias[j] = (v - (sq ? sq[j] : 0.f)) * kappa;
+}
+
+__global__ void finalize_kernel(const float *__restrict__ part, int nsplit, int64_t np,
+                                const float *__restrict__ psq, const float *__restrict__ base,
+                                int mode, float eps, float kappa_next, float *__restrict__ out,
+                                float *__restrict__ out_bias, int *__restrict__ first_bad,
+                                int step) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= np) return;
+  float L = combine_log2(part + i, nsplit, np);
+  float sq = psq ? psq[i] : 0.f;
+  float c = eps * kLn2;
+  float v;
+  if (mode == OTK_FIN_SOLVER) {
+    v = fmaf(eps, base[i], sq) - c * L;
+  } else {
+    v = (base[i] - sq) + c * L;
+  }
+  out[i] = v;
+  if (out_bias != nullptr) out_bias[i] = (v - sq) * kappa_next;
+  if (first_bad != nullptr && bad_potential(v)) atomicMin(first_bad, step);
+}
+
+// ---------------------------------------------------------------- K5 check
+constexpr int kCheckBlocks = 148;
+constexpr int kCheckThreads = 256;
+constexpr int kCheckVals = 8;
+
+template <int N>
+__device__ void block_reduce_d(double (&v)[N], double *smem /* [N][kCheckThreads] */) {
+  int t = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < N; ++k) smem[k * kCheckThreads + t] = v[k];
+  __syncthreads();
+  for (int s = kCheckThreads / 2; s > 0; s >>= 1) {
+    if (t < s) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) smem[k * kCheckThreads + t] += smem[k * kCheckThreads + t + s];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = smem[k * kCheckThreads];
+}
+
+__global__ void __launch_bounds__(kCheckThreads) check_kernel(
+    const float *__restrict__ f_prev, const float *__restrict__ f_next, const float *__restrict__ a,
+    int64_t n, const float *__restrict__ g, const float *__restrict__ b, int64_t m, double eps,
+    double *__restrict__ out, double *__restrict__ ws, unsigned *__restrict__ counter) {
+  __shared__ double smem[kCheckVals * kCheckThreads];
+  __shared__ bool last;
+  double v[kCheckVals] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const double inv_eps = 1.0 / eps;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double fp = f_prev[i];
+    double ai = a[i];
+    if (f_next != nullptr) {
+      double r = (ai > 0.0) ? ai * exp((fp - (double)f_next[i]) * inv_eps) : 0.0;
+      v[0] += fabs(r - ai);
+      v[1] += r;
+    }
+    if (ai > 0.0) v[2] += ai * fp;
+    v[4] += (fp != fp) ? 1.0 : 0.0;
+    v[6] += (fp == INFINITY) ? 1.0 : 0.0;
+  }
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += stride) {
+    double gj = g[j];
+    double bj = b[j];
+    if (bj > 0.0) v[3] += bj * gj;
+    v[5] += (gj != gj) ? 1.0 : 0.0;
+    v[7] += (gj == INFINITY) ? 1.0 : 0.0;
+  }
+  block_reduce_d(v, smem);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < kCheckVals; ++k) ws[blockIdx.x * kCheckVals + k] = v[k];
+    __threadfence();
+    unsigned done = atomicAdd(counter, 1u);
+    last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // Fixed-order final reduction over block partials: deterministic.
+  if (threadIdx.x < kCheckVals) {
+    double acc = 0.0;
+    for (int blk = 0; blk < (int)gridDim.x; ++blk)
+      acc += ((volatile double *)ws)[blk * kCheckVals + threadIdx.x];
+    out[threadIdx.x] = acc;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+}  // namespace otk
+
+using namespace otk;
+
+extern "C" {
+
+int otk_abi_version(void) { return OTK_ABI_VERSION; }
+
+const char *otk_last_error(void) { return g_err; }
+
+int otk_device_query(int device, int *sm_count, int *cc_major, int *cc_minor) {
+  OTK_CUDA(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, device));
+  OTK_CUDA(cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, device));
+  OTK_CUDA(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, device));
+  return OTK_OK;
+}
+
+int otk_prep_points(const float *pts, int64_t n, int32_t d, float *sqnorm, uint16_t *hi,
+                    uint16_t *lo, int32_t dpad, float split_scale, void *stream) {
+  OTK_CHECK_ARG(pts && sqnorm && n > 0 && d > 0, "otk_prep_points: bad arguments");
+  OTK_CHECK_ARG((hi == nullptr) == (lo == nullptr), "otk_prep_points: hi/lo must both be set");
+  OTK_CHECK_ARG(hi == nullptr || dpad >= d, "otk_prep_points: dpad < d");
+  const int warps = 8;
+  int64_t blocks = (n + warps - 1) / warps;
+  prep_kernel<<<(unsigned)blocks, warps * 32, 0, as_stream(stream)>>>(
+      pts, n, d, sqnorm, reinterpret_cast<__half *>(hi), reinterpret_cast<__half *>(lo), dpad,
+      split_scale);
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}
+
+int otk_absmax(const float *pts, int64_t count, float *out, void *stream) {
+  OTK_CHECK_ARG(pts && out && count > 0, "otk_absmax: bad arguments");
+  OTK_CUDA(cudaMemsetAsync(out, 0, sizeof(float), as_stream(stream)));
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
+  absmax_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(pts, count,
+                                                                  reinterpret_cast<unsigned *>(out));
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}
+
+int otk_make_bias(const float *pot, const float *sq, int64_t m, float kappa, float *bias,
+                  int32_t *first_bad, int32_t step, void *stream) {
+  OTK_CHECK_ARG(pot && bias && m > 0, "otk_make_bias: bad arguments");
+  bias_kernel<<<(unsigned)((m + 255) / 256), 256, 0, as_stream(stream)>>>(pot, sq, m, kappa, bias,
+                                                                           first_bad, step);
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}
+
+int otk_lse_finalize(const float *partial, int32_t nsplit, int64_t np, const float *p_sq,
+                     const float *base, int32_t mode, float eps, float kappa_next, float *out_pot,
+                     float *out_bias, int32_t *first_bad, int32_t step, void *stream) {
+  OTK_CHECK_ARG(partial && base && out_pot && np > 0 && nsplit >= 1, "otk_lse_finalize: bad arguments");
+  OTK_CHECK_ARG(mode == OTK_FIN_SOLVER || mode == OTK_FIN_APPLY, "otk_lse_finalize: bad mode");
+  finalize_kernel<<<(unsigned)((np + 255) / 256), 256, 0, as_stream(stream)>>>(
+      partial, nsplit, np, p_sq, base, mode, eps, kappa_next, out_pot, out_bias, first_bad, step);
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}
+
+size_t otk_check_workspace_bytes(void) {
+  return (size_t)kCheckBlocks * kCheckVals * sizeof(double) + 256;
+}
+
+int otk_check(const float *f_prev, const float *f_next, const float *a, int64_t n, const float *g,
+              const float *b, int64_t m, double eps, double *out, void *ws, void *stream) {
+  OTK_CHECK_ARG(f_prev && a && g && b && out && ws && n > 0 && m > 0, "otk_check: bad arguments");
+  double *part = reinterpret_cast<double *>(ws);
+  unsigned *counter = reinterpret_cast<unsigned *>(part + kCheckBlocks * kCheckVals);
+  check_kernel<<<kCheckBlocks, kCheckThreads, 0, as_stream(stream)>>>(f_prev, f_next, a, n, g, b, m,
+                                                                      eps, out, part, counter);
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// Shared helpers for the sm_100a Sinkhorn library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "otk.h"
+
+namespace otk {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+// ---- error reporting (thread-local message, returned status) ----
+void set_error(const char *fmt, ...);
+int cuda_status(cudaError_t e, const char *what);
+
+#define OTK_CHECK_ARG(cond, ...)          \
+  do {                                    \
+    if (!(cond)) {                        \
+      ::otk::set_error(__VA_ARGS__);      \
+      return OTK_EINVAL;                  \
+    }                                     \
+  } while (0)
+
+#define OTK_CUDA(call)                                        \
+  do {                                                        \
+    cudaError_t _e = (call);                                  \
+    if (_e != cudaSuccess) return ::otk::cuda_status(_e, #call); \
+  } while (0)
+
+#define OTK_LAUNCH_CHECK() OTK_CUDA(cudaGetLastError())
+
+int num_sms();
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- device math ----
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Online log2-sum-exp2 state: value = m + log2(s).  m = -inf means empty.
+struct Lse2 {
+  float m, s;
+  __device__ __forceinline__ void init() { m = -INFINITY; s = 0.f; }
+  // merge another (m2, s2)
+  __device__ __forceinline__ void merge(float m2, float s2) {
+    float mm = fmaxf(m, m2);
+    if (mm == -INFINITY) return;
+    s = s * ex2(m - mm) + s2 * ex2(m2 - mm);
+    m = mm;
+  }
+  __device__ __forceinline__ float value() const {
+    if (s != s) return s;  // NaN propagates
+    return (s > 0.f) ? m + lg2(s) : -INFINITY;
+  }
+};
+
+// log2-sum of a fixed-order list of partial log2 values.
+__device__ __forceinline__ float combine_log2(const float *part, int nsplit, int64_t stride) {
+  if (nsplit == 1) return part[0];
+  float mx = -INFINITY;
+  bool nan = false;
+  for (int s = 0; s < nsplit; ++s) {
+    float v = part[s * stride];
+    nan |= (v != v);
+    mx = fmaxf(mx, v);
+  }
+  if (nan) return __int_as_float(0x7fc00000);
+  if (mx == -INFINITY) return mx;  // empty
+  if (mx == INFINITY) return INFINITY;
+  float acc = 0.f;
+  for (int s = 0; s < nsplit; ++s) acc += ex2(part[s * stride] - mx);
+  return mx + lg2(acc);
+}
+
+__device__ __forceinline__ bool bad_potential(float v) { return (v != v) || v == INFINITY; }
+
+}  // namespace otk

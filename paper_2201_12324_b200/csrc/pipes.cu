@@ -1,0 +1,80 @@
+// Pipe-throughput microbenchmarks used by bench.py to measure the
+// denominators of the online kernel's compute roof on the box itself:
+// MUFU ex2 (one per cell per half-step) and FP32 FFMA.
+#include "otk_common.cuh"
+
+namespace otk {
+
+constexpr int PB_CHAINS = 8;
+
+__global__ void __launch_bounds__(256) ex2_pipe_kernel(float *out, int iters, float seed) {
+  float v[PB_CHAINS];
+#pragma unroll
+  for (int c = 0; c < PB_CHAINS; ++c) v[c] = seed * (threadIdx.x + c) * 1e-7f - 0.5f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < PB_CHAINS; ++c) v[c] = ex2(v[c]) - 1.0f;  // stays in (-0.5, 0.5)
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < PB_CHAINS; ++c) s += v[c];
+  if (s == 12345.f) out[threadIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) fma_pipe_kernel(float *out, int iters, float seed) {
+  float v[PB_CHAINS];
+#pragma unroll
+  for (int c = 0; c < PB_CHAINS; ++c) v[c] = seed * (threadIdx.x + c);
+  const float a = 0.999999f, b = 1e-7f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < PB_CHAINS; ++c) v[c] = fmaf(v[c], a, b);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < PB_CHAINS; ++c) s += v[c];
+  if (s == 12345.f) out[threadIdx.x] = s;
+}
+
+}  // namespace otk
+
+using namespace otk;
+
+extern "C" int otk_bench_pipes(double *ex2_per_s, double *ffma_per_s, void *stream) {
+  OTK_CHECK_ARG(ex2_per_s && ffma_per_s, "otk_bench_pipes: null output");
+  cudaStream_t st = as_stream(stream);
+  float *scratch = nullptr;
+  OTK_CUDA(cudaMallocAsync(&scratch, 256 * sizeof(float), st));
+  const int blocks = num_sms() * 8, threads = 256, iters = 4096;
+  cudaEvent_t e0, e1;
+  OTK_CUDA(cudaEventCreate(&e0));
+  OTK_CUDA(cudaEventCreate(&e1));
+  float ms = 0.f;
+  double ops = (double)blocks * threads * PB_CHAINS * iters;
+  // warm up + measure (best of 3)
+  double best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0, st);
+    ex2_pipe_kernel<<<blocks, threads, 0, st>>>(scratch, iters, 1.f);
+    cudaEventRecord(e1, st);
+    OTK_CUDA(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0) best = std::max(best, ops / (ms * 1e-3));
+  }
+  *ex2_per_s = best;
+  best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0, st);
+    fma_pipe_kernel<<<blocks, threads, 0, st>>>(scratch, iters, 1.f);
+    cudaEventRecord(e1, st);
+    OTK_CUDA(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0) best = std::max(best, ops / (ms * 1e-3));
+  }
+  *ffma_per_s = best;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  OTK_CUDA(cudaFreeAsync(scratch, st));
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}

@@ -1,0 +1,354 @@
+// Half-step dispatch (K1 SIMT / K2 tcgen05) and the native solver loop that
+// replaces the reference's Python loop sinkhorn._sinkhorn_iterations
+// (reference sinkhorn.py:151-200) for point clouds.
+//
+// Loop (t = 1..max_iters, eps_t from the schedule, kappa = log2(e)/eps_t):
+//   f-half  h=2t-1: partial = LSE over y of (2k<x,y> + bias_y);  f = finalize(log a)
+//   g-half  h=2t  : partial = LSE over x of (2k<y,x> + bias_x);  g = finalize(log b)
+// Every finalize also writes the bias of its side for the next half-step and
+// records the first half-step index h that would CONSUME a NaN/+inf
+// potential; the reference raises ValueError at exactly that call
+// (geometry.py:65-72, via apply_lse_kernel).  At a check iteration
+// (t % inner == 0 or t == max_iters, sinkhorn.py:175) the next f half-step
+// f_{t+1} is computed into a second buffer and the fused check kernel
+// derives the row marginal r_i = a_i exp((f_t - f_{t+1})/eps), which equals
+// exp(apply_lse_kernel(f_t, g_t, rows)/eps) (sinkhorn.py:183): the third
+// full pass of the reference is folded into the next iteration's work.
+// Constant-eps check periods are captured once as CUDA graphs and replayed.
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <vector>
+
+#include "otk_common.cuh"
+
+namespace otk {
+int lse_simt_launch(const float *p, const float *p_sq, int64_t np, const float *q,
+                    const float *q_sq, int64_t nq, int d, const float *q_bias, float kappa,
+                    int flags, int nsplit, float *partial, cudaStream_t st);
+int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, int64_t np, const uint16_t *q_hi,
+                  const uint16_t *q_lo, int64_t nq, int dpad, float two_kappa_scaled,
+                  const float *q_bias, int nsplit, float *partial, cudaStream_t st);
+bool tc_available();
+}  // namespace otk
+
+using namespace otk;
+
+static bool want_tc(int flags, int d) {
+  if (flags & OTK_IMPL_SIMT) return false;
+  if (flags & OTK_IMPL_TC) return true;
+  return tc_available() && d >= 32;
+}
+
+extern "C" int otk_lse_suggest_nsplit(int64_t np, int64_t nq, int32_t d, int32_t flags) {
+  const int sms = num_sms();
+  if (want_tc(flags, d)) {
+    // TC kernel: 128-row tiles, 256-column tiles; aim for >= 8 work units per SM.
+    int64_t row_tiles = (np + 127) / 128;
+    int64_t col_tiles = (nq + 255) / 256;
+    int64_t want = (8LL * sms + row_tiles - 1) / row_tiles;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(want, col_tiles));
+  }
+  int64_t row_tiles = (np + 63) / 64;
+  int64_t col_tiles = (nq + 63) / 64;
+  int64_t want = (16LL * sms + row_tiles - 1) / row_tiles;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, col_tiles));
+}
+
+extern "C" int otk_lse_partial(const float *p, const float *p_sq, const uint16_t *p_hi,
+                               const uint16_t *p_lo, int64_t np, const float *q, const float *q_sq,
+                               const uint16_t *q_hi, const uint16_t *q_lo, int64_t nq, int32_t d,
+                               int32_t dpad, float split_inv, const float *q_bias, float kappa,
+                               int32_t flags, int32_t nsplit, float *partial, void *stream) {
+  OTK_CHECK_ARG(np > 0 && nq > 0 && d > 0 && nsplit >= 1 && q_bias && partial,
+                "otk_lse_partial: bad arguments");
+  OTK_CHECK_ARG(nsplit <= 65535, "otk_lse_partial: nsplit too large");
+  if (want_tc(flags, d)) {
+    OTK_CHECK_ARG(p_hi && p_lo && q_hi && q_lo && dpad % 64 == 0 && dpad >= d,
+                  "otk_lse_partial: TC path needs split planes with dpad %% 64 == 0");
+    if (!tc_available()) {
+      set_error("otk_lse_partial: tcgen05 path requires an sm_100 device");
+      return OTK_ENOTSUP;
+    }
+    return lse_tc_launch(p_hi, p_lo, np, q_hi, q_lo, nq, dpad, 2.f * kappa * split_inv, q_bias,
+                         nsplit, partial, as_stream(stream));
+  }
+  OTK_CHECK_ARG(p && q, "otk_lse_partial: SIMT path needs fp32 points");
+  OTK_CHECK_ARG(!(flags & (OTK_CLAMP | OTK_SAME_POINTS)) || (p_sq && q_sq),
+                "otk_lse_partial: OTK_CLAMP needs squared norms");
+  return lse_simt_launch(p, p_sq, np, q, q_sq, nq, d, q_bias, kappa, flags, nsplit, partial,
+                         as_stream(stream));
+}
+
+// ------------------------------------------------------------------ solver
+namespace {
+
+struct Carver {
+  char *base;
+  size_t off = 0;
+  template <class T>
+  T *take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T *p = reinterpret_cast<T *>(base ? base + off : nullptr);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+struct Layout {
+  float *fA, *fB, *g, *xsq, *ysq, *bias_x, *bias_y, *part;
+  uint16_t *xhi, *xlo, *yhi, *ylo;
+  float *absmax;
+  double *chk;
+  void *chk_ws;
+  int *first_bad;
+  int nsr, nsc, dpad;
+  bool tc;
+  size_t bytes;
+};
+
+Layout plan(const otk_solve_args *A, void *ws) {
+  Layout L{};
+  L.tc = want_tc(A->flags, A->d);
+  L.dpad = (A->d + 63) / 64 * 64;
+  L.nsr = otk_lse_suggest_nsplit(A->n, A->m, A->d, A->flags);
+  L.nsc = otk_lse_suggest_nsplit(A->m, A->n, A->d, A->flags);
+  Carver c{reinterpret_cast<char *>(ws)};
+  L.fA = c.take<float>(A->n);
+  L.fB = c.take<float>(A->n);
+  L.g = c.take<float>(A->m);
+  L.xsq = c.take<float>(A->n);
+  L.ysq = c.take<float>(A->m);
+  L.bias_x = c.take<float>(A->n);
+  L.bias_y = c.take<float>(A->m);
+  L.part = c.take<float>(std::max((size_t)L.nsr * A->n, (size_t)L.nsc * A->m));
+  if (L.tc) {
+    L.xhi = c.take<uint16_t>((size_t)A->n * L.dpad);
+    L.xlo = c.take<uint16_t>((size_t)A->n * L.dpad);
+    L.yhi = c.take<uint16_t>((size_t)A->m * L.dpad);
+    L.ylo = c.take<uint16_t>((size_t)A->m * L.dpad);
+  } else {
+    L.xhi = L.xlo = L.yhi = L.ylo = nullptr;
+  }
+  L.absmax = c.take<float>(2);
+  L.chk = c.take<double>(8);
+  L.chk_ws = c.take<char>(otk_check_workspace_bytes());
+  L.first_bad = c.take<int>(1);
+  L.bytes = c.off + 256;
+  return L;
+}
+
+inline double eps_at(const otk_solve_args *A, int t) {
+  return std::max(A->eps_target, A->eps_target * A->eps_init_scale * std::pow(A->eps_decay, (double)t));
+}
+
+}  // namespace
+
+extern "C" size_t otk_solve_workspace_bytes(const otk_solve_args *A) {
+  if (!A) return 0;
+  return plan(A, nullptr).bytes;
+}
+
+#define OTK_TRY(expr)          \
+  do {                         \
+    int _r = (expr);           \
+    if (_r != OTK_OK) return _r; \
+  } while (0)
+
+struct HalfStep {
+  const otk_solve_args *A;
+  Layout *L;
+  cudaStream_t st;
+  float sinv;  // 1/(s_x*s_y) for the TC operand scaling
+  int kflags;
+  int launches = 0;
+
+  int rows(float kappa, float eps, float kappa_next, float *f_out, int step) {
+    launches += 2;
+    OTK_TRY(otk_lse_partial(A->x, L->xsq, L->xhi, L->xlo, A->n, A->y, L->ysq, L->yhi, L->ylo, A->m,
+                            A->d, L->dpad, sinv, L->bias_y, kappa, kflags, L->nsr, L->part, st));
+    return otk_lse_finalize(L->part, L->nsr, A->n, L->xsq, A->log_a, OTK_FIN_SOLVER, eps,
+                            kappa_next, f_out, L->bias_x, L->first_bad, step, st);
+  }
+  int cols(float kappa, float eps, float kappa_next, int step) {
+    launches += 2;
+    OTK_TRY(otk_lse_partial(A->y, L->ysq, L->yhi, L->ylo, A->m, A->x, L->xsq, L->xhi, L->xlo, A->n,
+                            A->d, L->dpad, sinv, L->bias_x, kappa, kflags, L->nsc, L->part, st));
+    return otk_lse_finalize(L->part, L->nsc, A->m, L->ysq, A->log_b, OTK_FIN_SOLVER, eps,
+                            kappa_next, L->g, L->bias_y, L->first_bad, step, st);
+  }
+};
+
+static float pow2_scale_for(float amax) {
+  // largest power of two s with s*amax <= 2^14 (fp16 headroom for hi + lo)
+  if (!(amax > 0.f) || !std::isfinite(amax)) return 1.f;
+  int e = (int)std::floor(std::log2(16384.0 / amax));
+  e = std::max(-60, std::min(60, e));
+  return std::ldexp(1.f, e);
+}
+
+extern "C" int otk_solve_pointcloud(otk_solve_args *A) {
+  OTK_CHECK_ARG(A && A->x && A->y && A->a && A->b && A->log_a && A->log_b && A->f_out && A->g_out,
+                "otk_solve_pointcloud: missing pointers");
+  OTK_CHECK_ARG(A->n > 0 && A->m > 0 && A->d > 0, "otk_solve_pointcloud: bad shape");
+  OTK_CHECK_ARG(A->max_iters >= 1 && A->inner_iters >= 1, "max_iters and inner_iters must be >= 1");
+  OTK_CHECK_ARG(A->threshold > 0, "threshold must be positive");
+  OTK_CHECK_ARG(A->eps_target > 0, "eps must be positive");
+  OTK_CHECK_ARG(A->errors && A->duals && A->max_checks >= 1, "otk_solve_pointcloud: no trace buffers");
+  Layout L = plan(A, A->workspace);
+  OTK_CHECK_ARG(A->workspace && A->workspace_bytes >= L.bytes,
+                "otk_solve_pointcloud: workspace too small (%zu < %zu)", A->workspace_bytes, L.bytes);
+  cudaStream_t st = as_stream(A->stream);
+  A->n_checks = 0;
+  A->iterations = 0;
+  A->converged = 0;
+  A->fail_iter = 0;
+
+  // ---- prep (K0)
+  float sx = 1.f, sy = 1.f;
+  if (L.tc) {
+    float amax[2];
+    OTK_TRY(otk_absmax(A->x, A->n * (int64_t)A->d, L.absmax, st));
+    OTK_TRY(otk_absmax(A->y, A->m * (int64_t)A->d, L.absmax + 1, st));
+    OTK_CUDA(cudaMemcpyAsync(amax, L.absmax, sizeof(amax), cudaMemcpyDeviceToHost, st));
+    OTK_CUDA(cudaStreamSynchronize(st));
+    sx = pow2_scale_for(amax[0]);
+    sy = pow2_scale_for(amax[1]);
+  }
+  OTK_TRY(otk_prep_points(A->x, A->n, A->d, L.xsq, L.xhi, L.xlo, L.dpad, sx, st));
+  OTK_TRY(otk_prep_points(A->y, A->m, A->d, L.ysq, L.yhi, L.ylo, L.dpad, sy, st));
+  OTK_CUDA(cudaMemsetAsync(L.first_bad, 0x7f, sizeof(int), st));
+  OTK_CUDA(cudaMemsetAsync(L.chk_ws, 0, otk_check_workspace_bytes(), st));
+
+  HalfStep H{A, &L, st, 1.f / (sx * sy),
+             (A->flags & (OTK_IMPL_SIMT | OTK_IMPL_TC)) | OTK_CLAMP |
+                 (A->same_points ? OTK_SAME_POINTS : 0)};
+
+  // ---- initial g (zeros or warm start) and its bias for h = 1
+  const double e0 = eps_at(A, 0);
+  if (A->g_init)
+    OTK_CUDA(cudaMemcpyAsync(L.g, A->g_init, A->m * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  else
+    OTK_CUDA(cudaMemsetAsync(L.g, 0, A->m * sizeof(float), st));
+  OTK_TRY(otk_make_bias(L.g, L.ysq, A->m, (float)(1.4426950408889634 / e0), L.bias_y, L.first_bad, 1, st));
+
+  float *f = L.fA, *fn = L.fB;
+  bool f_ready = false;
+  int t = 0;
+  int status = OTK_OK;
+
+  // CUDA graph cache for a constant-eps period (f/fn ping-pong -> 2 graphs)
+  cudaGraphExec_t period_exec[2] = {nullptr, nullptr};
+  int graph_launches = 0;
+  const bool graphs = A->use_graphs != 0;
+  int extra_launches = 2 + 1 + (L.tc ? 2 : 0);  // prep x/y, bias, absmax x/y
+
+  for (t = 1; t <= A->max_iters; ++t) {
+    const double e = eps_at(A, t - 1);
+    const float kap = (float)(1.4426950408889634 / e);
+    const float kap_next = (float)(1.4426950408889634 / eps_at(A, t));
+
+    // Graph fast path: a whole constant-eps period t..t+inner-1 ending at a check.
+    const int t_end = t + A->inner_iters - 1;
+    if (graphs && f_ready && (t - 1) % A->inner_iters == 0 && t_end <= A->max_iters &&
+        t_end % A->inner_iters == 0 && e == A->eps_target && eps_at(A, t_end) == A->eps_target) {
+      const int which = (f == L.fA) ? 0 : 1;
+      if (!period_exec[which]) {
+        cudaGraph_t graph;
+        OTK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        int rc = OTK_OK;
+        const int before = H.launches;
+        // steps are recorded relative; the bad-potential index is only used as a
+        // "before the check" marker inside graphs (see below)
+        for (int k = 0; k < A->inner_iters && rc == OTK_OK; ++k) {
+          if (k > 0) rc = H.rows(kap, (float)e, kap, f, 2);
+          if (rc == OTK_OK) rc = H.cols(kap, (float)e, kap, k + 1 == A->inner_iters ? 3 : 2);
+        }
+        if (rc == OTK_OK) rc = H.rows(kap, (float)e, kap, fn, 4);
+        if (rc == OTK_OK) rc = otk_check(f, fn, A->a, A->n, L.g, A->b, A->m, e, L.chk, L.chk_ws, st);
+        cudaError_t ce = cudaStreamEndCapture(st, &graph);
+        graph_launches = H.launches - before + 1;
+        H.launches = before;
+        if (rc != OTK_OK) return rc;
+        if (ce != cudaSuccess) return cuda_status(ce, "cudaStreamEndCapture");
+        // Relative step ids inside the period: 2 = consumed before the check
+        // (the reference raises ValueError there), 3 = g_t consumed by the
+        // check itself, 4 = f_{t+1} (after the check).
+        OTK_CUDA(cudaGraphInstantiate(&period_exec[which], graph, 0));
+        cudaGraphDestroy(graph);
+      }
+      OTK_CUDA(cudaMemsetAsync(L.first_bad, 0x7f, sizeof(int), st));
+      OTK_CUDA(cudaGraphLaunch(period_exec[which], st));
+      extra_launches += graph_launches;
+      t = t_end;
+      double out[8];
+      int fb;
+      OTK_CUDA(cudaMemcpyAsync(out, L.chk, sizeof(out), cudaMemcpyDeviceToHost, st));
+      OTK_CUDA(cudaMemcpyAsync(&fb, L.first_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+      OTK_CUDA(cudaStreamSynchronize(st));
+      if (fb <= 2) { status = OTK_BAD_POTENTIAL; A->fail_iter = t; break; }
+      if (out[4] > 0 || out[5] > 0) { status = OTK_DIVERGED; A->fail_iter = t; break; }
+      if (out[7] > 0) { status = OTK_BAD_POTENTIAL; A->fail_iter = t; break; }
+      const double err = out[0];
+      const double dual = out[2] + out[3] - e * (out[1] - 1.0);
+      if (A->n_checks < A->max_checks) {
+        A->errors[A->n_checks] = err;
+        A->duals[A->n_checks] = dual;
+        A->n_checks++;
+      }
+      if (err <= A->threshold) { A->converged = 1; break; }
+      if (t < A->max_iters) {
+        std::swap(f, fn);
+        f_ready = true;
+      }
+      // step ids inside graphs are relative; restore absolute numbering
+      OTK_CUDA(cudaMemsetAsync(L.first_bad, 0x7f, sizeof(int), st));
+      continue;
+    }
+
+    if (!f_ready) { if ((status = H.rows(kap, (float)e, kap, f, 2 * t)) != OTK_OK) break; }
+    f_ready = false;
+    if ((status = H.cols(kap, (float)e, kap_next, 2 * t + 1)) != OTK_OK) break;
+
+    if (t % A->inner_iters == 0 || t == A->max_iters) {
+      const bool measure = !(e > A->eps_target);
+      if (measure) {
+        if ((status = H.rows(kap, (float)e, kap, fn, 2 * t + 2)) != OTK_OK) break;
+      }
+      if ((status = otk_check(f, measure ? fn : nullptr, A->a, A->n, L.g, A->b, A->m, e, L.chk,
+                              L.chk_ws, st)) != OTK_OK)
+        break;
+      extra_launches += 1;
+      double out[8];
+      int fb;
+      OTK_CUDA(cudaMemcpyAsync(out, L.chk, sizeof(out), cudaMemcpyDeviceToHost, st));
+      OTK_CUDA(cudaMemcpyAsync(&fb, L.first_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+      OTK_CUDA(cudaStreamSynchronize(st));
+      if (fb <= 2 * t) { status = OTK_BAD_POTENTIAL; A->fail_iter = (fb + 1) / 2; break; }
+      if (out[4] > 0 || out[5] > 0) { status = OTK_DIVERGED; A->fail_iter = t; break; }
+      if (!measure) continue;
+      if (fb == 2 * t + 1) { status = OTK_BAD_POTENTIAL; A->fail_iter = t; break; }
+      const double err = out[0];
+      const double dual = out[2] + out[3] - e * (out[1] - 1.0);
+      if (A->n_checks < A->max_checks) {
+        A->errors[A->n_checks] = err;
+        A->duals[A->n_checks] = dual;
+        A->n_checks++;
+      }
+      if (err <= A->threshold) { A->converged = 1; break; }
+      if (t < A->max_iters) {
+        std::swap(f, fn);
+        f_ready = true;
+      }
+    }
+  }
+  for (auto &ex : period_exec)
+    if (ex) cudaGraphExecDestroy(ex);
+  A->iterations = std::min(t, A->max_iters);
+  A->launches = H.launches + extra_launches;
+  if (status < 0) return status;
+  OTK_CUDA(cudaMemcpyAsync(A->f_out, f, A->n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  OTK_CUDA(cudaMemcpyAsync(A->g_out, L.g, A->m * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  OTK_CUDA(cudaStreamSynchronize(st));
+  return status;
+}

@@ -1,0 +1,342 @@
+"""Cost geometries backed by the sm_100a library (drop-in for reference geometry.py).
+
+Mirrors the reference's Geometry plugin API (geometry.py:100-168): solvers
+only touch ``shape``, ``epsilon_default``, ``apply_lse_kernel`` and
+``cost_matrix``.  Points, potentials and costs live on the GPU in float32;
+inputs may be numpy arrays (results come back as float64 numpy, like the
+reference) or CUDA torch tensors (results stay on the device).
+
+Implemented: ``PointCloudGeometry`` with the squared-Euclidean cost (never
+materialised: the online kernels of csrc/lse_simt.cu and csrc/lse_tc.cu),
+``DenseGeometry`` (stored cost, csrc/dense.cu) and ``EpsilonSchedule``.
+Out of scope for this hot-path build: the ``eucl`` /
+``cosine`` costs, the non-log ``apply_kernel`` and ``GridGeometry``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+from ._device import (as_device_f32, device, is_torch, stream, to_output, validate_potential)
+
+__all__ = [
+    "Geometry",
+    "DenseGeometry",
+    "PointCloudGeometry",
+    "EpsilonSchedule",
+    "DEFAULT_EPSILON_SCALE",
+    "DEFAULT_BLOCK_SIZE",
+    "DEFAULT_DENSE_CAP",
+    "COST_FNS",
+]
+
+DEFAULT_EPSILON_SCALE = 0.05        # geometry.py:40
+_MEAN_COST_SAMPLES = 1000           # geometry.py:42
+DEFAULT_BLOCK_SIZE = 256            # geometry.py:44 (accepted, performance-only)
+DEFAULT_DENSE_CAP = 4_000_000       # geometry.py:46
+COST_FNS = ("sqeucl",)              # reference: ("sqeucl", "eucl", "cosine"); see module doc
+_REFERENCE_COST_FNS = ("sqeucl", "eucl", "cosine")
+_LOG2E = 1.4426950408889634
+
+
+def _check_axis(axis: str) -> None:
+    if axis not in ("rows", "cols"):
+        raise ValueError(f"axis must be 'rows' or 'cols', got {axis!r}")
+
+
+class EpsilonSchedule:
+    """Geometric decay toward a target: eps_t = max(target, target*init_scale*decay**t).
+
+    Same parameters and validation as the reference (geometry.py:75-97).
+    """
+
+    def __init__(self, target: float, init_scale: float = 1.0, decay: float = 1.0):
+        if not (target > 0):
+            raise ValueError("target must be positive")
+        if init_scale < 1.0:
+            raise ValueError("init_scale must be >= 1")
+        if not (0.0 < decay <= 1.0):
+            raise ValueError("decay must lie in (0, 1]")
+        if init_scale > 1.0 and decay == 1.0:
+            raise ValueError("schedule with init_scale > 1 and decay = 1 never reaches its target")
+        self.target = float(target)
+        self.init_scale = float(init_scale)
+        self.decay = float(decay)
+
+    def at(self, t: int) -> float:
+        return max(self.target, self.target * self.init_scale * self.decay ** t)
+
+
+class Geometry:
+    """Abstract cost structure between n source and m target locations."""
+
+    _shape: tuple[int, int]
+    _epsilon_default: float | None
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return self._shape
+
+    @property
+    def epsilon_default(self) -> float:
+        if self._epsilon_default is None:
+            self._epsilon_default = DEFAULT_EPSILON_SCALE * self.mean_cost()
+        return self._epsilon_default
+
+    def mean_cost(self) -> float:
+        raise NotImplementedError
+
+    def cost_matrix(self, max_entries: int | None = None):
+        raise NotImplementedError
+
+    def apply_kernel(self, v, eps=None, axis="rows"):
+        raise NotImplementedError(
+            "apply_kernel (non-log Gibbs kernel) is outside this build's hot path; "
+            "use apply_lse_kernel")
+
+    def apply_lse_kernel(self, f, g, eps=None, axis="rows"):
+        raise NotImplementedError
+
+    def _resolve_eps(self, eps) -> float:
+        if eps is None:
+            return self.epsilon_default
+        eps = float(eps)
+        if not (eps > 0):
+            raise ValueError("eps must be positive")
+        return eps
+
+    def _check_cap(self, max_entries: int | None) -> None:
+        # Reads the module global at call time, like the reference (geometry.py:162-168).
+        cap = DEFAULT_DENSE_CAP if max_entries is None else int(max_entries)
+        n, m = self.shape
+        if n * m > cap:
+            raise ValueError(
+                f"cost matrix with {n}x{m} = {n * m} entries exceeds the materialization cap {cap}")
+
+
+def _validate_points(p, name):
+    if is_torch(p):
+        if p.ndim != 2:
+            raise ValueError("x and y must be 2-D arrays of shape (num_points, dim)")
+        if p.shape[0] == 0:
+            raise ValueError("point sets must be non-empty")
+        return p
+    p = np.asarray(p, dtype=float)
+    if p.ndim != 2:
+        raise ValueError("x and y must be 2-D arrays of shape (num_points, dim)")
+    if p.shape[0] == 0:
+        raise ValueError("point sets must be non-empty")
+    return p
+
+
+def _all_finite(p) -> bool:
+    if is_torch(p):
+        import torch
+        return bool(torch.isfinite(p).all().item())
+    return bool(np.all(np.isfinite(p)))
+
+
+class _Cloud:
+    """Device-resident point set: fp32 points, squared norms, split-fp16 planes."""
+
+    def __init__(self, pts):
+        import torch
+        self.p = as_device_f32(pts).contiguous()
+        self.n, self.d = self.p.shape
+        self.sq = torch.empty(self.n, dtype=torch.float32, device=self.p.device)
+        self.dpad = (self.d + 63) // 64 * 64
+        self.hi = self.lo = None
+        self.scale = 1.0
+        lib = N.lib()
+        if self.d >= 32:
+            amax = torch.empty(1, dtype=torch.float32, device=self.p.device)
+            N.check(lib.otk_absmax(N.ptr(self.p), self.n * self.d, N.ptr(amax), stream()), "absmax")
+            a = float(amax.item())
+            self.scale = 1.0 if not (a > 0 and np.isfinite(a)) else float(
+                2.0 ** np.clip(np.floor(np.log2(16384.0 / a)), -60, 60))
+            self.hi = torch.empty((self.n, self.dpad), dtype=torch.float16, device=self.p.device)
+            self.lo = torch.empty_like(self.hi)
+        N.check(lib.otk_prep_points(N.ptr(self.p), self.n, self.d, N.ptr(self.sq), N.ptr(self.hi),
+                                    N.ptr(self.lo), self.dpad, self.scale, stream()), "prep")
+
+
+class PointCloudGeometry(Geometry):
+    """Squared-Euclidean costs between two point sets, never materialised.
+
+    Same constructor and validation as the reference (geometry.py:226-261).
+    ``block_size`` is accepted for API compatibility; like the reference it
+    never changes results (the GPU kernels pick their own tiles).
+    """
+
+    def __init__(self, x, y, cost_fn: str = "sqeucl", epsilon_default: float | None = None,
+                 block_size: int = DEFAULT_BLOCK_SIZE):
+        same_obj = x is y
+        x = _validate_points(x, "x")
+        y = x if same_obj else _validate_points(y, "y")
+        if x.shape[1] != y.shape[1]:
+            raise ValueError(f"dimension mismatch: x has d={x.shape[1]}, y has d={y.shape[1]}")
+        if not (_all_finite(x) and (same_obj or _all_finite(y))):
+            raise ValueError("points contain non-finite entries")
+        if cost_fn not in _REFERENCE_COST_FNS:
+            raise ValueError(f"cost_fn must be one of {_REFERENCE_COST_FNS}, got {cost_fn!r}")
+        if cost_fn not in COST_FNS:
+            raise NotImplementedError(
+                f"cost_fn {cost_fn!r} is outside this build's hot path (sqeucl only)")
+        if epsilon_default is not None and not (epsilon_default > 0):
+            raise ValueError("epsilon_default must be positive")
+        if block_size < 1:
+            raise ValueError("block_size must be >= 1")
+        self.x = x
+        self.y = y
+        self.cost_fn = cost_fn
+        self.block_size = int(block_size)
+        self._shape = (int(x.shape[0]), int(y.shape[0]))
+        self._epsilon_default = epsilon_default
+        if same_obj:
+            self._same_points = True
+        elif is_torch(x) or is_torch(y):
+            import torch
+            self._same_points = bool(x.shape == y.shape and torch.equal(
+                as_device_f32(x), as_device_f32(y)))
+        else:
+            self._same_points = bool(x.shape == y.shape and np.array_equal(x, y))
+        self._dev = None
+        self.impl_flags = 0  # N.OTK_IMPL_SIMT / N.OTK_IMPL_TC to force a kernel
+
+    # ---- device state (lazy: construction and validation need no GPU)
+    def _clouds(self):
+        if self._dev is None:
+            device()
+            cx = _Cloud(self.x)
+            cy = cx if self._same_points else _Cloud(self.y)
+            self._dev = (cx, cy)
+        return self._dev
+
+    @property
+    def _flags(self):
+        return N.OTK_CLAMP | (N.OTK_SAME_POINTS if self._same_points else 0) | self.impl_flags
+
+    def mean_cost(self) -> float:
+        """0.05 * this is epsilon_default; subsampled like geometry.py:294-312."""
+        import torch
+        n, m = self.shape
+        cx, cy = self._clouds()
+        if n * m <= _MEAN_COST_SAMPLES:
+            return float(torch.as_tensor(self.cost_matrix(max_entries=n * m)).mean())
+        rng = np.random.default_rng(0)
+        i = rng.integers(0, n, size=_MEAN_COST_SAMPLES)
+        j = rng.integers(0, m, size=_MEAN_COST_SAMPLES)
+        ii = torch.as_tensor(i, device=cx.p.device)
+        jj = torch.as_tensor(j, device=cx.p.device)
+        diff = cx.p[ii].double() - cy.p[jj].double()
+        vals = torch.clamp((diff * diff).sum(dim=1), min=0.0)
+        if self._same_points:
+            vals = torch.where(ii == jj, torch.zeros_like(vals), vals)
+        return float(vals.mean().item())
+
+    def cost_matrix(self, max_entries: int | None = None):
+        """Materialise C on the GPU (difference form); refuses past the cap."""
+        import torch
+        self._check_cap(max_entries)
+        cx, cy = self._clouds()
+        n, m = self.shape
+        out = torch.empty((n, m), dtype=torch.float32, device=cx.p.device)
+        N.check(N.lib().otk_dense_cost(N.ptr(cx.p), N.ptr(cy.p), 1, n, m, cx.d,
+                                       N.OTK_SAME_POINTS if self._same_points else 0, N.ptr(out),
+                                       stream()), "cost_matrix")
+        return to_output(out, self.x)
+
+    def apply_lse_kernel(self, f, g, eps=None, axis="rows"):
+        """rows: f_i + eps*LSE_j((g_j - C_ij)/eps); cols: the same over i (geometry.py:336-354)."""
+        import torch
+        _check_axis(axis)
+        eps = self._resolve_eps(eps)
+        n, m = self.shape
+        like = f
+        f = validate_potential(f, n, "f")
+        g = validate_potential(g, m, "g")
+        cx, cy = self._clouds()
+        kappa = float(np.float32(_LOG2E / eps))
+        if axis == "rows":
+            P, Q, base, qpot, npts, nq = cx, cy, f, g, n, m
+        else:
+            P, Q, base, qpot, npts, nq = cy, cx, g, f, m, n
+        lib = N.lib()
+        st = stream()
+        bias = torch.empty(nq, dtype=torch.float32, device=cx.p.device)
+        N.check(lib.otk_make_bias(N.ptr(qpot), N.ptr(Q.sq), nq, kappa, N.ptr(bias), None, 0, st))
+        flags = self._flags
+        nsplit = lib.otk_lse_suggest_nsplit(npts, nq, cx.d, flags)
+        part = torch.empty(nsplit * npts, dtype=torch.float32, device=cx.p.device)
+        sinv = 1.0 / (P.scale * Q.scale)
+        N.check(lib.otk_lse_partial(N.ptr(P.p), N.ptr(P.sq), N.ptr(P.hi), N.ptr(P.lo), npts,
+                                    N.ptr(Q.p), N.ptr(Q.sq), N.ptr(Q.hi), N.ptr(Q.lo), nq, cx.d,
+                                    cx.dpad, sinv, N.ptr(bias), kappa, flags, nsplit, N.ptr(part),
+                                    st), "apply_lse_kernel")
+        out = torch.empty(npts, dtype=torch.float32, device=cx.p.device)
+        N.check(lib.otk_lse_finalize(N.ptr(part), nsplit, npts, N.ptr(P.sq), N.ptr(base),
+                                     N.OTK_FIN_APPLY, float(eps), 0.0, N.ptr(out), None, None, 0,
+                                     st), "finalize")
+        return to_output(out, like)
+
+
+class DenseGeometry(Geometry):
+    """Geometry backed by an explicit cost matrix (geometry.py:171-211), stored on the GPU."""
+
+    def __init__(self, cost, epsilon_default: float | None = None):
+        if is_torch(cost):
+            if cost.ndim != 2 or cost.numel() == 0:
+                raise ValueError(f"cost must be a non-empty 2-D array, got shape {tuple(cost.shape)}")
+        else:
+            cost = np.asarray(cost, dtype=float)
+            if cost.ndim != 2 or cost.size == 0:
+                raise ValueError(f"cost must be a non-empty 2-D array, got shape {cost.shape}")
+        if not _all_finite(cost):
+            raise ValueError("cost matrix contains non-finite entries")
+        if epsilon_default is not None and not (epsilon_default > 0):
+            raise ValueError("epsilon_default must be positive")
+        self._cost_in = cost
+        self._shape = (int(cost.shape[0]), int(cost.shape[1]))
+        self._epsilon_default = epsilon_default
+        self._dev = None
+
+    def _c(self):
+        if self._dev is None:
+            device()
+            self._dev = as_device_f32(self._cost_in).contiguous()
+        return self._dev
+
+    def mean_cost(self) -> float:
+        if is_torch(self._cost_in):
+            return float(self._cost_in.double().mean().item())
+        return float(self._cost_in.mean())
+
+    def cost_matrix(self, max_entries: int | None = None):
+        self._check_cap(max_entries)
+        return self._cost_in
+
+    def apply_lse_kernel(self, f, g, eps=None, axis="rows"):
+        import torch
+        _check_axis(axis)
+        eps = self._resolve_eps(eps)
+        n, m = self.shape
+        like = f
+        f = validate_potential(f, n, "f")
+        g = validate_potential(g, m, "g")
+        C = self._c()
+        kappa = float(np.float32(_LOG2E / eps))
+        if axis == "rows":
+            qpot, base, nout, nq = g, f, n, m
+        else:
+            qpot, base, nout, nq = f, g, m, n
+        in_bias = torch.empty(nq, dtype=torch.float32, device=C.device)
+        N.check(N.lib().otk_make_bias(N.ptr(qpot), None, nq, kappa, N.ptr(in_bias), None, 0,
+                                      stream()))
+        eps_t = torch.tensor([eps], dtype=torch.float32, device=C.device)
+        out = torch.empty(nout, dtype=torch.float32, device=C.device)
+        N.check(N.lib().otk_dense_lse(N.ptr(C), 1, n, m, 0 if axis == "rows" else 1,
+                                      N.ptr(in_bias), N.ptr(base), N.OTK_FIN_APPLY,
+                                      N.ptr(eps_t), None, None, N.ptr(out), None, None, 0,
+                                      stream()), "apply_lse_kernel")
+        return to_output(out, like)

@@ -1,0 +1,301 @@
+"""CUDA path vs the oracle / reference golden fixtures (needs a B200).
+
+Tolerances (BASELINE.json north_star, float32 device arithmetic):
+  potentials f, g: ||delta||_inf / ||ref||_inf <= 1e-4
+  regularised OT cost (transport, dual): relative <= 1e-5
+  iteration count and converged flag: identical to the reference.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import load_golden
+from paper_2201_12324_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+POT_TOL = 1e-4
+COST_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def otk():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_12324_b200 as m
+    from paper_2201_12324_b200 import _native
+    _native.lib()
+    return m
+
+
+def rel_inf(got, want):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    fin = np.isfinite(want)
+    assert np.array_equal(np.isfinite(got), fin), "finite pattern differs"
+    assert np.array_equal(got[~fin], want[~fin])
+    if not fin.any():
+        return 0.0
+    return float(np.max(np.abs(got[fin] - want[fin])) / max(np.max(np.abs(want[fin])), 1e-30))
+
+
+# ------------------------------------------------------------------ kernels
+@pytest.mark.parametrize("impl", ["simt", "auto"])
+def test_apply_lse_kernel_matches_reference_cases(otk, impl):
+    fx = load_golden("lse_pointcloud")
+    keys = sorted({k.split("__")[0] for k in fx})
+    for key in keys:
+        c = {k.split("__")[1]: v for k, v in fx.items() if k.startswith(key + "__")}
+        x = c["x"]
+        y = x if bool(c["same"]) else c["y"]
+        geom = otk.PointCloudGeometry(x, y, block_size=37)
+        if impl == "simt":
+            from paper_2201_12324_b200 import _native
+            geom.impl_flags = _native.OTK_IMPL_SIMT
+        eps = float(c["eps"])
+        for axis in ("rows", "cols"):
+            got = geom.apply_lse_kernel(c["f"], c["g"], eps, axis)
+            err = rel_inf(got, c[axis])
+            assert err <= 2e-5, f"{key} {axis}: {err:.2e}"
+
+
+def test_lse_kernel_known_answers(otk):
+    ka = load_golden("known_answers")
+    geom = otk.DenseGeometry(np.zeros((2, 2)))
+    np.testing.assert_allclose(geom.apply_lse_kernel(np.zeros(2), np.zeros(2), 1.0, "rows"),
+                               ka["log2"], rtol=1e-6)
+    out = geom.apply_lse_kernel(np.zeros(2), np.array([0.0, -np.inf]), 1.0, "rows")
+    np.testing.assert_allclose(out, 0.0, atol=1e-6)
+    with pytest.raises(ValueError):
+        geom.apply_lse_kernel(np.array([0.0, np.nan]), np.zeros(2), 1.0, "rows")
+    # huge offsets stay finite (test_geometry.py:160-168)
+    rng = np.random.default_rng(4)
+    dg = otk.DenseGeometry(rng.random((3, 4)))
+    f = rng.standard_normal(3)
+    g = rng.standard_normal(4)
+    base = dg.apply_lse_kernel(f, g, 0.5, "rows")
+    shifted = dg.apply_lse_kernel(f - 1e6, g, 0.5, "rows")
+    assert np.all(np.isfinite(shifted))
+    np.testing.assert_allclose(shifted + 1e6, base, atol=0.2)  # float32 ulp at 1e6 is 0.0625
+    # point cloud: all-equal points -> log(m) offsets
+    pc = otk.PointCloudGeometry(np.zeros((3, 2)), np.zeros((5, 2)))
+    np.testing.assert_allclose(pc.apply_lse_kernel(np.zeros(3), np.zeros(5), 1.0, "rows"),
+                               np.log(5.0), rtol=1e-6)
+
+
+@pytest.mark.parametrize("k", [2, 4, 5])
+def test_full_size_half_step_spot_checks(otk, k):
+    """Exact reference half-steps on 256 rows / columns at the FULL config sizes."""
+    fx = load_golden(f"spot_cfg{k}")
+    wl = workloads.make(k)
+    geom = otk.PointCloudGeometry(wl.x, wl.y)
+    eps = float(fx["eps"])
+    n, m = wl.shape
+    rows0 = geom.apply_lse_kernel(np.zeros(n), np.zeros(m), eps, "rows")[fx["rows"]]
+    assert rel_inf(rows0, fx["rows_g0"]) <= 2e-5
+    rows_g = geom.apply_lse_kernel(np.zeros(n), fx["g"].astype(np.float64), eps, "rows")[fx["rows"]]
+    assert rel_inf(rows_g, fx["rows_g"]) <= 2e-5
+    cols_f = geom.apply_lse_kernel(fx["f"].astype(np.float64), np.zeros(m), eps, "cols")[fx["cols"]]
+    assert rel_inf(cols_f, fx["cols_f"]) <= 2e-5
+
+
+# ------------------------------------------------------------------ solves
+def _solve_golden(otk, name, **kw):
+    fx = load_golden(name)
+    gen = getattr(workloads, str(fx["gen"]))
+    wl = gen(**json.loads(str(fx["kw"])))
+    prob = otk.LinearProblem(otk.PointCloudGeometry(wl.x, wl.y), wl.a, wl.b)
+    return fx, wl, prob
+
+
+@pytest.mark.parametrize("name", ["cfg1_small", "cfg1_full", "cfg2_small", "cfg4_small",
+                                  "cfg5_small", "short_nonconv", "nonuniform_small"])
+@pytest.mark.parametrize("impl", ["auto", "simt"])
+def test_solve_matches_reference(otk, name, impl):
+    fx, wl, prob = _solve_golden(otk, "solve_" + name)
+    out = otk.solve_sinkhorn(prob, float(fx["eps"]), threshold=float(fx["threshold"]),
+                             max_iters=int(fx["max_iters"]), impl=impl)
+    assert out.iterations == int(fx["iterations"])
+    assert out.converged == bool(fx["converged"])
+    assert len(out.errors) == len(fx["errors"])
+    assert rel_inf(out.f, fx["f"]) <= POT_TOL
+    assert rel_inf(out.g, fx["g"]) <= POT_TOL
+    # marginal errors agree above the float32 floor (~1e-6)
+    big = fx["errors"] > 1e-4
+    np.testing.assert_allclose(out.errors[big], fx["errors"][big], rtol=2e-2)
+    cost = otk.reg_ot_cost(out, prob)
+    assert abs(cost.transport_cost - float(fx["transport"])) <= COST_TOL * abs(float(fx["transport"]))
+    assert abs(cost.dual_objective - float(fx["dual"])) <= COST_TOL * abs(float(fx["dual"])) + 1e-6
+
+
+@pytest.mark.parametrize("name", ["cfg1_fixed200", "cfg2_fixed20", "cfg4_fixed20", "cfg5_fixed30"])
+def test_fixed_iteration_runs(otk, name):
+    fx = load_golden("fixed_" + name)
+    wl = getattr(workloads, str(fx["gen"]))(**json.loads(str(fx["kw"])))
+    prob = otk.LinearProblem(otk.PointCloudGeometry(wl.x, wl.y), wl.a, wl.b)
+    out = otk.solve_sinkhorn(prob, float(fx["eps"]), threshold=1e-300, max_iters=int(fx["iters"]))
+    assert out.iterations == int(fx["iters"]) and not out.converged
+    assert rel_inf(out.f, fx["f"]) <= POT_TOL, rel_inf(out.f, fx["f"])
+    assert rel_inf(out.g, fx["g"]) <= POT_TOL, rel_inf(out.g, fx["g"])
+    cost = otk.reg_ot_cost(out, prob)
+    assert abs(cost.transport_cost / float(fx["transport"]) - 1) <= COST_TOL
+    assert abs(cost.dual_objective / float(fx["dual"]) - 1) <= COST_TOL
+
+
+def test_bitwise_determinism(otk):
+    wl = workloads.cfg2(n=1500, m=1300)
+    prob = otk.LinearProblem(otk.PointCloudGeometry(wl.x, wl.y))
+    o1 = otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=25)
+    o2 = otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=25)
+    np.testing.assert_array_equal(o1.f, o2.f)
+    np.testing.assert_array_equal(o1.g, o2.g)
+    np.testing.assert_array_equal(o1.errors, o2.errors)
+    np.testing.assert_array_equal(o1.dual_trace, o2.dual_trace)
+
+
+def test_graphs_do_not_change_results(otk):
+    wl = workloads.cfg1(n=700, m=500)
+    prob = otk.LinearProblem(otk.PointCloudGeometry(wl.x, wl.y))
+    o1 = otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=37, use_graphs=True)
+    o2 = otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=37, use_graphs=False)
+    np.testing.assert_array_equal(o1.f, o2.f)
+    np.testing.assert_array_equal(o1.g, o2.g)
+    np.testing.assert_array_equal(o1.errors, o2.errors)
+
+
+# ------------------------------------------------------------------ pinned examples
+def test_pinned_point_cloud_examples(otk):
+    ka = load_golden("known_answers")
+    geom = otk.PointCloudGeometry(np.array([[0.0], [1.0]]), np.array([[0.5], [2.0]]))
+    prob = otk.LinearProblem(geom)
+    out = otk.solve_sinkhorn(prob, float(ka["two_point_eps"]))
+    assert out.converged and out.iterations == int(ka["two_point_iters"])
+    cost = otk.reg_ot_cost(out, prob)
+    assert abs(cost.transport_cost - 0.625) <= 1e-2
+    plan = otk.transport_matrix(out, prob).matrix
+    assert plan[0, 1] + plan[1, 0] <= 1e-3
+    # self-matching
+    xs = np.array([[0.0], [1.0], [2.0], [3.0]])
+    geom = otk.PointCloudGeometry(xs, xs)
+    prob = otk.LinearProblem(geom)
+    out = otk.solve_sinkhorn(prob, float(ka["self_eps"]))
+    assert otk.reg_ot_cost(out, prob).transport_cost <= 1e-6
+    plan = otk.transport_matrix(out, prob).matrix
+    np.testing.assert_array_equal(plan.argmax(axis=1), np.arange(4))
+    np.testing.assert_allclose(plan, np.eye(4) / 4.0, atol=1e-6)
+    # singleton: cost 9, P = [[1]]
+    geom = otk.PointCloudGeometry(np.array([[0.0]]), np.array([[3.0]]))
+    prob = otk.LinearProblem(geom)
+    out = otk.solve_sinkhorn(prob, 1.0)
+    np.testing.assert_allclose(otk.transport_matrix(out, prob).matrix, [[1.0]], atol=1e-6)
+    np.testing.assert_allclose(otk.reg_ot_cost(out, prob), ka["single_cost"], rtol=1e-6)
+    # large eps -> independent coupling
+    geom = otk.PointCloudGeometry(np.array([[0.0], [1.0]]), np.array([[0.0], [1.0]]))
+    prob = otk.LinearProblem(geom)
+    out = otk.solve_sinkhorn(prob, float(ka["bigeps_eps"]))
+    np.testing.assert_allclose(otk.transport_matrix(out, prob).matrix, ka["bigeps_plan"], atol=1e-6)
+    # zero-weight column empties the plan column
+    geom = otk.PointCloudGeometry(np.array([[0.0], [1.0]]), np.array([[0.2], [0.9]]))
+    prob = otk.LinearProblem(geom, None, np.array([1.0, 0.0]))
+    out = otk.solve_sinkhorn(prob, 0.5)
+    plan = otk.transport_matrix(out, prob).matrix
+    np.testing.assert_allclose(plan[:, 1], 0.0, atol=1e-12)
+    np.testing.assert_allclose(plan, ka["zerow_plan"], atol=1e-6)
+    assert out.g[1] == -np.inf
+    # epsilon schedule
+    geom = otk.PointCloudGeometry(np.array([[0.0], [1.0]]), np.array([[0.5], [2.0]]))
+    prob = otk.LinearProblem(geom)
+    sched = otk.EpsilonSchedule(float(ka["sched_target"]), init_scale=100.0, decay=0.5)
+    out = otk.solve_sinkhorn(prob, sched, threshold=1e-6, max_iters=10_000)
+    assert out.converged and out.eps == float(ka["sched_target"])
+    assert out.iterations == int(ka["sched_iters"])
+    assert abs(otk.reg_ot_cost(out, prob).transport_cost - 0.625) <= 1e-2
+
+
+def test_failure_modes(otk):
+    cost = np.array([[0.0, 2.0, 3.0], [2.0, 0.0, 3.0]])
+    prob = otk.LinearProblem(otk.DenseGeometry(cost), None, np.array([0.5, 0.5, 0.0]))
+    with pytest.raises(otk.DivergedError) as exc:
+        otk.solve_sinkhorn(prob, 1e-320, inner_iters=1)
+    assert exc.value.iteration >= 1
+    prob = otk.LinearProblem(otk.DenseGeometry(np.ones((2, 2))))
+    with pytest.raises(ValueError):
+        otk.solve_sinkhorn(prob, 0.0)
+    with pytest.raises(ValueError):
+        otk.solve_sinkhorn(prob, 1.0, threshold=0.0)
+    with pytest.raises(ValueError):
+        otk.solve_sinkhorn(prob, 1.0, max_iters=0)
+
+
+# ------------------------------------------------------------------ dense / batched
+def test_dense_geometry_solves_match_reference(otk):
+    fx = load_golden("dense_cfg3")
+    wl = workloads.cfg3(batch=3)
+    for k in range(3):
+        cost = oracle.PointCloudOracle(wl.x[k].astype(np.float64),
+                                       wl.y[k].astype(np.float64)).cost_matrix()
+        prob = otk.LinearProblem(otk.DenseGeometry(cost))
+        out = otk.solve_sinkhorn(prob, float(wl.eps[k]), threshold=wl.threshold,
+                                 max_iters=wl.max_iters)
+        assert out.iterations == int(fx[f"p{k}_iters"])
+        assert rel_inf(out.f, fx[f"p{k}_f"]) <= POT_TOL
+        assert rel_inf(out.g, fx[f"p{k}_g"]) <= POT_TOL
+        rc = otk.reg_ot_cost(out, prob)
+        np.testing.assert_allclose(rc, fx[f"p{k}_cost"], rtol=COST_TOL)
+
+
+def test_batched_cfg3_matches_reference(otk):
+    fx = load_golden("dense_cfg3")
+    wl = workloads.cfg3(batch=6)
+    outs, costs = otk.solve_sinkhorn_batched(wl.x, wl.y, wl.eps, threshold=wl.threshold,
+                                             max_iters=wl.max_iters, return_cost=True)
+    for k in range(6):
+        assert outs[k].iterations == int(fx[f"p{k}_iters"])
+        assert outs[k].converged
+        assert rel_inf(outs[k].f, fx[f"p{k}_f"]) <= POT_TOL
+        assert rel_inf(outs[k].g, fx[f"p{k}_g"]) <= POT_TOL
+        np.testing.assert_allclose(costs[k], fx[f"p{k}_cost"], rtol=COST_TOL)
+
+
+def test_dense_reference_style_properties(otk):
+    # test_sinkhorn.py:72-94 settings (float32 tolerances)
+    rng = np.random.default_rng(8)
+    geom = otk.DenseGeometry(rng.random((5, 4)))
+    a = rng.random(5) + 0.2
+    a /= a.sum()
+    b = rng.random(4) + 0.2
+    b /= b.sum()
+    prob = otk.LinearProblem(geom, a, b)
+    out = otk.solve_sinkhorn(prob, 0.05 * geom.mean_cost(), threshold=1e-5, max_iters=10_000)
+    assert out.converged
+    plan = otk.transport_matrix(out, prob)
+    assert np.abs(plan.row_marginal() - a).sum() <= 1e-5
+    assert np.abs(plan.col_marginal() - b).sum() <= 2e-5
+    rng = np.random.default_rng(9)
+    geom = otk.DenseGeometry(rng.random((6, 6)))
+    out = otk.solve_sinkhorn(otk.LinearProblem(geom), 0.01 * geom.mean_cost(), threshold=1e-5,
+                             max_iters=20_000)
+    assert len(out.dual_trace) == len(out.errors)
+    assert np.all(np.diff(out.dual_trace) >= -1e-6)
+
+
+# ------------------------------------------------------------------ full-size properties
+@pytest.mark.parametrize("k", [2])
+def test_full_size_properties(otk, k):
+    """At BASELINE sizes: first f half-step equals the reference spot values, the
+    dual trace is nondecreasing and the marginal error drops."""
+    wl = workloads.make(k)
+    prob = otk.LinearProblem(otk.PointCloudGeometry(wl.x, wl.y))
+    out = otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=30)
+    assert np.all(np.isfinite(out.f)) and np.all(np.isfinite(out.g))
+    assert np.all(np.diff(out.dual_trace) >= -1e-6 * np.abs(out.dual_trace[:-1]))
+    assert out.errors[-1] < out.errors[0]
+    fx = load_golden(f"spot_cfg{k}")
+    one = otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=1)
+    # f_1 = eps*log(1/n) - eps*LSE_j(-C_ij/eps)
+    f1_ref = wl.eps * np.log(1.0 / wl.shape[0]) - fx["rows_g0"]
+    assert rel_inf(one.f[fx["rows"]], f1_ref) <= 2e-5
