@@ -329,9 +329,11 @@ def _count_launches(otk, prob, wl, args):
         captured["launches"] = ctypes.cast(ptr, ctypes.POINTER(S.N.SolveArgs)).contents.launches
         return rc
 
+    real = S.N.lib()
+
     class Proxy:
         def __getattr__(self, name):
-            return spy if name == "otk_solve_pointcloud" else getattr(S.N.lib(), name)
+            return spy if name == "otk_solve_pointcloud" else getattr(real, name)
 
     saved = S.N.lib
     S.N.lib = lambda: Proxy()

@@ -187,6 +187,8 @@ static float pow2_scale_for(float amax) {
   return std::ldexp(1.f, e);
 }
 
+static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st);
+
 extern "C" int otk_solve_pointcloud(otk_solve_args *A) {
   OTK_CHECK_ARG(A && A->x && A->y && A->a && A->b && A->log_a && A->log_b && A->f_out && A->g_out,
                 "otk_solve_pointcloud: missing pointers");
@@ -198,7 +200,27 @@ extern "C" int otk_solve_pointcloud(otk_solve_args *A) {
   Layout L = plan(A, A->workspace);
   OTK_CHECK_ARG(A->workspace && A->workspace_bytes >= L.bytes,
                 "otk_solve_pointcloud: workspace too small (%zu < %zu)", A->workspace_bytes, L.bytes);
-  cudaStream_t st = as_stream(A->stream);
+  // Work runs on a private non-blocking stream ordered after the caller's
+  // stream (graph capture is not allowed on the legacy default stream).
+  cudaStream_t caller = as_stream(A->stream);
+  cudaStream_t st;
+  cudaEvent_t ev_in, ev_out;
+  OTK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  OTK_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+  OTK_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+  OTK_CUDA(cudaEventRecord(ev_in, caller));
+  OTK_CUDA(cudaStreamWaitEvent(st, ev_in, 0));
+  int rc = solve_on_stream(A, L, st);
+  cudaEventRecord(ev_out, st);
+  cudaStreamWaitEvent(caller, ev_out, 0);
+  cudaStreamSynchronize(st);
+  cudaEventDestroy(ev_in);
+  cudaEventDestroy(ev_out);
+  cudaStreamDestroy(st);
+  return rc;
+}
+
+static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st) {
   A->n_checks = 0;
   A->iterations = 0;
   A->converged = 0;
