@@ -1,0 +1,94 @@
+"""tcgen05 (split-fp16) half-step kernel vs the FP32 kernel and the float64 oracle."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def otk():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_12324_b200 as m
+    from paper_2201_12324_b200 import _native
+    _native.lib()
+    return m
+
+
+def _half_steps(otk, x, y, f, g, eps, impl):
+    from paper_2201_12324_b200 import _native as N
+    geom = otk.PointCloudGeometry(x, y)
+    geom.impl_flags = N.OTK_IMPL_TC if impl == "tc" else N.OTK_IMPL_SIMT
+    return (geom.apply_lse_kernel(f, g, eps, "rows"), geom.apply_lse_kernel(f, g, eps, "cols"))
+
+
+@pytest.mark.parametrize("n,m,d", [(128, 256, 64), (300, 517, 64), (1000, 700, 128),
+                                   (257, 1031, 96), (640, 384, 256), (200, 300, 1024),
+                                   (4096, 4096, 64), (1, 1, 40)])
+def test_tc_matches_oracle(otk, n, m, d):
+    rng = np.random.default_rng(n * 7 + m + d)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    y = (1.3 * rng.standard_normal((m, d)) + 0.2).astype(np.float32)
+    geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64))
+    eps = 0.05 * float(np.mean([np.sum((x[i] - y[j]) ** 2) for i, j in
+                                zip(rng.integers(0, n, 200), rng.integers(0, m, 200))]))
+    f = (rng.standard_normal(n) * eps).astype(np.float32).astype(np.float64)
+    g = (rng.standard_normal(m) * eps).astype(np.float32).astype(np.float64)
+    ref_r = geom64.apply_lse_kernel(f, g, eps, "rows")
+    ref_c = geom64.apply_lse_kernel(f, g, eps, "cols")
+    tr, tcol = _half_steps(otk, x, y, f, g, eps, "tc")
+    scale_r = np.max(np.abs(ref_r))
+    scale_c = np.max(np.abs(ref_c))
+    assert np.max(np.abs(tr - ref_r)) / scale_r <= 1e-5
+    assert np.max(np.abs(tcol - ref_c)) / scale_c <= 1e-5
+
+
+def test_tc_unit_sphere_small_eps(otk):
+    """cfg5-like regime (unit vectors, eps = 0.01 * mean)."""
+    rng = np.random.default_rng(5)
+    n, m, d = 512, 640, 1024
+    x = rng.standard_normal((n, d))
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    y = rng.standard_normal((m, d))
+    y /= np.linalg.norm(y, axis=1, keepdims=True)
+    x, y = x.astype(np.float32), y.astype(np.float32)
+    eps = 0.02
+    geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64))
+    f = np.zeros(n)
+    g = (rng.standard_normal(m) * 0.01).astype(np.float32).astype(np.float64)
+    ref = geom64.apply_lse_kernel(f, g, eps, "rows")
+    got, _ = _half_steps(otk, x, y, f, g, eps, "tc")
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) <= 1e-5
+
+
+def test_tc_minus_inf_bias_columns(otk):
+    rng = np.random.default_rng(1)
+    n, m, d = 300, 600, 64
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    y = rng.standard_normal((m, d)).astype(np.float32)
+    g = rng.standard_normal(m) * 5
+    g[rng.random(m) < 0.5] = -np.inf
+    f = np.zeros(n)
+    geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64))
+    ref = geom64.apply_lse_kernel(f, g, 10.0, "rows")
+    got, _ = _half_steps(otk, x, y, f, g, 10.0, "tc")
+    assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) <= 1e-5
+    g[:] = -np.inf
+    got, _ = _half_steps(otk, x, y, f, g, 10.0, "tc")
+    assert np.all(got == -np.inf)
+
+
+def test_tc_deterministic(otk):
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((3000, 64)).astype(np.float32)
+    y = rng.standard_normal((2500, 64)).astype(np.float32)
+    f = np.zeros(3000)
+    g = rng.standard_normal(2500)
+    a1, b1 = _half_steps(otk, x, y, f, g, 7.0, "tc")
+    a2, b2 = _half_steps(otk, x, y, f, g, 7.0, "tc")
+    np.testing.assert_array_equal(a1, a2)
+    np.testing.assert_array_equal(b1, b2)
