@@ -128,6 +128,7 @@ struct Params {
   int64_t np, nq;
   int kb;                 // K-blocks (dpad / 64)
   int row_tiles, ntiles, tps, nsplit, num_units;
+  int order;              // MMA product order (accuracy experiments)
   const float *qbias;
   float c2k;              // 2*kappa/(s_p*s_q)
   float *partial;         // [nsplit][np]
@@ -263,14 +264,40 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t al = smem_u32(A_RES ? a_tile(ab, k, 1) : st_a(stage, 1));
             const uint32_t bh = smem_u32(st_b(stage, 0));
             const uint32_t bl = smem_u32(st_b(stage, 1));
+            if (prm.order == 0) {
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint32_t off = kk * 32;  // 16 fp16 = 32 B along the swizzled row
-              const uint64_t dah = sw128_desc(ah + off), dal = sw128_desc(al + off);
-              const uint64_t dbh = sw128_desc(bh + off), dbl = sw128_desc(bl + off);
-              umma_f16(d_tmem, dah, dbh, (k | kk) != 0 ? 1u : 0u);
-              umma_f16(d_tmem, dah, dbl, 1u);
-              umma_f16(d_tmem, dal, dbh, 1u);
+              for (int kk = 0; kk < BK / 16; ++kk) {
+                const uint32_t off = kk * 32;  // 16 fp16 = 32 B along the swizzled row
+                const uint64_t dah = sw128_desc(ah + off), dal = sw128_desc(al + off);
+                const uint64_t dbh = sw128_desc(bh + off), dbl = sw128_desc(bl + off);
+                umma_f16(d_tmem, dah, dbh, (k | kk) != 0 ? 1u : 0u);
+                umma_f16(d_tmem, dah, dbl, 1u);
+                umma_f16(d_tmem, dal, dbh, 1u);
+              }
+            } else if (prm.order == 1) {  // small cross terms first, then hi*hi
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk) {
+                const uint32_t off = kk * 32;
+                umma_f16(d_tmem, sw128_desc(ah + off), sw128_desc(bl + off), (k | kk) != 0 ? 1u : 0u);
+                umma_f16(d_tmem, sw128_desc(al + off), sw128_desc(bh + off), 1u);
+              }
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk) {
+                const uint32_t off = kk * 32;
+                umma_f16(d_tmem, sw128_desc(ah + off), sw128_desc(bh + off), 1u);
+              }
+            } else {  // hi*hi first, then cross terms
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk) {
+                const uint32_t off = kk * 32;
+                umma_f16(d_tmem, sw128_desc(ah + off), sw128_desc(bh + off), (k | kk) != 0 ? 1u : 0u);
+              }
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk) {
+                const uint32_t off = kk * 32;
+                umma_f16(d_tmem, sw128_desc(ah + off), sw128_desc(bl + off), 1u);
+                umma_f16(d_tmem, sw128_desc(al + off), sw128_desc(bh + off), 1u);
+              }
             }
             umma_commit(&empty[stage]);  // smem stage free once these MMAs retire
             if (++stage == NS) {
@@ -468,6 +495,10 @@ int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, int64_t np, const 
   prm.tps = (prm.ntiles + nsplit - 1) / nsplit;
   prm.num_units = prm.row_tiles * nsplit;
   prm.qbias = q_bias;
+  {
+    const char *o = getenv("OTK_TC_ORDER");
+    prm.order = o ? atoi(o) : 0;
+  }
   prm.c2k = two_kappa_scaled;
   prm.partial = partial;
   if (prm.kb == 1) return launch_variant<true, 2, 2>(maps, prm, st);
