@@ -175,13 +175,13 @@ def kernel_roofline(otk, geom, wl, reps=20):
     nsplit = lib.otk_lse_suggest_nsplit(n, m, cx.d, flags)
     part = torch.empty(nsplit * n, dtype=torch.float32, device=cx.p.device)
     st = stream()
-    sinv = 1.0 / (cx.scale * cy.scale)
+    sinv = 1.0 / (cx.scale * cx.scale)
 
     def launch():
-        N.check(lib.otk_lse_partial(N.ptr(cx.p), N.ptr(cx.sq), N.ptr(cx.hi), N.ptr(cx.lo), n,
-                                    N.ptr(cy.p), N.ptr(cy.sq), N.ptr(cy.hi), N.ptr(cy.lo), m, cx.d,
-                                    cx.dpad, sinv, N.ptr(bias), kappa, flags, nsplit, N.ptr(part),
-                                    st))
+        N.check(lib.otk_lse_partial(N.ptr(cx.p), N.ptr(cx.sq), N.ptr(cx.hi), N.ptr(cx.lo),
+                                    N.ptr(cx.ext_a), n, N.ptr(cy.p), N.ptr(cy.sq), N.ptr(cy.hi),
+                                    N.ptr(cy.lo), N.ptr(cy.ext_b), m, cx.d, cx.dpad, sinv,
+                                    N.ptr(bias), kappa, flags, nsplit, N.ptr(part), st))
     for _ in range(3):
         launch()
     e0 = torch.cuda.Event(enable_timing=True)

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define OTK_ABI_VERSION 1
+#define OTK_ABI_VERSION 2
 
 enum otk_status {
   OTK_OK = 0,
@@ -48,60 +48,70 @@ enum otk_status {
 #define OTK_IMPL_TC 0x20    /* force the tcgen05 split-fp16 kernel                                 */
 
 /* finalize modes */
-#define OTK_FIN_SOLVER 0 /* out = eps*logw + |p|^2 - eps*ln2*L   (sinkhorn.py:173-174)            */
-#define OTK_FIN_APPLY 1  /* out = f - |p|^2 + eps*ln2*L           (geometry.py:336-354, axis=rows) */
+#define OTK_FIN_SOLVER 0 /* out = eps*logw - eps*ln2*L   (sinkhorn.py:173-174)                     */
+#define OTK_FIN_APPLY 1  /* out = f + eps*ln2*L           (geometry.py:336-354)                     */
 
 int otk_abi_version(void);
 const char *otk_last_error(void);
 int otk_device_query(int device, int *sm_count, int *cc_major, int *cc_minor);
 
 /* K0 -- per-point preparation.  Replaces the norm einsums of _cost_block
- * (geometry.py:269-270).  sqnorm[i] = |p_i|^2 (float64 accumulate).  If hi/lo
- * are non-NULL also writes the split-fp16 operand planes used by the
- * tcgen05 kernel: hi = fp16(s*p), lo = fp16(s*p - hi), row pitch dpad >= d
- * (zero padded), s = split_scale (a power of two). */
+ * (geometry.py:269-270).  sqnorm[i] = |p_i|^2 (float64 accumulate).  If hi is
+ * non-NULL also writes the split-fp16 operand planes of the tcgen05 kernel
+ * (row pitch dpad >= d, zero padded, s = split_scale a power of two):
+ *   hi = fp16(s*p), lo = fp16(s*p - hi)                      [n, dpad]
+ * and the two 16-column norm planes that add -s^2 (|p_i|^2 + |q_j|^2)/2 in one
+ * MMA at the end of every TC tile (so the accumulators end at -s^2 C_ij/2):
+ *   ext_a[i, 0:16] = [-w0,-w1,-w2, 2^15,2^15,2^15, 0...]   (A role)
+ *   ext_b[i, 0:16] = [2^15,2^15,2^15, -w0,-w1,-w2, 0...]   (B role)
+ * with w0+w1+w2 = s^2 |p_i|^2 / 2^16 in three fp16 pieces.  [n, 16].
+ * s must come from otk_split_scale (fp16 range of hi/lo and the pieces). */
 int otk_prep_points(const float *pts, int64_t n, int32_t d, float *sqnorm,
-                    uint16_t *hi, uint16_t *lo, int32_t dpad, float split_scale,
-                    void *stream);
+                    uint16_t *hi, uint16_t *lo, uint16_t *ext_a, uint16_t *ext_b,
+                    int32_t dpad, float split_scale, void *stream);
 
 /* max |p_ik| over the array (for choosing split_scale); out is one float. */
 int otk_absmax(const float *pts, int64_t count, float *out, void *stream);
 
-/* Bias of the reduced side for the next half-step: bias_j = kappa*(pot_j - sq_j)
- * (sq may be NULL -> 0).  NaN/+inf in pot -> atomicMin(first_bad, step). */
-int otk_make_bias(const float *pot, const float *sq, int64_t m, float kappa,
-                  float *bias, int32_t *first_bad, int32_t step, void *stream);
+/* The power-of-two operand scale for point sets of dimension d whose largest
+ * |coordinate| is amax (one common scale for both sets of a geometry). */
+float otk_split_scale(float amax, int32_t d);
+
+/* Scaled potential of the reduced side for the next half-step:
+ * bias_j = kappa * pot_j.  NaN/+inf in pot -> atomicMin(first_bad, step). */
+int otk_make_bias(const float *pot, int64_t m, float kappa, float *bias,
+                  int32_t *first_bad, int32_t step, void *stream);
 
 /* K1/K2 -- online half-step partials.  Replaces PointCloudGeometry.apply_lse_kernel
  * (geometry.py:336-354) and its _cost_rows/_cost_cols blocks (263-292), never
- * materialising C.  With kappa = log2(e)/eps and
- *     u_ij = 2*kappa*<p_i, q_j> + q_bias_j,
- * writes partial[s*np + i] = log2 sum_{j in split s} 2^(u_ij)   (-inf if empty).
- * Columns are split into `nsplit` equal contiguous ranges (fixed order).
- * OTK_CLAMP / OTK_SAME_POINTS reproduce max(C,0) and the zero diagonal;
- * they need p_sq / q_sq.  The TC path needs the hi/lo planes (dpad % 64 == 0);
- * split_inv = 1/(s_p*s_q) undoes the operand scaling. */
+ * materialising C.  With kappa = log2(e)/eps and q_bias_j = kappa*pot_j:
+ *     partial[s*np + i] = log2 sum_{j in split s} 2^(q_bias_j - kappa*C_ij)
+ * (-inf if empty).  Columns are split into `nsplit` equal contiguous ranges
+ * (fixed order).  C_ij = |p_i|^2 + |q_j|^2 - 2<p_i,q_j> from the squared norms
+ * (FP32 path; OTK_CLAMP / OTK_SAME_POINTS reproduce max(C,0) and the zero
+ * diagonal) or from the split planes (TC path: hi/lo/ext_a of P, hi/lo/ext_b
+ * of Q, dpad % 64 == 0, split_inv = 1/s^2 with one common scale s). */
 int otk_lse_partial(const float *p, const float *p_sq, const uint16_t *p_hi,
-                    const uint16_t *p_lo, int64_t np, const float *q,
-                    const float *q_sq, const uint16_t *q_hi, const uint16_t *q_lo,
-                    int64_t nq, int32_t d, int32_t dpad, float split_inv,
-                    const float *q_bias, float kappa, int32_t flags,
-                    int32_t nsplit, float *partial, void *stream);
+                    const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
+                    const float *q, const float *q_sq, const uint16_t *q_hi,
+                    const uint16_t *q_lo, const uint16_t *q_ext, int64_t nq,
+                    int32_t d, int32_t dpad, float split_inv, const float *q_bias,
+                    float kappa, int32_t flags, int32_t nsplit, float *partial,
+                    void *stream);
 
 /* Suggested split count for otk_lse_partial on this device. */
 int otk_lse_suggest_nsplit(int64_t np, int64_t nq, int32_t d, int32_t flags);
 
 /* Combine partials (fixed split order) and produce the potential:
- *   SOLVER: out_i = eps*base_i + p_sq_i - eps*ln2*L_i      (base = log w)
- *   APPLY:  out_i = base_i - p_sq_i + eps*ln2*L_i          (base = f)
- * p_sq may be NULL (0).  If out_bias != NULL also writes the bias of this
- * side for the next half-step: (out_i - p_sq_i)*kappa_next.  NaN/+inf in
- * out -> atomicMin(first_bad, step) (first_bad may be NULL). */
+ *   SOLVER: out_i = eps*base_i - eps*ln2*L_i    (base = log w; sinkhorn.py:173-174)
+ *   APPLY:  out_i = base_i + eps*ln2*L_i        (base = f; apply_lse_kernel)
+ * If out_bias != NULL also writes kappa_next*out_i (this side's bias for the
+ * next half-step).  NaN/+inf in out -> atomicMin(first_bad, step) (first_bad
+ * may be NULL). */
 int otk_lse_finalize(const float *partial, int32_t nsplit, int64_t np,
-                     const float *p_sq, const float *base, int32_t mode,
-                     float eps, float kappa_next, float *out_pot,
-                     float *out_bias, int32_t *first_bad, int32_t step,
-                     void *stream);
+                     const float *base, int32_t mode, float eps, float kappa_next,
+                     float *out_pot, float *out_bias, int32_t *first_bad,
+                     int32_t step, void *stream);
 
 /* K5 -- fused convergence check (sinkhorn.py:175-189 + _dual_objective 115-119).
  * From f_prev = f_t, f_next = f_{t+1} (the next rows half-step) and g = g_t:

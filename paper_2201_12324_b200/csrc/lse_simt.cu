@@ -6,10 +6,10 @@
 //   C_ij = |p_i|^2 + |q_j|^2 - 2 <p_i, q_j>       (rank d+2)
 // and never materialised.  In log2 units with kappa = log2(e)/eps:
 //   (pot_j - C_ij) * kappa = u_ij - kappa*|p_i|^2,
-//   u_ij = 2*kappa*<p_i,q_j> + bias_j,  bias_j = kappa*(pot_j - |q_j|^2)
-// The row term is added back by the finalize kernel.  OTK_CLAMP applies
-// max(C,0) exactly (u <= kappa*(pot_j + |p_i|^2)); OTK_SAME_POINTS forces the
-// zero diagonal (geometry.py:278-292).
+//   u_ij = 2*kappa*<p_i,q_j> + kappa*(pot_j - |q_j|^2)      (bias_j = kappa*pot_j)
+// The row term is subtracted once per row from the reduced value.  OTK_CLAMP
+// applies max(C,0) exactly (u <= bias_j + kappa*|p_i|^2); OTK_SAME_POINTS
+// forces the zero diagonal (geometry.py:278-292).
 //
 // CTA tile: 64 rows (P) x 64 columns (Q), 256 threads, 4x4 per thread.  Each
 // CTA streams a contiguous column range (split) of Q through shared memory
@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(SB_T) lse_simt_kernel(
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     int64_t row = row0 + ty * 4 + r;
-    cp[r] = (CLAMP && row < np) ? kappa * psq[row] : 0.f;
+    cp[r] = (row < np) ? kappa * psq[row] : 0.f;
     st[r].init();
   }
 
@@ -89,8 +89,8 @@ __global__ void __launch_bounds__(SB_T) lse_simt_kernel(
     for (int c = 0; c < 4; ++c) {
       int64_t j = col0 + tx * 4 + c;
       ok[c] = j < c_end;
-      hb[c] = ok[c] ? qbias[j] : 0.f;
-      cq[c] = (CLAMP && ok[c]) ? fmaf(kappa, qsq[j], hb[c]) : 0.f;
+      cq[c] = ok[c] ? qbias[j] : 0.f;
+      hb[c] = ok[c] ? fmaf(-kappa, qsq[j], cq[c]) : 0.f;
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(SB_T) lse_simt_kernel(
       st[r].merge(m2, s2);
     }
     int64_t row = row0 + ty * 4 + r;
-    if (tx == 0 && row < np) partial[(int64_t)split * np + row] = st[r].value();
+    if (tx == 0 && row < np) partial[(int64_t)split * np + row] = st[r].value() - cp[r];
   }
 }
 

@@ -3,48 +3,75 @@
 // streaming log2-sum-exp2 epilogue read straight out of TMEM.
 //
 // Replaces PointCloudGeometry.apply_lse_kernel (reference geometry.py:336-354)
-// for d >= 32.  Same math as the FP32 kernel (csrc/lse_simt.cu):
-//     u_ij = 2*kappa*<p_i, q_j> + bias_j,   partial_i = log2 sum_j 2^u_ij
-// but the dot products run on the tensor cores in split-fp16 ("3xFP16"):
-// every fp32 coordinate is pre-split (K0, otk_prep_points) into
-// hi = fp16(s*x), lo = fp16(s*x - hi) with a power-of-two scale s, and
-//     s_p s_q <p,q> ~= hi_p.hi_q + hi_p.lo_q + lo_p.hi_q
-// (error ~2^-22 |p||q|: float32 quality, SURVEY.md §7 "hard parts").
+// for d >= 32.  Contract (include/otk.h, otk_lse_partial):
+//     partial_i = log2 sum_j 2^(kappa*g_j - kappa*C_ij),  C_ij = |p_i|^2+|q_j|^2-2<p_i,q_j>
+// The dot products run on the tensor cores in split-fp16 ("3xFP16"): every
+// fp32 coordinate is pre-split (K0, otk_prep_points) into hi = fp16(s*x),
+// lo = fp16(s*x - hi) with one power-of-two scale s for both point sets, and
+//     s^2 <p,q> ~= hi_p.hi_q + hi_p.lo_q + lo_p.hi_q          (error ~2^-22)
+// One more MMA per tile, issued last, adds -s^2(|p_i|^2 + |q_j|^2)/2 from the
+// 16-column "norm planes" (three fp16 pieces per point times 2^15), so the
+// accumulators end at -s^2 C_ij / 2 and the epilogue gets
+//     u_ij = (2 kappa / s^2) * acc + kappa g_j = kappa (g_j - C_ij)
+// from a single FFMA.
+//
+// Accuracy (measured, tools/diag_tc_bias.py): every tcgen05.mma rounds its
+// fp32 accumulator toward zero (~0.3-0.5 ulp of the running sum), so a long
+// chain of dot-product MMAs drifts low.  The chain is therefore split across
+// several TMEM accumulators and summed in fp32 by the epilogue:
+//   V1 (d <= 64):    1 accumulator, 2 tile buffers, 256-column tiles
+//   V2 (d <= 256):   hi*hi | cross terms, 2 tile buffers, 128-column tiles
+//   V4 (d  > 256):   hi*hi split over 3 accumulators (K-blocks round-robin) |
+//                    cross terms, 1 tile buffer, 128-column tiles
+// (TMEM holds 512 fp32 columns per SM: NACC * NBUF * BN = 512.)
 //
 // CTA = one SM, persistent over work units (row tile of 128 P rows) x
 // (contiguous column split of Q).  Warp roles (384 threads):
-//   warp 0      TMA producer: A (P hi/lo, resident per unit) + B stages
-//               (Q hi/lo K-blocks of 256 rows x 64 fp16, 128B swizzle)
+//   warp 0      TMA producer: A (P hi/lo + norm plane, resident per unit when it
+//               fits), B stages (Q hi/lo K-blocks, BN rows x 64 fp16, 128B
+//               swizzle) and per-tile extras (kappa*g_j vector via 1-D TMA,
+//               Q norm plane, 32B swizzle)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//               (M=128, N=256, K=16, fp32 accumulate, 2 TMEM accumulators)
-//   warps 4-11  two epilogue warpgroups, one per TMEM accumulator: each
-//               thread owns one row (TMEM lane), pulls 32 columns per
-//               tcgen05.ld, and keeps an online (max, sum) in registers;
-//               the two groups merge per unit in a fixed order.
-// Pipelines: smem full/empty mbarriers (TMA <-> MMA), tfull/tempty
-// (MMA <-> epilogue), afull/aempty (A operand reuse).  Deterministic: no
-// atomics, fixed reduction order.
+//               (M=128, N=BN, K=16, fp32 accumulate)
+//   warps 4-11  two epilogue warpgroups: each thread owns one row (TMEM lane),
+//               streams its columns with software-pipelined tcgen05.ld and
+//               keeps an online (max, sum); with 2 tile buffers the groups
+//               alternate tiles, with 1 buffer they split its columns.  The
+//               groups merge per unit in a fixed order (deterministic).
 #include <cuda.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <mutex>
-#include <unordered_map>
 
 #include "otk_common.cuh"
 
 namespace otk {
 namespace tc {
 
-constexpr int BM = 128;                   // P rows per tile (MMA M, TMEM lanes)
-constexpr int BN = 256;                   // Q rows per tile (MMA N, TMEM columns)
-constexpr int BK = 64;                    // fp16 K-block = one 128-byte swizzle row
-constexpr int A_TILE = BM * BK * 2;       // 16 KB
-constexpr int B_TILE = BN * BK * 2;       // 32 KB
+constexpr int BM = 128;                 // P rows per tile (MMA M, TMEM lanes)
+constexpr int BK = 64;                  // fp16 K-block = one 128-byte swizzle row
+constexpr int A_TILE = BM * BK * 2;     // 16 KB
+constexpr int EXT_K = 16;               // norm-plane columns (one MMA K step)
+constexpr int A_EXT = BM * EXT_K * 2;   // 4 KB
 constexpr int THREADS = 384;
 constexpr int EPI_WARP0 = 4;
-constexpr int NUM_EPI = 256;
-// kind::f16 instruction descriptor: D=f32 (bit 4), A=B=f16, K-major, N>>3 @17, M>>4 @24
-constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+constexpr int NSLOT = 2;                // per-tile extras ring (bias vector + Q norm plane [+ A norm plane])
+
+template <int V>
+struct Cfg {
+  static constexpr int NACC = V;                    // accumulators per tile (1, 2 or 4)
+  static constexpr int NBUF = (V == 4) ? 1 : 2;     // tile buffers in TMEM
+  static constexpr int BN = 512 / (NACC * NBUF);    // Q rows per tile: 256, 128, 128
+  static constexpr int B_TILE = BN * BK * 2;
+  static constexpr int B_EXT = BN * EXT_K * 2;
+  static constexpr int CH = 32 / NACC;              // columns per epilogue chunk
+  static constexpr int NCH = BN / CH;               // chunks per tile
+  static constexpr int NCH_G = NCH / (3 - NBUF);    // chunks per epilogue group per tile
+  static constexpr int EPI_ARRIVE = 128 * (3 - NBUF);
+  // kind::f16 instruction descriptor: D=f32 (bit 4), A=B=f16, K-major, N>>3 @17, M>>4 @24
+  static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+};
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -78,6 +105,13 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_1d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0)
+      : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -87,6 +121,7 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
+template <uint32_t IDESC>
 __device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                          uint32_t accumulate) {
   asm volatile(
@@ -101,7 +136,7 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar) {
           smem_u32(bar))
       : "memory");
 }
-// K-major operand, 128-byte swizzle, rows of 128 B, 8-row atoms 1024 B apart.
+// K-major operand, 128-byte swizzle: rows of 128 B, 8-row atoms 1024 B apart.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
   d |= (uint64_t)1 << 16;              // leading byte offset (unused for swizzled K-major)
@@ -110,7 +145,18 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= (uint64_t)2 << 61;              // SWIZZLE_128B
   return d;
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+// K-major 16-column norm plane, 32-byte swizzle: rows of 32 B, 8-row atoms 256 B apart.
+__device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;              // SWIZZLE_32B
+  return d;
+}
+
+// tcgen05.ld of 32 lanes x N consecutive 32-bit columns (async until tmem_wait).
+__device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, uint32_t *v) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
       "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -121,46 +167,109 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t *v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_x8(uint32_t taddr, uint32_t *v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "r"(taddr));
+}
+// Wait for outstanding tcgen05.ld; the 32 registers are tied in/out so the
+// compiler cannot move their uses above the wait.
+__device__ __forceinline__ void tmem_wait(uint32_t *v) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                 "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]), "+r"(v[17]),
+                 "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+                 "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]),
+                 "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
 }
 
 struct Params {
   int64_t np, nq;
   int kb;                 // K-blocks (dpad / 64)
   int row_tiles, ntiles, tps, nsplit, num_units;
-  int order;              // MMA product order (accuracy experiments)
-  const float *qbias;
-  float c2k;              // 2*kappa/(s_p*s_q)
+  float c2k;              // 2*kappa/s^2
   float *partial;         // [nsplit][np]
 };
 
-template <bool A_RES, int NS, int ABUF>
-struct Layout {
-  static constexpr int STAGE = 2 * B_TILE + (A_RES ? 0 : 2 * A_TILE);
-  __host__ __device__ static constexpr int a_bytes(int kb) { return A_RES ? ABUF * kb * 2 * A_TILE : 0; }
+template <int V, bool A_RES, int NS, int ABUF>
+struct Plan {
+  using C = Cfg<V>;
+  static constexpr int A_KB = 2 * A_TILE;                          // one K-block of A: hi, lo
+  static constexpr int STAGE = 2 * C::B_TILE + (A_RES ? 0 : A_KB);
+  static constexpr int BIAS_BYTES = ((C::BN * 4 + 1023) / 1024) * 1024;
+  static constexpr int SLOT = BIAS_BYTES + C::B_EXT + (A_RES ? 0 : A_EXT);
+  __host__ __device__ static constexpr int a_bytes(int kb) { return A_RES ? ABUF * (kb * A_KB + A_EXT) : 0; }
   __host__ __device__ static constexpr int smem_bytes(int kb) {
-    return 1024 /*align slack*/ + a_bytes(kb) + NS * STAGE + 1024 /*barriers etc.*/ +
+    return 1024 /*align slack*/ + a_bytes(kb) + NS * STAGE + NSLOT * SLOT + 256 /*barriers*/ +
            2 * 2 * BM * (int)sizeof(float);
   }
 };
 
-template <bool A_RES, int NS, int ABUF>
+// Online update of one row state with CH columns (accumulators already summed).
+template <int CH, bool MASK>
+__device__ __forceinline__ void lse_chunk(const float *acc, const float *bias, float c2k, int valid,
+                                          float &m, float &s) {
+  float u[CH];
+  float cm = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    u[i] = fmaf(acc[i], c2k, bias[i]);
+    if (MASK && i >= valid) u[i] = -INFINITY;
+    cm = fmaxf(cm, u[i]);
+  }
+  if (cm > m + 8.f) {  // lazy rescale: terms may exceed m by at most 2^8
+    s *= ex2(m - cm);
+    m = cm;
+  }
+  const float ms = (m == -INFINITY) ? 0.f : m;
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int i = 0; i < CH; i += 2) {
+    s0 += ex2(u[i] - ms);
+    s1 += ex2(u[i + 1] - ms);
+  }
+  s += s0 + s1;
+}
+
+template <int V, bool A_RES, int NS, int ABUF>
 __global__ void __launch_bounds__(THREADS, 1)
     lse_tc_kernel(const __grid_constant__ CUtensorMap tm_phi, const __grid_constant__ CUtensorMap tm_plo,
                   const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo,
-                  const Params prm) {
-  using L = Layout<A_RES, NS, ABUF>;
+                  const __grid_constant__ CUtensorMap tm_pext, const __grid_constant__ CUtensorMap tm_qext,
+                  const __grid_constant__ CUtensorMap tm_bias, const Params prm) {
+  using C = Cfg<V>;
+  using L = Plan<V, A_RES, NS, ABUF>;
+  constexpr int BN = C::BN;
+  constexpr int NACC = C::NACC;
+  constexpr int NBUF = C::NBUF;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int kb = prm.kb;
-  uint8_t *a_region = smem;                                  // [ABUF][kb][hi,lo] 16 KB tiles
-  uint8_t *stage_region = smem + L::a_bytes(kb);             // [NS][B hi, B lo, (A hi, A lo)]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(stage_region + NS * L::STAGE);
+  uint8_t *a_region = smem;                                   // [ABUF][kb x (hi, lo)][A norm plane]
+  uint8_t *stage_region = smem + L::a_bytes(kb);              // [NS][B hi, B lo, (A hi, A lo)]
+  uint8_t *slot_region = stage_region + NS * L::STAGE;        // [NSLOT][bias, Q norm, (P norm)]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(slot_region + NSLOT * L::SLOT);
   uint64_t *full = bars, *empty = bars + NS;
   uint64_t *afull = bars + 2 * NS, *aempty = afull + 2;
   uint64_t *tfull = aempty + 2, *tempty = tfull + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-  float *comb = reinterpret_cast<float *>(bars + 128);        // [2][BM][2]
+  uint64_t *xfull = tempty + 2, *xempty = xfull + NSLOT;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(xempty + NSLOT);
+  float *comb = reinterpret_cast<float *>(bars + 32);          // [2][BM][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -173,7 +282,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&afull[b], 1);
       mbar_init(&aempty[b], 1);
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], NUM_EPI / 2);
+      mbar_init(&tempty[b], C::EPI_ARRIVE);
+    }
+    for (int b = 0; b < NSLOT; ++b) {
+      mbar_init(&xfull[b], 1);
+      mbar_init(&xempty[b], C::EPI_ARRIVE);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -182,6 +295,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     tma_prefetch_desc(&tm_plo);
     tma_prefetch_desc(&tm_qhi);
     tma_prefetch_desc(&tm_qlo);
+    tma_prefetch_desc(&tm_pext);
+    tma_prefetch_desc(&tm_qext);
+    tma_prefetch_desc(&tm_bias);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
@@ -195,32 +311,37 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   auto a_tile = [&](int buf, int k, int lo) -> uint8_t * {
-    return a_region + ((size_t)(buf * kb + k) * 2 + lo) * A_TILE;
+    return a_region + (size_t)buf * (kb * L::A_KB + A_EXT) + (size_t)k * L::A_KB + lo * A_TILE;
   };
-  auto st_b = [&](int s, int lo) -> uint8_t * { return stage_region + (size_t)s * L::STAGE + lo * B_TILE; };
+  auto a_ext = [&](int buf) -> uint8_t * { return a_region + (size_t)buf * (kb * L::A_KB + A_EXT) + kb * L::A_KB; };
+  auto st_b = [&](int s, int lo) -> uint8_t * { return stage_region + (size_t)s * L::STAGE + lo * C::B_TILE; };
   auto st_a = [&](int s, int lo) -> uint8_t * {
-    return stage_region + (size_t)s * L::STAGE + 2 * B_TILE + lo * A_TILE;
+    return stage_region + (size_t)s * L::STAGE + 2 * C::B_TILE + lo * A_TILE;
   };
+  auto slot_bias = [&](int x) -> float * { return reinterpret_cast<float *>(slot_region + (size_t)x * L::SLOT); };
+  auto slot_qext = [&](int x) -> uint8_t * { return slot_region + (size_t)x * L::SLOT + L::BIAS_BYTES; };
+  auto slot_pext = [&](int x) -> uint8_t * { return slot_region + (size_t)x * L::SLOT + L::BIAS_BYTES + C::B_EXT; };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int stage = 0;
       uint32_t sphase = 0;
-      int uc = 0;
+      int uc = 0, tcount = 0;
       for (int u = blockIdx.x; u < prm.num_units; u += gridDim.x, ++uc) {
         const int split = u / prm.row_tiles, rt = u % prm.row_tiles;
         const int t0 = split * prm.tps, t1 = min(prm.ntiles, t0 + prm.tps);
         if (A_RES) {
           const int ab = uc % ABUF;
           mbar_wait(&aempty[ab], ((uc / ABUF) & 1) ^ 1);
-          mbar_expect_tx(&afull[ab], (uint32_t)(kb * 2 * A_TILE));
+          mbar_expect_tx(&afull[ab], (uint32_t)(kb * L::A_KB + A_EXT));
           for (int k = 0; k < kb; ++k) {
             tma_load_2d(a_tile(ab, k, 0), &tm_phi, &afull[ab], k * BK, rt * BM);
             tma_load_2d(a_tile(ab, k, 1), &tm_plo, &afull[ab], k * BK, rt * BM);
           }
+          tma_load_2d(a_ext(ab), &tm_pext, &afull[ab], 0, rt * BM);
         }
-        for (int t = t0; t < t1; ++t) {
+        for (int t = t0; t < t1; ++t, ++tcount) {
           for (int k = 0; k < kb; ++k) {
             mbar_wait(&empty[stage], sphase ^ 1);
             mbar_expect_tx(&full[stage], (uint32_t)L::STAGE);
@@ -235,6 +356,13 @@ __global__ void __launch_bounds__(THREADS, 1)
               sphase ^= 1;
             }
           }
+          // per-tile extras: kappa*g_j for the epilogue, norm planes for the last MMA
+          const int x = tcount % NSLOT;
+          mbar_wait(&xempty[x], ((tcount / NSLOT) & 1) ^ 1);
+          mbar_expect_tx(&xfull[x], (uint32_t)(BN * 4 + C::B_EXT + (A_RES ? 0 : A_EXT)));
+          tma_load_1d(slot_bias(x), &tm_bias, &xfull[x], t * BN);
+          tma_load_2d(slot_qext(x), &tm_qext, &xfull[x], 0, t * BN);
+          if (!A_RES) tma_load_2d(slot_pext(x), &tm_pext, &xfull[x], 0, rt * BM);
         }
       }
     }
@@ -253,10 +381,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc_fence_after();
         }
         for (int t = t0; t < t1; ++t, ++tcount) {
-          const int acc = tcount & 1;
-          mbar_wait(&tempty[acc], ((tcount >> 1) & 1) ^ 1);
+          const int buf = tcount % NBUF;
+          mbar_wait(&tempty[buf], ((tcount / NBUF) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+          const uint32_t d0 = tmem_base + (uint32_t)(buf * NACC * BN);
+          const uint32_t d_cross = d0 + (uint32_t)((NACC - 1) * BN);
           for (int k = 0; k < kb; ++k) {
             mbar_wait(&full[stage], sphase);
             tc_fence_after();
@@ -264,39 +393,24 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t al = smem_u32(A_RES ? a_tile(ab, k, 1) : st_a(stage, 1));
             const uint32_t bh = smem_u32(st_b(stage, 0));
             const uint32_t bl = smem_u32(st_b(stage, 1));
-            if (prm.order == 0) {
+            // hi*hi accumulator of this K-block (V4: three slices round-robin)
+            const int slice = (NACC == 4) ? (k % 3) : 0;
+            const uint32_t d_main = d0 + (uint32_t)(slice * BN);
+            const bool main_first = (NACC == 4) ? (k < 3) : (k == 0);
 #pragma unroll
-              for (int kk = 0; kk < BK / 16; ++kk) {
-                const uint32_t off = kk * 32;  // 16 fp16 = 32 B along the swizzled row
-                const uint64_t dah = sw128_desc(ah + off), dal = sw128_desc(al + off);
-                const uint64_t dbh = sw128_desc(bh + off), dbl = sw128_desc(bl + off);
-                umma_f16(d_tmem, dah, dbh, (k | kk) != 0 ? 1u : 0u);
-                umma_f16(d_tmem, dah, dbl, 1u);
-                umma_f16(d_tmem, dal, dbh, 1u);
-              }
-            } else if (prm.order == 1) {  // small cross terms first, then hi*hi
-#pragma unroll
-              for (int kk = 0; kk < BK / 16; ++kk) {
-                const uint32_t off = kk * 32;
-                umma_f16(d_tmem, sw128_desc(ah + off), sw128_desc(bl + off), (k | kk) != 0 ? 1u : 0u);
-                umma_f16(d_tmem, sw128_desc(al + off), sw128_desc(bh + off), 1u);
-              }
-#pragma unroll
-              for (int kk = 0; kk < BK / 16; ++kk) {
-                const uint32_t off = kk * 32;
-                umma_f16(d_tmem, sw128_desc(ah + off), sw128_desc(bh + off), 1u);
-              }
-            } else {  // hi*hi first, then cross terms
-#pragma unroll
-              for (int kk = 0; kk < BK / 16; ++kk) {
-                const uint32_t off = kk * 32;
-                umma_f16(d_tmem, sw128_desc(ah + off), sw128_desc(bh + off), (k | kk) != 0 ? 1u : 0u);
-              }
-#pragma unroll
-              for (int kk = 0; kk < BK / 16; ++kk) {
-                const uint32_t off = kk * 32;
-                umma_f16(d_tmem, sw128_desc(ah + off), sw128_desc(bl + off), 1u);
-                umma_f16(d_tmem, sw128_desc(al + off), sw128_desc(bh + off), 1u);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t off = kk * 32;  // 16 fp16 = 32 B along the swizzled row
+              const uint64_t dah = sw128_desc(ah + off), dal = sw128_desc(al + off);
+              const uint64_t dbh = sw128_desc(bh + off), dbl = sw128_desc(bl + off);
+              const uint32_t acc_main = (main_first && kk == 0) ? 0u : 1u;
+              const uint32_t acc_cross = (k == 0 && kk == 0) ? 0u : 1u;
+              umma_f16<C::IDESC>(d_main, dah, dbh, acc_main);
+              if (NACC == 1) {
+                umma_f16<C::IDESC>(d_main, dah, dbl, 1u);
+                umma_f16<C::IDESC>(d_main, dal, dbh, 1u);
+              } else {
+                umma_f16<C::IDESC>(d_cross, dah, dbl, acc_cross);
+                umma_f16<C::IDESC>(d_cross, dal, dbh, 1u);
               }
             }
             umma_commit(&empty[stage]);  // smem stage free once these MMAs retire
@@ -305,14 +419,20 @@ __global__ void __launch_bounds__(THREADS, 1)
               sphase ^= 1;
             }
           }
-          umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+          // last MMA of the tile: -s^2(|p|^2 + |q|^2)/2 into the (small) cross accumulator
+          const int x = tcount % NSLOT;
+          mbar_wait(&xfull[x], (tcount / NSLOT) & 1);
+          tc_fence_after();
+          umma_f16<C::IDESC>(d_cross, sw32_desc(smem_u32(A_RES ? a_ext(ab) : slot_pext(x))),
+                             sw32_desc(smem_u32(slot_qext(x))), 1u);
+          umma_commit(&tfull[buf]);  // accumulators ready for the epilogue
         }
         if (A_RES) umma_commit(&aempty[ab]);
       }
     }
   } else if (warp >= EPI_WARP0) {
     // ------------------------------------------------------------ epilogue
-    const int eg = (warp - EPI_WARP0) >> 2;  // accumulator / warpgroup
+    const int eg = (warp - EPI_WARP0) >> 2;  // warpgroup 0 / 1
     const int quarter = warp & 3;             // TMEM lane quarter of this warp
     const int row_local = quarter * 32 + lane;
     const uint32_t t_lane = (uint32_t)(quarter * 32) << 16;
@@ -323,67 +443,83 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int t0 = split * prm.tps, t1 = min(prm.ntiles, t0 + prm.tps);
       float m = -INFINITY, s = 0.f;
       for (int t = t0; t < t1; ++t, ++tcount) {
-        if ((tcount & 1) != eg) continue;
-        mbar_wait(&tfull[eg], (tcount >> 1) & 1);
+        if (NBUF == 2 && (tcount & 1) != eg) continue;
+        const int buf = tcount % NBUF;
+        const int x = tcount % NSLOT;
+        mbar_wait(&tfull[buf], (tcount / NBUF) & 1);
+        mbar_wait(&xfull[x], (tcount / NSLOT) & 1);
         tc_fence_after();
         const int64_t j0 = (int64_t)t * BN;
         const int valid = (int)(prm.nq - j0 < BN ? prm.nq - j0 : (int64_t)BN);
-        const uint32_t taddr = tmem_base + (uint32_t)(eg * BN) + t_lane;
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld32(taddr + c * 32, v);
-          float b[32];
-          const int cbase = c * 32;
-          if (cbase + 32 <= valid) {
-            const float4 *bp = reinterpret_cast<const float4 *>(prm.qbias + j0 + cbase);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              float4 q = __ldg(bp + i);
-              b[4 * i] = q.x;
-              b[4 * i + 1] = q.y;
-              b[4 * i + 2] = q.z;
-              b[4 * i + 3] = q.w;
-            }
+        const uint32_t tbase = tmem_base + (uint32_t)(buf * NACC * BN) + t_lane;
+        const float *bias = slot_bias(x);
+        const int cfirst = (NBUF == 1) ? eg * C::NCH_G : 0;
+        // software pipeline: chunk c+1's tcgen05.ld is in flight while chunk c computes
+        uint32_t va[32], vb[32];
+        auto issue = [&](int c, uint32_t *v) {
+          if (NACC == 1) {
+            tmem_ld_x32(tbase + c * 32, v);
+          } else if (NACC == 2) {
+            tmem_ld_x16(tbase + c * 16, v);
+            tmem_ld_x16(tbase + BN + c * 16, v + 16);
           } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) b[i] = (cbase + i < valid) ? prm.qbias[j0 + cbase + i] : -INFINITY;
+            for (int a = 0; a < 4; ++a) tmem_ld_x8(tbase + a * BN + c * 8, v + 8 * a);
           }
-          float uu[32];
-          float cm = -INFINITY;
+        };
+        auto consume = [&](int c, uint32_t *v) {
+          float accv[C::CH];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            uu[i] = fmaf(__uint_as_float(v[i]), c2k, b[i]);
-            cm = fmaxf(cm, uu[i]);
+          for (int i = 0; i < C::CH; ++i) {
+            float a0 = __uint_as_float(v[i]);
+            if (NACC == 2) a0 += __uint_as_float(v[16 + i]);
+            if (NACC == 4)
+              a0 = (__uint_as_float(v[i]) + __uint_as_float(v[8 + i])) +
+                   (__uint_as_float(v[16 + i]) + __uint_as_float(v[24 + i]));
+            accv[i] = a0;
           }
-          if (cm > m + 8.f) {  // lazy rescale: terms may exceed m by at most 2^8
-            s *= ex2(m - cm);
-            m = cm;
-          }
-          const float ms = (m == -INFINITY) ? 0.f : m;
-          float s0 = 0.f, s1 = 0.f;
+          const float4 *bp = reinterpret_cast<const float4 *>(bias + c * C::CH);
+          float bv[C::CH];
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            s0 += ex2(uu[i] - ms);
-            s1 += ex2(uu[i + 1] - ms);
+          for (int i = 0; i < C::CH / 4; ++i) {
+            float4 q = bp[i];
+            bv[4 * i] = q.x;
+            bv[4 * i + 1] = q.y;
+            bv[4 * i + 2] = q.z;
+            bv[4 * i + 3] = q.w;
           }
-          s += s0 + s1;
+          if (valid >= BN)
+            lse_chunk<C::CH, false>(accv, bv, c2k, 0, m, s);
+          else
+            lse_chunk<C::CH, true>(accv, bv, c2k, valid - c * C::CH, m, s);
+        };
+        issue(cfirst, va);
+        tmem_wait(va);
+#pragma unroll
+        for (int c = 0; c < C::NCH_G; c += 2) {
+          issue(cfirst + c + 1, vb);
+          consume(cfirst + c, va);
+          tmem_wait(vb);
+          if (c + 2 < C::NCH_G) issue(cfirst + c + 2, va);
+          consume(cfirst + c + 1, vb);
+          if (c + 2 < C::NCH_G) tmem_wait(va);
         }
         tc_fence_before();
-        mbar_arrive(&tempty[eg]);
+        mbar_arrive(&tempty[buf]);
+        mbar_arrive(&xempty[x]);
       }
       // merge the two warpgroups' row states (fixed order: group 0 then group 1)
-      float *buf = comb + (uc & 1) * (2 * BM);
+      float *cb = comb + (uc & 1) * (2 * BM);
       if (eg == 1) {
-        buf[2 * row_local] = m;
-        buf[2 * row_local + 1] = s;
+        cb[2 * row_local] = m;
+        cb[2 * row_local + 1] = s;
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (eg == 0) {
         Lse2 st;
         st.m = m;
         st.s = s;
-        st.merge(buf[2 * row_local], buf[2 * row_local + 1]);
+        st.merge(cb[2 * row_local], cb[2 * row_local + 1]);
         const int64_t row = (int64_t)rt * BM + row_local;
         if (row < prm.np) prm.partial[(int64_t)split * prm.np + row] = st.value();
       }
@@ -417,44 +553,79 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-static int make_map(CUtensorMap *map, const void *base, int64_t rows, int dpad, int box_rows) {
+// 2-D fp16 plane [rows, cols], box = box_cols x box_rows; 128B swizzle for the 64-wide
+// K-blocks, 32B swizzle for the 16-wide norm planes.
+static int make_plane_map(CUtensorMap *map, const void *base, int64_t rows, int cols, int box_rows,
+                          int box_cols) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return OTK_ENOTSUP;
   }
-  cuuint64_t dims[2] = {(cuuint64_t)dpad, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)dpad * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  box_cols == BK ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled failed (%d) rows=%lld dpad=%d", (int)r, (long long)rows, dpad);
+    set_error("cuTensorMapEncodeTiled(plane) failed (%d) rows=%lld cols=%d", (int)r, (long long)rows, cols);
     return OTK_EINVAL;
   }
   return OTK_OK;
 }
 
-template <bool A_RES, int NS, int ABUF>
-static int launch_variant(const CUtensorMap (&maps)[4], const Params &prm, cudaStream_t st) {
-  using L = Layout<A_RES, NS, ABUF>;
+// 1-D fp32 vector [n], box = box elements (OOB reads as 0; masked by the epilogue).
+static int make_vec_map(CUtensorMap *map, const float *base, int64_t n, int box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return OTK_ENOTSUP;
+  }
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0) {
+    set_error("lse_tc: bias vector must be 16-byte aligned");
+    return OTK_EINVAL;
+  }
+  cuuint64_t dims[1] = {(cuuint64_t)n};
+  cuuint64_t unused_strides[1] = {(cuuint64_t)n * 4};  // must be non-NULL even for rank 1 (probed)
+  cuuint32_t boxd[1] = {(cuuint32_t)box};
+  cuuint32_t estr[1] = {1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<float *>(base), dims,
+                  unused_strides, boxd, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled(bias) failed (%d) n=%lld", (int)r, (long long)n);
+    return OTK_EINVAL;
+  }
+  return OTK_OK;
+}
+
+template <int V, bool A_RES, int NS, int ABUF>
+static int launch_variant(const CUtensorMap (&maps)[7], const Params &prm, cudaStream_t st) {
+  using L = Plan<V, A_RES, NS, ABUF>;
   const int smem = L::smem_bytes(prm.kb);
-  auto kern = lse_tc_kernel<A_RES, NS, ABUF>;
+  auto kern = lse_tc_kernel<V, A_RES, NS, ABUF>;
   static bool attr_set = false;
+  if (smem > 227 * 1024) {
+    set_error("lse_tc: shared memory plan too large (%d B, kb=%d)", smem, prm.kb);
+    return OTK_ENOTSUP;
+  }
   if (!attr_set) {
     OTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
-  if (smem > 227 * 1024) {
-    set_error("lse_tc: shared memory plan too large (%d B)", smem);
-    return OTK_ENOTSUP;
-  }
   const int grid = std::min(prm.num_units, num_sms());
-  kern<<<grid, THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], prm);
+  kern<<<grid, THREADS, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], prm);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? OTK_OK : cuda_status(e, "lse_tc_kernel");
+}
+
+static int variant_for(int kb) {
+  if (const char *v = getenv("OTK_TC_VARIANT")) return atoi(v);
+  return kb <= 1 ? 1 : (kb <= 4 ? 2 : 4);
 }
 
 }  // namespace tc
@@ -471,39 +642,56 @@ bool tc_available() {
   return ok == 1;
 }
 
-int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, int64_t np, const uint16_t *q_hi,
-                  const uint16_t *q_lo, int64_t nq, int dpad, float two_kappa_scaled,
-                  const float *q_bias, int nsplit, float *partial, cudaStream_t st) {
+// Tile width used by the TC kernel for this depth (drives the split planning).
+int tc_tile_cols(int dpad) { return tc::variant_for(dpad / tc::BK) == 1 ? 256 : 128; }
+
+int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
+                  const uint16_t *q_hi, const uint16_t *q_lo, const uint16_t *q_ext, int64_t nq,
+                  int dpad, float two_kappa_scaled, const float *q_bias, int nsplit,
+                  float *partial, cudaStream_t st) {
   using namespace tc;
   if (np > (int64_t)INT32_MAX || nq > (int64_t)INT32_MAX) {
     set_error("lse_tc: too many points");
     return OTK_EINVAL;
   }
-  CUtensorMap maps[4];
+  const int kb = dpad / BK;
+  const int v = variant_for(kb);
+  const int bn = (v == 1) ? 256 : 128;
+  if (v == 4 && kb < 3) {
+    set_error("lse_tc: variant 4 needs d > 128");
+    return OTK_EINVAL;
+  }
+  CUtensorMap maps[7];
   int rc;
-  if ((rc = make_map(&maps[0], p_hi, np, dpad, BM)) != OTK_OK) return rc;
-  if ((rc = make_map(&maps[1], p_lo, np, dpad, BM)) != OTK_OK) return rc;
-  if ((rc = make_map(&maps[2], q_hi, nq, dpad, BN)) != OTK_OK) return rc;
-  if ((rc = make_map(&maps[3], q_lo, nq, dpad, BN)) != OTK_OK) return rc;
+  if ((rc = make_plane_map(&maps[0], p_hi, np, dpad, BM, BK)) != OTK_OK) return rc;
+  if ((rc = make_plane_map(&maps[1], p_lo, np, dpad, BM, BK)) != OTK_OK) return rc;
+  if ((rc = make_plane_map(&maps[2], q_hi, nq, dpad, bn, BK)) != OTK_OK) return rc;
+  if ((rc = make_plane_map(&maps[3], q_lo, nq, dpad, bn, BK)) != OTK_OK) return rc;
+  if ((rc = make_plane_map(&maps[4], p_ext, np, EXT_K, BM, EXT_K)) != OTK_OK) return rc;
+  if ((rc = make_plane_map(&maps[5], q_ext, nq, EXT_K, bn, EXT_K)) != OTK_OK) return rc;
+  if ((rc = make_vec_map(&maps[6], q_bias, nq, bn)) != OTK_OK) return rc;
   Params prm;
   prm.np = np;
   prm.nq = nq;
-  prm.kb = dpad / BK;
+  prm.kb = kb;
   prm.row_tiles = (int)((np + BM - 1) / BM);
-  prm.ntiles = (int)((nq + BN - 1) / BN);
+  prm.ntiles = (int)((nq + bn - 1) / bn);
   prm.nsplit = nsplit;
   prm.tps = (prm.ntiles + nsplit - 1) / nsplit;
   prm.num_units = prm.row_tiles * nsplit;
-  prm.qbias = q_bias;
-  {
-    const char *o = getenv("OTK_TC_ORDER");
-    prm.order = o ? atoi(o) : 0;
-  }
   prm.c2k = two_kappa_scaled;
   prm.partial = partial;
-  if (prm.kb == 1) return launch_variant<true, 2, 2>(maps, prm, st);
-  if (prm.kb == 2) return launch_variant<true, 2, 1>(maps, prm, st);
-  return launch_variant<false, 2, 1>(maps, prm, st);
+  if (v == 1) {
+    if (kb == 1) return launch_variant<1, true, 2, 2>(maps, prm, st);
+    if (kb == 2) return launch_variant<1, true, 2, 1>(maps, prm, st);
+    return launch_variant<1, false, 2, 1>(maps, prm, st);
+  }
+  if (v == 2) {
+    if (kb <= 2) return launch_variant<2, true, 4, 1>(maps, prm, st);
+    if (kb <= 4) return launch_variant<2, true, 2, 1>(maps, prm, st);
+    return launch_variant<2, false, 3, 1>(maps, prm, st);
+  }
+  return launch_variant<4, false, 3, 1>(maps, prm, st);
 }
 
 }  // namespace otk

@@ -36,10 +36,12 @@ int num_sms() {
 }
 
 // ---------------------------------------------------------------- K0 prep
-// One warp per point: |p|^2 in float64, optional split-fp16 planes.
+// One warp per point: |p|^2 in float64; optional split-fp16 planes and the
+// per-K-block norm planes of the tcgen05 kernel (see include/otk.h).
 __global__ void prep_kernel(const float *__restrict__ pts, int64_t n, int d,
                             float *__restrict__ sq, __half *__restrict__ hi,
-                            __half *__restrict__ lo, int dpad, float scale) {
+                            __half *__restrict__ lo, __half *__restrict__ ext_a,
+                            __half *__restrict__ ext_b, int dpad, float scale) {
   int64_t warp = (int64_t)(blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32);
   int lane = threadIdx.x & 31;
   if (warp >= n) return;
@@ -52,15 +54,35 @@ __global__ void prep_kernel(const float *__restrict__ pts, int64_t n, int d,
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) sq[warp] = (float)acc;
-  if (hi != nullptr) {
-    __half *hrow = hi + warp * dpad;
-    __half *lrow = lo + warp * dpad;
-    for (int k = lane; k < dpad; k += 32) {
-      float v = (k < d) ? row[k] * scale : 0.f;
-      __half h = __float2half_rn(v);
-      hrow[k] = h;
-      lrow[k] = __float2half_rn(v - __half2float(h));
+  if (hi == nullptr) return;
+  __half *hrow = hi + warp * dpad;
+  __half *lrow = lo + warp * dpad;
+  for (int k = lane; k < dpad; k += 32) {
+    float v = (k < d) ? row[k] * scale : 0.f;
+    __half h = __float2half_rn(v);
+    hrow[k] = h;
+    lrow[k] = __float2half_rn(v - __half2float(h));
+  }
+  if (ext_a == nullptr) return;
+  // norm planes: -s^2 |p|^2 / 2 as three fp16 pieces times 2^15 (see include/otk.h)
+  const double w = acc * (double)scale * (double)scale * (1.0 / 65536.0);
+  const __half p0 = __double2half(w);
+  const double r1 = w - (double)__half2float(p0);
+  const __half p1 = __double2half(r1);
+  const __half p2 = __double2half(r1 - (double)__half2float(p1));
+  if (lane < 16) {
+    const __half big = __float2half_rn(32768.f);
+    const __half zero = __float2half_rn(0.f);
+    __half ea = zero, eb = zero;
+    if (lane < 3) {
+      ea = __hneg(lane == 0 ? p0 : (lane == 1 ? p1 : p2));
+      eb = big;
+    } else if (lane < 6) {
+      ea = big;
+      eb = __hneg(lane == 3 ? p0 : (lane == 4 ? p1 : p2));
     }
+    ext_a[warp * 16 + lane] = ea;
+    ext_b[warp * 16 + lane] = eb;
   }
 }
 
@@ -74,34 +96,27 @@ __global__ void absmax_kernel(const float *__restrict__ p, int64_t count, unsign
   if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));
 }
 
-__global__ void bias_kernel(const float *__restrict__ pot, const float *__restrict__ sq, int64_t m,
-                            float kappa, float *__restrict__ bias, int *__restrict__ first_bad,
-                            int step) {
+__global__ void bias_kernel(const float *__restrict__ pot, int64_t m, float kappa,
+                            float *__restrict__ bias, int *__restrict__ first_bad, int step) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= m) return;
   float v = pot[j];
   if (first_bad != nullptr && bad_potential(v)) atomicMin(first_bad, step);
-  bias[j] = (v - (sq ? sq[j] : 0.f)) * kappa;
+  bias[j] = v * kappa;
 }
 
 __global__ void finalize_kernel(const float *__restrict__ part, int nsplit, int64_t np,
-                                const float *__restrict__ psq, const float *__restrict__ base,
-                                int mode, float eps, float kappa_next, float *__restrict__ out,
+                                const float *__restrict__ base, int mode, float eps,
+                                float kappa_next, float *__restrict__ out,
                                 float *__restrict__ out_bias, int *__restrict__ first_bad,
                                 int step) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= np) return;
-  float L = combine_log2(part + i, nsplit, np);
-  float sq = psq ? psq[i] : 0.f;
-  float c = eps * kLn2;
-  float v;
-  if (mode == OTK_FIN_SOLVER) {
-    v = fmaf(eps, base[i], sq) - c * L;
-  } else {
-    v = (base[i] - sq) + c * L;
-  }
+  const float L = combine_log2(part + i, nsplit, np);
+  const float c = eps * kLn2;
+  const float v = (mode == OTK_FIN_SOLVER) ? eps * base[i] - c * L : base[i] + c * L;
   out[i] = v;
-  if (out_bias != nullptr) out_bias[i] = (v - sq) * kappa_next;
+  if (out_bias != nullptr) out_bias[i] = v * kappa_next;
   if (first_bad != nullptr && bad_potential(v)) atomicMin(first_bad, step);
 }
 
@@ -194,17 +209,30 @@ int otk_device_query(int device, int *sm_count, int *cc_major, int *cc_minor) {
 }
 
 int otk_prep_points(const float *pts, int64_t n, int32_t d, float *sqnorm, uint16_t *hi,
-                    uint16_t *lo, int32_t dpad, float split_scale, void *stream) {
+                    uint16_t *lo, uint16_t *ext_a, uint16_t *ext_b, int32_t dpad,
+                    float split_scale, void *stream) {
   OTK_CHECK_ARG(pts && sqnorm && n > 0 && d > 0, "otk_prep_points: bad arguments");
   OTK_CHECK_ARG((hi == nullptr) == (lo == nullptr), "otk_prep_points: hi/lo must both be set");
-  OTK_CHECK_ARG(hi == nullptr || dpad >= d, "otk_prep_points: dpad < d");
+  OTK_CHECK_ARG((ext_a == nullptr) == (ext_b == nullptr), "otk_prep_points: ext_a/ext_b must both be set");
+  OTK_CHECK_ARG(ext_a == nullptr || hi != nullptr, "otk_prep_points: ext planes need hi/lo");
+  OTK_CHECK_ARG(hi == nullptr || (dpad >= d && dpad % 64 == 0), "otk_prep_points: dpad must be >= d and a multiple of 64");
   const int warps = 8;
   int64_t blocks = (n + warps - 1) / warps;
   prep_kernel<<<(unsigned)blocks, warps * 32, 0, as_stream(stream)>>>(
-      pts, n, d, sqnorm, reinterpret_cast<__half *>(hi), reinterpret_cast<__half *>(lo), dpad,
-      split_scale);
+      pts, n, d, sqnorm, reinterpret_cast<__half *>(hi), reinterpret_cast<__half *>(lo),
+      reinterpret_cast<__half *>(ext_a), reinterpret_cast<__half *>(ext_b), dpad, split_scale);
   OTK_LAUNCH_CHECK();
   return OTK_OK;
+}
+
+float otk_split_scale(float amax, int32_t d) {
+  // largest power of two s with s*amax <= 2^12 and s^2 * d * amax^2 <= 2^31, which
+  // keeps hi/lo and the fp16 norm pieces (<= s^2|p|^2/2^16) in range
+  if (!(amax > 0.f) || !std::isfinite(amax) || d <= 0) return 1.f;
+  const double lim = std::min(4096.0, std::pow(2.0, 15.5) / std::sqrt((double)d)) / amax;
+  int e = (int)std::floor(std::log2(lim));
+  e = e < -60 ? -60 : (e > 60 ? 60 : e);
+  return std::ldexp(1.f, e);
 }
 
 int otk_absmax(const float *pts, int64_t count, float *out, void *stream) {
@@ -218,22 +246,22 @@ int otk_absmax(const float *pts, int64_t count, float *out, void *stream) {
   return OTK_OK;
 }
 
-int otk_make_bias(const float *pot, const float *sq, int64_t m, float kappa, float *bias,
-                  int32_t *first_bad, int32_t step, void *stream) {
+int otk_make_bias(const float *pot, int64_t m, float kappa, float *bias, int32_t *first_bad,
+                  int32_t step, void *stream) {
   OTK_CHECK_ARG(pot && bias && m > 0, "otk_make_bias: bad arguments");
-  bias_kernel<<<(unsigned)((m + 255) / 256), 256, 0, as_stream(stream)>>>(pot, sq, m, kappa, bias,
+  bias_kernel<<<(unsigned)((m + 255) / 256), 256, 0, as_stream(stream)>>>(pot, m, kappa, bias,
                                                                            first_bad, step);
   OTK_LAUNCH_CHECK();
   return OTK_OK;
 }
 
-int otk_lse_finalize(const float *partial, int32_t nsplit, int64_t np, const float *p_sq,
-                     const float *base, int32_t mode, float eps, float kappa_next, float *out_pot,
-                     float *out_bias, int32_t *first_bad, int32_t step, void *stream) {
+int otk_lse_finalize(const float *partial, int32_t nsplit, int64_t np, const float *base,
+                     int32_t mode, float eps, float kappa_next, float *out_pot, float *out_bias,
+                     int32_t *first_bad, int32_t step, void *stream) {
   OTK_CHECK_ARG(partial && base && out_pot && np > 0 && nsplit >= 1, "otk_lse_finalize: bad arguments");
   OTK_CHECK_ARG(mode == OTK_FIN_SOLVER || mode == OTK_FIN_APPLY, "otk_lse_finalize: bad mode");
   finalize_kernel<<<(unsigned)((np + 255) / 256), 256, 0, as_stream(stream)>>>(
-      partial, nsplit, np, p_sq, base, mode, eps, kappa_next, out_pot, out_bias, first_bad, step);
+      partial, nsplit, np, base, mode, eps, kappa_next, out_pot, out_bias, first_bad, step);
   OTK_LAUNCH_CHECK();
   return OTK_OK;
 }

@@ -26,10 +26,12 @@ namespace otk {
 int lse_simt_launch(const float *p, const float *p_sq, int64_t np, const float *q,
                     const float *q_sq, int64_t nq, int d, const float *q_bias, float kappa,
                     int flags, int nsplit, float *partial, cudaStream_t st);
-int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, int64_t np, const uint16_t *q_hi,
-                  const uint16_t *q_lo, int64_t nq, int dpad, float two_kappa_scaled,
-                  const float *q_bias, int nsplit, float *partial, cudaStream_t st);
+int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
+                  const uint16_t *q_hi, const uint16_t *q_lo, const uint16_t *q_ext, int64_t nq,
+                  int dpad, float two_kappa_scaled, const float *q_bias, int nsplit,
+                  float *partial, cudaStream_t st);
 bool tc_available();
+int tc_tile_cols(int dpad);
 }  // namespace otk
 
 using namespace otk;
@@ -43,9 +45,10 @@ static bool want_tc(int flags, int d) {
 extern "C" int otk_lse_suggest_nsplit(int64_t np, int64_t nq, int32_t d, int32_t flags) {
   const int sms = num_sms();
   if (want_tc(flags, d)) {
-    // TC kernel: 128-row tiles, 256-column tiles; aim for >= 8 work units per SM.
+    // TC kernel: 128-row tiles, 256- or 128-column tiles; aim for >= 8 work units per SM.
+    const int bn = tc_tile_cols((d + 63) / 64 * 64);
     int64_t row_tiles = (np + 127) / 128;
-    int64_t col_tiles = (nq + 255) / 256;
+    int64_t col_tiles = (nq + bn - 1) / bn;
     int64_t want = (8LL * sms + row_tiles - 1) / row_tiles;
     return (int)std::max<int64_t>(1, std::min<int64_t>(want, col_tiles));
   }
@@ -56,26 +59,25 @@ extern "C" int otk_lse_suggest_nsplit(int64_t np, int64_t nq, int32_t d, int32_t
 }
 
 extern "C" int otk_lse_partial(const float *p, const float *p_sq, const uint16_t *p_hi,
-                               const uint16_t *p_lo, int64_t np, const float *q, const float *q_sq,
-                               const uint16_t *q_hi, const uint16_t *q_lo, int64_t nq, int32_t d,
+                               const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
+                               const float *q, const float *q_sq, const uint16_t *q_hi,
+                               const uint16_t *q_lo, const uint16_t *q_ext, int64_t nq, int32_t d,
                                int32_t dpad, float split_inv, const float *q_bias, float kappa,
                                int32_t flags, int32_t nsplit, float *partial, void *stream) {
   OTK_CHECK_ARG(np > 0 && nq > 0 && d > 0 && nsplit >= 1 && q_bias && partial,
                 "otk_lse_partial: bad arguments");
   OTK_CHECK_ARG(nsplit <= 65535, "otk_lse_partial: nsplit too large");
   if (want_tc(flags, d)) {
-    OTK_CHECK_ARG(p_hi && p_lo && q_hi && q_lo && dpad % 64 == 0 && dpad >= d,
-                  "otk_lse_partial: TC path needs split planes with dpad %% 64 == 0");
+    OTK_CHECK_ARG(p_hi && p_lo && p_ext && q_hi && q_lo && q_ext && dpad % 64 == 0 && dpad >= d,
+                  "otk_lse_partial: TC path needs split + norm planes with dpad %% 64 == 0");
     if (!tc_available()) {
       set_error("otk_lse_partial: tcgen05 path requires an sm_100 device");
       return OTK_ENOTSUP;
     }
-    return lse_tc_launch(p_hi, p_lo, np, q_hi, q_lo, nq, dpad, 2.f * kappa * split_inv, q_bias,
-                         nsplit, partial, as_stream(stream));
+    return lse_tc_launch(p_hi, p_lo, p_ext, np, q_hi, q_lo, q_ext, nq, dpad,
+                         2.f * kappa * split_inv, q_bias, nsplit, partial, as_stream(stream));
   }
-  OTK_CHECK_ARG(p && q, "otk_lse_partial: SIMT path needs fp32 points");
-  OTK_CHECK_ARG(!(flags & (OTK_CLAMP | OTK_SAME_POINTS)) || (p_sq && q_sq),
-                "otk_lse_partial: OTK_CLAMP needs squared norms");
+  OTK_CHECK_ARG(p && q && p_sq && q_sq, "otk_lse_partial: FP32 path needs points and squared norms");
   return lse_simt_launch(p, p_sq, np, q, q_sq, nq, d, q_bias, kappa, flags, nsplit, partial,
                          as_stream(stream));
 }
@@ -97,7 +99,7 @@ struct Carver {
 
 struct Layout {
   float *fA, *fB, *g, *xsq, *ysq, *bias_x, *bias_y, *part;
-  uint16_t *xhi, *xlo, *yhi, *ylo;
+  uint16_t *xhi, *xlo, *yhi, *ylo, *xea, *xeb, *yea, *yeb;
   float *absmax;
   double *chk;
   void *chk_ws;
@@ -127,8 +129,12 @@ Layout plan(const otk_solve_args *A, void *ws) {
     L.xlo = c.take<uint16_t>((size_t)A->n * L.dpad);
     L.yhi = c.take<uint16_t>((size_t)A->m * L.dpad);
     L.ylo = c.take<uint16_t>((size_t)A->m * L.dpad);
+    L.xea = c.take<uint16_t>((size_t)A->n * 16);
+    L.xeb = c.take<uint16_t>((size_t)A->n * 16);
+    L.yea = c.take<uint16_t>((size_t)A->m * 16);
+    L.yeb = c.take<uint16_t>((size_t)A->m * 16);
   } else {
-    L.xhi = L.xlo = L.yhi = L.ylo = nullptr;
+    L.xhi = L.xlo = L.yhi = L.ylo = L.xea = L.xeb = L.yea = L.yeb = nullptr;
   }
   L.absmax = c.take<float>(2);
   L.chk = c.take<double>(8);
@@ -159,33 +165,28 @@ struct HalfStep {
   const otk_solve_args *A;
   Layout *L;
   cudaStream_t st;
-  float sinv;  // 1/(s_x*s_y) for the TC operand scaling
+  float sinv;  // 1/s^2 for the TC operand scaling (one common scale s)
   int kflags;
   int launches = 0;
 
   int rows(float kappa, float eps, float kappa_next, float *f_out, int step) {
     launches += 2;
-    OTK_TRY(otk_lse_partial(A->x, L->xsq, L->xhi, L->xlo, A->n, A->y, L->ysq, L->yhi, L->ylo, A->m,
-                            A->d, L->dpad, sinv, L->bias_y, kappa, kflags, L->nsr, L->part, st));
-    return otk_lse_finalize(L->part, L->nsr, A->n, L->xsq, A->log_a, OTK_FIN_SOLVER, eps,
-                            kappa_next, f_out, L->bias_x, L->first_bad, step, st);
+    OTK_TRY(otk_lse_partial(A->x, L->xsq, L->xhi, L->xlo, L->xea, A->n, A->y, L->ysq, L->yhi,
+                            L->ylo, L->yeb, A->m, A->d, L->dpad, sinv, L->bias_y, kappa, kflags,
+                            L->nsr, L->part, st));
+    return otk_lse_finalize(L->part, L->nsr, A->n, A->log_a, OTK_FIN_SOLVER, eps, kappa_next, f_out,
+                            L->bias_x, L->first_bad, step, st);
   }
   int cols(float kappa, float eps, float kappa_next, int step) {
     launches += 2;
-    OTK_TRY(otk_lse_partial(A->y, L->ysq, L->yhi, L->ylo, A->m, A->x, L->xsq, L->xhi, L->xlo, A->n,
-                            A->d, L->dpad, sinv, L->bias_x, kappa, kflags, L->nsc, L->part, st));
-    return otk_lse_finalize(L->part, L->nsc, A->m, L->ysq, A->log_b, OTK_FIN_SOLVER, eps,
-                            kappa_next, L->g, L->bias_y, L->first_bad, step, st);
+    OTK_TRY(otk_lse_partial(A->y, L->ysq, L->yhi, L->ylo, L->yea, A->m, A->x, L->xsq, L->xhi,
+                            L->xlo, L->xeb, A->n, A->d, L->dpad, sinv, L->bias_x, kappa, kflags,
+                            L->nsc, L->part, st));
+    return otk_lse_finalize(L->part, L->nsc, A->m, A->log_b, OTK_FIN_SOLVER, eps, kappa_next, L->g,
+                            L->bias_y, L->first_bad, step, st);
   }
 };
 
-static float pow2_scale_for(float amax) {
-  // largest power of two s with s*amax <= 2^14 (fp16 headroom for hi + lo)
-  if (!(amax > 0.f) || !std::isfinite(amax)) return 1.f;
-  int e = (int)std::floor(std::log2(16384.0 / amax));
-  e = std::max(-60, std::min(60, e));
-  return std::ldexp(1.f, e);
-}
 
 static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st);
 
@@ -227,22 +228,21 @@ static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st) {
   A->fail_iter = 0;
 
   // ---- prep (K0)
-  float sx = 1.f, sy = 1.f;
+  float s = 1.f;  // one common power-of-two operand scale for x and y
   if (L.tc) {
     float amax[2];
     OTK_TRY(otk_absmax(A->x, A->n * (int64_t)A->d, L.absmax, st));
     OTK_TRY(otk_absmax(A->y, A->m * (int64_t)A->d, L.absmax + 1, st));
     OTK_CUDA(cudaMemcpyAsync(amax, L.absmax, sizeof(amax), cudaMemcpyDeviceToHost, st));
     OTK_CUDA(cudaStreamSynchronize(st));
-    sx = pow2_scale_for(amax[0]);
-    sy = pow2_scale_for(amax[1]);
+    s = otk_split_scale(std::max(amax[0], amax[1]), A->d);
   }
-  OTK_TRY(otk_prep_points(A->x, A->n, A->d, L.xsq, L.xhi, L.xlo, L.dpad, sx, st));
-  OTK_TRY(otk_prep_points(A->y, A->m, A->d, L.ysq, L.yhi, L.ylo, L.dpad, sy, st));
+  OTK_TRY(otk_prep_points(A->x, A->n, A->d, L.xsq, L.xhi, L.xlo, L.xea, L.xeb, L.dpad, s, st));
+  OTK_TRY(otk_prep_points(A->y, A->m, A->d, L.ysq, L.yhi, L.ylo, L.yea, L.yeb, L.dpad, s, st));
   OTK_CUDA(cudaMemsetAsync(L.first_bad, 0x7f, sizeof(int), st));
   OTK_CUDA(cudaMemsetAsync(L.chk_ws, 0, otk_check_workspace_bytes(), st));
 
-  HalfStep H{A, &L, st, 1.f / (sx * sy),
+  HalfStep H{A, &L, st, 1.f / (s * s),
              (A->flags & (OTK_IMPL_SIMT | OTK_IMPL_TC)) | OTK_CLAMP |
                  (A->same_points ? OTK_SAME_POINTS : 0)};
 
@@ -252,7 +252,7 @@ static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st) {
     OTK_CUDA(cudaMemcpyAsync(L.g, A->g_init, A->m * sizeof(float), cudaMemcpyDeviceToDevice, st));
   else
     OTK_CUDA(cudaMemsetAsync(L.g, 0, A->m * sizeof(float), st));
-  OTK_TRY(otk_make_bias(L.g, L.ysq, A->m, (float)(1.4426950408889634 / e0), L.bias_y, L.first_bad, 1, st));
+  OTK_TRY(otk_make_bias(L.g, A->m, (float)(1.4426950408889634 / e0), L.bias_y, L.first_bad, 1, st));
 
   float *f = L.fA, *fn = L.fB;
   bool f_ready = false;

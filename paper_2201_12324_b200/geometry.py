@@ -138,7 +138,9 @@ def _all_finite(p) -> bool:
 
 
 class _Cloud:
-    """Device-resident point set: fp32 points, squared norms, split-fp16 planes."""
+    """Device-resident point set: fp32 points, squared norms and, for d >= 32,
+    the split-fp16 operand planes (hi, lo) and norm planes (ext_a, ext_b) of
+    the tcgen05 kernel, all scaled by the geometry's common power-of-two s."""
 
     def __init__(self, pts):
         import torch
@@ -146,19 +148,28 @@ class _Cloud:
         self.n, self.d = self.p.shape
         self.sq = torch.empty(self.n, dtype=torch.float32, device=self.p.device)
         self.dpad = (self.d + 63) // 64 * 64
-        self.hi = self.lo = None
+        self.hi = self.lo = self.ext_a = self.ext_b = None
         self.scale = 1.0
-        lib = N.lib()
-        if self.d >= 32:
-            amax = torch.empty(1, dtype=torch.float32, device=self.p.device)
-            N.check(lib.otk_absmax(N.ptr(self.p), self.n * self.d, N.ptr(amax), stream()), "absmax")
-            a = float(amax.item())
-            self.scale = 1.0 if not (a > 0 and np.isfinite(a)) else float(
-                2.0 ** np.clip(np.floor(np.log2(16384.0 / a)), -60, 60))
-            self.hi = torch.empty((self.n, self.dpad), dtype=torch.float16, device=self.p.device)
+
+    def absmax(self) -> float:
+        import torch
+        amax = torch.empty(1, dtype=torch.float32, device=self.p.device)
+        N.check(N.lib().otk_absmax(N.ptr(self.p), self.n * self.d, N.ptr(amax), stream()), "absmax")
+        return float(amax.item())
+
+    def prepare(self, scale: float, planes: bool):
+        import torch
+        self.scale = float(scale)
+        if planes:
+            dev = self.p.device
+            self.hi = torch.empty((self.n, self.dpad), dtype=torch.float16, device=dev)
             self.lo = torch.empty_like(self.hi)
-        N.check(lib.otk_prep_points(N.ptr(self.p), self.n, self.d, N.ptr(self.sq), N.ptr(self.hi),
-                                    N.ptr(self.lo), self.dpad, self.scale, stream()), "prep")
+            self.ext_a = torch.empty((self.n, 16), dtype=torch.float16, device=dev)
+            self.ext_b = torch.empty_like(self.ext_a)
+        N.check(N.lib().otk_prep_points(N.ptr(self.p), self.n, self.d, N.ptr(self.sq),
+                                        N.ptr(self.hi), N.ptr(self.lo), N.ptr(self.ext_a),
+                                        N.ptr(self.ext_b), self.dpad, self.scale, stream()), "prep")
+        return self
 
 
 class PointCloudGeometry(Geometry):
@@ -210,6 +221,14 @@ class PointCloudGeometry(Geometry):
             device()
             cx = _Cloud(self.x)
             cy = cx if self._same_points else _Cloud(self.y)
+            planes = cx.d >= 32
+            scale = 1.0
+            if planes:
+                amax = max(cx.absmax(), cy.absmax())
+                scale = float(N.lib().otk_split_scale(amax, cx.d))
+            cx.prepare(scale, planes)
+            if cy is not cx:
+                cy.prepare(scale, planes)
             self._dev = (cx, cy)
         return self._dev
 
@@ -265,19 +284,19 @@ class PointCloudGeometry(Geometry):
         lib = N.lib()
         st = stream()
         bias = torch.empty(nq, dtype=torch.float32, device=cx.p.device)
-        N.check(lib.otk_make_bias(N.ptr(qpot), N.ptr(Q.sq), nq, kappa, N.ptr(bias), None, 0, st))
+        N.check(lib.otk_make_bias(N.ptr(qpot), nq, kappa, N.ptr(bias), None, 0, st))
         flags = self._flags
         nsplit = lib.otk_lse_suggest_nsplit(npts, nq, cx.d, flags)
         part = torch.empty(nsplit * npts, dtype=torch.float32, device=cx.p.device)
-        sinv = 1.0 / (P.scale * Q.scale)
-        N.check(lib.otk_lse_partial(N.ptr(P.p), N.ptr(P.sq), N.ptr(P.hi), N.ptr(P.lo), npts,
-                                    N.ptr(Q.p), N.ptr(Q.sq), N.ptr(Q.hi), N.ptr(Q.lo), nq, cx.d,
-                                    cx.dpad, sinv, N.ptr(bias), kappa, flags, nsplit, N.ptr(part),
-                                    st), "apply_lse_kernel")
+        sinv = 1.0 / (cx.scale * cx.scale)
+        N.check(lib.otk_lse_partial(N.ptr(P.p), N.ptr(P.sq), N.ptr(P.hi), N.ptr(P.lo),
+                                    N.ptr(P.ext_a), npts, N.ptr(Q.p), N.ptr(Q.sq), N.ptr(Q.hi),
+                                    N.ptr(Q.lo), N.ptr(Q.ext_b), nq, cx.d, cx.dpad, sinv,
+                                    N.ptr(bias), kappa, flags, nsplit, N.ptr(part), st),
+                "apply_lse_kernel")
         out = torch.empty(npts, dtype=torch.float32, device=cx.p.device)
-        N.check(lib.otk_lse_finalize(N.ptr(part), nsplit, npts, N.ptr(P.sq), N.ptr(base),
-                                     N.OTK_FIN_APPLY, float(eps), 0.0, N.ptr(out), None, None, 0,
-                                     st), "finalize")
+        N.check(lib.otk_lse_finalize(N.ptr(part), nsplit, npts, N.ptr(base), N.OTK_FIN_APPLY,
+                                     float(eps), 0.0, N.ptr(out), None, None, 0, st), "finalize")
         return to_output(out, like)
 
 
@@ -331,8 +350,7 @@ class DenseGeometry(Geometry):
         else:
             qpot, base, nout, nq = f, g, m, n
         in_bias = torch.empty(nq, dtype=torch.float32, device=C.device)
-        N.check(N.lib().otk_make_bias(N.ptr(qpot), None, nq, kappa, N.ptr(in_bias), None, 0,
-                                      stream()))
+        N.check(N.lib().otk_make_bias(N.ptr(qpot), nq, kappa, N.ptr(in_bias), None, 0, stream()))
         eps_t = torch.tensor([eps], dtype=torch.float32, device=C.device)
         out = torch.empty(nout, dtype=torch.float32, device=C.device)
         N.check(N.lib().otk_dense_lse(N.ptr(C), 1, n, m, 0 if axis == "rows" else 1,

@@ -298,7 +298,7 @@ def _dense_loop(C, weights, scheds, threshold, max_iters, inner_iters, g_init=No
     kap_d = dev_f32(_LOG2E / e0)
     # initial bias of the column side: g * kappa (per problem)
     for bb in range(B):
-        N.check(lib.otk_make_bias(N.ptr(g[bb]), None, m, float(np.float32(_LOG2E / e0[bb])),
+        N.check(lib.otk_make_bias(N.ptr(g[bb]), m, float(np.float32(_LOG2E / e0[bb])),
                                   N.ptr(bias_y[bb]), N.ptr(first_bad[bb:bb + 1]), 1, st))
     f_ready = False
     cur_fac = factor(0)
