@@ -9,7 +9,8 @@ import sys
 
 
 def main(path):
-    rows = list(csv.DictReader(open(path)))
+    lines = [ln for ln in open(path) if not ln.startswith("==")]
+    rows = list(csv.DictReader(lines))
     agg = collections.OrderedDict()
     for r in rows:
         if r.get("Metric Name") != "gpu__time_duration.sum":

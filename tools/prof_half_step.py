@@ -1,0 +1,39 @@
+"""Launch the dominant kernel (one rows half-step, otk_lse_partial) of a config
+a few times -- a short command for `ncu --set full -k regex:lse_` captures.
+
+usage: python tools/prof_half_step.py [--config 2] [--reps 5] [--kernel auto|simt|tc]
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2201_12324_b200 as otk  # noqa: E402
+from paper_2201_12324_b200 import _native as N, workloads  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tc"])
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    wl = workloads.make(args.config)
+    geom = otk.PointCloudGeometry(torch.from_numpy(wl.x).cuda(), torch.from_numpy(wl.y).cuda())
+    if args.kernel == "simt":
+        geom.impl_flags = N.OTK_IMPL_SIMT
+    elif args.kernel == "tc":
+        geom.impl_flags = N.OTK_IMPL_TC
+    sec, cells, nsplit = bench.kernel_roofline(otk, geom, wl, reps=args.reps)
+    print(f"config {args.config}: {sec * 1e3:.3f} ms per half-step, {cells / sec:.3e} cells/s, "
+          f"nsplit {nsplit}")
+
+
+if __name__ == "__main__":
+    main()
