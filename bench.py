@@ -1,20 +1,22 @@
 """Benchmark: Sinkhorn cell-updates/s (n*m*iters/s) and time-to-tolerance.
 
 Default workload = BASELINE.json configs[1] (cfg2: n = m = 65536, d = 64,
-fp32, eps = 0.05 x subsample mean, tolerance 1e-3, checks every 10).
-One STEP = one complete ``solve_sinkhorn`` to tolerance on inputs already
-resident in HBM (so ms_per_step is the time-to-tolerance and
-value = n*m*iterations / step time).  Between timed steps L2 is flushed by
-writing a 512 MiB buffer (inputs are ~64 MiB, below the 126 MB L2).
+fp32, eps = 0.05 x subsample mean, tolerance 1e-3, checks every 10).  One
+STEP = one complete solve to tolerance on inputs already resident in HBM, so
+ms_per_step is the time-to-tolerance and value = n*m*iterations / step time.
+L2 is flushed (512 MiB write) before every timed step.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config k]
 
-Multi-GPU (torchrun, one rank per GPU): each rank runs an independent
-replica of the workload (replicas; the row-sharded NCCL solver is reported
-separately) -- value is the sum over ranks of n*m*iters / max-over-ranks time.
+N > 1 (torchrun, one rank per GPU, NCCL): the row-sharded solver
+(paper_2201_12324_b200/sharded.py) on the SAME problem --
+x split in N row shards, one NCCL all-gather of m floats per g half-step --
+so the scaling is strong; value = n*m*iters / max-over-ranks step time.
+--config 3 runs the batched materialised path (512 problems of 512^2).
 
-``--impl reference`` times the CPU oracle (the numpy restatement of the
-reference, oracle/) on a bounded sample of the same workload on rank 0.
+``--impl reference`` times the reference's CPU algorithm (the float64 numpy
+restatement under oracle/; the reference itself is pure Python/numpy) on a
+bounded sample of the same workload on rank 0's host cores.
 """
 
 from __future__ import annotations
@@ -34,6 +36,9 @@ sys.path.insert(0, ROOT)
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+METRIC = "sinkhorn_cell_updates_per_s"
+UNIT = "cell-updates/s"
+DATA = "synthetic (seeded numpy draws with the BASELINE.json shapes/distributions, workloads.py)"
 
 
 def parse():
@@ -52,21 +57,31 @@ def parse():
 def peaks():
     try:
         with open(PEAKS_FILE) as fh:
-            return json.load(fh), "measured"
+            return json.load(fh), "measured (MEASURED_PEAKS.json)"
     except OSError:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback (B200_PROFILING.md)"
+
+
+def traffic_for(name):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+    try:
+        with open(TRAFFIC_FILE) as fh:
+            v = json.load(fh).get(name)
+        return float(v) if v is not None else None
+    except (OSError, ValueError):
+        return None
 
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """Samples SM clock and throttle reasons (NVML) while the timed region runs."""
 
-    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
-               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
-               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
-               0x100: "display_clock_setting"}
+    REASONS = {0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, index=0, period=0.05):
+    def __init__(self, index=0, period=0.02):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self.period = period
         self._stop = threading.Event()
@@ -85,7 +100,7 @@ class ClockSampler:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
                 mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
-                    if mask & bit and name != "gpu_idle":
+                    if mask & bit:
                         self.reasons.add(name)
             except Exception:  # noqa: BLE001
                 pass
@@ -109,270 +124,449 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-# ------------------------------------------------------------------ reference arm
-def cpu_sample_rate(wl, budget_s=12.0, rows=None):
-    """Time the oracle (reference restatement) on a bounded sample of one full
-    iteration: a rows half-step on `rows` rows and a cols half-step on `rows`
-    columns, each reducing over the FULL other axis.  Returns cell-updates/s."""
+# ------------------------------------------------------------------ CPU reference arm
+def cpu_sample_rate(wl, budget_s=10.0):
+    """The oracle (float64 numpy restatement of the reference) on a bounded sample of
+    the workload, repeated until ~budget_s of CPU work: online configs run a rows
+    half-step on R rows and a cols half-step on R columns, each reducing over the
+    FULL other axis (= R*(n+m)/2 cell-updates); the batched config runs full
+    iterations of a few of its problems.  Returns (cell-updates/s, seconds, desc)."""
     import oracle
+    t0 = time.perf_counter()
+    cells, reps = 0.0, 0
+    if wl.materialised:
+        B = wl.x.shape[0]
+        k = min(B, 4)
+        probs = []
+        for p in range(k):
+            geom = oracle.PointCloudOracle(wl.x[p].astype(np.float64), wl.y[p].astype(np.float64))
+            probs.append((oracle.DenseOracle(geom.cost_matrix()), geom.shape, float(wl.eps[p])))
+        t0 = time.perf_counter()
+        while reps == 0 or time.perf_counter() - t0 < budget_s:
+            for dense, (n, m), e in probs:
+                g = np.zeros(m)
+                f = -dense.apply_lse_kernel(np.zeros(n), g, e, "rows")
+                g = -dense.apply_lse_kernel(f, np.zeros(m), e, "cols")
+                cells += n * m
+            reps += 1
+        dt = time.perf_counter() - t0
+        return cells / dt, dt, (f"{reps} x one full iteration of {k} of {B} problems "
+                                "(DenseGeometry, float64 numpy)")
     n, m = wl.shape
     geom = oracle.PointCloudOracle(wl.x.astype(np.float64), wl.y.astype(np.float64))
-    rows = rows or max(256, min(n, m, int(1.5e7 // max(n, m))))
-    rows = min(rows, n, m)
-    g = np.zeros(m)
-    f = np.zeros(n)
+    rows = min(n, m, max(256, int(1e8 // max(n, m))))
     t0 = time.perf_counter()
-    geom.rows_lse_subset(np.arange(rows), g, wl.eps)
-    geom.cols_lse_subset(np.arange(rows), f, wl.eps)
+    while reps == 0 or time.perf_counter() - t0 < budget_s:
+        geom.rows_lse_subset(np.arange(rows), np.zeros(m), wl.eps)
+        geom.cols_lse_subset(np.arange(rows), np.zeros(n), wl.eps)
+        cells += rows * (n + m) / 2.0
+        reps += 1
     dt = time.perf_counter() - t0
-    cells = rows * m + rows * n          # cells touched by the two partial half-steps
-    return (cells / 2.0) / dt, dt, f"rows half-step on {rows} rows x {m} cols + cols half-step on {rows} cols x {n} rows (float64 numpy, oracle/)"
+    return cells / dt, dt, (f"{reps} x (rows half-step on {rows} rows x {m} cols + cols "
+                            f"half-step on {rows} cols x {n} rows), float64 numpy (oracle/)")
+
+
+def cpu_cores():
+    return len(os.sched_getaffinity(0))
 
 
 def run_reference(args, wl, rank):
     if rank != 0:
         return
-    cores = len(os.sched_getaffinity(0))
-    vals = []
-    desc = ""
     for _ in range(args.warmup):
-        cpu_sample_rate(wl)
-    t_total = 0.0
+        cpu_sample_rate(wl, budget_s=2.0)
+    vals, t_total, desc = [], 0.0, ""
     for _ in range(args.steps):
-        v, dt, desc = cpu_sample_rate(wl)
+        v, dt, desc = cpu_sample_rate(wl, budget_s=15.0)
         vals.append(v)
         t_total += dt
     value = float(np.mean(vals))
     line = {
-        "impl": "reference", "metric": "sinkhorn_cell_updates_per_s", "value": value,
-        "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy, workloads.py)",
-        "config": {"workload": wl.name, "n": wl.shape[0], "m": wl.shape[1], "d": wl.d,
-                   "eps": wl.eps, "parallelism": "cpu"},
-        "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cores, "kind": "port",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": workload_config(wl, "cpu (oracle port of the reference, rank 0)"),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
                          "sample": desc},
-        "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-# ------------------------------------------------------------------ our arm
-def kernel_roofline(otk, geom, wl, reps=20):
-    """Average duration of the dominant kernel (the rows half-step, otk_lse_partial)
-    measured with CUDA events on its stream; algorithmic flops per launch =
-    (2d+8) per cell."""
+def workload_config(wl, parallelism):
+    n, m = wl.shape
+    cfg = {"workload": wl.name, "n": n, "m": m, "d": wl.d, "threshold": wl.threshold,
+           "max_iters": wl.max_iters, "parallelism": parallelism,
+           "l2": "flushed (512 MiB write) before every timed step"}
+    if wl.materialised:
+        cfg["batch"] = int(wl.x.shape[0])
+        cfg["eps"] = "per problem: 0.05 x exact mean cost"
+    else:
+        cfg["eps"] = wl.eps
+    return cfg
+
+
+# ------------------------------------------------------------------ device timing helpers
+def event_time(fn, reps, stream_ptr=None):
+    """Mean seconds of fn() over reps, CUDA events on torch's current stream
+    (the stream every library call in fn is launched on)."""
+    import torch
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3 / reps
+
+
+def pipes():
+    import ctypes
+    from paper_2201_12324_b200 import _native as N
+    from paper_2201_12324_b200._device import stream
+    ex2, ffma = ctypes.c_double(), ctypes.c_double()
+    N.check(N.lib().otk_bench_pipes(ctypes.byref(ex2), ctypes.byref(ffma), stream()))
+    return ex2.value, ffma.value
+
+
+def online_roofline(geom, wl, reps=10):
+    """Dominant kernel of the online path: one rows half-step (otk_lse_partial),
+    timed with CUDA events on its stream.  Algorithmic work per cell (SURVEY.md
+    §8d): 2d dot-product flops + 8 epilogue flops + 1 exp."""
     import torch
     from paper_2201_12324_b200 import _native as N
     from paper_2201_12324_b200._device import stream
     cx, cy = geom._clouds()
-    n, m = wl.shape
+    n, m = geom.shape
     lib = N.lib()
     kappa = float(np.float32(1.4426950408889634 / wl.eps))
     bias = torch.zeros(m, dtype=torch.float32, device=cx.p.device)
     flags = geom._flags
     nsplit = lib.otk_lse_suggest_nsplit(n, m, cx.d, flags)
     part = torch.empty(nsplit * n, dtype=torch.float32, device=cx.p.device)
-    st = stream()
     sinv = 1.0 / (cx.scale * cx.scale)
+    tc = cx.hi is not None and not (flags & N.OTK_IMPL_SIMT)
 
     def launch():
         N.check(lib.otk_lse_partial(N.ptr(cx.p), N.ptr(cx.sq), N.ptr(cx.hi), N.ptr(cx.lo),
                                     N.ptr(cx.ext_a), n, N.ptr(cy.p), N.ptr(cy.sq), N.ptr(cy.hi),
                                     N.ptr(cy.lo), N.ptr(cy.ext_b), m, cx.d, cx.dpad, sinv,
-                                    N.ptr(bias), kappa, flags, nsplit, N.ptr(part), st))
+                                    N.ptr(bias), kappa, flags, nsplit, N.ptr(part), stream()))
     for _ in range(3):
         launch()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(reps):
-        launch()
-    e1.record()
-    torch.cuda.synchronize()
-    sec = e0.elapsed_time(e1) * 1e-3 / reps
+    sec = event_time(launch, reps)
     cells = float(n) * m
-    return sec, cells, nsplit
+    pk, pk_kind = peaks()
+    ex2, ffma = pipes()
+    cps = cells / sec
+    d = wl.d
+    if tc:
+        peak = float(pk.get("bf16_tflops", 1590.0)) / 3.0
+        achieved = 2.0 * d * cps / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak,
+                "peak_note": f"{pk_kind} dense bf16 / 3: the 3-product split-fp16 contraction "
+                             "that carries fp32 accuracy (SURVEY.md §8d P_dot)",
+                "achieved_note": "2d dot-product flops per cell / kernel time "
+                                 "(the 8 epilogue flops + 1 exp run on FP32/MUFU)"}
+    else:
+        achieved = (2.0 * d + 8.0) * cps / 1e12
+        peak = 2.0 * ffma / 1e12
+        roof = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "peak_note": "FP32 FFMA rate measured on this GPU x 2"}
+    roof.update({
+        "traffic": traffic_for(wl.name), "kernel": "otk_lse_partial (rows half-step)",
+        "kernel_ms": sec * 1e3, "cells_per_launch": cells,
+        "algorithmic_flops_per_launch": (2.0 * d + 8.0) * cells,
+        "pipes": {"ex2_per_s": ex2, "ffma_per_s": ffma, "cells_per_s": cps,
+                  "mufu_frac": cps / ex2,
+                  "note": "one MUFU ex2 per cell per half-step; tcgen05.ld reads 4 B of TMEM "
+                          "per cell (~64 B/clk/SM) -- the measured binding resource (profiles/)"},
+    })
+    return roof
+
+
+def dense_roofline(C, wl, reps=5):
+    """Dominant kernel of the materialised path: one batched rows half-step
+    (otk_dense_lse axis 0) streaming C once: 4 algorithmic bytes per cell."""
+    import torch
+    from paper_2201_12324_b200 import _native as N
+    from paper_2201_12324_b200._device import stream
+    B, n, m = C.shape
+    dev = C.device
+    bias = torch.zeros((B, m), dtype=torch.float32, device=dev)
+    base = torch.zeros((B, n), dtype=torch.float32, device=dev)
+    eps = torch.tensor(np.asarray(wl.eps, dtype=np.float32), device=dev)
+    out = torch.empty((B, n), dtype=torch.float32, device=dev)
+    lib = N.lib()
+
+    def launch():
+        N.check(lib.otk_dense_lse(N.ptr(C), B, n, m, 0, N.ptr(bias), N.ptr(base), N.OTK_FIN_SOLVER,
+                                  N.ptr(eps), N.ptr(eps), None, N.ptr(out), None, None, 0,
+                                  stream()))
+    for _ in range(3):
+        launch()
+    sec = event_time(launch, reps)
+    pk, pk_kind = peaks()
+    nbytes = 4.0 * B * n * m
+    gbs = nbytes / sec / 1e9
+    return {"bound": "hbm", "achieved": gbs, "peak": float(pk["hbm_gbs"]), "unit": "GB/s",
+            "frac": gbs / float(pk["hbm_gbs"]), "traffic": traffic_for(wl.name),
+            "kernel": "otk_dense_lse (batched rows half-step)", "kernel_ms": sec * 1e3,
+            "algorithmic_bytes_per_launch": nbytes, "peak_note": pk_kind}
+
+
+# ------------------------------------------------------------------ our arm
+def timed_steps(solve, steps, dev, flush):
+    """Barrier-free local timing of `steps` solves, CUDA events, L2 flushed before each."""
+    import torch
+    times, outs = [], []
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    for _ in range(steps):
+        flush.fill_(1.0)
+        ev0.record()
+        out = solve()
+        ev1.record()
+        ev1.synchronize()
+        times.append(ev0.elapsed_time(ev1) * 1e-3)
+        outs.append(out)
+    return times, outs
 
 
 def run_ours(args, wl, rank, world):
     import torch
     import paper_2201_12324_b200 as otk
     from paper_2201_12324_b200 import _native as N
-    from paper_2201_12324_b200._device import stream
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     N.lib()
-    n, m = wl.shape
-    xd = torch.from_numpy(wl.x).to(dev)
-    yd = torch.from_numpy(wl.y).to(dev)
-    geom = otk.PointCloudGeometry(xd, yd)
-    prob = otk.LinearProblem(geom, wl.a, wl.b)
     flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
+    n, m = wl.shape
 
-    def solve():
-        return otk.solve_sinkhorn(prob, wl.eps, threshold=wl.threshold, max_iters=wl.max_iters,
-                                  impl=args.kernel)
+    if wl.materialised:
+        xd = torch.from_numpy(wl.x).to(dev)
+        yd = torch.from_numpy(wl.y).to(dev)
+
+        def solve():
+            return otk.solve_sinkhorn_batched(xd, yd, wl.eps, threshold=wl.threshold,
+                                              max_iters=wl.max_iters)
+
+        def cells_of(outs):
+            return float(n) * m * sum(o.iterations for o in outs)
+        parallelism = "single GPU, batched"
+    elif world > 1:
+        from paper_2201_12324_b200.sharded import TorchComm, shard_rows
+        comm = TorchComm()
+        lo, hi = shard_rows(n, world, rank)
+        xd = torch.from_numpy(wl.x[lo:hi]).to(dev)
+        yd = torch.from_numpy(wl.y).to(dev)
+        a_loc = None if wl.a is None else wl.a[lo:hi]
+
+        def solve():
+            return otk.solve_sinkhorn_sharded(xd, yd, wl.eps, a_loc, wl.b, x_is_local=True,
+                                              n_total=n, threshold=wl.threshold,
+                                              max_iters=wl.max_iters, comm=comm, impl=args.kernel)
+
+        def cells_of(out):
+            return float(n) * m * out.iterations
+        parallelism = f"row-sharded x{world} (NCCL all-gather per g half-step)"
+    else:
+        xd = torch.from_numpy(wl.x).to(dev)
+        yd = torch.from_numpy(wl.y).to(dev)
+        geom = otk.PointCloudGeometry(xd, yd)
+        prob = otk.LinearProblem(geom, wl.a, wl.b)
+
+        def solve():
+            return otk.solve_sinkhorn(prob, wl.eps, threshold=wl.threshold,
+                                      max_iters=wl.max_iters, impl=args.kernel)
+
+        def cells_of(out):
+            return float(n) * m * out.iterations
+        parallelism = "single GPU"
 
     for _ in range(args.warmup):
-        out = solve()
-    times, iters, launches = [], [], []
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+        solve()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     with ClockSampler(dev.index) as clocks:
-        for _ in range(args.steps):
-            flush.fill_(1.0)  # L2 flush (untimed)
-            ev0.record()
-            out = solve()
-            ev1.record()
-            ev1.synchronize()
-            times.append(ev0.elapsed_time(ev1) * 1e-3)
-            iters.append(out.iterations)
+        times, outs = timed_steps(solve, args.steps, dev, flush)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     total = sum(times)
-    cell_updates = float(n) * m * sum(iters)
     if world > 1:
         t = torch.tensor([total], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total = float(t.item())
-    value = cell_updates * world / total
-
-    # launch count of one step (native solver reports it)
-    from paper_2201_12324_b200.sinkhorn import _solve_pointcloud  # noqa: F401
+    cell_updates = sum(cells_of(o) for o in outs)
+    value = cell_updates / total
+    last = outs[-1]
+    iters = (int(np.mean([o.iterations for o in last])) if wl.materialised else last.iterations)
+    conv = (all(o.converged for o in last) if wl.materialised else bool(last.converged))
+    config = workload_config(wl, parallelism)
+    config.update({"iterations_per_step": iters, "converged": conv,
+                   "step": "one complete solve to tolerance (inputs resident in HBM)",
+                   "time_to_tolerance_ms": 1e3 * total / args.steps, "kernel": args.kernel})
     result = {
-        "metric": "sinkhorn_cell_updates_per_s", "value": value, "unit": "cell-updates/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded numpy draws, paper_2201_12324_b200/workloads.py)",
-        "config": {"workload": wl.name, "n": n, "m": m, "d": wl.d, "eps": wl.eps,
-                   "threshold": wl.threshold, "iterations_per_step": int(np.mean(iters)),
-                   "converged": bool(out.converged), "step": "one solve_sinkhorn to tolerance",
-                   "time_to_tolerance_ms": 1e3 * total / args.steps,
-                   "l2": "flushed (512 MiB write) before every timed step",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "kernel": args.kernel},
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": DATA, "config": config,
         "clocks": clocks.summary(),
     }
-    if rank != 0:
-        return
 
-    # ---- gpu launches per step
-    result["gpu_launches"] = _count_launches(otk, prob, wl, args) * args.steps
+    # launches of our kernels per step (native solver count / sharded engine count)
+    result["gpu_launches"] = count_launches(otk, wl, args, solve, world) * args.steps
 
-    # ---- roofline of the dominant kernel
-    sec, cells, nsplit = kernel_roofline(otk, geom, wl)
-    pk, pk_kind = peaks()
-    flops = (2 * wl.d + 8) * cells
-    achieved_tf = flops / sec / 1e12
-    peak_tf = float(pk.get("bf16_tflops", 1590.0))
-    traffic = None
-    try:
-        with open(TRAFFIC_FILE) as fh:
-            traffic = json.load(fh).get(wl.name)
-    except OSError:
-        pass
-    ex2, ffma = ctypes_pipes()
-    cells_per_s = cells / sec
-    roof_cells = min(ex2, ffma / (2 * wl.d + 8)) if geom._clouds()[0].hi is None else ex2
-    result["roofline"] = {
-        "bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-        "frac": achieved_tf / peak_tf, "traffic": traffic,
-        "kernel": "otk_lse_partial (rows half-step)", "kernel_ms": sec * 1e3,
-        "algorithmic_flops_per_launch": flops, "cells_per_launch": cells,
-        "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({pk_kind})",
-        "compute_roof": {
-            "note": "exp-bound roof: one MUFU ex2 per cell per half-step (SURVEY.md §8d); "
-                    "pipe rates measured on this GPU by otk_bench_pipes",
-            "ex2_per_s": ex2, "ffma_per_s": ffma, "roof_cells_per_s": roof_cells,
-            "achieved_cells_per_s": cells_per_s, "frac": cells_per_s / roof_cells},
-    }
-
-    # ---- e2e through the public API from pinned host buffers
     if not args.no_e2e:
-        result["e2e"] = _e2e(otk, wl, args, dev)
+        e2e = run_e2e(otk, wl, args, dev, world, rank)
+        if e2e is not None:
+            result["e2e"] = e2e
+    if rank == 0:
+        if wl.materialised:
+            C = torch.empty((wl.x.shape[0], n, m), dtype=torch.float32, device=dev)
+            N.check(N.lib().otk_dense_cost(N.ptr(xd), N.ptr(yd), wl.x.shape[0], n, m, wl.d, 0,
+                                           N.ptr(C), torch.cuda.current_stream().cuda_stream))
+            result["roofline"] = dense_roofline(C, wl)
+            del C
+        elif world == 1:
+            result["roofline"] = online_roofline(geom, wl)
+        else:
+            g1 = otk.PointCloudGeometry(xd, yd)
+            result["roofline"] = online_roofline(g1, wl)
+            result["roofline"]["note"] = "rank 0's shard (n/N rows x m)"
+        if not args.no_cpu and world == 1:
+            v, dt, desc = cpu_sample_rate(wl)
+            result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cpu_cores(),
+                                      "kind": "port", "sample": f"{desc}, {dt:.1f} s"}
+        print(json.dumps(result), flush=True)
 
-    # ---- CPU baseline (oracle on the host cores, bounded sample)
-    if not args.no_cpu and world == 1:
-        v, dt, desc = cpu_sample_rate(wl)
-        result["cpu_baseline"] = {"value": v, "unit": "cell-updates/s",
-                                  "cores": len(os.sched_getaffinity(0)), "kind": "port",
-                                  "sample": desc + f", {dt:.1f}s"}
-    print(json.dumps(result), flush=True)
 
-
-def ctypes_pipes():
+def count_launches(otk, wl, args, solve, world):
+    """Kernels of ours launched by one step: the native solver reports its count
+    (graph nodes included); the sharded engine and the dense loop count theirs."""
     import ctypes
     from paper_2201_12324_b200 import _native as N
-    from paper_2201_12324_b200._device import stream
-    ex2 = ctypes.c_double()
-    ffma = ctypes.c_double()
-    N.check(N.lib().otk_bench_pipes(ctypes.byref(ex2), ctypes.byref(ffma), stream()))
-    return ex2.value, ffma.value
-
-
-def _count_launches(otk, prob, wl, args):
-    import ctypes
+    from paper_2201_12324_b200 import sharded as SH
     from paper_2201_12324_b200 import sinkhorn as S
+    if wl.materialised:
+        calls = {"n": 0}
+        real = N.lib()
+
+        class Counting:
+            def __getattr__(self, name):
+                fn = getattr(real, name)
+                if not name.startswith("otk_") or name in ("otk_last_error", "otk_abi_version"):
+                    return fn
+
+                def wrapped(*a):
+                    calls["n"] += 1
+                    return fn(*a)
+                return wrapped
+        saved = S.N.lib
+        S.N.lib = lambda: Counting()
+        try:
+            solve()
+        finally:
+            S.N.lib = saved
+        return calls["n"]
+    if world > 1:
+        orig = SH.CudaShardEngine.__init__
+        box = {}
+
+        def init(self, *a, **k):
+            orig(self, *a, **k)
+            box["eng"] = self
+        SH.CudaShardEngine.__init__ = init
+        try:
+            solve()
+        finally:
+            SH.CudaShardEngine.__init__ = orig
+        return int(box["eng"].launches)
     captured = {}
-    orig = S.N.lib().otk_solve_pointcloud
-
-    def spy(ptr):
-        rc = orig(ptr)
-        captured["launches"] = ctypes.cast(ptr, ctypes.POINTER(S.N.SolveArgs)).contents.launches
-        return rc
-
-    real = S.N.lib()
+    real = N.lib()
 
     class Proxy:
         def __getattr__(self, name):
-            return spy if name == "otk_solve_pointcloud" else getattr(real, name)
-
+            if name == "otk_solve_pointcloud":
+                def spy(ptr):
+                    rc = real.otk_solve_pointcloud(ptr)
+                    captured["launches"] = ctypes.cast(ptr, ctypes.POINTER(N.SolveArgs)).contents.launches
+                    return rc
+                return spy
+            return getattr(real, name)
     saved = S.N.lib
     S.N.lib = lambda: Proxy()
     try:
-        otk.solve_sinkhorn(prob, wl.eps, threshold=wl.threshold, max_iters=wl.max_iters,
-                           impl=args.kernel)
+        solve()
     finally:
         S.N.lib = saved
     return int(captured.get("launches", 0))
 
 
-def _e2e(otk, wl, args, dev):
+def run_e2e(otk, wl, args, dev, world, rank):
+    """Same metric through the public API from pinned HOST buffers: every step
+    copies its inputs host->device and reads the potentials back."""
     import torch
-    xh = torch.from_numpy(wl.x).pin_memory()
-    yh = torch.from_numpy(wl.y).pin_memory()
     n, m = wl.shape
+    if wl.materialised:
+        xh = torch.from_numpy(wl.x).pin_memory()
+        yh = torch.from_numpy(wl.y).pin_memory()
 
-    def step():
-        prob = otk.LinearProblem(otk.PointCloudGeometry(xh, yh), wl.a, wl.b)
-        out = otk.solve_sinkhorn(prob, wl.eps, threshold=wl.threshold, max_iters=wl.max_iters,
-                                 impl=args.kernel)
-        return out  # out.f / out.g are host float64 arrays (D2H inside the timed region)
+        def step():
+            outs = otk.solve_sinkhorn_batched(xh, yh, wl.eps, threshold=wl.threshold,
+                                              max_iters=wl.max_iters)
+            return sum(o.iterations for o in outs)
+        h2d = wl.x.nbytes + wl.y.nbytes
+        d2h = 4 * (n + m) * wl.x.shape[0]
+    elif world > 1:
+        from paper_2201_12324_b200.sharded import TorchComm, shard_rows
+        lo, hi = shard_rows(n, world, rank)
+        xh = torch.from_numpy(wl.x[lo:hi]).pin_memory()
+        yh = torch.from_numpy(wl.y).pin_memory()
+        comm = TorchComm()
 
+        def step():
+            out = otk.solve_sinkhorn_sharded(xh, yh, wl.eps, None if wl.a is None else wl.a[lo:hi],
+                                             wl.b, x_is_local=True, n_total=n,
+                                             threshold=wl.threshold, max_iters=wl.max_iters,
+                                             comm=comm, impl=args.kernel)
+            return out.iterations
+        h2d = (hi - lo) * wl.d * 4 + wl.y.nbytes + 8 * (hi - lo + m)
+        d2h = 4 * (hi - lo + m)
+    else:
+        xh = torch.from_numpy(wl.x).pin_memory()
+        yh = torch.from_numpy(wl.y).pin_memory()
+
+        def step():
+            prob = otk.LinearProblem(otk.PointCloudGeometry(xh, yh), wl.a, wl.b)
+            out = otk.solve_sinkhorn(prob, wl.eps, threshold=wl.threshold,
+                                     max_iters=wl.max_iters, impl=args.kernel)
+            return out.iterations  # out.f / out.g: float64 host arrays (D2H in the region)
+        h2d = wl.x.nbytes + wl.y.nbytes + 4 * (n + m) * 2
+        d2h = 4 * (n + m)
     for _ in range(args.warmup):
         step()
+    if world > 1:
+        torch.distributed.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     its = 0
     for _ in range(args.steps):
-        out = step()
-        its += out.iterations
+        its += step()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    h2d = wl.x.nbytes + wl.y.nbytes + 4 * (n + m) * 2   # points + weights + log-weights (fp32)
-    d2h = 4 * (n + m)                                  # f, g (fp32)
-    return {"value": float(n) * m * its / dt, "unit": "cell-updates/s",
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "ms_per_step": 1e3 * dt / args.steps,
-            "api": "solve_sinkhorn(LinearProblem(PointCloudGeometry(pinned host x, y)))"}
+    if world > 1:
+        t = torch.tensor([dt], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dt = float(t.item())
+    return {"value": float(n) * m * its / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * dt / args.steps,
+            "api": "public API on pinned host arrays (H2D + D2H inside the timed region)"}
 
 
 def main():
@@ -380,18 +574,23 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     from paper_2201_12324_b200 import workloads
-    wl = workloads.make(args.config)
     if args.impl == "reference":
-        run_reference(args, wl, rank)
+        if rank != 0:
+            return
+        run_reference(args, workloads.make(args.config), rank)
         return
+    wl = workloads.make(args.config)
     if world > 1:
         import torch
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        torch.distributed.init_process_group("nccl")
-    run_ours(args, wl, rank, world)
-    if world > 1:
-        import torch
-        torch.distributed.destroy_process_group()
+        torch.distributed.init_process_group(
+            "nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
+    try:
+        run_ours(args, wl, rank, world)
+    finally:
+        if world > 1:
+            import torch
+            torch.distributed.destroy_process_group()
 
 
 if __name__ == "__main__":

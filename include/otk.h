@@ -50,6 +50,8 @@ enum otk_status {
 /* finalize modes */
 #define OTK_FIN_SOLVER 0 /* out = eps*logw - eps*ln2*L   (sinkhorn.py:173-174)                     */
 #define OTK_FIN_APPLY 1  /* out = f + eps*ln2*L           (geometry.py:336-354)                     */
+#define OTK_FIN_LOG2 2   /* out = L (this shard's column partial for the multi-GPU g update;
+                            base, out_bias, first_bad unused)                                      */
 
 int otk_abi_version(void);
 const char *otk_last_error(void);
@@ -105,6 +107,9 @@ int otk_lse_suggest_nsplit(int64_t np, int64_t nq, int32_t d, int32_t flags);
 /* Combine partials (fixed split order) and produce the potential:
  *   SOLVER: out_i = eps*base_i - eps*ln2*L_i    (base = log w; sinkhorn.py:173-174)
  *   APPLY:  out_i = base_i + eps*ln2*L_i        (base = f; apply_lse_kernel)
+ *   LOG2:   out_i = L_i                         (row-sharded solve: the shard's
+ *           column partial, all-gathered across ranks and combined again with
+ *           nsplit = world size, rank order -- SURVEY.md §8e / K7)
  * If out_bias != NULL also writes kappa_next*out_i (this side's bias for the
  * next half-step).  NaN/+inf in out -> atomicMin(first_bad, step) (first_bad
  * may be NULL). */

@@ -27,6 +27,7 @@ from .sinkhorn import (
     solve_sinkhorn_batched,
     transport_matrix,
 )
+from .sharded import reg_ot_cost_sharded, solve_sinkhorn_sharded
 
 __version__ = "0.1.0"
 
@@ -50,4 +51,6 @@ __all__ = [
     "reg_ot_cost",
     "grad_weights",
     "grad_points",
+    "solve_sinkhorn_sharded",
+    "reg_ot_cost_sharded",
 ]

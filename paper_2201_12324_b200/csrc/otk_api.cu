@@ -113,6 +113,10 @@ __global__ void finalize_kernel(const float *__restrict__ part, int nsplit, int6
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= np) return;
   const float L = combine_log2(part + i, nsplit, np);
+  if (mode == OTK_FIN_LOG2) {  // shard partial for the multi-GPU exchange
+    out[i] = L;
+    return;
+  }
   const float c = eps * kLn2;
   const float v = (mode == OTK_FIN_SOLVER) ? eps * base[i] - c * L : base[i] + c * L;
   out[i] = v;
@@ -258,8 +262,10 @@ int otk_make_bias(const float *pot, int64_t m, float kappa, float *bias, int32_t
 int otk_lse_finalize(const float *partial, int32_t nsplit, int64_t np, const float *base,
                      int32_t mode, float eps, float kappa_next, float *out_pot, float *out_bias,
                      int32_t *first_bad, int32_t step, void *stream) {
-  OTK_CHECK_ARG(partial && base && out_pot && np > 0 && nsplit >= 1, "otk_lse_finalize: bad arguments");
-  OTK_CHECK_ARG(mode == OTK_FIN_SOLVER || mode == OTK_FIN_APPLY, "otk_lse_finalize: bad mode");
+  OTK_CHECK_ARG(partial && out_pot && np > 0 && nsplit >= 1, "otk_lse_finalize: bad arguments");
+  OTK_CHECK_ARG(mode == OTK_FIN_SOLVER || mode == OTK_FIN_APPLY || mode == OTK_FIN_LOG2,
+                "otk_lse_finalize: bad mode");
+  OTK_CHECK_ARG(base || mode == OTK_FIN_LOG2, "otk_lse_finalize: base required");
   finalize_kernel<<<(unsigned)((np + 255) / 256), 256, 0, as_stream(stream)>>>(
       partial, nsplit, np, base, mode, eps, kappa_next, out_pot, out_bias, first_bad, step);
   OTK_LAUNCH_CHECK();

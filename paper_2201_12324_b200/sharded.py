@@ -1,0 +1,428 @@
+"""Row-sharded multi-GPU Sinkhorn (no reference equivalent).
+
+The reference loop (sinkhorn.py:151-200) is single-process.  Here x (with f
+and the weights a) is split into W contiguous row shards, one per rank /
+GPU; y, g and b are replicated:
+
+* f half-step (sinkhorn.py:173) reduces over j -- all of g is local, so it is
+  a plain local ``otk_lse_partial`` + ``otk_lse_finalize``.
+* g half-step (sinkhorn.py:174) reduces over i -- each rank reduces its own
+  rows into one log2-partial per column (``otk_lse_partial`` +
+  ``otk_lse_finalize(mode=OTK_FIN_LOG2)``), the W partials are all-gathered
+  (NCCL over NVLink; m floats per rank) and every rank combines them in rank
+  order with the same finalize kernel, so g stays bitwise identical on all
+  ranks and a 1-rank run is bitwise identical to the single-GPU solver.
+* the check (sinkhorn.py:175-189) runs the fused check kernel on the local
+  rows; the 8 partial sums are all-gathered and added in rank order on the
+  host, so every rank takes the same converged / diverged decision.
+
+The loop itself (``sharded_loop``) is host logic over two small interfaces:
+an *engine* (the device half-steps: ``CudaShardEngine``, the sm_100a library)
+and a *comm* (``TorchComm`` = ``torch.distributed``; ``ThreadComm`` = ranks
+emulated by threads of one process, for single-GPU tests).  The CPU tests
+drive the same loop with a float64 numpy engine over ``gloo``.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import threading
+
+import numpy as np
+
+from . import _native as N
+from ._device import as_device_f32, device, stream
+from .errors import DivergedError
+from .geometry import EpsilonSchedule
+
+__all__ = [
+    "shard_rows",
+    "ShardedSinkhornOutput",
+    "TorchComm",
+    "ThreadComm",
+    "CudaShardEngine",
+    "sharded_loop",
+    "solve_sinkhorn_sharded",
+    "reg_ot_cost_sharded",
+]
+
+_LOG2E = 1.4426950408889634
+
+
+def shard_rows(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous balanced row range [lo, hi) of ``rank`` (first n % world shards get +1)."""
+    if not (0 <= rank < world):
+        raise ValueError("rank must lie in [0, world)")
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+@dataclasses.dataclass(frozen=True, eq=False)
+class ShardedSinkhornOutput:
+    f_local: np.ndarray          # this rank's rows of f (float64)
+    g: np.ndarray                # replicated (float64)
+    errors: np.ndarray
+    dual_trace: np.ndarray
+    iterations: int
+    converged: bool
+    eps: float
+    row_offset: int
+    n_total: int
+    f: np.ndarray | None = None  # all rows (gather_f=True)
+    f_device: object = dataclasses.field(default=None, repr=False)
+    g_device: object = dataclasses.field(default=None, repr=False)
+
+
+# ---------------------------------------------------------------- comms
+class TorchComm:
+    """torch.distributed process group (NCCL for CUDA tensors, gloo for CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_gather_rows(self, local):
+        import torch
+        local = local.contiguous().reshape(-1)
+        out = torch.empty(self.world * local.numel(), dtype=local.dtype, device=local.device)
+        self.dist.all_gather_into_tensor(out, local, group=self.group)
+        return out.view(self.world, -1)
+
+    def _host(self, arr, like_device):
+        import torch
+        return torch.as_tensor(np.asarray(arr, dtype=np.float64), device=like_device)
+
+    def all_gather_host(self, vec: np.ndarray, device) -> np.ndarray:
+        """[k] float64 per rank -> [world, k] on every rank (collective on ``device``)."""
+        t = self._host(vec, device)
+        return self.all_gather_rows(t).cpu().numpy()
+
+
+class ThreadComm:
+    """W ranks emulated by W threads of one process (shared device, host barrier).
+
+    Used to run the sharded loop on one GPU: no kernel ever waits on another
+    rank's kernel -- every exchange goes through the host after a stream sync.
+    """
+
+    class _Shared:
+        def __init__(self, world):
+            self.world = world
+            self.barrier = threading.Barrier(world)
+            self.slots = [None] * world
+
+    def __init__(self, shared: "ThreadComm._Shared", rank: int):
+        self.shared = shared
+        self.rank = rank
+        self.world = shared.world
+
+    @classmethod
+    def group(cls, world: int):
+        sh = cls._Shared(world)
+        return [cls(sh, r) for r in range(world)]
+
+    def _exchange(self, obj):
+        sh = self.shared
+        sh.barrier.wait()
+        sh.slots[self.rank] = obj
+        sh.barrier.wait()
+        out = list(sh.slots)
+        sh.barrier.wait()
+        return out
+
+    def all_gather_rows(self, local):
+        import torch
+        if local.is_cuda:
+            torch.cuda.current_stream(local.device).synchronize()
+        parts = self._exchange(local)
+        return torch.stack([p.to(local.device) for p in parts])
+
+    def all_gather_host(self, vec: np.ndarray, device=None) -> np.ndarray:
+        return np.stack(self._exchange(np.asarray(vec, dtype=np.float64).copy()))
+
+
+# ---------------------------------------------------------------- device engine
+class CudaShardEngine:
+    """Device half-steps of one rank (libotk_sm100.so), mirroring solve.cu's HalfStep."""
+
+    def __init__(self, x_local, y, a_local, b, flags: int = 0, amax_reduce=None):
+        """``amax_reduce(local_amax) -> global_amax`` makes the split-fp16 operand
+        scale common to all ranks (None: this rank's own)."""
+        import torch
+        from .geometry import _Cloud
+        device()
+        self.cx = _Cloud(x_local)
+        self.cy = _Cloud(y)
+        if self.cx.d != self.cy.d:
+            raise ValueError("x and y must have the same dimension")
+        self.n, self.m, self.d = self.cx.n, self.cy.n, self.cx.d
+        lib = N.lib()
+        planes = (flags & N.OTK_IMPL_SIMT) == 0 and bool(self.d >= 32 or flags & N.OTK_IMPL_TC)
+        scale = 1.0
+        if planes:
+            amax = max(self.cx.absmax(), self.cy.absmax())
+            if amax_reduce is not None:
+                amax = amax_reduce(amax)
+            scale = float(lib.otk_split_scale(amax, self.d))
+        self.cx.prepare(scale, planes)
+        self.cy.prepare(scale, planes)
+        self.sinv = 1.0 / (scale * scale)
+        self.flags = (flags & (N.OTK_IMPL_SIMT | N.OTK_IMPL_TC)) | N.OTK_CLAMP
+        dev = self.cx.p.device
+        with np.errstate(divide="ignore"):
+            la, lb = np.log(np.asarray(a_local, dtype=np.float64)), np.log(np.asarray(b, dtype=np.float64))
+        self.a, self.b = as_device_f32(a_local), as_device_f32(b)
+        self.la, self.lb = as_device_f32(la), as_device_f32(lb)
+        self.nsr = lib.otk_lse_suggest_nsplit(self.n, self.m, self.d, self.flags)
+        self.nsc = lib.otk_lse_suggest_nsplit(self.m, self.n, self.d, self.flags)
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.part = torch.empty(max(self.nsr * self.n, self.nsc * self.m), **f32)
+        self.f = [torch.zeros(self.n, **f32), torch.zeros(self.n, **f32)]
+        self.g = torch.zeros(self.m, **f32)
+        self.bias_x = torch.empty(self.n, **f32)
+        self.bias_y = torch.empty(self.m, **f32)
+        self.lcol = torch.empty(self.m, **f32)
+        self.first_bad = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=dev)
+        self.chk = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.chk_ws = torch.zeros(lib.otk_check_workspace_bytes(), dtype=torch.uint8, device=dev)
+        self.device = dev
+        self.launches = 0
+
+    def set_g(self, g_init, kappa):
+        if g_init is None:
+            self.g.zero_()
+        else:
+            self.g.copy_(as_device_f32(g_init))
+        N.check(N.lib().otk_make_bias(N.ptr(self.g), self.m, kappa, N.ptr(self.bias_y),
+                                      N.ptr(self.first_bad), 1, stream()), "make_bias")
+
+    def rows(self, kappa, eps, kappa_next, which, step):
+        cx, cy, lib = self.cx, self.cy, N.lib()
+        st = stream()
+        N.check(lib.otk_lse_partial(N.ptr(cx.p), N.ptr(cx.sq), N.ptr(cx.hi), N.ptr(cx.lo),
+                                    N.ptr(cx.ext_a), self.n, N.ptr(cy.p), N.ptr(cy.sq), N.ptr(cy.hi),
+                                    N.ptr(cy.lo), N.ptr(cy.ext_b), self.m, self.d, cx.dpad,
+                                    self.sinv, N.ptr(self.bias_y), kappa, self.flags, self.nsr,
+                                    N.ptr(self.part), st), "rows half-step")
+        N.check(lib.otk_lse_finalize(N.ptr(self.part), self.nsr, self.n, N.ptr(self.la),
+                                     N.OTK_FIN_SOLVER, eps, kappa_next, N.ptr(self.f[which]),
+                                     N.ptr(self.bias_x), N.ptr(self.first_bad), step, st), "finalize")
+        self.launches += 2
+
+    def cols_partial(self, kappa):
+        cx, cy, lib = self.cx, self.cy, N.lib()
+        st = stream()
+        N.check(lib.otk_lse_partial(N.ptr(cy.p), N.ptr(cy.sq), N.ptr(cy.hi), N.ptr(cy.lo),
+                                    N.ptr(cy.ext_a), self.m, N.ptr(cx.p), N.ptr(cx.sq), N.ptr(cx.hi),
+                                    N.ptr(cx.lo), N.ptr(cx.ext_b), self.n, self.d, cx.dpad,
+                                    self.sinv, N.ptr(self.bias_x), kappa, self.flags, self.nsc,
+                                    N.ptr(self.part), st), "cols half-step")
+        N.check(lib.otk_lse_finalize(N.ptr(self.part), self.nsc, self.m, None, N.OTK_FIN_LOG2, 0.0,
+                                     0.0, N.ptr(self.lcol), None, None, 0, st), "shard partial")
+        self.launches += 2
+        return self.lcol
+
+    def cols_finalize(self, lall, eps, kappa_next, step):
+        W = lall.shape[0]
+        N.check(N.lib().otk_lse_finalize(N.ptr(lall), W, self.m, N.ptr(self.lb), N.OTK_FIN_SOLVER,
+                                         eps, kappa_next, N.ptr(self.g), N.ptr(self.bias_y),
+                                         N.ptr(self.first_bad), step, stream()), "combine")
+        self.launches += 1
+
+    def check(self, which, measure, eps):
+        fn = self.f[1 - which] if measure else None
+        N.check(N.lib().otk_check(N.ptr(self.f[which]), N.ptr(fn), N.ptr(self.a), self.n,
+                                  N.ptr(self.g), N.ptr(self.b), self.m, eps, N.ptr(self.chk),
+                                  N.ptr(self.chk_ws), stream()), "check")
+        self.launches += 1
+        return self.chk.cpu().numpy().copy()
+
+    def read_first_bad(self) -> int:
+        return int(self.first_bad.item())
+
+    def reset_first_bad(self):
+        self.first_bad.fill_(2 ** 31 - 1)
+
+    def f_result(self, which):
+        return self.f[which]
+
+    def g_result(self):
+        return self.g
+
+
+# ---------------------------------------------------------------- the loop
+def sharded_loop(engine, comm, sched: EpsilonSchedule, threshold: float, max_iters: int,
+                 inner_iters: int, g_init=None):
+    """The reference loop (sinkhorn.py:151-200) over row shards.
+
+    Returns (which_f, iterations, converged, errors, duals).  Raises
+    DivergedError / ValueError at the same iteration the single-GPU solver
+    (solve.cu) would.  Same step numbering as solve.cu: the finalize of f_t
+    records step 2t, g_t records 2t+1, the check's f_{t+1} records 2t+2.
+    """
+    target = sched.target
+    engine.set_g(g_init, float(np.float32(_LOG2E / sched.at(0))))
+    which, f_ready = 0, False
+    errors, duals = [], []
+    converged = False
+    t = 0
+    for t in range(1, max_iters + 1):
+        e = sched.at(t - 1)
+        kap = float(np.float32(_LOG2E / e))
+        kap_next = float(np.float32(_LOG2E / sched.at(t)))
+        if not f_ready:
+            engine.rows(kap, e, kap, which, 2 * t)
+        f_ready = False
+        lall = comm.all_gather_rows(engine.cols_partial(kap))
+        engine.cols_finalize(lall, e, kap_next, 2 * t + 1)
+        if t % inner_iters == 0 or t == max_iters:
+            measure = not (e > target)
+            if measure:
+                engine.rows(kap, e, kap, 1 - which, 2 * t + 2)
+            local = engine.check(which, measure, e)
+            fb = engine.read_first_bad()
+            rows = comm.all_gather_host(np.append(local, float(fb)), engine.device)
+            tot = np.zeros(8)
+            for r in range(rows.shape[0]):          # fixed rank order: deterministic
+                tot += rows[r, :8]
+            for k in (3, 5, 7):                      # g terms are replicated: count once
+                tot[k] = rows[0, k]
+            fb = int(rows[:, 8].min())
+            if fb <= 2 * t:
+                raise ValueError(f"g contains NaN or +inf entries (potential fed to iteration "
+                                 f"{(fb + 1) // 2})")
+            if tot[4] > 0 or tot[5] > 0:
+                raise DivergedError("NaN in Sinkhorn potentials; eps is likely too small for the "
+                                    "cost scale", iteration=t)
+            if not measure:
+                continue
+            if fb == 2 * t + 1:
+                raise ValueError(f"g contains NaN or +inf entries (potential fed to iteration {t})")
+            err = float(tot[0])
+            errors.append(err)
+            duals.append(float(tot[2] + tot[3] - e * (tot[1] - 1.0)))
+            if err <= threshold:
+                converged = True
+                break
+            if t < max_iters:
+                which, f_ready = 1 - which, True
+    return which, min(t, max_iters), converged, np.asarray(errors), np.asarray(duals)
+
+
+def _global_weights(w, n_total, lo, hi, name):
+    if w is None:
+        return np.full(hi - lo, 1.0 / n_total)
+    w = np.asarray(w.detach().double().cpu().numpy() if hasattr(w, "detach") else w, dtype=float)
+    if w.shape == (n_total,):
+        w = w[lo:hi]
+    if w.shape != (hi - lo,):
+        raise ValueError(f"{name} must have shape ({n_total},) or the shard's ({hi - lo},)")
+    if not np.all(np.isfinite(w)) or np.any(w < 0):
+        raise ValueError(f"{name} must be entrywise finite and nonnegative")
+    return w
+
+
+def solve_sinkhorn_sharded(x, y, eps, a=None, b=None, *, threshold: float = 1e-3,
+                           max_iters: int = 2000, inner_iters: int = 10, g_init=None,
+                           comm=None, x_is_local: bool = False, n_total: int | None = None,
+                           impl: str = "auto", gather_f: bool = False) -> ShardedSinkhornOutput:
+    """Row-sharded ``solve_sinkhorn`` on a point cloud (one rank per GPU).
+
+    ``x``: the full [n, d] points (each rank takes its ``shard_rows`` slice) or,
+    with ``x_is_local``, this rank's rows (then pass ``n_total``).  ``y`` [m, d],
+    ``b`` [m] replicated; ``a`` global [n] (or the local slice).  ``comm``:
+    ``TorchComm()`` (default, needs an initialised process group) or a
+    ``ThreadComm``.  Same validation, loop and errors as ``solve_sinkhorn``.
+    """
+    from .sinkhorn import _fp32_guard, _impl_flags
+    if max_iters < 1 or inner_iters < 1:
+        raise ValueError("max_iters and inner_iters must be >= 1")
+    if not (threshold > 0):
+        raise ValueError("threshold must be positive")
+    sched = eps if isinstance(eps, EpsilonSchedule) else EpsilonSchedule(float(eps))
+    _fp32_guard(sched, inner_iters, max_iters)
+    comm = comm or TorchComm()
+    if x_is_local:
+        if n_total is None:
+            raise ValueError("n_total is required with x_is_local")
+        sizes = comm.all_gather_host(np.array([float(x.shape[0])]), _dev_of(x))[:, 0].astype(int)
+        lo = int(sizes[:comm.rank].sum())
+        hi = lo + int(x.shape[0])
+        if int(sizes.sum()) != n_total:
+            raise ValueError("local shards do not add up to n_total")
+        x_local = x
+    else:
+        n_total = int(x.shape[0])
+        lo, hi = shard_rows(n_total, comm.world, comm.rank)
+        x_local = x[lo:hi]
+    m = int(y.shape[0])
+    a_loc = _global_weights(a, n_total, lo, hi, "a")
+    b_w = _global_weights(b, m, 0, m, "b")
+    tot_a = comm.all_gather_host(np.array([a_loc.sum()]), _dev_of(x))[:, 0].sum()
+    if abs(tot_a - 1.0) > 1e-8 or abs(b_w.sum() - 1.0) > 1e-8:
+        raise ValueError("a and b must each sum to 1")
+    flags = _impl_flags(impl)
+    dev = _dev_of(x)
+
+    def amax_reduce(v):  # one common split scale on every rank
+        return float(comm.all_gather_host(np.array([v]), dev)[:, 0].max())
+
+    eng = CudaShardEngine(x_local, y, a_loc, b_w, flags=flags, amax_reduce=amax_reduce)
+    which, iters, conv, errs, duals = sharded_loop(eng, comm, sched, threshold, max_iters,
+                                                   inner_iters, g_init)
+    f_dev = eng.f_result(which)
+    g_dev = eng.g_result()
+    f_full = None
+    if gather_f:
+        import torch
+        width = -(-n_total // comm.world) + 1
+        pad = torch.full((width,), float("nan"), dtype=torch.float32, device=f_dev.device)
+        pad[: hi - lo] = f_dev
+        allf = comm.all_gather_rows(pad).cpu().numpy().astype(np.float64)
+        f_full = np.concatenate([allf[r, : shard_rows(n_total, comm.world, r)[1]
+                                       - shard_rows(n_total, comm.world, r)[0]]
+                                 for r in range(comm.world)])
+    return ShardedSinkhornOutput(
+        f_local=f_dev.cpu().numpy().astype(np.float64), g=g_dev.cpu().numpy().astype(np.float64),
+        errors=errs, dual_trace=duals, iterations=iters, converged=conv, eps=sched.target,
+        row_offset=lo, n_total=n_total, f=f_full, f_device=f_dev, g_device=g_dev)
+
+
+def _dev_of(x):
+    import torch
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        return x.device
+    return device()
+
+
+def reg_ot_cost_sharded(out: ShardedSinkhornOutput, x_local, y, a_local, b, comm=None):
+    """reg_ot_cost (sinkhorn.py:210-216) over row shards: online local sums + rank-order total."""
+    import torch
+    from .geometry import _Cloud
+    comm = comm or TorchComm()
+    cx, cy = _Cloud(x_local), _Cloud(y)
+    cx.prepare(1.0, False)
+    cy.prepare(1.0, False)
+    lib = N.lib()
+    ws = torch.empty(lib.otk_cost_workspace_bytes(cx.n, cy.n), dtype=torch.uint8, device=cx.p.device)
+    res = torch.zeros(2, dtype=torch.float64, device=cx.p.device)
+    f_d = as_device_f32(out.f_device if out.f_device is not None else out.f_local)
+    g_d = as_device_f32(out.g_device if out.g_device is not None else out.g)
+    N.check(lib.otk_cost_partial(N.ptr(cx.p), N.ptr(cx.sq), cx.n, N.ptr(cy.p), N.ptr(cy.sq), cy.n,
+                                 cx.d, N.ptr(f_d), N.ptr(g_d), float(out.eps), 0, N.ptr(res),
+                                 N.ptr(ws), stream()), "reg_ot_cost")
+    a_local = np.asarray(a_local, dtype=float)
+    b = np.asarray(b, dtype=float)
+    with np.errstate(invalid="ignore"):
+        fa = float(np.where(a_local > 0, out.f_local * a_local, 0.0).sum())
+    loc = np.array([*res.cpu().numpy(), fa])
+    rows = comm.all_gather_host(loc, cx.p.device)
+    transport, mass, fa_tot = (float(sum(rows[r, k] for r in range(rows.shape[0]))) for k in range(3))
+    with np.errstate(invalid="ignore"):
+        gb = float(np.where(b > 0, out.g * b, 0.0).sum())
+    from .sinkhorn import RegOTCost
+    return RegOTCost(transport, fa_tot + gb - out.eps * (mass - 1.0))

@@ -30,9 +30,9 @@ def main():
         geom.impl_flags = N.OTK_IMPL_SIMT
     elif args.kernel == "tc":
         geom.impl_flags = N.OTK_IMPL_TC
-    sec, cells, nsplit = bench.kernel_roofline(otk, geom, wl, reps=args.reps)
-    print(f"config {args.config}: {sec * 1e3:.3f} ms per half-step, {cells / sec:.3e} cells/s, "
-          f"nsplit {nsplit}")
+    r = bench.online_roofline(geom, wl, reps=args.reps)
+    print(f"config {args.config}: {r['kernel_ms']:.3f} ms per half-step, "
+          f"{r['pipes']['cells_per_s']:.3e} cells/s, {r['bound']} frac {r['frac']:.3f}")
 
 
 if __name__ == "__main__":
