@@ -307,3 +307,19 @@ def test_full_size_properties(otk, k):
     # f_1 = eps*log(1/n) - eps*LSE_j(-C_ij/eps)
     f1_ref = wl.eps * np.log(1.0 / wl.shape[0]) - fx["rows_g0"]
     assert rel_inf(one.f[fx["rows"]], f1_ref) <= 2e-5
+
+
+def test_reference_loop_drives_the_drop_in_geometry(otk):
+    """The reference's loop (its oracle restatement of _sinkhorn_iterations,
+    sinkhorn.py:151-200) runs unchanged on top of our PointCloudGeometry: every
+    half-step is otk_lse_partial + otk_lse_finalize."""
+    for gen, kw in (("cfg1", dict(n=300, m=257)), ("cfg2", dict(n=384, m=320, d=64))):
+        wl = getattr(workloads, gen)(**kw)
+        ours = oracle.sinkhorn(otk.PointCloudGeometry(wl.x, wl.y), None, None, wl.eps,
+                               threshold=1e-300, max_iters=20)
+        ref = oracle.sinkhorn(oracle.PointCloudOracle(wl.x.astype(np.float64),
+                                                      wl.y.astype(np.float64)),
+                              None, None, wl.eps, threshold=1e-300, max_iters=20)
+        assert ours["iterations"] == ref["iterations"]
+        assert rel_inf(ours["f"], ref["f"]) <= POT_TOL
+        assert rel_inf(ours["g"], ref["g"]) <= POT_TOL
