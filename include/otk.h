@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define OTK_ABI_VERSION 2
+#define OTK_ABI_VERSION 3
 
 enum otk_status {
   OTK_OK = 0,
@@ -148,10 +148,16 @@ int otk_transport_matrix(const float *p, const float *p_sq, int64_t np,
 /* ---------------- materialised / batched path (DenseGeometry) ---------------- */
 
 /* K4 -- C[b,i,j] = sum_k (x_bik - y_bjk)^2 (PointCloudGeometry.cost_matrix,
- * geometry.py:314-316; exact-zero diagonal with OTK_SAME_POINTS). */
+ * geometry.py:314-316; exact-zero diagonal with OTK_SAME_POINTS).  If cost_t
+ * is non-NULL also writes C^T[b,j,i] (the column half-steps then run the
+ * coalesced row kernel over C^T: otk_dense_lse(cost_t, batch, m, n, 0, ...)). */
 int otk_dense_cost(const float *x, const float *y, int64_t batch, int64_t n,
                    int64_t m, int32_t d, int32_t flags, float *cost,
-                   void *stream);
+                   float *cost_t, void *stream);
+
+/* C^T[b] = C[b]^T for a stored cost (DenseGeometry, geometry.py:171-211). */
+int otk_dense_transpose(const float *cost, int64_t batch, int64_t n, int64_t m,
+                        float *cost_t, void *stream);
 
 /* K3 -- DenseGeometry.apply_lse_kernel (geometry.py:204-211), batched, fused
  * with the finalize step.  axis 0 ("rows"): out[b,i] from reduction over j;

@@ -16,6 +16,7 @@ from .geometry import (
     PointCloudGeometry,
 )
 from .sinkhorn import (
+    BatchedSinkhornOutput,
     Coupling,
     LinearProblem,
     RegOTCost,
@@ -47,6 +48,7 @@ __all__ = [
     "RegOTCost",
     "solve_sinkhorn",
     "solve_sinkhorn_batched",
+    "BatchedSinkhornOutput",
     "transport_matrix",
     "reg_ot_cost",
     "grad_weights",

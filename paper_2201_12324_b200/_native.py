@@ -18,7 +18,7 @@ OTK_OK, OTK_EINVAL, OTK_ECUDA, OTK_ENOTSUP, OTK_ENCCL = 0, -1, -2, -3, -4
 OTK_DIVERGED, OTK_BAD_POTENTIAL = 1, 2
 OTK_SAME_POINTS, OTK_CLAMP, OTK_IMPL_SIMT, OTK_IMPL_TC = 0x1, 0x2, 0x10, 0x20
 OTK_FIN_SOLVER, OTK_FIN_APPLY, OTK_FIN_LOG2 = 0, 1, 2
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 P = C.c_void_p
 I64, I32, F32, F64, SZ = C.c_int64, C.c_int32, C.c_float, C.c_double, C.c_size_t
@@ -57,7 +57,8 @@ SIGNATURES = {
     "otk_cost_workspace_bytes": (SZ, [I64, I64]),
     "otk_cost_partial": (C.c_int, [P, P, I64, P, P, I64, I32, P, P, F64, I32, P, P, P]),
     "otk_transport_matrix": (C.c_int, [P, P, I64, P, P, I64, I32, P, P, F64, I32, P, P]),
-    "otk_dense_cost": (C.c_int, [P, P, I64, I64, I64, I32, I32, P, P]),
+    "otk_dense_cost": (C.c_int, [P, P, I64, I64, I64, I32, I32, P, P, P]),
+    "otk_dense_transpose": (C.c_int, [P, I64, I64, I64, P, P]),
     "otk_dense_lse": (C.c_int, [P, I64, I64, I64, I32, P, P, I32, P, P, P, P, P, P, I32, P]),
     "otk_check_batched": (C.c_int, [P, P, P, I64, P, P, I64, I64, P, P, P, P]),
     "otk_dense_plan": (C.c_int, [P, I64, I64, P, P, F64, P, P]),

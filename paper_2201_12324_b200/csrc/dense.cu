@@ -12,39 +12,93 @@
 //                 row groups merge through shared memory in fixed order.
 // Batched check and reg_ot_cost reductions run one CTA per problem with
 // fixed-order float64 tree reductions (deterministic).
+#include <algorithm>
+
 #include "otk_common.cuh"
 
 namespace otk {
 
 // ------------------------------------------------------------------ K4
-constexpr int DC_T = 32;
+constexpr int DC_T = 32;   // transpose tile
+constexpr int DC_B = 64;   // cost tile: 64 x 64 outputs per CTA, 4 x 4 per thread
 
+// C[b,i,j] = sum_k (x_bik - y_bjk)^2 in the difference form (no cancellation).
+// Also writes C^T[b, j, i] when cost_t != NULL, staged through shared memory
+// so both stores are coalesced: the column half-steps then stream C^T with
+// the row kernel instead of striding down the columns of C.
 __global__ void __launch_bounds__(256) dense_cost_kernel(const float *__restrict__ x,
                                                          const float *__restrict__ y, int64_t n,
                                                          int64_t m, int d, int same,
-                                                         float *__restrict__ cost) {
-  extern __shared__ float sm[];  // xs[32][d+1], ys[32][d+1]
+                                                         float *__restrict__ cost,
+                                                         float *__restrict__ cost_t) {
+  extern __shared__ float sm[];  // xs[64][d+1], ys[64][d+1]; reused as the [64][65] out tile
   const int b = blockIdx.z;
-  const int64_t i0 = (int64_t)blockIdx.y * DC_T, j0 = (int64_t)blockIdx.x * DC_T;
+  const int64_t i0 = (int64_t)blockIdx.y * DC_B, j0 = (int64_t)blockIdx.x * DC_B;
   const float *xb = x + (int64_t)b * n * d;
   const float *yb = y + (int64_t)b * m * d;
-  float *xs = sm, *ys = sm + DC_T * (d + 1);
-  for (int idx = threadIdx.x; idx < DC_T * d; idx += blockDim.x) {
-    int r = idx / d, k = idx % d;
-    xs[r * (d + 1) + k] = (i0 + r < n) ? xb[(i0 + r) * d + k] : 0.f;
-    ys[r * (d + 1) + k] = (j0 + r < m) ? yb[(j0 + r) * d + k] : 0.f;
+  const int ld = d + 1;
+  float *xs = sm, *ys = sm + DC_B * ld;
+  for (int idx = threadIdx.x; idx < DC_B * d; idx += blockDim.x) {
+    const int r = idx / d, k = idx % d;
+    xs[r * ld + k] = (i0 + r < n) ? xb[(i0 + r) * d + k] : 0.f;
+    ys[r * ld + k] = (j0 + r < m) ? yb[(j0 + r) * d + k] : 0.f;
   }
   __syncthreads();
-  const int tj = threadIdx.x & 31, ti = threadIdx.x >> 5;  // 8 row lanes x 32 cols
-  for (int r = ti; r < DC_T; r += 8) {
-    int64_t i = i0 + r, j = j0 + tj;
-    float acc = 0.f;
-    for (int k = 0; k < d; ++k) {
-      float df = xs[r * (d + 1) + k] - ys[tj * (d + 1) + k];
-      acc = fmaf(df, df, acc);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // rows ty + 16*r, cols tx + 16*c
+  float acc[4][4] = {};
+  for (int k = 0; k < d; ++k) {
+    float xv[4], yv[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) xv[r] = xs[(ty + 16 * r) * ld + k];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) yv[c] = ys[(tx + 16 * c) * ld + k];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float df = xv[r] - yv[c];
+        acc[r][c] = fmaf(df, df, acc[r][c]);
+      }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int64_t i = i0 + ty + 16 * r, j = j0 + tx + 16 * c;
+      if (same && i == j) acc[r][c] = 0.f;
+      if (i < n && j < m) cost[((int64_t)b * n + i) * m + j] = acc[r][c];
     }
-    if (same && i == j) acc = 0.f;
-    if (i < n && j < m) cost[((int64_t)b * n + i) * m + j] = acc;
+  if (cost_t == nullptr) return;
+  __syncthreads();  // operands no longer needed: reuse smem for the output tile
+  float *tile = sm;  // [64][65]
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tile[(ty + 16 * r) * (DC_B + 1) + tx + 16 * c] = acc[r][c];
+  __syncthreads();
+  const int lane = threadIdx.x & 63, grp = threadIdx.x >> 6;  // 4 groups of 64 lanes
+  for (int jj = grp; jj < DC_B; jj += 4) {  // row jj of C^T = column j0+jj of C
+    const int64_t j = j0 + jj, i = i0 + lane;
+    if (i < n && j < m) cost_t[((int64_t)b * m + j) * n + i] = tile[lane * (DC_B + 1) + jj];
+  }
+}
+
+// C^T[b] = C[b]^T for a stored cost (DenseGeometry): 32x32 shared tiles.
+__global__ void __launch_bounds__(256) dense_transpose_kernel(const float *__restrict__ C,
+                                                              int64_t n, int64_t m,
+                                                              float *__restrict__ CT) {
+  __shared__ float tile[DC_T][DC_T + 1];
+  const int b = blockIdx.z;
+  const int64_t i0 = (int64_t)blockIdx.y * DC_T, j0 = (int64_t)blockIdx.x * DC_T;
+  const int tj = threadIdx.x & 31, ti = threadIdx.x >> 5;
+  for (int r = ti; r < DC_T; r += 8) {
+    const int64_t i = i0 + r, j = j0 + tj;
+    tile[r][tj] = (i < n && j < m) ? C[((int64_t)b * n + i) * m + j] : 0.f;
+  }
+  __syncthreads();
+  for (int r = ti; r < DC_T; r += 8) {
+    const int64_t j = j0 + r, i = i0 + tj;
+    if (i < n && j < m) CT[((int64_t)b * m + j) * n + i] = tile[tj][r];
   }
 }
 
@@ -332,17 +386,28 @@ using namespace otk;
 extern "C" {
 
 int otk_dense_cost(const float *x, const float *y, int64_t batch, int64_t n, int64_t m, int32_t d,
-                   int32_t flags, float *cost, void *stream) {
+                   int32_t flags, float *cost, float *cost_t, void *stream) {
   OTK_CHECK_ARG(x && y && cost && batch > 0 && n > 0 && m > 0 && d > 0, "otk_dense_cost: bad arguments");
   OTK_CHECK_ARG(batch <= 65535, "otk_dense_cost: batch too large");
-  size_t smem = 2 * DC_T * (size_t)(d + 1) * sizeof(float);
+  size_t smem = std::max(2 * DC_B * (size_t)(d + 1), (size_t)DC_B * (DC_B + 1)) * sizeof(float);
   OTK_CHECK_ARG(smem <= 200 * 1024, "otk_dense_cost: d too large");
   if (smem > 48 * 1024)
     OTK_CUDA(cudaFuncSetAttribute(dense_cost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-  dim3 grid((unsigned)((m + DC_T - 1) / DC_T), (unsigned)((n + DC_T - 1) / DC_T), (unsigned)batch);
+  dim3 grid((unsigned)((m + DC_B - 1) / DC_B), (unsigned)((n + DC_B - 1) / DC_B), (unsigned)batch);
   dense_cost_kernel<<<grid, 256, smem, as_stream(stream)>>>(x, y, n, m, d,
-                                                            (flags & OTK_SAME_POINTS) ? 1 : 0, cost);
+                                                            (flags & OTK_SAME_POINTS) ? 1 : 0, cost,
+                                                            cost_t);
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}
+
+int otk_dense_transpose(const float *cost, int64_t batch, int64_t n, int64_t m, float *cost_t,
+                        void *stream) {
+  OTK_CHECK_ARG(cost && cost_t && batch > 0 && batch <= 65535 && n > 0 && m > 0,
+                "otk_dense_transpose: bad arguments");
+  dim3 grid((unsigned)((m + DC_T - 1) / DC_T), (unsigned)((n + DC_T - 1) / DC_T), (unsigned)batch);
+  dense_transpose_kernel<<<grid, 256, 0, as_stream(stream)>>>(cost, n, m, cost_t);
   OTK_LAUNCH_CHECK();
   return OTK_OK;
 }

@@ -284,6 +284,14 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 // Packed f32x2 arithmetic (FFMA2 / FADD2) halves the issue slots of the
 // per-cell work; EP of every 8 column pairs take their exps from the FMA-pipe
 // polynomial instead of MUFU.
+//
+// Optimistic rescale: the chunk is summed against the CURRENT shift m first;
+// only if that sum exceeds 2^16 (some term beat m by > 16 in log2 units, or
+// overflowed) is the chunk's max taken and the row state rescaled -- rare
+// after the first chunks, and it keeps the max reduction off the common path.
+// Invariant: m never exceeds the running max, and every term summed is
+// <= 2^16 * 2^m, so s stays far inside fp32 range.  m = -inf (nothing finite
+// seen yet) takes the max path, which reproduces the empty-slice -inf result.
 template <int CH, bool MASK, int EP>
 __device__ __forceinline__ void lse_chunk(const float *acc, const float *bias, float c2k, int valid,
                                           float &m, float &s) {
@@ -298,26 +306,56 @@ __device__ __forceinline__ void lse_chunk(const float *acc, const float *bias, f
       if (2 * i + 1 >= valid) u[i].y = -INFINITY;
     }
   }
-  float cm = -INFINITY;
+  auto chunk_sum = [&](float shift) {
+    const float2 nms = make_float2(-shift, -shift);
+    float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-  for (int i = 0; i < CH / 2; ++i) cm = fmaxf(cm, fmaxf(u[i].x, u[i].y));
-  if (cm > m + 8.f) {  // lazy rescale: terms may exceed m by at most 2^8
-    s *= ex2(m - cm);
+    for (int i = 0; i < CH / 2; ++i) {
+      const float2 x = __fadd2_rn(u[i], nms);
+      float2 e;
+      if (i % 8 < EP) {
+        e = ex2_poly2(x);
+      } else {
+        e = make_float2(ex2(x.x), ex2(x.y));
+      }
+      acc2[i & 1] = __fadd2_rn(acc2[i & 1], e);
+    }
+    const float2 t2 = __fadd2_rn(acc2[0], acc2[1]);
+    return t2.x + t2.y;
+  };
+  float cs = (m == -INFINITY) ? INFINITY : chunk_sum(m);
+  if (!(cs <= 65536.f)) {  // slow path: new running max (also NaN / inf / first chunk)
+    float cm = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < CH / 2; ++i) cm = fmaxf(cm, fmaxf(u[i].x, u[i].y));
+    if (cm > m) {
+      s *= ex2(m - cm);
+      m = cm;
+    }
+    cs = chunk_sum(m == -INFINITY ? 0.f : m);
+  }
+  s += cs;
+}
+
+// Timing probe 5: a fixed per-row shift instead of the running max.
+template <int CH>
+__device__ __forceinline__ void lse_chunk_fixed(const float *acc, const float *bias, float c2k,
+                                                float &m, float &s) {
+  const float2 k2 = make_float2(c2k, c2k);
+  if (m == -INFINITY) {
+    float cm = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) cm = fmaxf(cm, fmaf(acc[i], c2k, bias[i]));
     m = cm;
   }
-  const float ms = (m == -INFINITY) ? 0.f : m;
-  const float2 nms = make_float2(-ms, -ms);
+  const float2 nms = make_float2(-m, -m);
   float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
   for (int i = 0; i < CH / 2; ++i) {
-    const float2 x = __fadd2_rn(u[i], nms);
-    float2 e;
-    if (i % 8 < EP) {
-      e = ex2_poly2(x);
-    } else {
-      e = make_float2(ex2(x.x), ex2(x.y));
-    }
-    acc2[i & 1] = __fadd2_rn(acc2[i & 1], e);
+    const float2 u = __ffma2_rn(make_float2(acc[2 * i], acc[2 * i + 1]), k2,
+                                make_float2(bias[2 * i], bias[2 * i + 1]));
+    const float2 x = __fadd2_rn(u, nms);
+    acc2[i & 1] = __fadd2_rn(acc2[i & 1], make_float2(ex2(x.x), ex2(x.y)));
   }
   const float2 t2 = __fadd2_rn(acc2[0], acc2[1]);
   s += t2.x + t2.y;
@@ -570,6 +608,10 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
           }
           const float4 *bp = reinterpret_cast<const float4 *>(bias + c * C::CH);
           float bv[C::CH];
+          if (prm.probe == 6) {  // timing probe: no bias loads
+#pragma unroll
+            for (int i = 0; i < C::CH; ++i) bv[i] = 0.25f * (float)(i & 3);
+          } else
 #pragma unroll
           for (int i = 0; i < C::CH / 4; ++i) {
             float4 q = bp[i];
@@ -583,6 +625,8 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
           } else if (prm.probe == 2) {
 #pragma unroll
             for (int i = 0; i < C::CH; ++i) s += fmaf(accv[i], c2k, bv[i]);
+          } else if (prm.probe == 5) {
+            lse_chunk_fixed<C::CH>(accv, bv, c2k, m, s);
           } else if (valid >= BN)
             lse_chunk<C::CH, false, EP>(accv, bv, c2k, 0, m, s);
           else

@@ -263,7 +263,7 @@ class PointCloudGeometry(Geometry):
         out = torch.empty((n, m), dtype=torch.float32, device=cx.p.device)
         N.check(N.lib().otk_dense_cost(N.ptr(cx.p), N.ptr(cy.p), 1, n, m, cx.d,
                                        N.OTK_SAME_POINTS if self._same_points else 0, N.ptr(out),
-                                       stream()), "cost_matrix")
+                                       None, stream()), "cost_matrix")
         return to_output(out, self.x)
 
     def apply_lse_kernel(self, f, g, eps=None, axis="rows"):
@@ -325,6 +325,18 @@ class DenseGeometry(Geometry):
             device()
             self._dev = as_device_f32(self._cost_in).contiguous()
         return self._dev
+
+    def _c_ct(self):
+        """(C, C^T) on the device; C^T lets the column half-steps stream row-major."""
+        import torch
+        C = self._c()
+        if getattr(self, "_ct", None) is None:
+            n, m = self.shape
+            ct = torch.empty((m, n), dtype=torch.float32, device=C.device)
+            N.check(N.lib().otk_dense_transpose(N.ptr(C), 1, n, m, N.ptr(ct), stream()),
+                    "dense_transpose")
+            self._ct = ct
+        return C, self._ct
 
     def mean_cost(self) -> float:
         if is_torch(self._cost_in):

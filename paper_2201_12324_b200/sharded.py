@@ -139,7 +139,11 @@ class ThreadComm:
         if local.is_cuda:
             torch.cuda.current_stream(local.device).synchronize()
         parts = self._exchange(local)
-        return torch.stack([p.to(local.device) for p in parts])
+        out = torch.stack([p.to(local.device) for p in parts])
+        if local.is_cuda:  # every copy done before any rank overwrites its buffer
+            torch.cuda.current_stream(local.device).synchronize()
+        self.shared.barrier.wait()
+        return out
 
     def all_gather_host(self, vec: np.ndarray, device=None) -> np.ndarray:
         return np.stack(self._exchange(np.asarray(vec, dtype=np.float64).copy()))

@@ -23,6 +23,8 @@ import logging
 from typing import NamedTuple
 
 import ctypes
+from collections.abc import Sequence
+
 import numpy as np
 
 from . import _native as N
@@ -39,6 +41,7 @@ __all__ = [
     "RegOTCost",
     "solve_sinkhorn",
     "solve_sinkhorn_batched",
+    "BatchedSinkhornOutput",
     "transport_matrix",
     "reg_ot_cost",
     "grad_weights",
@@ -99,6 +102,49 @@ class SinkhornOutput:
     eps: float
     f_device: object = dataclasses.field(default=None, repr=False)
     g_device: object = dataclasses.field(default=None, repr=False)
+
+
+class BatchedSinkhornOutput(Sequence):
+    """The B results of ``solve_sinkhorn_batched`` (extension; no reference equivalent).
+
+    A read-only sequence: element k is the ``SinkhornOutput`` an independent
+    ``solve_sinkhorn`` call on problem k returns (built on first access).  The
+    batched arrays are also exposed directly -- ``f`` [B,n], ``g`` [B,m]
+    (float64), ``iterations``, ``converged``, ``eps`` ([B]) and the float32
+    device tensors ``f_device`` / ``g_device`` -- so callers of big batches
+    need not materialise B Python objects.
+    """
+
+    def __init__(self, f, g, err_tab, dual_tab, n_rec, iterations, converged, eps, f_device,
+                 g_device):
+        self.f, self.g = f, g
+        self._err, self._dual, self._n = err_tab, dual_tab, n_rec
+        self.iterations, self.converged, self.eps = iterations, converged, eps
+        self.f_device, self.g_device = f_device, g_device
+        self._cache = {}
+
+    def __len__(self):
+        return len(self.iterations)
+
+    def _one(self, k):
+        if k not in self._cache:
+            nk = int(self._n[k])
+            self._cache[k] = SinkhornOutput(
+                f=self.f[k], g=self.g[k], errors=self._err[k, :nk].copy(),
+                dual_trace=self._dual[k, :nk].copy(), iterations=int(self.iterations[k]),
+                converged=bool(self.converged[k]), eps=float(self.eps[k]),
+                f_device=self.f_device[k], g_device=self.g_device[k])
+        return self._cache[k]
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self._one(i) for i in range(*k.indices(len(self)))]
+        k = int(k)
+        if k < 0:
+            k += len(self)
+        if not 0 <= k < len(self):
+            raise IndexError(k)
+        return self._one(k)
 
 
 @dataclasses.dataclass(frozen=True, eq=False)
@@ -170,7 +216,8 @@ def solve_sinkhorn(prob: LinearProblem, eps=None, *, threshold: float = 1e-3, ma
         return _solve_pointcloud(prob, sched, threshold, max_iters, inner_iters, g_init, impl,
                                  use_graphs)
     if isinstance(geom, DenseGeometry):
-        outs = _dense_loop(geom._c()[None], prob._weights(), [sched], threshold, max_iters,
+        C, CT = geom._c_ct()
+        outs = _dense_loop(C[None], CT[None], prob._weights(), [sched], threshold, max_iters,
                            inner_iters, g_init=g_init)
         return outs[0]
     raise TypeError(f"unsupported geometry {type(geom).__name__}")
@@ -244,15 +291,18 @@ def _solve_pointcloud(prob, sched, threshold, max_iters, inner_iters, g_init, im
 
 
 # ---------------------------------------------------------------- dense / batched
-def _dense_loop(C, weights, scheds, threshold, max_iters, inner_iters, g_init=None,
+def _dense_loop(C, CT, weights, scheds, threshold, max_iters, inner_iters, g_init=None,
                 raise_on_fail=True):
     """Lock-step Sinkhorn over B stored-cost problems C[B,n,m] (csrc/dense.cu kernels).
 
     Each problem follows the reference loop (sinkhorn.py:151-200) exactly:
     its own eps schedule target, check cadence, NaN / bad-potential handling
-    and convergence; converged problems are frozen (active mask).
+    and convergence; converged problems are frozen (active mask).  Both
+    half-steps stream their cost row-major: rows over C, columns over
+    CT = C^T[B,m,n] (built once), so each is one coalesced HBM pass.
     weights = (a, b, log a, log b) as float32 CUDA tensors of shape [B,n] / [B,m]
-    (or [n] / [m] when B == 1).
+    (or [n] / [m] when B == 1).  Per-problem bookkeeping at the checks is
+    vectorised (numpy on the B check records; device index copies to freeze).
     """
     import torch
     lib = N.lib()
@@ -285,8 +335,10 @@ def _dense_loop(C, weights, scheds, threshold, max_iters, inner_iters, g_init=No
     active = torch.ones(B, dtype=torch.int32, device=dev)
     host_active = np.ones(B, dtype=bool)
     chk = torch.zeros((B, 8), dtype=torch.float64, device=dev)
-    errors = [[] for _ in range(B)]
-    duals = [[] for _ in range(B)]
+    max_checks = max_iters // inner_iters + 2
+    err_tab = np.zeros((B, max_checks))
+    dual_tab = np.zeros((B, max_checks))
+    n_rec = np.zeros(B, dtype=int)
     iters = np.zeros(B, dtype=int)
     conv = np.zeros(B, dtype=bool)
 
@@ -296,10 +348,13 @@ def _dense_loop(C, weights, scheds, threshold, max_iters, inner_iters, g_init=No
     e0 = eps_vec(0)
     eps_d = dev_f32(e0)
     kap_d = dev_f32(_LOG2E / e0)
-    # initial bias of the column side: g * kappa (per problem)
-    for bb in range(B):
-        N.check(lib.otk_make_bias(N.ptr(g[bb]), m, float(np.float32(_LOG2E / e0[bb])),
-                                  N.ptr(bias_y[bb]), N.ptr(first_bad[bb:bb + 1]), 1, st))
+    # initial bias of the column side: g * kappa (per problem); zero for a cold start
+    if g_init is None:
+        bias_y.zero_()
+    else:
+        for bb in range(B):
+            N.check(lib.otk_make_bias(N.ptr(g[bb]), m, float(np.float32(_LOG2E / e0[bb])),
+                                      N.ptr(bias_y[bb]), N.ptr(first_bad[bb:bb + 1]), 1, st))
     f_ready = False
     cur_fac = factor(0)
 
@@ -309,9 +364,14 @@ def _dense_loop(C, weights, scheds, threshold, max_iters, inner_iters, g_init=No
                                   N.ptr(bias_x), N.ptr(first_bad), step, st), "dense rows")
 
     def cols(kap_next_d, step):
-        N.check(lib.otk_dense_lse(N.ptr(C), B, n, m, 1, N.ptr(bias_x), N.ptr(lb), N.OTK_FIN_SOLVER,
+        N.check(lib.otk_dense_lse(N.ptr(CT), B, m, n, 0, N.ptr(bias_x), N.ptr(lb), N.OTK_FIN_SOLVER,
                                   N.ptr(eps_d), N.ptr(kap_next_d), N.ptr(active), N.ptr(g),
                                   N.ptr(bias_y), N.ptr(first_bad), step, st), "dense cols")
+
+    def freeze(idx_np):
+        idx = torch.as_tensor(idx_np.astype(np.int64), device=dev)
+        f_fin.index_copy_(0, idx, f.index_select(0, idx))
+        g_fin.index_copy_(0, idx, g.index_select(0, idx))
 
     t = 0
     for t in range(1, max_iters + 1):
@@ -336,50 +396,44 @@ def _dense_loop(C, weights, scheds, threshold, max_iters, inner_iters, g_init=No
                                           N.ptr(chk), st), "check")
             out = chk.cpu().numpy()
             fb = first_bad.cpu().numpy()
-            e_now = eps_vec(t - 1)
-            done = []
-            for bb in np.nonzero(host_active)[0]:
-                iters[bb] = t
-                if fb[bb] <= 2 * t or (measure and fb[bb] == 2 * t + 1):
-                    if raise_on_fail:
-                        raise ValueError(f"problem {bb}: g contains NaN or +inf entries")
-                    done.append(bb)
-                    continue
-                if out[bb, 4] > 0 or out[bb, 5] > 0:
-                    if raise_on_fail:
-                        raise DivergedError("NaN in Sinkhorn potentials; eps is likely too small "
-                                            "for the cost scale", iteration=t)
-                    done.append(bb)
-                    continue
-                if not measure:
-                    continue
-                err = float(out[bb, 0])
-                errors[bb].append(err)
-                duals[bb].append(float(out[bb, 2] + out[bb, 3] - e_now[bb] * (out[bb, 1] - 1.0)))
-                if err <= threshold:
-                    conv[bb] = True
-                    done.append(bb)
-            for bb in done:
-                host_active[bb] = False
-                f_fin[bb].copy_(f[bb])
-                g_fin[bb].copy_(g[bb])
-            if done:
+            act = host_active.copy()
+            iters[act] = t
+            bad = act & ((fb <= 2 * t) | (measure & (fb == 2 * t + 1)))
+            nan = act & ~bad & ((out[:, 4] > 0) | (out[:, 5] > 0))
+            if raise_on_fail and bad.any():
+                raise ValueError(f"problem {int(np.argmax(bad))}: g contains NaN or +inf entries")
+            if raise_on_fail and nan.any():
+                raise DivergedError("NaN in Sinkhorn potentials; eps is likely too small "
+                                    "for the cost scale", iteration=t)
+            done = bad | nan
+            if measure:
+                rec = act & ~done
+                k = n_rec[rec]
+                err = out[rec, 0]
+                err_tab[rec, k] = err
+                dual_tab[rec, k] = out[rec, 2] + out[rec, 3] - eps_vec(t - 1)[rec] * (out[rec, 1] - 1.0)
+                n_rec[rec] += 1
+                hit = np.zeros(B, dtype=bool)
+                hit[rec] = err <= threshold
+                conv |= hit
+                done |= hit
+            if done.any():
+                host_active &= ~done
+                freeze(np.nonzero(done)[0])
                 active.copy_(torch.as_tensor(host_active.astype(np.int32), device=dev))
             if not host_active.any():
                 break
             if measure and t < max_iters:
                 f, fn = fn, f
                 f_ready = True
-    for bb in np.nonzero(host_active)[0]:
-        iters[bb] = min(t, max_iters)
-        f_fin[bb].copy_(f[bb])
-        g_fin[bb].copy_(g[bb])
+    rest = np.nonzero(host_active)[0]
+    if len(rest):
+        iters[rest] = min(t, max_iters)
+        freeze(rest)
     fh = f_fin.cpu().numpy().astype(np.float64)
     gh = g_fin.cpu().numpy().astype(np.float64)
-    return [SinkhornOutput(f=fh[bb], g=gh[bb], errors=np.asarray(errors[bb]),
-                           dual_trace=np.asarray(duals[bb]), iterations=int(iters[bb]),
-                           converged=bool(conv[bb]), eps=float(targets[bb]),
-                           f_device=f_fin[bb], g_device=g_fin[bb]) for bb in range(B)]
+    return BatchedSinkhornOutput(fh, gh, err_tab, dual_tab, n_rec, iters, conv, targets, f_fin,
+                                 g_fin)
 
 
 def solve_sinkhorn_batched(x, y, eps, a=None, b=None, *, threshold: float = 1e-3,
@@ -407,16 +461,23 @@ def solve_sinkhorn_batched(x, y, eps, a=None, b=None, *, threshold: float = 1e-3
     if not np.all(eps > 0):
         raise ValueError("eps must be positive")
     scheds = [EpsilonSchedule(float(e)) for e in eps]
-    for s in scheds:
-        _fp32_guard(s, inner_iters, max_iters)
-    aw = np.stack([_as_weights(None if a is None else a[k], n, "a") for k in range(B)])
-    bw = np.stack([_as_weights(None if b is None else b[k], m, "b") for k in range(B)])
-    with np.errstate(divide="ignore"):
-        weights = tuple(as_device_f32(v) for v in (aw, bw, np.log(aw), np.log(bw)))
-    C = torch.empty((B, n, m), dtype=torch.float32, device=xd.device)
-    N.check(N.lib().otk_dense_cost(N.ptr(xd), N.ptr(yd), B, n, m, d, 0, N.ptr(C), stream()),
-            "dense_cost")
-    outs = _dense_loop(C, weights, scheds, threshold, max_iters, inner_iters)
+    _fp32_guard(EpsilonSchedule(float(eps.min())), inner_iters, max_iters)
+    dev = xd.device
+
+    def weights_of(w, size, name):
+        if w is None:  # uniform: built on the device
+            u = torch.full((B, size), 1.0 / size, dtype=torch.float32, device=dev)
+            return np.full((B, size), 1.0 / size), u, torch.full_like(u, float(-np.log(size)))
+        ww = np.stack([_as_weights(w[k], size, name) for k in range(B)])
+        with np.errstate(divide="ignore"):
+            return ww, as_device_f32(ww), as_device_f32(np.log(ww))
+    aw, a_d, la_d = weights_of(a, n, "a")
+    bw, b_d, lb_d = weights_of(b, m, "b")
+    C = torch.empty((B, n, m), dtype=torch.float32, device=dev)
+    CT = torch.empty((B, m, n), dtype=torch.float32, device=dev)
+    N.check(N.lib().otk_dense_cost(N.ptr(xd), N.ptr(yd), B, n, m, d, 0, N.ptr(C), N.ptr(CT),
+                                   stream()), "dense_cost")
+    outs = _dense_loop(C, CT, (a_d, b_d, la_d, lb_d), scheds, threshold, max_iters, inner_iters)
     if not return_cost:
         return outs
     costs = _dense_costs(C, outs, aw, bw)
@@ -426,15 +487,14 @@ def solve_sinkhorn_batched(x, y, eps, a=None, b=None, *, threshold: float = 1e-3
 def _dense_costs(C, outs, aw, bw):
     import torch
     B, n, m = C.shape
-    f = torch.stack([o.f_device for o in outs]).contiguous()
-    g = torch.stack([o.g_device for o in outs]).contiguous()
-    eps = torch.tensor([o.eps for o in outs], dtype=torch.float32, device=C.device)
+    f, g = outs.f_device, outs.g_device
+    eps = torch.as_tensor(np.asarray(outs.eps, dtype=np.float32), device=C.device)
     res = torch.zeros((B, 2), dtype=torch.float64, device=C.device)
     N.check(N.lib().otk_dense_cost_reduce(N.ptr(C), B, n, m, N.ptr(f), N.ptr(g), N.ptr(eps),
                                           N.ptr(res), stream()), "dense_cost_reduce")
     r = res.cpu().numpy()
-    return [RegOTCost(float(r[k, 0]), _dual_objective(outs[k].f, outs[k].g, aw[k], bw[k],
-                                                      outs[k].eps, float(r[k, 1])))
+    return [RegOTCost(float(r[k, 0]), _dual_objective(outs.f[k], outs.g[k], aw[k], bw[k],
+                                                      float(outs.eps[k]), float(r[k, 1])))
             for k in range(B)]
 
 
