@@ -46,6 +46,7 @@ enum otk_status {
 #define OTK_CLAMP 0x2       /* clamp C >= 0 (geometry.py:273)                                      */
 #define OTK_IMPL_SIMT 0x10  /* force the FP32 FMA kernel                                           */
 #define OTK_IMPL_TC 0x20    /* force the tcgen05 split-fp16 kernel                                 */
+#define OTK_IMPL_NOPERSIST 0x40 /* otk_solve_pointcloud: never use the one-kernel small-problem solve */
 
 /* finalize modes */
 #define OTK_FIN_SOLVER 0 /* out = eps*logw - eps*ln2*L   (sinkhorn.py:173-174)                     */
@@ -225,7 +226,11 @@ size_t otk_solve_workspace_bytes(const otk_solve_args *args);
 int otk_bench_pipes(double *ex2_per_s, double *ffma_per_s, void *stream);
 
 /* Whole solve_sinkhorn (sinkhorn.py:122-200) on device.  Returns OTK_OK,
- * OTK_DIVERGED (fail_iter = t) or OTK_BAD_POTENTIAL (fail_iter = t). */
+ * OTK_DIVERGED (fail_iter = t) or OTK_BAD_POTENTIAL (fail_iter = t).
+ * Small FP32-path problems with a constant eps (both point sets fit in one
+ * SM's shared memory, d <= 7) run as ONE persistent cooperative kernel
+ * (grid-wide barriers between half-steps, fused check, launches = 1);
+ * everything else runs the general loop (CUDA graphs per check period). */
 int otk_solve_pointcloud(otk_solve_args *args);
 
 #ifdef __cplusplus

@@ -323,3 +323,40 @@ def test_reference_loop_drives_the_drop_in_geometry(otk):
         assert ours["iterations"] == ref["iterations"]
         assert rel_inf(ours["f"], ref["f"]) <= POT_TOL
         assert rel_inf(ours["g"], ref["g"]) <= POT_TOL
+
+
+@pytest.mark.parametrize("d,same,nonuniform", [(3, False, False), (1, False, True), (5, False, False),
+                                               (3, True, False), (7, False, True)])
+def test_persistent_small_solve_matches_general_loop_and_oracle(otk, d, same, nonuniform):
+    """The one-kernel small-problem solve (csrc/solve_small.cu) against the
+    general launch-per-half-step loop (OTK_IMPL_NOPERSIST) and the oracle:
+    same iterations / converged flag / check trace length, f and g within
+    the float32 tolerance, bitwise-reproducible reruns."""
+    from paper_2201_12324_b200 import _native as N
+    rng = np.random.default_rng(100 + d)
+    n, m = 700, (700 if same else 555)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    y = x if same else (rng.standard_normal((m, d)) + 0.4).astype(np.float32)
+    a = b = None
+    if nonuniform:
+        a = rng.uniform(0.5, 1.5, n)
+        a[7] = 0.0
+        a /= a.sum()
+        b = rng.uniform(0.5, 1.5, m)
+        b /= b.sum()
+    geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64))
+    eps = 0.05 * float(np.mean(geom64.cost_matrix()))
+    ref = oracle.sinkhorn(geom64, a, b, eps, threshold=1e-3, max_iters=500)
+
+    def run(flags):
+        g = otk.PointCloudGeometry(x, y)
+        g.impl_flags = flags
+        return otk.solve_sinkhorn(otk.LinearProblem(g, a, b), eps, threshold=1e-3, max_iters=500)
+    fast, fast2, gen = run(0), run(0), run(N.OTK_IMPL_NOPERSIST)
+    for out in (fast, gen):
+        assert out.iterations == ref["iterations"] and out.converged == ref["converged"]
+        assert len(out.errors) == len(ref["errors"])
+        assert rel_inf(out.f, ref["f"]) <= POT_TOL
+        assert rel_inf(out.g, ref["g"]) <= POT_TOL
+    assert np.array_equal(fast.f, fast2.f) and np.array_equal(fast.g, fast2.g)
+    np.testing.assert_allclose(fast.errors, gen.errors, rtol=1e-3, atol=1e-6)
