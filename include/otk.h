@@ -146,6 +146,14 @@ int otk_transport_matrix(const float *p, const float *p_sq, int64_t np,
                          int32_t d, const float *f, const float *g, double eps,
                          int32_t flags, float *plan, void *stream);
 
+/* Envelope gradient in the source points (sinkhorn.py:232-246), online, no
+ * n*m cap: grad[i*d+k] = 2 (r_i p_ik - sum_j P_ij q_jk), r_i = sum_j P_ij,
+ * P_ij = exp((f_i + g_j - C_ij)/eps).  FP32, [np, d] row-major output. */
+int otk_grad_points(const float *p, const float *p_sq, int64_t np, const float *q,
+                    const float *q_sq, int64_t nq, int32_t d, const float *f,
+                    const float *g, double eps, int32_t flags, float *grad,
+                    void *stream);
+
 /* ---------------- materialised / batched path (DenseGeometry) ---------------- */
 
 /* K4 -- C[b,i,j] = sum_k (x_bik - y_bjk)^2 (PointCloudGeometry.cost_matrix,

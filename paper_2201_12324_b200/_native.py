@@ -58,6 +58,7 @@ SIGNATURES = {
     "otk_cost_workspace_bytes": (SZ, [I64, I64]),
     "otk_cost_partial": (C.c_int, [P, P, I64, P, P, I64, I32, P, P, F64, I32, P, P, P]),
     "otk_transport_matrix": (C.c_int, [P, P, I64, P, P, I64, I32, P, P, F64, I32, P, P]),
+    "otk_grad_points": (C.c_int, [P, P, I64, P, P, I64, I32, P, P, F64, I32, P, P]),
     "otk_dense_cost": (C.c_int, [P, P, I64, I64, I64, I32, I32, P, P, P]),
     "otk_dense_transpose": (C.c_int, [P, I64, I64, I64, P, P]),
     "otk_dense_lse": (C.c_int, [P, I64, I64, I64, I32, P, P, I32, P, P, P, P, P, P, I32, P]),

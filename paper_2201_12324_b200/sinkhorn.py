@@ -28,7 +28,7 @@ from collections.abc import Sequence
 import numpy as np
 
 from . import _native as N
-from ._device import as_device_f32, device, is_torch, stream
+from ._device import as_device_f32, device, is_torch, stream, to_output
 from .errors import DivergedError
 from .geometry import DenseGeometry, EpsilonSchedule, Geometry, PointCloudGeometry
 
@@ -562,15 +562,27 @@ def grad_weights(out: SinkhornOutput, prob: LinearProblem) -> np.ndarray:
     return out.f - out.f.mean()
 
 
-def grad_points(out: SinkhornOutput, prob: LinearProblem) -> np.ndarray:
-    """Envelope gradient in x: 2(rowmass*x - P y) (sinkhorn.py:232-246), small problems."""
+def grad_points(out: SinkhornOutput, prob: LinearProblem):
+    """Envelope gradient in x: 2(rowmass*x - P y) (sinkhorn.py:232-246).
+
+    Computed online on the GPU (otk_grad_points): the plan is rebuilt tile by
+    tile and never stored, so unlike the reference (which materialises it
+    through transport_matrix) there is no n*m cap.  numpy in -> float64 numpy
+    out; CUDA tensors in -> float32 CUDA tensor out.
+    """
+    import torch
     if not out.converged:
         raise ValueError("grad_points requires a converged solution")
     geom = prob.geom
     if not isinstance(geom, PointCloudGeometry) or geom.cost_fn != "sqeucl":
         raise ValueError("grad_points requires a PointCloudGeometry with the sqeucl cost")
-    plan = transport_matrix(out, prob).matrix
-    x = np.asarray(geom.x.detach().cpu().numpy() if is_torch(geom.x) else geom.x, dtype=float)
-    y = np.asarray(geom.y.detach().cpu().numpy() if is_torch(geom.y) else geom.y, dtype=float)
-    row_mass = plan.sum(axis=1)
-    return 2.0 * (row_mass[:, None] * x - plan @ y)
+    cx, cy = geom._clouds()
+    n, m = geom.shape
+    f = as_device_f32(out.f_device if out.f_device is not None else out.f)
+    g = as_device_f32(out.g_device if out.g_device is not None else out.g)
+    grad = torch.empty((n, cx.d), dtype=torch.float32, device=cx.p.device)
+    N.check(N.lib().otk_grad_points(N.ptr(cx.p), N.ptr(cx.sq), n, N.ptr(cy.p), N.ptr(cy.sq), m,
+                                    cx.d, N.ptr(f), N.ptr(g), float(out.eps),
+                                    N.OTK_SAME_POINTS if geom._same_points else 0, N.ptr(grad),
+                                    stream()), "grad_points")
+    return to_output(grad, geom.x)

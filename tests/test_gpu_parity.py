@@ -360,3 +360,27 @@ def test_persistent_small_solve_matches_general_loop_and_oracle(otk, d, same, no
         assert rel_inf(out.g, ref["g"]) <= POT_TOL
     assert np.array_equal(fast.f, fast2.f) and np.array_equal(fast.g, fast2.g)
     np.testing.assert_allclose(fast.errors, gen.errors, rtol=1e-3, atol=1e-6)
+
+
+@pytest.mark.parametrize("d,n,m,same", [(3, 300, 257, False), (64, 200, 150, False),
+                                        (130, 100, 90, False), (3, 120, 120, True)])
+def test_grad_points_online_matches_reference_formula(otk, d, n, m, same):
+    """grad_points computed online on the GPU vs the
+    reference's materialised formula 2(r x - P y) (sinkhorn.py:244-246)
+    evaluated in float64 at the same potentials."""
+    rng = np.random.default_rng(d * 1000 + n)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    y = x if same else (rng.standard_normal((m, d)) * 1.2 + 0.3).astype(np.float32)
+    geom = otk.PointCloudGeometry(x, y)
+    prob = otk.LinearProblem(geom)
+    C = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64)).cost_matrix()
+    eps = 0.05 * float(C.mean())
+    out = otk.solve_sinkhorn(prob, eps, threshold=1e-4, max_iters=3000)
+    assert out.converged
+    got = otk.grad_points(out, prob)
+    plan = np.exp((out.f[:, None] + out.g[None, :] - C) / out.eps)
+    want = 2.0 * (plan.sum(axis=1)[:, None] * x.astype(np.float64) - plan @ y.astype(np.float64))
+    assert got.shape == want.shape and got.dtype == np.float64
+    assert np.max(np.abs(got - want)) <= 1e-4 * np.max(np.abs(want))
+    gw = otk.grad_weights(out, prob)
+    assert abs(gw.mean()) < 1e-9 and np.allclose(gw, out.f - out.f.mean())
