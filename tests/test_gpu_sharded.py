@@ -61,8 +61,11 @@ def test_world1_nccl_is_bitwise_the_single_gpu_solver(otk, nccl_world1, d, gen):
     from paper_2201_12324_b200.sharded import solve_sinkhorn_sharded
     kw = dict(n=640, m=512) if gen != "cfg2" else dict(n=640, m=512, d=d)
     wl = getattr(workloads, gen)(**kw)
-    single = otk.solve_sinkhorn(otk.LinearProblem(otk.PointCloudGeometry(wl.x, wl.y), wl.a, wl.b),
-                                wl.eps, threshold=wl.threshold, max_iters=60)
+    from paper_2201_12324_b200 import _native as N
+    geom = otk.PointCloudGeometry(wl.x, wl.y)
+    geom.impl_flags = N.OTK_IMPL_NOPERSIST  # the launch-per-half-step loop the shards run
+    single = otk.solve_sinkhorn(otk.LinearProblem(geom, wl.a, wl.b), wl.eps,
+                                threshold=wl.threshold, max_iters=60)
     sh = solve_sinkhorn_sharded(wl.x, wl.y, wl.eps, wl.a, wl.b, threshold=wl.threshold,
                                 max_iters=60)
     assert sh.iterations == single.iterations and sh.converged == single.converged
