@@ -437,11 +437,13 @@ def _dense_loop(C, CT, weights, scheds, threshold, max_iters, inner_iters, g_ini
 
 
 def solve_sinkhorn_batched(x, y, eps, a=None, b=None, *, threshold: float = 1e-3,
-                           max_iters: int = 2000, inner_iters: int = 10, return_cost: bool = False):
+                           max_iters: int = 2000, inner_iters: int = 10, return_cost: bool = False,
+                           g_init=None):
     """Solve B independent point-cloud problems with a materialised cost (cfg3).
 
     x: [B,n,d], y: [B,m,d] (numpy or CUDA tensors); eps: scalar or [B];
-    a: [B,n] / b: [B,m] or None (uniform).  Builds C[B,n,m] on the GPU
+    a: [B,n] / b: [B,m] or None (uniform); g_init: [B,m] warm start (the
+    reference's inner-solve use, quadratic.py:169-177).  Builds C[B,n,m] on the GPU
     (otk_dense_cost), then runs the lock-step dense loop.  Returns a list of
     SinkhornOutput (and the RegOTCost list when ``return_cost``).
     """
@@ -477,7 +479,8 @@ def solve_sinkhorn_batched(x, y, eps, a=None, b=None, *, threshold: float = 1e-3
     CT = torch.empty((B, m, n), dtype=torch.float32, device=dev)
     N.check(N.lib().otk_dense_cost(N.ptr(xd), N.ptr(yd), B, n, m, d, 0, N.ptr(C), N.ptr(CT),
                                    stream()), "dense_cost")
-    outs = _dense_loop(C, CT, (a_d, b_d, la_d, lb_d), scheds, threshold, max_iters, inner_iters)
+    outs = _dense_loop(C, CT, (a_d, b_d, la_d, lb_d), scheds, threshold, max_iters, inner_iters,
+                       g_init=g_init)
     if not return_cost:
         return outs
     costs = _dense_costs(C, outs, aw, bw)

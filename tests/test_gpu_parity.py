@@ -384,3 +384,43 @@ def test_grad_points_online_matches_reference_formula(otk, d, n, m, same):
     assert np.max(np.abs(got - want)) <= 1e-4 * np.max(np.abs(want))
     gw = otk.grad_weights(out, prob)
     assert abs(gw.mean()) < 1e-9 and np.allclose(gw, out.f - out.f.mean())
+
+
+@pytest.mark.parametrize("path", ["small", "general", "tc", "dense", "batched"])
+def test_warm_start_and_annealing_match_oracle(otk, path):
+    """g_init warm starts and eps annealing (the inner
+    solves of GW / low-rank / GMM, quadratic.py:169-177) on every device path
+    against the oracle loop with the same g_init / schedule."""
+    from paper_2201_12324_b200 import _native as N
+    rng = np.random.default_rng(31)
+    d = 64 if path == "tc" else 3
+    n, m = 260, 230
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    y = (rng.standard_normal((m, d)) + 0.3).astype(np.float32)
+    geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64))
+    C = geom64.cost_matrix()
+    eps = 0.05 * float(C.mean())
+    g0 = (rng.standard_normal(m) * eps).astype(np.float32).astype(np.float64)
+    anneal = path in ("general", "dense")
+    sched = otk.EpsilonSchedule(eps, init_scale=20.0, decay=0.6) if anneal else eps
+    osched = oracle.EpsilonScheduleOracle(eps, 20.0, 0.6) if anneal else eps
+    if path in ("dense", "batched"):
+        ref = oracle.sinkhorn(oracle.DenseOracle(C.astype(np.float32).astype(np.float64)), None,
+                              None, osched, threshold=1e-4, max_iters=400, g_init=g0)
+    else:
+        ref = oracle.sinkhorn(geom64, None, None, osched, threshold=1e-4, max_iters=400, g_init=g0)
+    if path == "batched":
+        outs = otk.solve_sinkhorn_batched(x[None], y[None], eps, threshold=1e-4, max_iters=400,
+                                          g_init=g0[None])
+        out = outs[0]
+    elif path == "dense":
+        out = otk.solve_sinkhorn(otk.LinearProblem(otk.DenseGeometry(C)), sched, threshold=1e-4,
+                                 max_iters=400, g_init=g0)
+    else:
+        geom = otk.PointCloudGeometry(x, y)
+        geom.impl_flags = {"small": 0, "general": N.OTK_IMPL_NOPERSIST, "tc": 0}[path]
+        out = otk.solve_sinkhorn(otk.LinearProblem(geom), sched, threshold=1e-4, max_iters=400,
+                                 g_init=g0)
+    assert out.iterations == ref["iterations"] and out.converged == ref["converged"]
+    assert rel_inf(out.f, ref["f"]) <= POT_TOL
+    assert rel_inf(out.g, ref["g"]) <= POT_TOL
