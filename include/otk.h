@@ -102,6 +102,10 @@ int otk_lse_partial(const float *p, const float *p_sq, const uint16_t *p_hi,
                     float kappa, int32_t flags, int32_t nsplit, float *partial,
                     void *stream);
 
+/* 1 if otk_lse_partial runs the tcgen05 kernel for this d / flags (the caller
+ * must then pass the split + norm planes), 0 for the FP32 FMA kernel. */
+int otk_lse_uses_tc(int32_t d, int32_t flags);
+
 /* Suggested split count for otk_lse_partial on this device. */
 int otk_lse_suggest_nsplit(int64_t np, int64_t nq, int32_t d, int32_t flags);
 

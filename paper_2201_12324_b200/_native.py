@@ -52,6 +52,7 @@ SIGNATURES = {
     "otk_lse_partial": (C.c_int, [P, P, P, P, P, I64, P, P, P, P, P, I64, I32, I32, F32, P, F32,
                                   I32, I32, P, P]),
     "otk_lse_suggest_nsplit": (C.c_int, [I64, I64, I32, I32]),
+    "otk_lse_uses_tc": (C.c_int, [I32, I32]),
     "otk_lse_finalize": (C.c_int, [P, I32, I64, P, I32, F32, F32, P, P, P, I32, P]),
     "otk_check_workspace_bytes": (SZ, []),
     "otk_check": (C.c_int, [P, P, P, I64, P, P, I64, F64, P, P, P]),

@@ -3,7 +3,7 @@
 // streaming log2-sum-exp2 epilogue read straight out of TMEM.
 //
 // Replaces PointCloudGeometry.apply_lse_kernel (reference geometry.py:336-354)
-// for d >= 32.  Contract (include/otk.h, otk_lse_partial):
+// for d >= 4 (solve.cu: want_tc).  Contract (include/otk.h, otk_lse_partial):
 //     partial_i = log2 sum_j 2^(kappa*g_j - kappa*C_ij),  C_ij = |p_i|^2+|q_j|^2-2<p_i,q_j>
 // The dot products run on the tensor cores in split-fp16 ("3xFP16"): every
 // fp32 coordinate is pre-split (K0, otk_prep_points) into hi = fp16(s*x),
@@ -237,6 +237,7 @@ struct Params {
   int row_tiles, ntiles, tps, nsplit, num_units;
   float c2k;              // 2*kappa/s^2
   float *partial;         // [nsplit][np]
+  int same;               // x is y: exact-zero diagonal, u_ii = kappa*g_i (geometry.py:278-292)
   int probe;              // pipeline probe (OTK_TC_PROBE, timing experiments only):
                           // 1 = epilogue skips the math, 2 = sums without exp,
                           // 3 = no B operand loads, 4 = one product per K step
@@ -294,7 +295,7 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 // seen yet) takes the max path, which reproduces the empty-slice -inf result.
 template <int CH, bool MASK, int EP>
 __device__ __forceinline__ void lse_chunk(const float *acc, const float *bias, float c2k, int valid,
-                                          float &m, float &s) {
+                                          int diag, float &m, float &s) {
   float2 u[CH / 2];
   const float2 k2 = make_float2(c2k, c2k);
 #pragma unroll
@@ -304,6 +305,13 @@ __device__ __forceinline__ void lse_chunk(const float *acc, const float *bias, f
     if (MASK) {
       if (2 * i >= valid) u[i].x = -INFINITY;
       if (2 * i + 1 >= valid) u[i].y = -INFINITY;
+    }
+  }
+  if (diag >= 0) {  // same point set: this row's own column has C == 0 exactly
+#pragma unroll
+    for (int i = 0; i < CH / 2; ++i) {
+      if (2 * i == diag) u[i].x = bias[2 * i];
+      if (2 * i + 1 == diag) u[i].y = bias[2 * i + 1];
     }
   }
   auto chunk_sum = [&](float shift) {
@@ -627,10 +635,17 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
             for (int i = 0; i < C::CH; ++i) s += fmaf(accv[i], c2k, bv[i]);
           } else if (prm.probe == 5) {
             lse_chunk_fixed<C::CH>(accv, bv, c2k, m, s);
-          } else if (valid >= BN)
-            lse_chunk<C::CH, false, EP>(accv, bv, c2k, 0, m, s);
-          else
-            lse_chunk<C::CH, true, EP>(accv, bv, c2k, valid - c * C::CH, m, s);
+          } else {
+            int diag = -1;
+            if (prm.same) {
+              const int64_t jc = j0 + (int64_t)c * C::CH, row = (int64_t)rt * BM + row_local;
+              if (row >= jc && row < jc + C::CH) diag = (int)(row - jc);
+            }
+            if (valid >= BN)
+              lse_chunk<C::CH, false, EP>(accv, bv, c2k, 0, diag, m, s);
+            else
+              lse_chunk<C::CH, true, EP>(accv, bv, c2k, valid - c * C::CH, diag, m, s);
+          }
         };
         issue(cfirst, va);
         wait(va);
@@ -822,7 +837,7 @@ int tc_tile_cols(int dpad) { return tc::variant_for(dpad / tc::BK) == 1 ? 256 : 
 
 int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
                   const uint16_t *q_hi, const uint16_t *q_lo, const uint16_t *q_ext, int64_t nq,
-                  int dpad, float two_kappa_scaled, const float *q_bias, int nsplit,
+                  int dpad, float two_kappa_scaled, const float *q_bias, int nsplit, int same,
                   float *partial, cudaStream_t st) {
   using namespace tc;
   if (np > (int64_t)INT32_MAX || nq > (int64_t)INT32_MAX) {
@@ -856,6 +871,7 @@ int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_
   prm.num_units = prm.row_tiles * nsplit;
   prm.c2k = two_kappa_scaled;
   prm.partial = partial;
+  prm.same = same;
   prm.probe = getenv("OTK_TC_PROBE") ? atoi(getenv("OTK_TC_PROBE")) : 0;
   if (v == 1) {
     if (kb == 1) return launch_variant<1, true, 2, 2>(maps, prm, st);

@@ -29,7 +29,7 @@ int lse_simt_launch(const float *p, const float *p_sq, int64_t np, const float *
                     int flags, int nsplit, float *partial, cudaStream_t st);
 int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
                   const uint16_t *q_hi, const uint16_t *q_lo, const uint16_t *q_ext, int64_t nq,
-                  int dpad, float two_kappa_scaled, const float *q_bias, int nsplit,
+                  int dpad, float two_kappa_scaled, const float *q_bias, int nsplit, int same,
                   float *partial, cudaStream_t st);
 bool tc_available();
 int tc_tile_cols(int dpad);
@@ -54,11 +54,17 @@ int small_solve_launch(const small::Args &A, bool same, cudaStream_t st);
 
 using namespace otk;
 
+// tcgen05 kernel for every d >= 4 (measured on B200 at n = m = 65536: 1.70 ms
+// per half-step for any d <= 64, vs 3.3 / 4.4 / 6.4 / 12.4 ms for the FP32
+// kernel at d = 2-3 / 8 / 16 / 31); FP32 FMA kernel for d <= 3.
+constexpr int kTcMinDim = 4;
 static bool want_tc(int flags, int d) {
   if (flags & OTK_IMPL_SIMT) return false;
   if (flags & OTK_IMPL_TC) return true;
-  return tc_available() && d >= 32;
+  return tc_available() && d >= kTcMinDim;
 }
+
+extern "C" int otk_lse_uses_tc(int32_t d, int32_t flags) { return want_tc(flags, d) ? 1 : 0; }
 
 extern "C" int otk_lse_suggest_nsplit(int64_t np, int64_t nq, int32_t d, int32_t flags) {
   const int sms = num_sms();
@@ -93,7 +99,8 @@ extern "C" int otk_lse_partial(const float *p, const float *p_sq, const uint16_t
       return OTK_ENOTSUP;
     }
     return lse_tc_launch(p_hi, p_lo, p_ext, np, q_hi, q_lo, q_ext, nq, dpad,
-                         2.f * kappa * split_inv, q_bias, nsplit, partial, as_stream(stream));
+                         2.f * kappa * split_inv, q_bias, nsplit, (flags & OTK_SAME_POINTS) ? 1 : 0,
+                         partial, as_stream(stream));
   }
   OTK_CHECK_ARG(p && q && p_sq && q_sq, "otk_lse_partial: FP32 path needs points and squared norms");
   return lse_simt_launch(p, p_sq, np, q, q_sq, nq, d, q_bias, kappa, flags, nsplit, partial,
@@ -131,15 +138,16 @@ struct Layout {
 
 // Whole-solve persistent kernel (solve_small.cu): FP32 path, constant eps,
 // points resident in shared memory.  OTK_IMPL_NOPERSIST forces the general loop.
-static bool use_small(const otk_solve_args *A, bool tc) {
-  if (tc || (A->flags & OTK_IMPL_NOPERSIST)) return false;
+static bool use_small(const otk_solve_args *A) {
+  if (A->flags & (OTK_IMPL_TC | OTK_IMPL_NOPERSIST)) return false;
   if (!(A->eps_init_scale <= 1.0)) return false;  // eps_t == target for every t
   return small_solve_fits(A->n, A->m, A->d);
 }
 
 Layout plan(const otk_solve_args *A, void *ws) {
   Layout L{};
-  L.tc = want_tc(A->flags, A->d);
+  L.small = use_small(A);
+  L.tc = !L.small && want_tc(A->flags, A->d);
   L.dpad = (A->d + 63) / 64 * 64;
   L.nsr = otk_lse_suggest_nsplit(A->n, A->m, A->d, A->flags);
   L.nsc = otk_lse_suggest_nsplit(A->m, A->n, A->d, A->flags);
@@ -168,7 +176,6 @@ Layout plan(const otk_solve_args *A, void *ws) {
   L.chk = c.take<double>(8);
   L.chk_ws = c.take<char>(otk_check_workspace_bytes());
   L.first_bad = c.take<int>(1);
-  L.small = use_small(A, L.tc);
   if (L.small) {
     L.slots = c.take<double>((size_t)num_sms() * 8);
     L.d_errors = c.take<double>(A->max_checks);

@@ -221,7 +221,7 @@ class PointCloudGeometry(Geometry):
             device()
             cx = _Cloud(self.x)
             cy = cx if self._same_points else _Cloud(self.y)
-            planes = cx.d >= 32
+            planes = bool(N.lib().otk_lse_uses_tc(cx.d, self.impl_flags))
             scale = 1.0
             if planes:
                 amax = max(cx.absmax(), cy.absmax())

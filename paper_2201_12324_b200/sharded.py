@@ -165,7 +165,7 @@ class CudaShardEngine:
             raise ValueError("x and y must have the same dimension")
         self.n, self.m, self.d = self.cx.n, self.cy.n, self.cx.d
         lib = N.lib()
-        planes = (flags & N.OTK_IMPL_SIMT) == 0 and bool(self.d >= 32 or flags & N.OTK_IMPL_TC)
+        planes = bool(lib.otk_lse_uses_tc(self.d, flags))
         scale = 1.0
         if planes:
             amax = max(self.cx.absmax(), self.cy.absmax())

@@ -22,9 +22,13 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--n", type=int)
+    ap.add_argument("--m", type=int)
+    ap.add_argument("--d", type=int)
     args = ap.parse_args()
     torch.cuda.set_device(0)
-    wl = workloads.make(args.config)
+    kw = {k: getattr(args, k) for k in ("n", "m", "d") if getattr(args, k) is not None}
+    wl = workloads.make(args.config, **kw)
     geom = otk.PointCloudGeometry(torch.from_numpy(wl.x).cuda(), torch.from_numpy(wl.y).cuda())
     if args.kernel == "simt":
         geom.impl_flags = N.OTK_IMPL_SIMT
