@@ -15,6 +15,8 @@
 // CTA streams a contiguous column range (split) of Q through shared memory
 // and keeps a per-row online (max, sum) in registers; the 16 threads sharing
 // a row merge with shuffles in a fixed order (deterministic).
+#include <cstdlib>
+
 #include "otk_common.cuh"
 
 namespace otk {
@@ -129,6 +131,129 @@ __global__ void __launch_bounds__(SB_T) lse_simt_kernel(
     }
     int64_t row = row0 + ty * 4 + r;
     if (tx == 0 && row < np) partial[(int64_t)split * np + row] = st[r].value() - cp[r];
+  }
+}
+
+// ---------------------------------------------------------------- K1 low-d
+// Low-dimension variant (d <= 7): every point is one / two float4
+// (coordinates, |q|^2 in slot d), staged into shared memory a chunk of
+// columns at a time.  A warp owns LD_R = 4 rows whose query vectors
+// p' = (2 kappa p, -kappa, 0..) live in registers, so one dot product gives
+// 2 kappa <p,q> - kappa |q|^2; rows are paired so the dot products run as
+// packed FFMA2 (two rows per instruction).  Lanes stride the chunk's columns
+// with a per-row online log2-sum-exp2 and merge with a fixed butterfly.
+constexpr int LD_T = 256, LD_WARPS = LD_T / 32, LD_R = 4, LD_CH = 512, LD_CB = 4;
+
+template <int NV, bool CLAMP, bool SAME>
+__global__ void __launch_bounds__(LD_T) lse_lowd_kernel(
+    const float *__restrict__ P, const float *__restrict__ psq, int64_t np,
+    const float *__restrict__ Q, const float *__restrict__ qsq, int64_t nq, int d,
+    const float *__restrict__ qbias, float kappa, int64_t cols_per_split,
+    float *__restrict__ partial) {
+  __shared__ float4 qs[LD_CH * NV];
+  __shared__ float bs[LD_CH];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row0 = ((int64_t)blockIdx.x * LD_WARPS + warp) * LD_R;
+  const int split = blockIdx.y;
+  const int64_t c_begin = (int64_t)split * cols_per_split;
+  const int64_t c_end = min(nq, c_begin + cols_per_split);
+  const float two_k = 2.f * kappa;
+  // query vectors, two rows per float2 (rows 2t and 2t+1)
+  float2 pv[LD_R / 2][4 * NV];
+  float cp[LD_R], mx[LD_R], sm[LD_R];
+#pragma unroll
+  for (int r = 0; r < LD_R; ++r) {
+    const int64_t i = min(row0 + r, np - 1);
+    cp[r] = kappa * psq[i];
+    mx[r] = -INFINITY;
+    sm[r] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4 * NV; ++k) {
+      const float v = (k < d) ? two_k * P[i * d + k] : (k == d ? -kappa : 0.f);
+      if (r & 1) pv[r / 2][k].y = v; else pv[r / 2][k].x = v;
+    }
+  }
+  for (int64_t j0 = c_begin; j0 < c_end; j0 += LD_CH) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < LD_CH; idx += LD_T) {
+      const int64_t j = j0 + idx;
+      float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      float b = -INFINITY;
+      if (j < c_end) {
+        for (int k = 0; k < d; ++k) v[k] = Q[j * d + k];
+        v[d] = qsq[j];
+        b = qbias[j];
+      }
+      qs[idx * NV] = make_float4(v[0], v[1], v[2], v[3]);
+      if (NV == 2) qs[idx * NV + 1] = make_float4(v[4], v[5], v[6], v[7]);
+      bs[idx] = b;
+    }
+    __syncthreads();
+    const int nvalid = (int)min((int64_t)LD_CH, c_end - j0);
+    for (int c0 = lane; c0 < nvalid; c0 += 32 * LD_CB) {
+      float u[LD_CB][LD_R];
+#pragma unroll
+      for (int cb = 0; cb < LD_CB; ++cb) {
+        const int c = c0 + 32 * cb;
+        const int cc = min(c, LD_CH - 1);
+        const float b = (c < nvalid) ? bs[cc] : -INFINITY;
+        float qv[4 * NV];
+        const float4 q0 = qs[cc * NV];
+        qv[0] = q0.x; qv[1] = q0.y; qv[2] = q0.z; qv[3] = q0.w;
+        if (NV == 2) {
+          const float4 q1 = qs[cc * NV + 1];
+          qv[4] = q1.x; qv[5] = q1.y; qv[6] = q1.z; qv[7] = q1.w;
+        }
+#pragma unroll
+        for (int t = 0; t < LD_R / 2; ++t) {
+          float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int k = 0; k < 4 * NV; ++k)
+            if (k <= d || k < 4) acc = __ffma2_rn(pv[t][k], make_float2(qv[k], qv[k]), acc);
+          float v0 = acc.x, v1 = acc.y;
+          if (CLAMP) {
+            v0 = fminf(v0, cp[2 * t]);
+            v1 = fminf(v1, cp[2 * t + 1]);
+          }
+          if (SAME) {
+            const int64_t j = j0 + c;
+            if (j == row0 + 2 * t) v0 = cp[2 * t];
+            if (j == row0 + 2 * t + 1) v1 = cp[2 * t + 1];
+          }
+          u[cb][2 * t] = v0 + b;
+          u[cb][2 * t + 1] = v1 + b;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < LD_R; ++r) {
+        float cm = -INFINITY;
+#pragma unroll
+        for (int cb = 0; cb < LD_CB; ++cb) cm = fmaxf(cm, u[cb][r]);
+        if (cm > mx[r] + 8.f) {
+          sm[r] *= ex2(mx[r] - cm);
+          mx[r] = cm;
+        }
+        const float ms = (mx[r] == -INFINITY) ? 0.f : mx[r];
+        float acc = 0.f;
+#pragma unroll
+        for (int cb = 0; cb < LD_CB; ++cb) acc += ex2(u[cb][r] - ms);
+        sm[r] += acc;
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < LD_R; ++r) {
+    Lse2 st;
+    st.m = mx[r];
+    st.s = sm[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, st.m, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, st.s, o);
+      st.merge(m2, s2);
+    }
+    const int64_t i = row0 + r;
+    if (lane == 0 && i < np) partial[(int64_t)split * np + i] = st.value() - cp[r];
   }
 }
 
@@ -290,8 +415,27 @@ int lse_simt_launch(const float *p, const float *p_sq, int64_t np, const float *
                     int flags, int nsplit, float *partial, cudaStream_t st) {
   int64_t cps = (nq + nsplit - 1) / nsplit;
   cps = (cps + SB_N - 1) / SB_N * SB_N;
-  dim3 grid((unsigned)((np + SB_M - 1) / SB_M), (unsigned)nsplit);
   const bool clamp = flags & OTK_CLAMP, same = flags & OTK_SAME_POINTS;
+  if (d <= 7 && !getenv("OTK_SIMT_TILED")) {
+    dim3 g2((unsigned)((np + LD_WARPS * LD_R - 1) / (LD_WARPS * LD_R)), (unsigned)nsplit);
+#define OTK_LOWD_CASE(NV, CL, SA)                                                         \
+    if ((d <= 3) == (NV == 1) && clamp == CL && same == SA) {                             \
+      lse_lowd_kernel<NV, CL, SA><<<g2, LD_T, 0, st>>>(p, p_sq, np, q, q_sq, nq, d, q_bias, \
+                                                       kappa, cps, partial);              \
+      cudaError_t e = cudaGetLastError();                                                 \
+      return e == cudaSuccess ? OTK_OK : cuda_status(e, "lse_lowd_kernel");               \
+    }
+    OTK_LOWD_CASE(1, false, false)
+    OTK_LOWD_CASE(1, true, false)
+    OTK_LOWD_CASE(1, true, true)
+    OTK_LOWD_CASE(2, false, false)
+    OTK_LOWD_CASE(2, true, false)
+    OTK_LOWD_CASE(2, true, true)
+#undef OTK_LOWD_CASE
+    set_error("lse_simt: OTK_SAME_POINTS requires OTK_CLAMP");
+    return OTK_EINVAL;
+  }
+  dim3 grid((unsigned)((np + SB_M - 1) / SB_M), (unsigned)nsplit);
   const int kc = pick_kc(d);
 #define OTK_SIMT_CASE(KC, CL, SA)                                                          \
   if (kc == KC && clamp == CL && same == SA) {                                             \
