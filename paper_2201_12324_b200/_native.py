@@ -11,7 +11,9 @@ import os
 
 from . import errors
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libotk_sm100.so")
+# OTK_LIB: an alternative build of the same ABI (A/B timing of kernel revisions)
+_LIB_PATH = os.environ.get("OTK_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libotk_sm100.so")
 _lib = None
 
 OTK_OK, OTK_EINVAL, OTK_ECUDA, OTK_ENOTSUP, OTK_ENCCL = 0, -1, -2, -3, -4
