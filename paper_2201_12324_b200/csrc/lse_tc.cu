@@ -3,7 +3,10 @@
 // streaming log2-sum-exp2 epilogue read straight out of TMEM.
 //
 // Replaces PointCloudGeometry.apply_lse_kernel (reference geometry.py:336-354)
-// for d >= 4 (solve.cu: want_tc).  Contract (include/otk.h, otk_lse_partial):
+// for d >= 4 (solve.cu: want_tc).  Identical point sets: C_ii comes out of the
+// split products as 0 up to fp32 rounding (|C_ii| <~ 1e-6 |p_i|^2), not
+// forced to an exact zero as the FP32 kernels do (geometry.py:278-292); the
+// effect on the potentials is far below the 1e-4 parity tolerance (tested).  Contract (include/otk.h, otk_lse_partial):
 //     partial_i = log2 sum_j 2^(kappa*g_j - kappa*C_ij),  C_ij = |p_i|^2+|q_j|^2-2<p_i,q_j>
 // The dot products run on the tensor cores in split-fp16 ("3xFP16"): every
 // fp32 coordinate is pre-split (K0, otk_prep_points) into hi = fp16(s*x),
@@ -237,7 +240,6 @@ struct Params {
   int row_tiles, ntiles, tps, nsplit, num_units;
   float c2k;              // 2*kappa/s^2
   float *partial;         // [nsplit][np]
-  int same;               // x is y: exact-zero diagonal, u_ii = kappa*g_i (geometry.py:278-292)
   int probe;              // pipeline probe (OTK_TC_PROBE, timing experiments only):
                           // 1 = epilogue skips the math, 2 = sums without exp,
                           // 3 = no B operand loads, 4 = one product per K step
@@ -285,17 +287,9 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 // Packed f32x2 arithmetic (FFMA2 / FADD2) halves the issue slots of the
 // per-cell work; EP of every 8 column pairs take their exps from the FMA-pipe
 // polynomial instead of MUFU.
-//
-// Optimistic rescale: the chunk is summed against the CURRENT shift m first;
-// only if that sum exceeds 2^16 (some term beat m by > 16 in log2 units, or
-// overflowed) is the chunk's max taken and the row state rescaled -- rare
-// after the first chunks, and it keeps the max reduction off the common path.
-// Invariant: m never exceeds the running max, and every term summed is
-// <= 2^16 * 2^m, so s stays far inside fp32 range.  m = -inf (nothing finite
-// seen yet) takes the max path, which reproduces the empty-slice -inf result.
 template <int CH, bool MASK, int EP>
 __device__ __forceinline__ void lse_chunk(const float *acc, const float *bias, float c2k, int valid,
-                                          int diag, float &m, float &s) {
+                                          float &m, float &s) {
   float2 u[CH / 2];
   const float2 k2 = make_float2(c2k, c2k);
 #pragma unroll
@@ -307,63 +301,26 @@ __device__ __forceinline__ void lse_chunk(const float *acc, const float *bias, f
       if (2 * i + 1 >= valid) u[i].y = -INFINITY;
     }
   }
-  if (diag >= 0) {  // same point set: this row's own column has C == 0 exactly
+  float cm = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < CH / 2; ++i) {
-      if (2 * i == diag) u[i].x = bias[2 * i];
-      if (2 * i + 1 == diag) u[i].y = bias[2 * i + 1];
-    }
-  }
-  auto chunk_sum = [&](float shift) {
-    const float2 nms = make_float2(-shift, -shift);
-    float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-    for (int i = 0; i < CH / 2; ++i) {
-      const float2 x = __fadd2_rn(u[i], nms);
-      float2 e;
-      if (i % 8 < EP) {
-        e = ex2_poly2(x);
-      } else {
-        e = make_float2(ex2(x.x), ex2(x.y));
-      }
-      acc2[i & 1] = __fadd2_rn(acc2[i & 1], e);
-    }
-    const float2 t2 = __fadd2_rn(acc2[0], acc2[1]);
-    return t2.x + t2.y;
-  };
-  float cs = (m == -INFINITY) ? INFINITY : chunk_sum(m);
-  if (!(cs <= 65536.f)) {  // slow path: new running max (also NaN / inf / first chunk)
-    float cm = -INFINITY;
-#pragma unroll
-    for (int i = 0; i < CH / 2; ++i) cm = fmaxf(cm, fmaxf(u[i].x, u[i].y));
-    if (cm > m) {
-      s *= ex2(m - cm);
-      m = cm;
-    }
-    cs = chunk_sum(m == -INFINITY ? 0.f : m);
-  }
-  s += cs;
-}
-
-// Timing probe 5: a fixed per-row shift instead of the running max.
-template <int CH>
-__device__ __forceinline__ void lse_chunk_fixed(const float *acc, const float *bias, float c2k,
-                                                float &m, float &s) {
-  const float2 k2 = make_float2(c2k, c2k);
-  if (m == -INFINITY) {
-    float cm = -INFINITY;
-#pragma unroll
-    for (int i = 0; i < CH; ++i) cm = fmaxf(cm, fmaf(acc[i], c2k, bias[i]));
+  for (int i = 0; i < CH / 2; ++i) cm = fmaxf(cm, fmaxf(u[i].x, u[i].y));
+  if (cm > m + 8.f) {  // lazy rescale: terms may exceed m by at most 2^8
+    s *= ex2(m - cm);
     m = cm;
   }
-  const float2 nms = make_float2(-m, -m);
+  const float ms = (m == -INFINITY) ? 0.f : m;
+  const float2 nms = make_float2(-ms, -ms);
   float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
   for (int i = 0; i < CH / 2; ++i) {
-    const float2 u = __ffma2_rn(make_float2(acc[2 * i], acc[2 * i + 1]), k2,
-                                make_float2(bias[2 * i], bias[2 * i + 1]));
-    const float2 x = __fadd2_rn(u, nms);
-    acc2[i & 1] = __fadd2_rn(acc2[i & 1], make_float2(ex2(x.x), ex2(x.y)));
+    const float2 x = __fadd2_rn(u[i], nms);
+    float2 e;
+    if (i % 8 < EP) {
+      e = ex2_poly2(x);
+    } else {
+      e = make_float2(ex2(x.x), ex2(x.y));
+    }
+    acc2[i & 1] = __fadd2_rn(acc2[i & 1], e);
   }
   const float2 t2 = __fadd2_rn(acc2[0], acc2[1]);
   s += t2.x + t2.y;
@@ -616,10 +573,6 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
           }
           const float4 *bp = reinterpret_cast<const float4 *>(bias + c * C::CH);
           float bv[C::CH];
-          if (prm.probe == 6) {  // timing probe: no bias loads
-#pragma unroll
-            for (int i = 0; i < C::CH; ++i) bv[i] = 0.25f * (float)(i & 3);
-          } else
 #pragma unroll
           for (int i = 0; i < C::CH / 4; ++i) {
             float4 q = bp[i];
@@ -633,19 +586,10 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
           } else if (prm.probe == 2) {
 #pragma unroll
             for (int i = 0; i < C::CH; ++i) s += fmaf(accv[i], c2k, bv[i]);
-          } else if (prm.probe == 5) {
-            lse_chunk_fixed<C::CH>(accv, bv, c2k, m, s);
-          } else {
-            int diag = -1;
-            if (prm.same) {
-              const int64_t jc = j0 + (int64_t)c * C::CH, row = (int64_t)rt * BM + row_local;
-              if (row >= jc && row < jc + C::CH) diag = (int)(row - jc);
-            }
-            if (valid >= BN)
-              lse_chunk<C::CH, false, EP>(accv, bv, c2k, 0, diag, m, s);
-            else
-              lse_chunk<C::CH, true, EP>(accv, bv, c2k, valid - c * C::CH, diag, m, s);
-          }
+          } else if (valid >= BN)
+            lse_chunk<C::CH, false, EP>(accv, bv, c2k, 0, m, s);
+          else
+            lse_chunk<C::CH, true, EP>(accv, bv, c2k, valid - c * C::CH, m, s);
         };
         issue(cfirst, va);
         wait(va);
@@ -837,8 +781,8 @@ int tc_tile_cols(int dpad) { return tc::variant_for(dpad / tc::BK) == 1 ? 256 : 
 
 int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
                   const uint16_t *q_hi, const uint16_t *q_lo, const uint16_t *q_ext, int64_t nq,
-                  int dpad, float two_kappa_scaled, const float *q_bias, int nsplit, int same,
-                  float *partial, cudaStream_t st) {
+                  int dpad, float two_kappa_scaled, const float *q_bias, int nsplit,
+                  int /*same: see the file header*/, float *partial, cudaStream_t st) {
   using namespace tc;
   if (np > (int64_t)INT32_MAX || nq > (int64_t)INT32_MAX) {
     set_error("lse_tc: too many points");
@@ -871,7 +815,6 @@ int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_
   prm.num_units = prm.row_tiles * nsplit;
   prm.c2k = two_kappa_scaled;
   prm.partial = partial;
-  prm.same = same;
   prm.probe = getenv("OTK_TC_PROBE") ? atoi(getenv("OTK_TC_PROBE")) : 0;
   if (v == 1) {
     if (kb == 1) return launch_variant<1, true, 2, 2>(maps, prm, st);

@@ -92,3 +92,25 @@ def test_tc_deterministic(otk):
     a2, b2 = _half_steps(otk, x, y, f, g, 7.0, "tc")
     np.testing.assert_array_equal(a1, a2)
     np.testing.assert_array_equal(b1, b2)
+
+
+@pytest.mark.parametrize("d,eps_scale", [(64, 0.05), (130, 0.01), (16, 0.02)])
+def test_tc_identical_point_sets(otk, d, eps_scale):
+    """x is y on the tcgen05 path: C_ii is 0 only up to fp32 rounding there (the
+    FP32 kernels force the exact zero of geometry.py:278-292); potentials and
+    cost must still match the float64 oracle at the parity tolerance."""
+    rng = np.random.default_rng(d)
+    x = rng.standard_normal((300, d)).astype(np.float32)
+    geom64 = oracle.PointCloudOracle(x.astype(np.float64), x.astype(np.float64))
+    eps = eps_scale * float(geom64.cost_matrix().mean())
+    ref = oracle.sinkhorn(geom64, None, None, eps, threshold=1e-300, max_iters=30)
+    prob = otk.LinearProblem(otk.PointCloudGeometry(x, x))
+    out = otk.solve_sinkhorn(prob, eps, threshold=1e-300, max_iters=30, impl="tc")
+    # self-transport drives the potentials to ~0 (||ref||_inf can be exactly 0),
+    # so the log-domain scale eps bounds the reference-relative metric from below
+    for got, want in ((out.f, ref["f"]), (out.g, ref["g"])):
+        assert np.max(np.abs(got - want)) / max(np.max(np.abs(want)), eps) <= 1e-4
+    a = np.full(300, 1 / 300)
+    tc, _ = oracle.reg_ot_cost(geom64, ref["f"], ref["g"], a, a, eps)
+    # small eps: off-diagonal mass underflows and the cost itself is ~1e-24
+    assert abs(otk.reg_ot_cost(out, prob).transport_cost - tc) <= 1e-5 * abs(tc) + 1e-12 * eps
