@@ -633,6 +633,352 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------- CTA-pair variant
+// The same half-step with the 2-SM MMA (tcgen05 cta_group::2, M = 256):
+// the two CTAs of a cluster take adjacent 128-row tiles of P and the SAME
+// 256-column tiles of Q.  Each CTA stages its own A rows and HALF of every B
+// tile (128 of the 256 rows); the leader CTA issues M=256 x N=256 x K=16 MMAs
+// that read both CTAs' shared memory and write each CTA's 128 rows into its
+// own TMEM.  Per SM this halves the B operand traffic (smem reads by the
+// tensor core and TMA writes): 64 instead of 96 B/clk of MMA operand reads.
+// Barriers: TMA bytes of both CTAs land on the leader's full/afull barriers
+// (cp.async.bulk.tensor .cta_group::2), the leader's MMA commits are
+// multicast to both CTAs' empty/aempty/tfull barriers, and every epilogue
+// warp of both CTAs arrives on the leader's tempty barrier.  V1 (one fp32
+// accumulator, d <= 128, A resident) only.
+namespace pair {
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t nclusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void *dst, const CUtensorMap *map, uint32_t mbar_cluster,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+template <uint32_t IDESC>
+__device__ __forceinline__ void umma2_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(IDESC), "r"(accumulate));
+}
+// commit the leader's outstanding MMAs to the same barrier in both CTAs
+__device__ __forceinline__ void commit2_w(uint64_t *bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+
+constexpr int BN = 256, HALF = 128, NS = 4, NG = 4;
+constexpr int THREADS = 32 * EPI_WARP0 + 128 * NG;
+constexpr int B_HALF = HALF * BK * 2;           // 16 KB (one of hi / lo)
+constexpr int B_EXT_HALF = HALF * EXT_K * 2;    // 4 KB
+constexpr int STAGE = 2 * B_HALF + B_EXT_HALF;  // the ext half is loaded on the last K-block
+constexpr int BIAS_BYTES = BN * 4;
+constexpr int CH = 16, NCH_G = BN / CH / NG;
+constexpr int EPI_WARPS = 4 * NG;
+// kind::f16, D f32, M = 256 (cta pair), N = 256
+constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+
+template <int KB>
+struct Plan2 {
+  static constexpr int ABUF = (KB == 1) ? 2 : 1;
+  static constexpr int A_BYTES = ABUF * (KB * 2 * A_TILE + A_EXT);
+  static constexpr int SMEM = 1024 + A_BYTES + NS * STAGE + NSLOT * BIAS_BYTES + 256 +
+                              2 * (NG - 1) * 2 * BM * (int)sizeof(float);
+};
+
+template <int KB>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    lse_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_phi, const __grid_constant__ CUtensorMap tm_plo,
+                       const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo,
+                       const __grid_constant__ CUtensorMap tm_pext, const __grid_constant__ CUtensorMap tm_qext,
+                       const __grid_constant__ CUtensorMap tm_bias, const Params prm) {
+  using L = Plan2<KB>;
+  constexpr int ABUF = L::ABUF;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t *a_region = smem;
+  uint8_t *stage_region = smem + L::A_BYTES;
+  uint8_t *slot_region = stage_region + NS * STAGE;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(slot_region + NSLOT * BIAS_BYTES);
+  uint64_t *full = bars, *empty = bars + NS;
+  uint64_t *afull = bars + 2 * NS, *aempty = afull + 2;
+  uint64_t *tfull = aempty + 2, *tempty = tfull + 2;
+  uint64_t *xfull = tempty + 2, *xempty = xfull + NSLOT;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(xempty + NSLOT);
+  float *comb = reinterpret_cast<float *>(bars + 32);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < NS; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&afull[b], 1);
+      mbar_init(&aempty[b], 1);
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 2 * EPI_WARPS);  // one arrival per epilogue warp of both CTAs
+    }
+    for (int b = 0; b < NSLOT; ++b) {
+      mbar_init(&xfull[b], 1);
+      mbar_init(&xempty[b], EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_phi);
+    tma_prefetch_desc(&tm_plo);
+    tma_prefetch_desc(&tm_qhi);
+    tma_prefetch_desc(&tm_qlo);
+    tma_prefetch_desc(&tm_pext);
+    tma_prefetch_desc(&tm_qext);
+    tma_prefetch_desc(&tm_bias);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // peer barriers initialised and TMEM allocated before any remote use
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto a_tile = [&](int buf, int k, int lo) -> uint8_t * {
+    return a_region + (size_t)buf * (KB * 2 * A_TILE + A_EXT) + (size_t)(2 * k + lo) * A_TILE;
+  };
+  auto a_ext = [&](int buf) -> uint8_t * {
+    return a_region + (size_t)buf * (KB * 2 * A_TILE + A_EXT) + KB * 2 * A_TILE;
+  };
+  auto st_b = [&](int q, int lo) -> uint8_t * { return stage_region + (size_t)q * STAGE + lo * B_HALF; };
+  auto st_ext = [&](int q) -> uint8_t * { return stage_region + (size_t)q * STAGE + 2 * B_HALF; };
+  auto slot_bias = [&](int x) -> float * { return reinterpret_cast<float *>(slot_region + (size_t)x * BIAS_BYTES); };
+
+  const int pair_rows = (prm.row_tiles + 1) / 2;
+  const int num_pairs = pair_rows * prm.nsplit;
+  const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      const uint32_t afull_l0 = mapa(smem_u32(&afull[0]), 0), afull_l1 = mapa(smem_u32(&afull[1]), 0);
+      int stage = 0;
+      uint32_t sphase = 0;
+      int uc = 0, tcount = 0;
+      for (int u = cid; u < num_pairs; u += ncl, ++uc) {
+        const int split = u / pair_rows, pr = u % pair_rows;
+        const int rt = 2 * pr + (int)rank;
+        const int t0 = split * prm.tps, t1 = min(prm.ntiles, t0 + prm.tps);
+        const int ab = uc % ABUF;
+        const uint32_t afl = ab ? afull_l1 : afull_l0;
+        mbar_wait(&aempty[ab], ((uc / ABUF) & 1) ^ 1);
+        if (leader) mbar_expect_tx(&afull[ab], (uint32_t)(2 * (KB * 2 * A_TILE + A_EXT)));
+        for (int k = 0; k < KB; ++k) {
+          tma_load_2d_pair(a_tile(ab, k, 0), &tm_phi, afl, k * BK, rt * BM);
+          tma_load_2d_pair(a_tile(ab, k, 1), &tm_plo, afl, k * BK, rt * BM);
+        }
+        tma_load_2d_pair(a_ext(ab), &tm_pext, afl, 0, rt * BM);
+        for (int t = t0; t < t1; ++t, ++tcount) {
+          for (int k = 0; k < KB; ++k) {
+            mbar_wait(&empty[stage], sphase ^ 1);
+            const uint32_t fl = mapa(smem_u32(&full[stage]), 0);
+            const bool last = (k == KB - 1);
+            if (leader) mbar_expect_tx(&full[stage], (uint32_t)(2 * (2 * B_HALF + (last ? B_EXT_HALF : 0))));
+            const int brow = t * BN + (int)rank * HALF;
+            tma_load_2d_pair(st_b(stage, 0), &tm_qhi, fl, k * BK, brow);
+            tma_load_2d_pair(st_b(stage, 1), &tm_qlo, fl, k * BK, brow);
+            if (last) tma_load_2d_pair(st_ext(stage), &tm_qext, fl, 0, brow);
+            if (++stage == NS) {
+              stage = 0;
+              sphase ^= 1;
+            }
+          }
+          // kappa*g_j of all 256 columns for this CTA's epilogue (local)
+          const int x = tcount % NSLOT;
+          mbar_wait(&xempty[x], ((tcount / NSLOT) & 1) ^ 1);
+          mbar_expect_tx(&xfull[x], (uint32_t)BIAS_BYTES);
+          tma_load_1d(slot_bias(x), &tm_bias, &xfull[x], t * BN);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
+    if (leader) {
+      int stage = 0;
+      uint32_t sphase = 0;
+      int tcount = 0, uc = 0;
+      for (int u = cid; u < num_pairs; u += ncl, ++uc) {
+        const int split = u / pair_rows;
+        const int t0 = split * prm.tps, t1 = min(prm.ntiles, t0 + prm.tps);
+        const int ab = uc % ABUF;
+        mbar_wait(&afull[ab], (uc / ABUF) & 1);
+        tc_fence_after();
+        for (int t = t0; t < t1; ++t, ++tcount) {
+          const int buf = tcount & 1;
+          mbar_wait(&tempty[buf], ((tcount >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem_base + (uint32_t)(buf * BN);
+          for (int k = 0; k < KB; ++k) {
+            mbar_wait(&full[stage], sphase);
+            tc_fence_after();
+            const uint64_t dah = sw128_desc(smem_u32(a_tile(ab, k, 0)));
+            const uint64_t dal = sw128_desc(smem_u32(a_tile(ab, k, 1)));
+            const uint64_t dbh = sw128_desc(smem_u32(st_b(stage, 0)));
+            const uint64_t dbl = sw128_desc(smem_u32(st_b(stage, 1)));
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t o = (uint64_t)(2 * kk);
+              umma2_w<IDESC>(d, dah + o, dbh + o, (k == 0 && kk == 0) ? 0u : 1u);
+              umma2_w<IDESC>(d, dah + o, dbl + o, 1u);
+              umma2_w<IDESC>(d, dal + o, dbh + o, 1u);
+            }
+            if (k == KB - 1)  // -s^2 (|p|^2 + |q|^2) / 2, last (see the file header)
+              umma2_w<IDESC>(d, sw32_desc(smem_u32(a_ext(ab))), sw32_desc(smem_u32(st_ext(stage))), 1u);
+            commit2_w(&empty[stage]);
+            if (++stage == NS) {
+              stage = 0;
+              sphase ^= 1;
+            }
+          }
+          commit2_w(&tfull[buf]);
+        }
+        commit2_w(&aempty[ab]);
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int eg = (warp - EPI_WARP0) >> 2;
+    const int quarter = warp & 3;
+    const int row_local = quarter * 32 + lane;
+    const uint32_t t_lane = (uint32_t)(quarter * 32) << 16;
+    const float c2k = prm.c2k;
+    const uint32_t tempty_l0 = mapa(smem_u32(&tempty[0]), 0), tempty_l1 = mapa(smem_u32(&tempty[1]), 0);
+    int tcount = 0, uc = 0;
+    for (int u = cid; u < num_pairs; u += ncl, ++uc) {
+      const int split = u / pair_rows, pr = u % pair_rows;
+      const int rt = 2 * pr + (int)rank;
+      const int t0 = split * prm.tps, t1 = min(prm.ntiles, t0 + prm.tps);
+      float m = -INFINITY, s = 0.f;
+      for (int t = t0; t < t1; ++t, ++tcount) {
+        const int buf = tcount & 1;
+        const int x = tcount % NSLOT;
+        mbar_wait(&tfull[buf], (tcount >> 1) & 1);
+        mbar_wait(&xfull[x], (tcount / NSLOT) & 1);
+        tc_fence_after();
+        const int64_t j0 = (int64_t)t * BN;
+        const int valid = (int)(prm.nq - j0 < BN ? prm.nq - j0 : (int64_t)BN);
+        const uint32_t tbase = tmem_base + (uint32_t)(buf * BN) + t_lane;
+        const float *bias = slot_bias(x);
+        const int cfirst = eg * NCH_G;
+        uint32_t va[16], vb[16];
+        auto consume = [&](int c, uint32_t *v) {
+          float accv[CH], bv[CH];
+#pragma unroll
+          for (int i = 0; i < CH; ++i) accv[i] = __uint_as_float(v[i]);
+          const float4 *bp = reinterpret_cast<const float4 *>(bias + c * CH);
+#pragma unroll
+          for (int i = 0; i < CH / 4; ++i) {
+            const float4 q = bp[i];
+            bv[4 * i] = q.x;
+            bv[4 * i + 1] = q.y;
+            bv[4 * i + 2] = q.z;
+            bv[4 * i + 3] = q.w;
+          }
+          if (valid >= BN)
+            lse_chunk<CH, false, 0>(accv, bv, c2k, 0, m, s);
+          else
+            lse_chunk<CH, true, 0>(accv, bv, c2k, valid - c * CH, m, s);
+        };
+        tmem_ld_x16(tbase + cfirst * CH, va);
+        tmem_wait16(va);
+#pragma unroll
+        for (int c = 0; c < NCH_G; c += 2) {
+          tmem_ld_x16(tbase + (cfirst + c + 1) * CH, vb);
+          consume(cfirst + c, va);
+          tmem_wait16(vb);
+          if (c + 2 < NCH_G) tmem_ld_x16(tbase + (cfirst + c + 2) * CH, va);
+          consume(cfirst + c + 1, vb);
+          if (c + 2 < NCH_G) tmem_wait16(va);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          arrive_remote(buf ? tempty_l1 : tempty_l0);  // the leader's MMA waits on both CTAs
+          mbar_arrive(&xempty[x]);
+        }
+      }
+      float *cb = comb + (uc & 1) * ((NG - 1) * 2 * BM);
+      if (eg > 0) {
+        cb[((eg - 1) * BM + row_local) * 2] = m;
+        cb[((eg - 1) * BM + row_local) * 2 + 1] = s;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(128 * NG) : "memory");
+      if (eg == 0) {
+        Lse2 st;
+        st.m = m;
+        st.s = s;
+#pragma unroll
+        for (int g = 0; g < NG - 1; ++g) st.merge(cb[(g * BM + row_local) * 2], cb[(g * BM + row_local) * 2 + 1]);
+        const int64_t row = (int64_t)rt * BM + row_local;
+        if (row < prm.np) prm.partial[(int64_t)split * prm.np + row] = st.value();
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // both CTAs done (the leader's MMAs wrote the peer's TMEM)
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+  }
+}
+
+}  // namespace pair
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
                                   const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
@@ -753,6 +1099,33 @@ static int launch_variant(const CUtensorMap (&maps)[7], const Params &prm, cudaS
             : launch_one<V, A_RES, NS, ABUF, 0, 2>(maps, prm, st);
 }
 
+// Same-box A/B (B200): cfg2 (d = 64, one K-block) 1.81 vs 1.50 ms per half-step
+// (slower: the pair's epilogues pace each other), cfg4 (d = 128, two K-blocks)
+// 19.2 / 18.9 vs 19.5 / 19.8 ms (faster: half the B operand traffic per SM).
+// Default: pair for two K-blocks only; OTK_TC_PAIR=0/1 overrides.
+static bool use_pair_kernel(int kb) {
+  if (const char *e = getenv("OTK_TC_PAIR")) return atoi(e) == 1;
+  return kb == 2;
+}
+
+template <int KB>
+static int launch_pair(const CUtensorMap (&maps)[7], const Params &prm, cudaStream_t st) {
+  using L = pair::Plan2<KB>;
+  auto kern = pair::lse_tc_pair_kernel<KB>;
+  static bool attr_set = false;
+  static_assert(L::SMEM <= 227 * 1024, "pair kernel shared memory plan too large");
+  if (!attr_set) {
+    OTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
+    attr_set = true;
+  }
+  const int num_pairs = ((prm.row_tiles + 1) / 2) * prm.nsplit;
+  const int grid = 2 * std::min(num_pairs, num_sms() / 2);
+  kern<<<grid, pair::THREADS, L::SMEM, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5],
+                                              maps[6], prm);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? OTK_OK : cuda_status(e, "lse_tc_pair_kernel");
+}
+
 static int variant_for(int kb) {
   if (const char *v = getenv("OTK_TC_VARIANT")) return atoi(v);
   // V1 (one accumulator) reads 4 B of TMEM per cell -- the epilogue's binding
@@ -795,14 +1168,18 @@ int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_
     set_error("lse_tc: variant 4 needs d > 128");
     return OTK_EINVAL;
   }
+  // CTA-pair (cta_group::2) variant for V1 with resident A (d <= 128), see
+  // pair::lse_tc_pair_kernel and use_pair_kernel
+  const bool use_pair = (v == 1 && kb <= 2 && use_pair_kernel(kb));
+  const int qbox = use_pair ? pair::HALF : bn;
   CUtensorMap maps[7];
   int rc;
   if ((rc = make_plane_map(&maps[0], p_hi, np, dpad, BM, BK)) != OTK_OK) return rc;
   if ((rc = make_plane_map(&maps[1], p_lo, np, dpad, BM, BK)) != OTK_OK) return rc;
-  if ((rc = make_plane_map(&maps[2], q_hi, nq, dpad, bn, BK)) != OTK_OK) return rc;
-  if ((rc = make_plane_map(&maps[3], q_lo, nq, dpad, bn, BK)) != OTK_OK) return rc;
+  if ((rc = make_plane_map(&maps[2], q_hi, nq, dpad, qbox, BK)) != OTK_OK) return rc;
+  if ((rc = make_plane_map(&maps[3], q_lo, nq, dpad, qbox, BK)) != OTK_OK) return rc;
   if ((rc = make_plane_map(&maps[4], p_ext, np, EXT_K, BM, EXT_K)) != OTK_OK) return rc;
-  if ((rc = make_plane_map(&maps[5], q_ext, nq, EXT_K, bn, EXT_K)) != OTK_OK) return rc;
+  if ((rc = make_plane_map(&maps[5], q_ext, nq, EXT_K, qbox, EXT_K)) != OTK_OK) return rc;
   if ((rc = make_vec_map(&maps[6], q_bias, nq, bn)) != OTK_OK) return rc;
   Params prm;
   prm.np = np;
@@ -816,6 +1193,7 @@ int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_
   prm.c2k = two_kappa_scaled;
   prm.partial = partial;
   prm.probe = getenv("OTK_TC_PROBE") ? atoi(getenv("OTK_TC_PROBE")) : 0;
+  if (use_pair) return kb == 1 ? launch_pair<1>(maps, prm, st) : launch_pair<2>(maps, prm, st);
   if (v == 1) {
     if (kb == 1) return launch_variant<1, true, 2, 2>(maps, prm, st);
     if (kb == 2) return launch_variant<1, true, 2, 1>(maps, prm, st);

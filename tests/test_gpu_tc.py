@@ -114,3 +114,24 @@ def test_tc_identical_point_sets(otk, d, eps_scale):
     tc, _ = oracle.reg_ot_cost(geom64, ref["f"], ref["g"], a, a, eps)
     # small eps: off-diagonal mass underflows and the cost itself is ~1e-24
     assert abs(otk.reg_ot_cost(out, prob).transport_cost - tc) <= 1e-5 * abs(tc) + 1e-12 * eps
+
+
+@pytest.mark.parametrize("n,m,d", [(128, 256, 64), (300, 517, 40), (1000, 700, 128), (129, 1031, 96)])
+def test_cta_pair_kernel_is_bitwise_the_single_cta_kernel(otk, n, m, d, monkeypatch):
+    """The cta_group::2 (2-SM MMA) variant computes every row with the same
+    MMA sequence as the 1-CTA kernel: outputs must be bitwise identical,
+    including odd row-tile counts (the pair's second CTA past the last row)."""
+    from paper_2201_12324_b200 import _native as N
+    rng = np.random.default_rng(n + m + d)
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    y = (1.3 * rng.standard_normal((m, d)) + 0.2).astype(np.float32)
+    eps = 0.15 * d
+    f = (rng.standard_normal(n) * eps).astype(np.float32).astype(np.float64)
+    g = (rng.standard_normal(m) * eps).astype(np.float32).astype(np.float64)
+    outs = []
+    for pair in ("0", "1"):
+        monkeypatch.setenv("OTK_TC_PAIR", pair)
+        geom = otk.PointCloudGeometry(x, y)
+        geom.impl_flags = N.OTK_IMPL_TC
+        outs.append((geom.apply_lse_kernel(f, g, eps, "rows"), geom.apply_lse_kernel(f, g, eps, "cols")))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
