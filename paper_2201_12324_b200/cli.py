@@ -13,7 +13,7 @@ atomic writes.  Differences, all on the side of doing more: the regularised
 cost is computed online (no 4e6-entry cap), and the n x m coupling is only
 materialised when --coupling-out asks for it (the reference always builds
 it, cli.py:157, so it refuses every problem above the cap).  The low-rank
-solver, the LP ``--verify`` oracle, the eucl/cosine costs and the other
+solver, the LP ``--verify`` oracle, the eucl cost and the other
 subcommands (quad, barycenter, softsort, gmm) are outside this build's hot
 path and exit with an input error.
 """
@@ -126,8 +126,8 @@ def _cmd_lin(args) -> int:
         raise _InputError("--solver lr (low-rank Sinkhorn) is outside this build's hot path")
     if args.verify:
         raise _InputError("--verify (exact LP oracle) is outside this build's hot path")
-    if args.cost != "sqeucl":
-        raise _InputError(f"--cost {args.cost} is outside this build's hot path (sqeucl only)")
+    if args.cost == "eucl":
+        raise _InputError("--cost eucl is outside this build's hot path (sqeucl, cosine)")
     if args.cost_matrix is not None:
         geom = DenseGeometry(read_matrix(args.cost_matrix))
     else:

@@ -7,10 +7,12 @@ inputs may be numpy arrays (results come back as float64 numpy, like the
 reference) or CUDA torch tensors (results stay on the device).
 
 Implemented: ``PointCloudGeometry`` with the squared-Euclidean cost (never
-materialised: the online kernels of csrc/lse_simt.cu and csrc/lse_tc.cu),
-``DenseGeometry`` (stored cost, csrc/dense.cu) and ``EpsilonSchedule``.
-Out of scope for this hot-path build: the ``eucl`` /
-``cosine`` costs, the non-log ``apply_kernel`` and ``GridGeometry``.
+materialised: the online kernels of csrc/lse_simt.cu and csrc/lse_tc.cu) and
+the cosine cost (1 - <x^,y^> = |x^/sqrt2 - y^/sqrt2|^2: the same kernels on
+normalised, 1/sqrt(2)-scaled points), ``DenseGeometry`` (stored cost,
+csrc/dense.cu), ``EpsilonSchedule`` and the non-log ``apply_kernel`` (built on
+the log-domain kernels).  Out of scope: the ``eucl``
+cost (a square root per cell in every kernel) and ``GridGeometry``.
 """
 
 from __future__ import annotations
@@ -35,7 +37,7 @@ DEFAULT_EPSILON_SCALE = 0.05        # geometry.py:40
 _MEAN_COST_SAMPLES = 1000           # geometry.py:42
 DEFAULT_BLOCK_SIZE = 256            # geometry.py:44 (accepted, performance-only)
 DEFAULT_DENSE_CAP = 4_000_000       # geometry.py:46
-COST_FNS = ("sqeucl",)              # reference: ("sqeucl", "eucl", "cosine"); see module doc
+COST_FNS = ("sqeucl", "cosine")     # reference: ("sqeucl", "eucl", "cosine"); see module doc
 _REFERENCE_COST_FNS = ("sqeucl", "eucl", "cosine")
 _LOG2E = 1.4426950408889634
 
@@ -91,9 +93,41 @@ class Geometry:
         raise NotImplementedError
 
     def apply_kernel(self, v, eps=None, axis="rows"):
-        raise NotImplementedError(
-            "apply_kernel (non-log Gibbs kernel) is outside this build's hot path; "
-            "use apply_lse_kernel")
+        """K v (rows) or K^T v (cols) with K = exp(-C/eps) (geometry.py:130-139).
+
+        Built on the log-domain kernel: with v = v+ - v-,
+        K v+ = exp(LSE_j(log v+_j - C_ij/eps)) = exp(apply_lse_kernel(0, eps log v+)/eps),
+        one device half-step per sign present.  float32 device arithmetic: the
+        result carries ~1e-6 relative error per part, and heavy cancellation
+        between the parts loses accuracy the float64 reference keeps.
+        """
+        _check_axis(axis)
+        eps = self._resolve_eps(eps)
+        n, m = self.shape
+        size, out_size = (m, n) if axis == "rows" else (n, m)
+        like = v
+        if is_torch(v):
+            v = v.detach().double().cpu().numpy()
+        v = np.asarray(v, dtype=float)
+        if v.shape != (size,):
+            raise ValueError(f"v must have shape ({size},), got {v.shape}")
+        if not np.all(np.isfinite(v)):
+            raise ValueError("v contains non-finite entries")
+        out = np.zeros(out_size)
+        for sign, part in ((1.0, np.maximum(v, 0.0)), (-1.0, np.maximum(-v, 0.0))):
+            if not np.any(part > 0):
+                continue
+            with np.errstate(divide="ignore"):
+                pot = eps * np.log(part)
+            zeros = np.zeros(out_size)
+            f, g = (zeros, pot) if axis == "rows" else (pot, zeros)
+            lse = np.asarray(self.apply_lse_kernel(f, g, eps, axis), dtype=float)
+            with np.errstate(over="ignore"):
+                out += sign * np.exp(lse / eps)
+        if is_torch(like):
+            import torch
+            return torch.as_tensor(out, dtype=torch.float32, device=device())
+        return out
 
     def apply_lse_kernel(self, f, g, eps=None, axis="rows"):
         raise NotImplementedError
@@ -128,6 +162,13 @@ def _validate_points(p, name):
     if p.shape[0] == 0:
         raise ValueError("point sets must be non-empty")
     return p
+
+
+def _has_zero_row(p) -> bool:
+    if is_torch(p):
+        import torch
+        return bool((torch.linalg.vector_norm(p.double(), dim=1) == 0).any().item())
+    return bool(np.any(np.linalg.norm(p, axis=1) == 0))
 
 
 def _all_finite(p) -> bool:
@@ -193,7 +234,9 @@ class PointCloudGeometry(Geometry):
             raise ValueError(f"cost_fn must be one of {_REFERENCE_COST_FNS}, got {cost_fn!r}")
         if cost_fn not in COST_FNS:
             raise NotImplementedError(
-                f"cost_fn {cost_fn!r} is outside this build's hot path (sqeucl only)")
+                f"cost_fn {cost_fn!r} is outside this build's hot path (sqeucl, cosine)")
+        if cost_fn == "cosine" and (_has_zero_row(x) or (not same_obj and _has_zero_row(y))):
+            raise ValueError("cosine cost is undefined for zero vectors")
         if epsilon_default is not None and not (epsilon_default > 0):
             raise ValueError("epsilon_default must be positive")
         if block_size < 1:
@@ -216,11 +259,21 @@ class PointCloudGeometry(Geometry):
         self.impl_flags = 0  # N.OTK_IMPL_SIMT / N.OTK_IMPL_TC to force a kernel
 
     # ---- device state (lazy: construction and validation need no GPU)
+    def _kernel_points(self, p):
+        """Points the sqeucl kernels see: cosine -> x/|x|/sqrt(2) (float64 math)."""
+        if self.cost_fn != "cosine":
+            return p
+        if is_torch(p):
+            q = as_device_f32(p).double()
+            return (q / q.norm(dim=1, keepdim=True) / np.sqrt(2.0)).float().contiguous()
+        q = np.asarray(p, dtype=np.float64)
+        return q / np.linalg.norm(q, axis=1, keepdims=True) / np.sqrt(2.0)
+
     def _clouds(self):
         if self._dev is None:
             device()
-            cx = _Cloud(self.x)
-            cy = cx if self._same_points else _Cloud(self.y)
+            cx = _Cloud(self._kernel_points(self.x))
+            cy = cx if self._same_points else _Cloud(self._kernel_points(self.y))
             planes = bool(N.lib().otk_lse_uses_tc(cx.d, self.impl_flags))
             scale = 1.0
             if planes:
@@ -246,6 +299,7 @@ class PointCloudGeometry(Geometry):
         rng = np.random.default_rng(0)
         i = rng.integers(0, n, size=_MEAN_COST_SAMPLES)
         j = rng.integers(0, m, size=_MEAN_COST_SAMPLES)
+        # cosine: the kernel points are x^/sqrt2, so |x'-y'|^2 = 1 - <x^,y^> (geometry.py:303-306)
         ii = torch.as_tensor(i, device=cx.p.device)
         jj = torch.as_tensor(j, device=cx.p.device)
         diff = cx.p[ii].double() - cy.p[jj].double()

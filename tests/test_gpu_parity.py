@@ -424,3 +424,60 @@ def test_warm_start_and_annealing_match_oracle(otk, path):
     assert out.iterations == ref["iterations"] and out.converged == ref["converged"]
     assert rel_inf(out.f, ref["f"]) <= POT_TOL
     assert rel_inf(out.g, ref["g"]) <= POT_TOL
+
+
+def _cosine_cost(x, y):
+    """Reference cosine cost, geometry.py:265-267 (float64)."""
+    xn = x / np.linalg.norm(x, axis=1, keepdims=True)
+    yn = y / np.linalg.norm(y, axis=1, keepdims=True)
+    return 1.0 - xn @ yn.T
+
+
+@pytest.mark.parametrize("d", [3, 64])
+def test_cosine_cost_solve_matches_reference_formula(otk, d):
+    """cost_fn="cosine": the sqeucl kernels on x^/sqrt2."""
+    rng = np.random.default_rng(40 + d)
+    x = (rng.standard_normal((220, d)) + 0.3).astype(np.float32)
+    y = (rng.standard_normal((190, d)) - 0.2).astype(np.float32)
+    C = _cosine_cost(x.astype(np.float64), y.astype(np.float64))
+    geom = otk.PointCloudGeometry(x, y, cost_fn="cosine")
+    np.testing.assert_allclose(geom.cost_matrix(), C, atol=2e-6)
+    eps = 0.05 * float(C.mean())
+    ref = oracle.sinkhorn(oracle.DenseOracle(C), None, None, eps, threshold=1e-300, max_iters=30)
+    prob = otk.LinearProblem(geom)
+    out = otk.solve_sinkhorn(prob, eps, threshold=1e-300, max_iters=30)
+    assert rel_inf(out.f, ref["f"]) <= POT_TOL and rel_inf(out.g, ref["g"]) <= POT_TOL
+    a = np.full(220, 1 / 220)
+    b = np.full(190, 1 / 190)
+    tc, dual = oracle.reg_ot_cost(oracle.DenseOracle(C), ref["f"], ref["g"], a, b, eps)
+    cost = otk.reg_ot_cost(out, prob)
+    assert abs(cost.transport_cost - tc) <= COST_TOL * abs(tc)
+    assert abs(geom.mean_cost() - float(np.mean(C))) < 0.1  # 1000-pair sample estimate
+
+
+@pytest.mark.parametrize("cost_fn", ["sqeucl", "cosine"])
+def test_apply_kernel_matches_dense_gibbs_product(otk, cost_fn):
+    """Non-log apply_kernel (geometry.py:130-139, 318-334) on the GPU vs
+    exp(-C/eps) @ v in float64, rows and cols, positive and signed v."""
+    rng = np.random.default_rng(7)
+    x = (rng.standard_normal((150, 3)) + 2.0).astype(np.float32)
+    y = (rng.standard_normal((130, 3)) + 2.0).astype(np.float32)
+    x64, y64 = x.astype(np.float64), y.astype(np.float64)
+    C = _cosine_cost(x64, y64) if cost_fn == "cosine" else \
+        oracle.PointCloudOracle(x64, y64).cost_matrix()
+    geom = otk.PointCloudGeometry(x, y, cost_fn=cost_fn)
+    eps = 0.5 * float(C.mean()) + 0.1
+    K = np.exp(-C / eps)
+    v, u = rng.random(130) + 0.1, rng.random(150) + 0.1
+    np.testing.assert_allclose(geom.apply_kernel(v, eps, "rows"), K @ v, rtol=1e-5)
+    np.testing.assert_allclose(geom.apply_kernel(u, eps, "cols"), K.T @ u, rtol=1e-5)
+    vs = rng.standard_normal(130)
+    got = geom.apply_kernel(vs, eps, "rows")
+    assert np.all(np.abs(got - K @ vs) <= 1e-5 * (np.abs(K) @ np.abs(vs)))
+    dense = otk.DenseGeometry(C)
+    np.testing.assert_allclose(dense.apply_kernel(v, eps, "rows"), K @ v, rtol=1e-5)
+    # known answers (test_geometry.py:61-68)
+    np.testing.assert_allclose(otk.DenseGeometry(np.array([[0.0]])).apply_kernel(
+        np.array([1.0]), 1.0, "rows"), [1.0], rtol=1e-6)
+    np.testing.assert_allclose(otk.DenseGeometry(np.zeros((2, 2))).apply_kernel(
+        np.array([1.0, 1.0]), 1.0, "rows"), [2.0, 2.0], rtol=1e-6)

@@ -127,3 +127,20 @@ def test_product_package_does_not_import_oracle():
             if fn.endswith(".py"):
                 src = open(os.path.join(dirpath, fn)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), fn
+
+
+def test_cosine_and_apply_kernel_validation_like_reference():
+    """test_geometry.py:211-223: zero vectors with cosine, bad axis / lengths /
+    eps for apply_kernel -- all raised before any device work."""
+    import paper_2201_12324_b200 as otk
+    with pytest.raises(ValueError):
+        otk.PointCloudGeometry(np.array([[0.0, 0.0]]), np.array([[1.0, 0.0]]), "cosine")
+    with pytest.raises(NotImplementedError):
+        otk.PointCloudGeometry(np.ones((2, 2)), np.ones((2, 2)), "eucl")
+    geom = otk.DenseGeometry(np.zeros((2, 3)))
+    with pytest.raises(ValueError):
+        geom.apply_kernel(np.ones(3), 1.0, "diagonal")
+    with pytest.raises(ValueError):
+        geom.apply_kernel(np.ones(2), 1.0, "rows")
+    with pytest.raises(ValueError):
+        geom.apply_kernel(np.ones(3), 0.0, "rows")
