@@ -341,7 +341,7 @@ def run_ours(args, wl, rank, world):
     import torch
     import paper_2201_12324_b200 as otk
     from paper_2201_12324_b200 import _native as N
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", local_device())
     torch.cuda.set_device(dev)
     N.lib()
     flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
@@ -449,6 +449,7 @@ def run_ours(args, wl, rank, world):
             g1 = otk.PointCloudGeometry(xd, yd)
             result["roofline"] = online_roofline(g1, wl)
             result["roofline"]["note"] = "rank 0's shard (n/N rows x m)"
+            result["roofline"]["traffic"] = None  # the committed ncu capture is single-GPU
         if not args.no_cpu and world == 1:
             v, dt, desc = cpu_sample_rate(wl)
             result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cpu_cores(),
@@ -579,6 +580,16 @@ def run_e2e(otk, wl, args, dev, world, rank):
             "api": "public API on pinned host arrays (H2D + D2H inside the timed region)"}
 
 
+def local_device() -> int:
+    """This rank's GPU.  OTK_BENCH_GLOO=1 (test only) puts every rank on GPU 0
+    over gloo: the N > 1 code path can then be exercised on a one-GPU box
+    without any kernel waiting on another rank's kernel (all exchanges go
+    through host memory); its timings are meaningless."""
+    if os.environ.get("OTK_BENCH_GLOO"):
+        return 0
+    return int(os.environ.get("LOCAL_RANK", 0))
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -592,9 +603,12 @@ def main():
     wl = workloads.make(args.config)
     if world > 1:
         import torch
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        torch.distributed.init_process_group(
-            "nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
+        torch.cuda.set_device(local_device())
+        if os.environ.get("OTK_BENCH_GLOO"):  # multi-rank plumbing test on ONE GPU (see below)
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.distributed.init_process_group(
+                "nccl", device_id=torch.device("cuda", local_device()))
     try:
         run_ours(args, wl, rank, world)
     finally:

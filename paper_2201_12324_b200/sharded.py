@@ -87,10 +87,13 @@ class TorchComm:
 
     def all_gather_rows(self, local):
         import torch
+        shape_dev = local.device
         local = local.contiguous().reshape(-1)
+        if local.is_cuda and self.dist.get_backend(self.group) == "gloo":
+            local = local.cpu()  # gloo moves host tensors
         out = torch.empty(self.world * local.numel(), dtype=local.dtype, device=local.device)
         self.dist.all_gather_into_tensor(out, local, group=self.group)
-        return out.view(self.world, -1)
+        return out.view(self.world, -1).to(shape_dev)
 
     def _host(self, arr, like_device):
         import torch
