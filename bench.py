@@ -366,10 +366,12 @@ def run_ours(args, wl, rank, world):
         yd = torch.from_numpy(wl.y).to(dev)
         a_loc = None if wl.a is None else wl.a[lo:hi]
 
+        sprob = otk.ShardedProblem(xd, yd, a_loc, wl.b, x_is_local=True, n_total=n, comm=comm,
+                                   impl=args.kernel)
+
         def solve():
-            return otk.solve_sinkhorn_sharded(xd, yd, wl.eps, a_loc, wl.b, x_is_local=True,
-                                              n_total=n, threshold=wl.threshold,
-                                              max_iters=wl.max_iters, comm=comm, impl=args.kernel)
+            return sprob.solve(wl.eps, threshold=wl.threshold, max_iters=wl.max_iters)
+        solve.sharded_problem = sprob
 
         def cells_of(out):
             return float(n) * m * out.iterations
@@ -462,7 +464,6 @@ def count_launches(otk, wl, args, solve, world):
     (graph nodes included); the sharded engine and the dense loop count theirs."""
     import ctypes
     from paper_2201_12324_b200 import _native as N
-    from paper_2201_12324_b200 import sharded as SH
     from paper_2201_12324_b200 import sinkhorn as S
     if wl.materialised:
         calls = {"n": 0}
@@ -486,18 +487,10 @@ def count_launches(otk, wl, args, solve, world):
             S.N.lib = saved
         return calls["n"]
     if world > 1:
-        orig = SH.CudaShardEngine.__init__
-        box = {}
-
-        def init(self, *a, **k):
-            orig(self, *a, **k)
-            box["eng"] = self
-        SH.CudaShardEngine.__init__ = init
-        try:
-            solve()
-        finally:
-            SH.CudaShardEngine.__init__ = orig
-        return int(box["eng"].launches)
+        eng = solve.sharded_problem.engine
+        before = eng.launches
+        solve()
+        return int(eng.launches - before)
     captured = {}
     real = N.lib()
 

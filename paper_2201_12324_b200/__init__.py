@@ -28,7 +28,7 @@ from .sinkhorn import (
     solve_sinkhorn_batched,
     transport_matrix,
 )
-from .sharded import reg_ot_cost_sharded, solve_sinkhorn_sharded
+from .sharded import ShardedProblem, reg_ot_cost_sharded, solve_sinkhorn_sharded
 
 __version__ = "0.1.0"
 
@@ -55,4 +55,5 @@ __all__ = [
     "grad_points",
     "solve_sinkhorn_sharded",
     "reg_ot_cost_sharded",
+    "ShardedProblem",
 ]

@@ -42,6 +42,7 @@ __all__ = [
     "ThreadComm",
     "CudaShardEngine",
     "sharded_loop",
+    "ShardedProblem",
     "solve_sinkhorn_sharded",
     "reg_ot_cost_sharded",
 ]
@@ -333,70 +334,97 @@ def _global_weights(w, n_total, lo, hi, name):
     return w
 
 
-def solve_sinkhorn_sharded(x, y, eps, a=None, b=None, *, threshold: float = 1e-3,
-                           max_iters: int = 2000, inner_iters: int = 10, g_init=None,
-                           comm=None, x_is_local: bool = False, n_total: int | None = None,
-                           impl: str = "auto", gather_f: bool = False) -> ShardedSinkhornOutput:
-    """Row-sharded ``solve_sinkhorn`` on a point cloud (one rank per GPU).
+class ShardedProblem:
+    """One rank's share of a row-sharded point-cloud problem, prepared once.
 
     ``x``: the full [n, d] points (each rank takes its ``shard_rows`` slice) or,
     with ``x_is_local``, this rank's rows (then pass ``n_total``).  ``y`` [m, d],
     ``b`` [m] replicated; ``a`` global [n] (or the local slice).  ``comm``:
-    ``TorchComm()`` (default, needs an initialised process group) or a
-    ``ThreadComm``.  Same validation, loop and errors as ``solve_sinkhorn``.
+    ``TorchComm()`` (default; needs an initialised process group) or a
+    ``ThreadComm``.  Construction validates the weights, uploads and prepares
+    the points (norms, split-fp16 planes with one scale common to all ranks);
+    ``solve`` can then be called repeatedly (like reusing a geometry).
     """
-    from .sinkhorn import _fp32_guard, _impl_flags
+
+    def __init__(self, x, y, a=None, b=None, *, comm=None, x_is_local: bool = False,
+                 n_total: int | None = None, impl: str = "auto"):
+        from .sinkhorn import _impl_flags
+        self.comm = comm = comm or TorchComm()
+        dev = _dev_of(x)
+        if x_is_local:
+            if n_total is None:
+                raise ValueError("n_total is required with x_is_local")
+            sizes = comm.all_gather_host(np.array([float(x.shape[0])]), dev)[:, 0].astype(int)
+            lo = int(sizes[:comm.rank].sum())
+            hi = lo + int(x.shape[0])
+            if int(sizes.sum()) != n_total:
+                raise ValueError("local shards do not add up to n_total")
+            x_local = x
+        else:
+            n_total = int(x.shape[0])
+            lo, hi = shard_rows(n_total, comm.world, comm.rank)
+            x_local = x[lo:hi]
+        m = int(y.shape[0])
+        a_loc = _global_weights(a, n_total, lo, hi, "a")
+        b_w = _global_weights(b, m, 0, m, "b")
+        tot_a = comm.all_gather_host(np.array([a_loc.sum()]), dev)[:, 0].sum()
+        if abs(tot_a - 1.0) > 1e-8 or abs(b_w.sum() - 1.0) > 1e-8:
+            raise ValueError("a and b must each sum to 1")
+
+        def amax_reduce(v):  # one common split scale on every rank
+            return float(comm.all_gather_host(np.array([v]), dev)[:, 0].max())
+
+        self.engine = CudaShardEngine(x_local, y, a_loc, b_w, flags=_impl_flags(impl),
+                                      amax_reduce=amax_reduce)
+        self.lo, self.hi, self.n_total, self.m = lo, hi, n_total, m
+
+    def solve(self, eps, *, threshold: float = 1e-3, max_iters: int = 2000,
+              inner_iters: int = 10, g_init=None, gather_f: bool = False) -> ShardedSinkhornOutput:
+        """The reference loop (sinkhorn.py:151-200) over the shards; same
+        validation and errors as ``solve_sinkhorn``."""
+        from .sinkhorn import _fp32_guard
+        if max_iters < 1 or inner_iters < 1:
+            raise ValueError("max_iters and inner_iters must be >= 1")
+        if not (threshold > 0):
+            raise ValueError("threshold must be positive")
+        sched = eps if isinstance(eps, EpsilonSchedule) else EpsilonSchedule(float(eps))
+        _fp32_guard(sched, inner_iters, max_iters)
+        comm, eng = self.comm, self.engine
+        eng.reset_first_bad()
+        which, iters, conv, errs, duals = sharded_loop(eng, comm, sched, threshold, max_iters,
+                                                       inner_iters, g_init)
+        f_dev, g_dev = eng.f_result(which).clone(), eng.g_result().clone()
+        f_full = None
+        if gather_f:
+            import torch
+            n_total, world = self.n_total, comm.world
+            width = -(-n_total // world) + 1
+            pad = torch.full((width,), float("nan"), dtype=torch.float32, device=f_dev.device)
+            pad[: self.hi - self.lo] = f_dev
+            allf = comm.all_gather_rows(pad).cpu().numpy().astype(np.float64)
+            f_full = np.concatenate([allf[r, : shard_rows(n_total, world, r)[1]
+                                           - shard_rows(n_total, world, r)[0]]
+                                     for r in range(world)])
+        return ShardedSinkhornOutput(
+            f_local=f_dev.cpu().numpy().astype(np.float64), g=g_dev.cpu().numpy().astype(np.float64),
+            errors=errs, dual_trace=duals, iterations=iters, converged=conv, eps=sched.target,
+            row_offset=self.lo, n_total=self.n_total, f=f_full, f_device=f_dev, g_device=g_dev)
+
+
+def solve_sinkhorn_sharded(x, y, eps, a=None, b=None, *, threshold: float = 1e-3,
+                           max_iters: int = 2000, inner_iters: int = 10, g_init=None,
+                           comm=None, x_is_local: bool = False, n_total: int | None = None,
+                           impl: str = "auto", gather_f: bool = False) -> ShardedSinkhornOutput:
+    """Row-sharded ``solve_sinkhorn`` on a point cloud (one rank per GPU):
+    ``ShardedProblem(x, y, a, b, ...).solve(eps, ...)``."""
     if max_iters < 1 or inner_iters < 1:
         raise ValueError("max_iters and inner_iters must be >= 1")
     if not (threshold > 0):
         raise ValueError("threshold must be positive")
-    sched = eps if isinstance(eps, EpsilonSchedule) else EpsilonSchedule(float(eps))
-    _fp32_guard(sched, inner_iters, max_iters)
-    comm = comm or TorchComm()
-    if x_is_local:
-        if n_total is None:
-            raise ValueError("n_total is required with x_is_local")
-        sizes = comm.all_gather_host(np.array([float(x.shape[0])]), _dev_of(x))[:, 0].astype(int)
-        lo = int(sizes[:comm.rank].sum())
-        hi = lo + int(x.shape[0])
-        if int(sizes.sum()) != n_total:
-            raise ValueError("local shards do not add up to n_total")
-        x_local = x
-    else:
-        n_total = int(x.shape[0])
-        lo, hi = shard_rows(n_total, comm.world, comm.rank)
-        x_local = x[lo:hi]
-    m = int(y.shape[0])
-    a_loc = _global_weights(a, n_total, lo, hi, "a")
-    b_w = _global_weights(b, m, 0, m, "b")
-    tot_a = comm.all_gather_host(np.array([a_loc.sum()]), _dev_of(x))[:, 0].sum()
-    if abs(tot_a - 1.0) > 1e-8 or abs(b_w.sum() - 1.0) > 1e-8:
-        raise ValueError("a and b must each sum to 1")
-    flags = _impl_flags(impl)
-    dev = _dev_of(x)
-
-    def amax_reduce(v):  # one common split scale on every rank
-        return float(comm.all_gather_host(np.array([v]), dev)[:, 0].max())
-
-    eng = CudaShardEngine(x_local, y, a_loc, b_w, flags=flags, amax_reduce=amax_reduce)
-    which, iters, conv, errs, duals = sharded_loop(eng, comm, sched, threshold, max_iters,
-                                                   inner_iters, g_init)
-    f_dev = eng.f_result(which)
-    g_dev = eng.g_result()
-    f_full = None
-    if gather_f:
-        import torch
-        width = -(-n_total // comm.world) + 1
-        pad = torch.full((width,), float("nan"), dtype=torch.float32, device=f_dev.device)
-        pad[: hi - lo] = f_dev
-        allf = comm.all_gather_rows(pad).cpu().numpy().astype(np.float64)
-        f_full = np.concatenate([allf[r, : shard_rows(n_total, comm.world, r)[1]
-                                       - shard_rows(n_total, comm.world, r)[0]]
-                                 for r in range(comm.world)])
-    return ShardedSinkhornOutput(
-        f_local=f_dev.cpu().numpy().astype(np.float64), g=g_dev.cpu().numpy().astype(np.float64),
-        errors=errs, dual_trace=duals, iterations=iters, converged=conv, eps=sched.target,
-        row_offset=lo, n_total=n_total, f=f_full, f_device=f_dev, g_device=g_dev)
+    prob = ShardedProblem(x, y, a, b, comm=comm, x_is_local=x_is_local, n_total=n_total,
+                          impl=impl)
+    return prob.solve(eps, threshold=threshold, max_iters=max_iters, inner_iters=inner_iters,
+                      g_init=g_init, gather_f=gather_f)
 
 
 def _dev_of(x):
