@@ -313,10 +313,17 @@ def dense_roofline(C, wl, reps=5):
     pk, pk_kind = peaks()
     nbytes = 4.0 * B * n * m
     gbs = nbytes / sec / 1e9
+    import ctypes
+    read_gbs = ctypes.c_double()
+    N.check(lib.otk_bench_read(N.ptr(C), int(nbytes), ctypes.byref(read_gbs), stream()))
     return {"bound": "hbm", "achieved": gbs, "peak": float(pk["hbm_gbs"]), "unit": "GB/s",
             "frac": gbs / float(pk["hbm_gbs"]), "traffic": traffic_for(wl.name),
             "kernel": "otk_dense_lse (batched rows half-step)", "kernel_ms": sec * 1e3,
-            "algorithmic_bytes_per_launch": nbytes, "peak_note": pk_kind}
+            "algorithmic_bytes_per_launch": nbytes, "peak_note": pk_kind,
+            "read_only_gbs": read_gbs.value,
+            "read_only_frac": gbs / read_gbs.value,
+            "read_only_note": "best streaming-read rate of the same buffer on this GPU "
+                              "(otk_bench_read): the kernel only reads C"}
 
 
 # ------------------------------------------------------------------ our arm

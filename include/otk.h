@@ -237,6 +237,10 @@ size_t otk_solve_workspace_bytes(const otk_solve_args *args);
  * MUFU ex2 results/s and FP32 FFMA/s (full chip, best of 3). */
 int otk_bench_pipes(double *ex2_per_s, double *ffma_per_s, void *stream);
 
+/* Streaming-read microbenchmark: best-of-5 HBM read rate (GB/s) over `bytes`
+ * of `buf` -- the achievable bound of the materialised-cost half-steps. */
+int otk_bench_read(const float *buf, int64_t bytes, double *gbs, void *stream);
+
 /* Whole solve_sinkhorn (sinkhorn.py:122-200) on device.  Returns OTK_OK,
  * OTK_DIVERGED (fail_iter = t) or OTK_BAD_POTENTIAL (fail_iter = t).
  * Small FP32-path problems with a constant eps (both point sets fit in one

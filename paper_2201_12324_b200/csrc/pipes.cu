@@ -36,9 +36,58 @@ __global__ void __launch_bounds__(256) fma_pipe_kernel(float *out, int iters, fl
   if (s == 12345.f) out[threadIdx.x] = s;
 }
 
+// Streaming read of a buffer (float4, grid-stride, 8 loads in flight per thread):
+// the achievable HBM READ rate that bounds the materialised-cost half-steps.
+__global__ void __launch_bounds__(256) read_bw_kernel(const float4 *__restrict__ p, int64_t n4,
+                                                      float *out) {
+  float acc = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + 7 * stride < n4; i += 8 * stride) {
+    float4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcs(p + i + k * stride);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += v[k].x + v[k].y + v[k].z + v[k].w;
+  }
+  for (; i < n4; i += stride) {
+    const float4 v = __ldcs(p + i);
+    acc += v.x + v.y + v.z + v.w;
+  }
+  if (acc == 12345.f) out[0] = acc;
+}
+
 }  // namespace otk
 
 using namespace otk;
+
+extern "C" int otk_bench_read(const float *buf, int64_t bytes, double *gbs, void *stream) {
+  OTK_CHECK_ARG(buf && gbs && bytes >= 16, "otk_bench_read: bad arguments");
+  cudaStream_t st = as_stream(stream);
+  float *scratch = nullptr;
+  OTK_CUDA(cudaMallocAsync(&scratch, sizeof(float), st));
+  cudaEvent_t e0, e1;
+  OTK_CUDA(cudaEventCreate(&e0));
+  OTK_CUDA(cudaEventCreate(&e1));
+  const int64_t n4 = bytes / 16;
+  const int blocks = num_sms() * 8;
+  double best = 0.0;
+  for (int rep = 0; rep < 6; ++rep) {
+    cudaEventRecord(e0, st);
+    read_bw_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4 *>(buf), n4, scratch);
+    cudaEventRecord(e1, st);
+    OTK_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0) best = std::max(best, (double)(n4 * 16) / (ms * 1e-3) / 1e9);
+  }
+  *gbs = best;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  OTK_CUDA(cudaFreeAsync(scratch, st));
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}
 
 extern "C" int otk_bench_pipes(double *ex2_per_s, double *ffma_per_s, void *stream) {
   OTK_CHECK_ARG(ex2_per_s && ffma_per_s, "otk_bench_pipes: null output");
