@@ -54,10 +54,13 @@ int small_solve_launch(const small::Args &A, bool same, cudaStream_t st);
 
 using namespace otk;
 
-// tcgen05 kernel for every d >= 4 (measured on B200 at n = m = 65536: 1.70 ms
-// per half-step for any d <= 64, vs 3.3 / 4.4 / 6.4 / 12.4 ms for the FP32
-// kernel at d = 2-3 / 8 / 16 / 31); FP32 FMA kernel for d <= 3.
-constexpr int kTcMinDim = 4;
+// tcgen05 kernel for every d (measured on B200 at n = m = 65536, ncu in
+// profiles/r01_ncu_route_*.txt: 1.40 ms per half-step at d = 3 and 1.50 ms at
+// d = 64, vs 2.27 ms for the FP32 low-d kernel at d = 3 -- issue-bound, 81 %
+// issue / 52 % MUFU -- and 6.4 ms for the tiled FP32 kernel at d = 16).  The
+// FP32 kernels remain for OTK_IMPL_SIMT and inside the persistent small-problem
+// solve (solve_small.cu), which the solver prefers whenever it fits.
+constexpr int kTcMinDim = 1;
 static bool want_tc(int flags, int d) {
   if (flags & OTK_IMPL_SIMT) return false;
   if (flags & OTK_IMPL_TC) return true;
