@@ -135,3 +135,32 @@ def test_cta_pair_kernel_is_bitwise_the_single_cta_kernel(otk, n, m, d, monkeypa
         geom.impl_flags = N.OTK_IMPL_TC
         outs.append((geom.apply_lse_kernel(f, g, eps, "rows"), geom.apply_lse_kernel(f, g, eps, "cols")))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_tc_random_shapes_every_d(otk, seed):
+    """The tcgen05 kernel serves every d: random n, m (odd, tiny, tile-crossing)
+    and d (1 .. 300, across the V1 / pair / V2 / V4 layouts) against the float64
+    oracle, both axes, including -inf potentials (zero weights)."""
+    rng = np.random.default_rng(1000 + seed)
+    d = int(rng.choice([1, 2, 3, 5, 17, 63, 64, 65, 100, 127, 128, 129, 200, 300]))
+    n = int(rng.integers(1, 700))
+    m = int(rng.integers(1, 700))
+    x = (rng.standard_normal((n, d)) * rng.uniform(0.2, 3.0)).astype(np.float32)
+    y = (rng.standard_normal((m, d)) * rng.uniform(0.2, 3.0) + rng.uniform(-1, 1)).astype(np.float32)
+    geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64))
+    eps = float(rng.uniform(0.02, 0.2)) * float(np.mean(geom64.cost_matrix()) + 1e-3)
+    f = (rng.standard_normal(n) * eps).astype(np.float32).astype(np.float64)
+    g = (rng.standard_normal(m) * eps).astype(np.float32).astype(np.float64)
+    if n > 3:
+        f[rng.integers(0, n)] = -np.inf
+    if m > 3:
+        g[rng.integers(0, m)] = -np.inf
+    ref_r = geom64.apply_lse_kernel(f, g, eps, "rows")
+    ref_c = geom64.apply_lse_kernel(f, g, eps, "cols")
+    tr, tcol = _half_steps(otk, x, y, f, g, eps, "tc")
+    for got, ref in ((tr, ref_r), (tcol, ref_c)):
+        fin = np.isfinite(ref)
+        assert np.array_equal(np.isfinite(got), fin)
+        scale = max(np.max(np.abs(ref[fin])), eps)
+        assert np.max(np.abs(got[fin] - ref[fin])) / scale <= 1e-5, (n, m, d)
