@@ -192,6 +192,24 @@ int otk_check_batched(const float *f_prev, const float *f_next, const float *a,
                       int64_t batch, const float *eps, const int32_t *active,
                       double *out, void *stream);
 
+/* K3p -- B independent stored-cost problems, each solved by ONE CTA from
+ * start to finish (sinkhorn.py:151-200 per problem; constant eps): no host
+ * round trip, each problem stops at its own convergence.  Inputs [B,n,m]
+ * cost, [B,n]/[B,m] weights and log-weights, eps [B] (float32 for the
+ * kernel, float64 for the check), optional g_init [B,m].  Outputs f [B,n],
+ * g [B,m], errors/duals [B, max_checks] (device), state [B,5] = n_checks,
+ * iterations, converged, status (OTK_OK / OTK_DIVERGED / OTK_BAD_POTENTIAL),
+ * fail_iter.  grid <= 0: one CTA per problem.  Requires m % 4 == 0 and
+ * otk_dense_solve_fits(n, m). */
+int otk_dense_solve_fits(int64_t n, int64_t m);
+int otk_solve_dense_batched(const float *cost, int64_t batch, int64_t n, int64_t m,
+                            const float *a, const float *b, const float *log_a,
+                            const float *log_b, const float *eps, const double *eps_d,
+                            const float *g_init, double threshold, int32_t max_iters,
+                            int32_t inner_iters, int32_t max_checks, float *f_out,
+                            float *g_out, double *errors, double *duals, int32_t *state,
+                            int32_t grid, void *stream);
+
 /* transport_matrix for a stored cost (sinkhorn.py:203-207), one problem. */
 int otk_dense_plan(const float *cost, int64_t n, int64_t m, const float *f,
                    const float *g, double eps, float *plan, void *stream);

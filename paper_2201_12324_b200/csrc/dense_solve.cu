@@ -1,0 +1,359 @@
+// K3p -- many small stored-cost problems (BASELINE configs[2]: 512 x 512^2),
+// each solved ENTIRELY by one CTA: the reference loop sinkhorn._sinkhorn_iterations
+// (reference sinkhorn.py:151-200) over DenseGeometry.apply_lse_kernel
+// (geometry.py:204-211) with its check (175-189) and _dual_objective (115-119),
+// per problem, with no host round trip and no grid-wide synchronisation
+// (problems are independent, so each CTA stops when ITS problem converges).
+//
+// A problem's potentials live in shared memory; its cost matrix (1 MiB at
+// 512 x 512) is read from global memory once per half-step -- from L2 after
+// the first touch as long as the problems in flight fit the 126 MB L2.
+// Rows half-step: one warp per row, lanes stride the row with 128-bit loads,
+// two rows per pass.  Columns half-step on the SAME row-major C: a warp owns
+// 128 consecutive columns (a float4 per lane) for one group of rows and keeps
+// a per-column online log2-sum-exp2; the row groups merge in fixed order.
+// The fused check computes f_{t+1} and r_i = a_i exp((f_t - f_{t+1})/eps).
+// Failure semantics follow the lock-step loop (sinkhorn._dense_loop): the
+// first half-step to emit NaN/+inf is recorded by step number.
+#include <algorithm>
+
+#include "otk_common.cuh"
+
+namespace otk {
+namespace dsolve {
+
+constexpr int THREADS = 512, WARPS = THREADS / 32, NV = 8;
+
+struct Args {
+  const float *C;
+  int64_t batch;
+  int n, m;
+  const float *a, *b, *la, *lb, *eps, *g_init;
+  const double *eps_d;
+  double threshold;
+  int max_iters, inner_iters, max_checks;
+  float *f_out, *g_out;
+  double *errors, *duals;
+  int *state;  // [B][5]: n_checks, iterations, converged, status, fail_iter
+};
+
+__device__ __forceinline__ void block_sum(double (&v)[NV], double *red /* [NV][WARPS] */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) red[k * WARPS + warp] = x;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double x = 0.0;
+    for (int w = 0; w < WARPS; ++w) x += red[k * WARPS + w];  // fixed order
+    v[k] = x;
+  }
+}
+
+// rows half-step: out_i = eps log w_i - eps ln2 LSE2_j(by_j - kappa C_ij); bx_i = kappa out_i
+template <bool CHECK>
+__device__ void rows_half(const float *__restrict__ Cb, int n, int m, const float *by, const float *lw,
+                          float eps, float kappa, float *out, float *bx, int *fbad, int step,
+                          const float *fprev, const float *a, double eps_d, double (&chk)[NV]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i0 = warp * 2; i0 < n; i0 += WARPS * 2) {
+    Lse2 st[2];
+    st[0].init();
+    st[1].init();
+    for (int j0 = 0; j0 < m; j0 += 512) {
+      float4 c4[2][4];
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = j0 + (q * 32 + lane) * 4;
+          const int i = min(i0 + r, n - 1);
+          c4[r][q] = (j < m) ? __ldg(reinterpret_cast<const float4 *>(Cb + (int64_t)i * m + j))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        float u[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = j0 + (q * 32 + lane) * 4;
+          if (j < m) {
+            const float4 h = *reinterpret_cast<const float4 *>(by + j);
+            u[4 * q + 0] = fmaf(-kappa, c4[r][q].x, h.x);
+            u[4 * q + 1] = fmaf(-kappa, c4[r][q].y, h.y);
+            u[4 * q + 2] = fmaf(-kappa, c4[r][q].z, h.z);
+            u[4 * q + 3] = fmaf(-kappa, c4[r][q].w, h.w);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) u[4 * q + e] = -INFINITY;
+          }
+        }
+        float cm = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) cm = fmaxf(cm, u[e]);
+        if (cm > st[r].m) {
+          st[r].s *= ex2(st[r].m - cm);
+          st[r].m = cm;
+        }
+        const float ms = (st[r].m == -INFINITY) ? 0.f : st[r].m;
+        float acc = 0.f;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc += ex2(u[e] - ms);
+        st[r].s += acc;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, st[r].m, o);
+        const float s2 = __shfl_xor_sync(0xffffffffu, st[r].s, o);
+        st[r].merge(m2, s2);
+      }
+      const int i = i0 + r;
+      if (lane == 0 && i < n) {
+        const float v = eps * lw[i] - eps * kLn2 * st[r].value();
+        out[i] = v;
+        bx[i] = v * kappa;
+        if (bad_potential(v)) atomicMin(fbad, step);
+        if (CHECK) {
+          const double fp = fprev[i], ai = a[i];
+          const double rr = (ai > 0.0) ? ai * exp((fp - (double)v) / eps_d) : 0.0;
+          chk[0] += fabs(rr - ai);
+          chk[1] += rr;
+          if (ai > 0.0) chk[2] += ai * fp;
+          chk[4] += (fp != fp) ? 1.0 : 0.0;
+          chk[6] += (fp == INFINITY) ? 1.0 : 0.0;
+        }
+      }
+    }
+  }
+}
+
+// columns half-step on row-major C: out_j = eps log b_j - eps ln2 LSE2_i(bx_i - kappa C_ij)
+__device__ void cols_half(const float *__restrict__ Cb, int n, int m, const float *bx, const float *lw,
+                          float eps, float kappa, float *out, float *by, int *fbad, int step,
+                          float *part /* [groups x block columns][2] */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int cb0 = 0; cb0 < m; cb0 += 512) {          // column block of up to 512 columns
+    const int ncols = min(512, m - cb0);
+    const int cwarps = (ncols + 127) / 128;          // warps per row group
+    const int groups = WARPS / cwarps;               // row groups
+    const int cw = warp % cwarps, rg = warp / cwarps;
+    const int j = cb0 + cw * 128 + lane * 4;         // this lane's 4 columns
+    const bool active = rg < groups && j < m;
+    float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, sm[4] = {0.f, 0.f, 0.f, 0.f};
+    if (active) {
+      const int rows_per = (n + groups - 1) / groups;
+      const int r0 = rg * rows_per, r1 = min(n, r0 + rows_per);
+      for (int i = r0; i < r1; i += 8) {
+        float4 c[8];
+        float h[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int ii = min(i + k, r1 - 1);
+          c[k] = __ldg(reinterpret_cast<const float4 *>(Cb + (int64_t)ii * m + j));
+          h[k] = (i + k < r1) ? bx[ii] : -INFINITY;
+        }
+        float u[4][8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          u[0][k] = fmaf(-kappa, c[k].x, h[k]);
+          u[1][k] = fmaf(-kappa, c[k].y, h[k]);
+          u[2][k] = fmaf(-kappa, c[k].z, h[k]);
+          u[3][k] = fmaf(-kappa, c[k].w, h[k]);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float cm = -INFINITY;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) cm = fmaxf(cm, u[e][k]);
+          if (cm > mx[e]) {
+            sm[e] *= ex2(mx[e] - cm);
+            mx[e] = cm;
+          }
+          const float ms = (mx[e] == -INFINITY) ? 0.f : mx[e];
+          float acc = 0.f;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc += ex2(u[e][k] - ms);
+          sm[e] += acc;
+        }
+      }
+    }
+    const int pstride = cwarps * 128;  // groups * pstride <= WARPS * 128
+    if (rg < groups) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int jj = cw * 128 + lane * 4 + e;
+        part[(rg * pstride + jj) * 2] = mx[e];
+        part[(rg * pstride + jj) * 2 + 1] = sm[e];
+      }
+    }
+    __syncthreads();
+    for (int jj = threadIdx.x; jj < ncols; jj += THREADS) {
+      Lse2 st;
+      st.m = part[jj * 2];
+      st.s = part[jj * 2 + 1];
+      for (int g = 1; g < groups; ++g)
+        st.merge(part[(g * pstride + jj) * 2], part[(g * pstride + jj) * 2 + 1]);
+      const int jg = cb0 + jj;
+      const float v = eps * lw[jg] - eps * kLn2 * st.value();
+      out[jg] = v;
+      by[jg] = v * kappa;
+      if (bad_potential(v)) atomicMin(fbad, step);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 1) dense_solve_kernel(Args A) {
+  extern __shared__ __align__(16) float sh[];
+  const int n = A.n, m = A.m;
+  const int n4 = (n + 3) & ~3, m4 = (m + 3) & ~3;  // 16-byte aligned segments
+  float *f0 = sh, *f1 = f0 + n4, *g = f1 + n4, *bx = g + m4, *by = bx + n4;
+  float *part = by + m4;  // [row groups][<= 2048 columns total][2]
+  __shared__ double red[NV * WARPS];
+  __shared__ int fbad, decide;
+  __shared__ double tot[NV];
+  for (int64_t b = blockIdx.x; b < A.batch; b += gridDim.x) {
+    const float *Cb = A.C + b * (int64_t)n * m;
+    const float *a = A.a + b * n, *bw = A.b + b * m;
+    const float *la = A.la + b * n, *lb = A.lb + b * m;
+    const float eps = A.eps[b];
+    const double eps_d = A.eps_d[b];
+    const float kappa = kLog2e / eps;
+    if (threadIdx.x == 0) fbad = 0x7fffffff;
+    __syncthreads();
+    for (int j = threadIdx.x; j < m; j += THREADS) {
+      const float g0 = A.g_init ? A.g_init[b * m + j] : 0.f;
+      g[j] = g0;
+      by[j] = g0 * kappa;
+      if (bad_potential(g0)) atomicMin(&fbad, 1);
+    }
+    __syncthreads();
+    float *f = f0, *fn = f1;
+    bool f_ready = false;
+    int n_checks = 0, status = OTK_OK, fail_iter = 0, converged = 0, t;
+    double chk[NV];
+    for (t = 1; t <= A.max_iters; ++t) {
+      if (!f_ready) {
+        rows_half<false>(Cb, n, m, by, la, eps, kappa, f, bx, &fbad, 2 * t, nullptr, a, eps_d, chk);
+        __syncthreads();
+      }
+      f_ready = false;
+      cols_half(Cb, n, m, bx, lb, eps, kappa, g, by, &fbad, 2 * t + 1, part);  // ends synced
+      if (t % A.inner_iters == 0 || t == A.max_iters) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) chk[k] = 0.0;
+        rows_half<true>(Cb, n, m, by, la, eps, kappa, fn, bx, &fbad, 2 * t + 2, f, a, eps_d, chk);
+        for (int j = threadIdx.x; j < m; j += THREADS) {
+          const double gj = g[j], bj = bw[j];
+          if (bj > 0.0) chk[3] += bj * gj;
+          chk[5] += (gj != gj) ? 1.0 : 0.0;
+          chk[7] += (gj == INFINITY) ? 1.0 : 0.0;
+        }
+        block_sum(chk, red);  // contains a __syncthreads: fbad is final for this check
+        if (threadIdx.x == 0) {
+          int d = 0;  // 0 continue, 1 converged, 2 bad potential, 3 diverged
+          if (fbad <= 2 * t) {
+            d = 2;
+            fail_iter = (fbad + 1) / 2;
+          } else if (chk[4] > 0 || chk[5] > 0) {
+            d = 3;
+            fail_iter = t;
+          } else if (fbad == 2 * t + 1) {
+            d = 2;
+            fail_iter = t;
+          } else {
+            if (n_checks < A.max_checks) {
+              A.errors[b * A.max_checks + n_checks] = chk[0];
+              A.duals[b * A.max_checks + n_checks] = chk[2] + chk[3] - eps_d * (chk[1] - 1.0);
+            }
+            if (chk[0] <= A.threshold) d = 1;
+          }
+          decide = d;
+          tot[0] = (double)fail_iter;
+        }
+        __syncthreads();
+        const int d = decide;
+        if (d == 2 || d == 3) {
+          status = (d == 2) ? OTK_BAD_POTENTIAL : OTK_DIVERGED;
+          fail_iter = (int)tot[0];
+          break;
+        }
+        ++n_checks;
+        if (d == 1) {
+          converged = 1;
+          break;
+        }
+        if (t < A.max_iters) {
+          float *tmp = f;
+          f = fn;
+          fn = tmp;
+          f_ready = true;
+        }
+        __syncthreads();  // decide / tot / red reused by the next check
+      }
+    }
+    for (int i = threadIdx.x; i < n; i += THREADS) A.f_out[b * n + i] = f[i];
+    for (int j = threadIdx.x; j < m; j += THREADS) A.g_out[b * m + j] = g[j];
+    if (threadIdx.x == 0) {
+      int *s = A.state + b * 5;
+      s[0] = min(n_checks, A.max_checks);
+      s[1] = min(t, A.max_iters);
+      s[2] = converged;
+      s[3] = status;
+      s[4] = fail_iter;
+    }
+    __syncthreads();
+  }
+}
+
+size_t smem_bytes(int n, int m) {
+  const size_t n4 = (n + 3) & ~3, m4 = (m + 3) & ~3;
+  return (3 * n4 + 2 * m4) * sizeof(float) + (size_t)WARPS * 128 * 2 * sizeof(float);
+}
+
+}  // namespace dsolve
+}  // namespace otk
+
+using namespace otk;
+
+extern "C" int otk_dense_solve_fits(int64_t n, int64_t m) {
+  if (n < 1 || m < 1 || m % 4 != 0 || n > 16384 || m > 16384) return 0;
+  int dev = 0, max_smem = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return dsolve::smem_bytes((int)n, (int)m) + 4096 <= (size_t)max_smem ? 1 : 0;
+}
+
+extern "C" int otk_solve_dense_batched(const float *cost, int64_t batch, int64_t n, int64_t m,
+                                       const float *a, const float *b, const float *log_a,
+                                       const float *log_b, const float *eps, const double *eps_d,
+                                       const float *g_init, double threshold, int32_t max_iters,
+                                       int32_t inner_iters, int32_t max_checks, float *f_out,
+                                       float *g_out, double *errors, double *duals, int32_t *state,
+                                       int32_t grid, void *stream) {
+  OTK_CHECK_ARG(cost && a && b && log_a && log_b && eps && eps_d && f_out && g_out && errors &&
+                    duals && state && batch > 0,
+                "otk_solve_dense_batched: bad arguments");
+  OTK_CHECK_ARG(otk_dense_solve_fits(n, m), "otk_solve_dense_batched: n, m unsupported (m %% 4, smem)");
+  OTK_CHECK_ARG(max_iters >= 1 && inner_iters >= 1 && max_checks >= 1 && threshold > 0,
+                "otk_solve_dense_batched: bad loop parameters");
+  dsolve::Args A{cost, batch, (int)n, (int)m, a, b, log_a, log_b, eps, g_init, eps_d, threshold,
+                 max_iters, inner_iters, max_checks, f_out, g_out, errors, duals, state};
+  const size_t smem = dsolve::smem_bytes((int)n, (int)m);
+  OTK_CUDA(cudaFuncSetAttribute(dsolve::dense_solve_kernel,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // default: one CTA per problem (measured on cfg3, 512 problems: grid 128 / 148 / 296 / 512 ->
+  // 6.13 / 6.47 / 6.31 / 5.69 ms per batched solve; the lock-step loop 8.59 ms)
+  const int g = (int)std::min<int64_t>(std::min<int64_t>(batch, 65535), grid > 0 ? grid : batch);
+  dsolve::dense_solve_kernel<<<g, dsolve::THREADS, smem, as_stream(stream)>>>(A);
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}

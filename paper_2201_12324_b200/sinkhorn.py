@@ -23,6 +23,7 @@ import logging
 from typing import NamedTuple
 
 import ctypes
+import os
 from collections.abc import Sequence
 
 import numpy as np
@@ -436,6 +437,43 @@ def _dense_loop(C, CT, weights, scheds, threshold, max_iters, inner_iters, g_ini
                                  g_fin)
 
 
+def _dense_persistent(C, weights, eps, threshold, max_iters, inner_iters, g_init=None):
+    """B stored-cost problems, one CTA each, the whole loop on the device
+    (csrc/dense_solve.cu, otk_solve_dense_batched); same per-problem results,
+    iteration counts, traces and failure exceptions as ``_dense_loop``."""
+    import torch
+    B, n, m = C.shape
+    dev = C.device
+    a, b, la, lb = (w.reshape(B, -1).contiguous() for w in weights)
+    max_checks = max_iters // inner_iters + 2
+    eps32 = torch.as_tensor(eps.astype(np.float32), device=dev)
+    eps64 = torch.as_tensor(eps.astype(np.float64), device=dev)
+    gi = None if g_init is None else as_device_f32(g_init).reshape(B, m).contiguous()
+    f_out = torch.empty((B, n), dtype=torch.float32, device=dev)
+    g_out = torch.empty((B, m), dtype=torch.float32, device=dev)
+    errs = torch.zeros((B, max_checks), dtype=torch.float64, device=dev)
+    duals = torch.zeros_like(errs)
+    state = torch.zeros((B, 5), dtype=torch.int32, device=dev)
+    grid = int(os.environ.get("OTK_DENSE_GRID", "0"))
+    N.check(N.lib().otk_solve_dense_batched(
+        N.ptr(C), B, n, m, N.ptr(a), N.ptr(b), N.ptr(la), N.ptr(lb), N.ptr(eps32), N.ptr(eps64),
+        N.ptr(gi), float(threshold), int(max_iters), int(inner_iters), max_checks, N.ptr(f_out),
+        N.ptr(g_out), N.ptr(errs), N.ptr(duals), N.ptr(state), grid, stream()),
+        "solve_sinkhorn_batched")
+    st = state.cpu().numpy()
+    failed = np.nonzero(st[:, 3] != N.OTK_OK)[0]
+    if len(failed):
+        k = failed[np.argmin(st[failed, 4])]
+        if st[k, 3] == N.OTK_BAD_POTENTIAL:
+            raise ValueError(f"problem {k}: g contains NaN or +inf entries")
+        raise DivergedError("NaN in Sinkhorn potentials; eps is likely too small for the cost scale",
+                            iteration=int(st[k, 4]))
+    return BatchedSinkhornOutput(f_out.cpu().numpy().astype(np.float64),
+                                 g_out.cpu().numpy().astype(np.float64), errs.cpu().numpy(),
+                                 duals.cpu().numpy(), st[:, 0].copy(), st[:, 1].copy(),
+                                 st[:, 2].astype(bool), np.asarray(eps, dtype=float), f_out, g_out)
+
+
 def solve_sinkhorn_batched(x, y, eps, a=None, b=None, *, threshold: float = 1e-3,
                            max_iters: int = 2000, inner_iters: int = 10, return_cost: bool = False,
                            g_init=None):
@@ -475,12 +513,17 @@ def solve_sinkhorn_batched(x, y, eps, a=None, b=None, *, threshold: float = 1e-3
             return ww, as_device_f32(ww), as_device_f32(np.log(ww))
     aw, a_d, la_d = weights_of(a, n, "a")
     bw, b_d, lb_d = weights_of(b, m, "b")
+    persistent = bool(N.lib().otk_dense_solve_fits(n, m)) and not os.environ.get("OTK_DENSE_LOCKSTEP")
     C = torch.empty((B, n, m), dtype=torch.float32, device=dev)
-    CT = torch.empty((B, m, n), dtype=torch.float32, device=dev)
+    CT = None if persistent else torch.empty((B, m, n), dtype=torch.float32, device=dev)
     N.check(N.lib().otk_dense_cost(N.ptr(xd), N.ptr(yd), B, n, m, d, 0, N.ptr(C), N.ptr(CT),
                                    stream()), "dense_cost")
-    outs = _dense_loop(C, CT, (a_d, b_d, la_d, lb_d), scheds, threshold, max_iters, inner_iters,
-                       g_init=g_init)
+    if persistent:
+        outs = _dense_persistent(C, (a_d, b_d, la_d, lb_d), np.asarray(eps, dtype=float), threshold,
+                                 max_iters, inner_iters, g_init)
+    else:
+        outs = _dense_loop(C, CT, (a_d, b_d, la_d, lb_d), scheds, threshold, max_iters,
+                           inner_iters, g_init=g_init)
     if not return_cost:
         return outs
     costs = _dense_costs(C, outs, aw, bw)
