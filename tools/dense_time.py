@@ -19,5 +19,5 @@ C = torch.empty((B, n, m), dtype=torch.float32, device=dev)
 N.check(N.lib().otk_dense_cost(N.ptr(xd), N.ptr(yd), B, n, m, d, 0, N.ptr(C), None,
                                torch.cuda.current_stream().cuda_stream))
 r = bench.dense_roofline(C, wl, reps=20)
-print(f"dense rows: {r['kernel_ms'] * 1e3:.1f} us  {r['achieved']:.0f} GB/s  frac {r['frac']:.3f}  "
+print(f"{r['kernel']}: {r['kernel_ms'] * 1e3:.1f} us  {r['achieved']:.0f} GB/s  frac {r['frac']:.3f}  "
       f"read-only roof {r['read_only_gbs']:.0f} GB/s -> {r['read_only_frac']:.3f}")
