@@ -6,6 +6,7 @@ Every computation runs in libotk_sm100.so (hand-written CUDA for sm_100a,
 C ABI in include/otk.h); there is no CPU fallback.
 """
 
+from .barycenter import BarycenterOutput, BarycenterProblem, solve_barycenter
 from .errors import DivergedError, OtkitError
 from .geometry import (
     COST_FNS,
@@ -56,4 +57,7 @@ __all__ = [
     "solve_sinkhorn_sharded",
     "reg_ot_cost_sharded",
     "ShardedProblem",
+    "BarycenterProblem",
+    "BarycenterOutput",
+    "solve_barycenter",
 ]

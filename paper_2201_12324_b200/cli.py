@@ -14,8 +14,17 @@ cost is computed online (no 4e6-entry cap), and the n x m coupling is only
 materialised when --coupling-out asks for it (the reference always builds
 it, cli.py:157, so it refuses every problem above the cap).  The low-rank
 solver, the LP ``--verify`` oracle, the eucl cost and the other
-subcommands (quad, barycenter, softsort, gmm) are outside this build's hot
-path and exit with an input error.
+subcommands (quad, softsort, gmm) are outside this build's hot path and exit
+with an input error.
+
+    python -m paper_2201_12324_b200 barycenter --support S.csv --hist H1.csv
+        --hist H2.csv [--weights 0.3,0.7 | --weights W.csv] [--cost sqeucl|cosine]
+        [--eps E | --eps-rel R] [--threshold T] [--max-iters N]
+        [--barycenter-out P.csv] [--out summary.json]
+
+mirrors the reference's barycenter subcommand (cli.py:233-273) on the
+one-launch GPU solve (csrc/bary.cu); ``--grid`` (separable GridGeometry)
+is not part of this build.
 """
 
 from __future__ import annotations
@@ -159,9 +168,62 @@ def _cmd_lin(args) -> int:
     return 0 if payload["converged"] else 2
 
 
+def _parse_weights_arg(raw: str | None, size: int):
+    """cli.py:262-272: a CSV path or comma-separated floats, checked like weights."""
+    if raw is None:
+        return None
+    if os.path.exists(raw):
+        w = read_vector(raw)
+    else:
+        try:
+            w = np.array([float(tok) for tok in raw.split(",")])
+        except ValueError:
+            raise _InputError(f"--weights must be a CSV path or comma-separated floats, "
+                              f"got {raw!r}") from None
+    return _as_cli_weights(w, size, "weights")
+
+
+def _cmd_barycenter(args) -> int:
+    from .barycenter import BarycenterProblem, solve_barycenter
+    from .geometry import PointCloudGeometry
+    if (args.support is None) == (args.grid is None):
+        raise _InputError("provide either --support or --grid")
+    if args.grid is not None:
+        raise _InputError("--grid (separable GridGeometry) is outside this build's hot path")
+    if args.cost == "eucl":
+        raise _InputError("--cost eucl is outside this build's hot path (sqeucl, cosine)")
+    support = read_matrix(args.support)
+    geom = PointCloudGeometry(support, support, args.cost)
+    hists = np.stack([read_vector(p) for p in args.hist])
+    hists = np.stack([_as_cli_weights(h, geom.shape[0], f"histogram {i}")
+                      for i, h in enumerate(hists)])
+    weights = _parse_weights_arg(args.weights, hists.shape[0])
+    bp = BarycenterProblem(geom, hists, weights)
+    eps = _resolve_eps(args, geom)
+    opts = {}
+    if args.threshold is not None:
+        opts["threshold"] = args.threshold
+    if args.max_iters is not None:
+        opts["max_iters"] = args.max_iters
+    out = solve_barycenter(bp, eps, **opts)
+    payload = {
+        "command": "barycenter",
+        "converged": out.converged,
+        "iterations": out.iterations,
+        "eps": out.eps,
+        "num_histograms": int(hists.shape[0]),
+        "support_size": int(geom.shape[0]),
+        "barycenter": out.barycenter.tolist(),
+    }
+    if args.barycenter_out:
+        write_matrix_atomic(args.barycenter_out, out.barycenter.reshape(-1, 1))
+    _emit(args, payload)
+    return 0 if out.converged else 2
+
+
 def _unsupported(args) -> int:
     raise _InputError(f"subcommand {args.command!r} is outside this build's hot path "
-                      "(only 'lin' with the Sinkhorn solver is provided)")
+                      "(only 'lin' with the Sinkhorn solver and 'barycenter' are provided)")
 
 
 def _build_parser() -> argparse.ArgumentParser:
@@ -186,7 +248,21 @@ def _build_parser() -> argparse.ArgumentParser:
     lin.add_argument("--max-iters", type=int, help="solver iteration cap")
     lin.add_argument("--out", help="write the JSON summary here instead of stdout")
     lin.set_defaults(handler=_cmd_lin)
-    for name in ("quad", "barycenter", "softsort", "gmm"):
+    bary = commands.add_parser("barycenter", help="fixed-support barycenter of histograms")
+    bary.add_argument("--support", help="support points CSV (dense mode)")
+    bary.add_argument("--grid", nargs="+", help="per-axis coordinate CSVs (not in this build)")
+    bary.add_argument("--cost", choices=("sqeucl", "eucl", "cosine"), default="sqeucl")
+    bary.add_argument("--hist", action="append", required=True,
+                      help="histogram CSV; repeat per input")
+    bary.add_argument("--weights", help="barycentric weights: comma-separated floats or a CSV path")
+    bary.add_argument("--barycenter-out", help="write the barycenter CSV here")
+    bary.add_argument("--eps", type=float, help="absolute regularization strength")
+    bary.add_argument("--eps-rel", type=float, help="regularization as a fraction of the mean cost")
+    bary.add_argument("--threshold", type=float, help="solver convergence threshold")
+    bary.add_argument("--max-iters", type=int, help="solver iteration cap")
+    bary.add_argument("--out", help="write the JSON summary here instead of stdout")
+    bary.set_defaults(handler=_cmd_barycenter)
+    for name in ("quad", "softsort", "gmm"):
         sub = commands.add_parser(name, help="(not in this build)")
         sub.set_defaults(handler=_unsupported)
     return parser
@@ -199,7 +275,7 @@ def main(argv: list[str] | None = None) -> int:
     parser = _build_parser()
     try:
         args, extra = parser.parse_known_args(argv)
-        if extra and args.command == "lin":
+        if extra and args.command in ("lin", "barycenter"):
             raise _InputError(f"unrecognized arguments: {' '.join(extra)}")
         return args.handler(args)
     except _InputError as err:

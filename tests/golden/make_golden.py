@@ -260,8 +260,75 @@ def spot_checks():
              f=fpot.astype(np.float32), rows_g0=rows_g0, rows_g=rows_g, cols_f=cols_f)
 
 
+def barycenter_cases():
+    """Fixed-support barycenters (otkit/barycenter.py:73-133), SURVEY.md §8f row 4.
+
+    Supports are fp32-representable (the GPU sees the same values); each case
+    stores its inputs and the reference's barycenter, log p, iterations and
+    converged flag.  The dense case uses a non-symmetric explicit cost.
+    """
+    res = {}
+
+    def line(n):
+        return np.linspace(0.0, 1.0, n).astype(np.float32).astype(np.float64)[:, None]
+
+    def dirac(n, i):
+        h = np.zeros(n)
+        h[i] = 1.0
+        return h
+
+    def rand_hists(rng, k, n, zero_frac=0.0):
+        h = rng.random((k, n))
+        if zero_frac:
+            h[rng.random((k, n)) < zero_frac] = 0.0
+        return h / h.sum(axis=1, keepdims=True)
+
+    rng = np.random.default_rng(4242)
+    cases = []
+    pts = line(21)
+    cases.append(("single", pts, None, rand_hists(np.random.default_rng(0), 1, 21), None, 1e-5, 1e-4, 1000))
+    pts = line(101)
+    cases.append(("diracs", pts, None, np.stack([dirac(101, 25), dirac(101, 75)]),
+                  np.array([0.3, 0.7]), 1e-3, 1e-4, 1000))
+    cases.append(("zeros", line(11), None, np.stack([dirac(11, 0), dirac(11, 10)]), None, 1e-3,
+                  1e-4, 1000))
+    pts = rng.standard_normal((64, 2)).astype(np.float32).astype(np.float64)
+    cases.append(("cloud2d", pts, None, rand_hists(rng, 3, 64), None, 0.05, 1e-4, 1000))
+    pts = rng.standard_normal((200, 3)).astype(np.float32).astype(np.float64)
+    w = rng.random(4)
+    cases.append(("cloud3d_zeros", pts, None, rand_hists(rng, 4, 200, 0.2), w / w.sum(), 0.02,
+                  1e-4, 1000))
+    pts = rng.standard_normal((130, 5)).astype(np.float32).astype(np.float64)
+    cases.append(("short", pts, None, rand_hists(rng, 2, 130), None, 0.01, 1e-6, 3))
+    cost = rng.uniform(0.0, 1.0, (50, 50)).astype(np.float32).astype(np.float64)
+    cases.append(("dense", None, cost, rand_hists(rng, 2, 50), np.array([0.6, 0.4]), 0.05, 1e-4,
+                  1000))
+    for name, support, cost, hists, weights, eps_rel, threshold, max_iters in cases:
+        if cost is None:
+            geom = otkit.PointCloudGeometry(support, support)
+        else:
+            geom = otkit.DenseGeometry(cost)
+        eps = eps_rel * geom.mean_cost()
+        bp = otkit.BarycenterProblem(geom, hists, weights)
+        out = otkit.solve_barycenter(bp, eps, threshold=threshold, max_iters=max_iters)
+        log_p = np.log(out.barycenter)  # normalised p; the stored target
+        res[f"{name}__support"] = support if support is not None else np.zeros((0, 1))
+        res[f"{name}__cost"] = cost if cost is not None else np.zeros((0, 0))
+        res[f"{name}__hists"] = hists
+        res[f"{name}__weights"] = bp.weights
+        res[f"{name}__eps"] = np.array(eps)
+        res[f"{name}__threshold"] = np.array(threshold)
+        res[f"{name}__max_iters"] = np.array(max_iters)
+        res[f"{name}__barycenter"] = out.barycenter
+        res[f"{name}__log_p"] = log_p
+        res[f"{name}__iterations"] = np.array(out.iterations)
+        res[f"{name}__converged"] = np.array(out.converged)
+        print(f"barycenter {name}: iters={out.iterations} converged={out.converged}")
+    save("barycenter", **res)
+
+
 def main():
-    which = sys.argv[1:] or ["lse", "known", "solve", "fixed", "dense", "spot"]
+    which = sys.argv[1:] or ["lse", "known", "solve", "fixed", "dense", "spot", "bary"]
     meta = dict(reference="/root/reference/pkg (otkit 0.1.0)", numpy=np.__version__,
                 scipy=scipy.__version__, python=platform.python_version(),
                 generated_by="tests/golden/make_golden.py", when=time.strftime("%Y-%m-%d"))
@@ -277,6 +344,8 @@ def main():
         dense_cases()
     if "spot" in which:
         spot_checks()
+    if "bary" in which:
+        barycenter_cases()
     with open(os.path.join(OUT, "MANIFEST.json"), "w") as fh:
         json.dump(meta, fh, indent=1)
 

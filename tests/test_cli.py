@@ -86,3 +86,46 @@ def test_cli_matches_library_and_oracle(tmp_path):
                          "--eps-rel", "0.05", "--max-iters", "3", "--out", str(out_json)],
                         cwd=ROOT).returncode
     assert rc == 2 and json.loads(out_json.read_text())["converged"] is False
+
+
+def test_barycenter_input_errors_exit_1(tmp_path, capsys):
+    s = _write(tmp_path / "s.csv", np.linspace(0, 1, 5)[:, None])
+    h = _write(tmp_path / "h.csv", np.full(5, 0.2))
+    bad = _write(tmp_path / "bad.csv", np.full(5, 0.3))
+    short = _write(tmp_path / "short.csv", np.full(4, 0.25))
+    assert cli.main(["barycenter", "--hist", h]) == 1                       # no support / grid
+    assert cli.main(["barycenter", "--grid", s, "--hist", h]) == 1          # grid not in build
+    assert cli.main(["barycenter", "--support", s, "--hist", bad]) == 1     # sums to 1.5
+    assert cli.main(["barycenter", "--support", s, "--hist", short]) == 1   # wrong length
+    assert cli.main(["barycenter", "--support", s, "--hist", h, "--hist", h,
+                     "--weights", "0.5,x"]) == 1
+    assert cli.main(["barycenter", "--support", s, "--hist", h, "--hist", h,
+                     "--weights", "0.5,0.6"]) == 1
+    assert cli.main(["barycenter", "--support", s, "--hist", h, "--cost", "eucl"]) == 1
+    assert cli.main(["barycenter", "--support", s, "--hist", h, "--eps", "1",
+                     "--eps-rel", "1"]) == 1
+    assert "error:" in capsys.readouterr().err
+
+
+@pytest.mark.gpu
+def test_barycenter_cli_matches_library(tmp_path, capsys):
+    """Reference test_cli.py:231-266 intent: the CLI JSON and CSV equal the library call."""
+    import paper_2201_12324_b200 as otk
+    pts = np.linspace(0.0, 1.0, 11)
+    h1, h2 = np.zeros(11), np.zeros(11)
+    h1[2] = 1.0
+    h2[8] = 1.0
+    support = _write(tmp_path / "support.csv", pts[:, None])
+    out_path = tmp_path / "bary.csv"
+    code = cli.main(["barycenter", "--support", support, "--hist", _write(tmp_path / "h1.csv", h1),
+                     "--hist", _write(tmp_path / "h2.csv", h2), "--weights", "0.5,0.5",
+                     "--eps-rel", "1e-3", "--barycenter-out", str(out_path)])
+    payload = json.loads(capsys.readouterr().out)
+    assert code == 0
+    geom = otk.PointCloudGeometry(pts[:, None], pts[:, None])
+    out = otk.solve_barycenter(otk.BarycenterProblem(geom, np.stack([h1, h2]), np.array([0.5, 0.5])),
+                               1e-3 * geom.mean_cost())
+    assert payload["barycenter"] == out.barycenter.tolist()
+    assert payload["iterations"] == out.iterations
+    np.testing.assert_array_equal(np.loadtxt(out_path, delimiter=","), out.barycenter)
+    assert int(np.argmax(out.barycenter)) == 5

@@ -115,3 +115,41 @@ def test_workload_eps_values_are_stable():
     # The quoted magnitudes from SURVEY.md §8d.
     assert abs(workloads.cfg1().eps - 0.339) < 0.01
     assert abs(workloads.cfg2(n=8192, m=8192).eps - 10.4) < 0.3
+
+
+def barycenter_cases():
+    """(name, dict) per barycenter fixture case (tests/golden/make_golden.py)."""
+    fx = load_golden("barycenter")
+    names = sorted({k.split("__")[0] for k in fx})
+    return [(nm, {k.split("__")[1]: v for k, v in fx.items() if k.startswith(nm + "__")})
+            for nm in names]
+
+
+def test_barycenter_oracle_matches_reference():
+    from oracle.barycenter_oracle import solve_barycenter
+    cases = barycenter_cases()
+    assert len(cases) == 7
+    for name, c in cases:
+        if c["cost"].size:
+            geom = oracle.DenseOracle(c["cost"])
+        else:
+            geom = oracle.PointCloudOracle(c["support"], c["support"])
+        p, conv, iters, _ = solve_barycenter(geom, c["hists"], c["weights"], float(c["eps"]),
+                                             float(c["threshold"]), int(c["max_iters"]))
+        assert iters == int(c["iterations"]), name
+        assert conv == bool(c["converged"]), name
+        np.testing.assert_allclose(p, c["barycenter"], rtol=1e-9, atol=1e-13, err_msg=name)
+
+
+def test_barycenter_oracle_validation():
+    from oracle.barycenter_oracle import solve_barycenter
+    geom = oracle.PointCloudOracle(np.linspace(0, 1, 5)[:, None], np.linspace(0, 1, 5)[:, None])
+    good = np.full((2, 5), 0.2)
+    for hists, w in ((np.full((2, 5), 0.3), None), (good, np.array([0.5, 0.6])),
+                     (np.full((2, 4), 0.25), None)):
+        with pytest.raises(ValueError):
+            solve_barycenter(geom, hists, w, 0.1)
+    with pytest.raises(ValueError):
+        solve_barycenter(oracle.DenseOracle(np.zeros((2, 3))), good, None, 0.1)
+    with pytest.raises(ValueError):
+        solve_barycenter(geom, good, None, -1.0)
