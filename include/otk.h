@@ -254,18 +254,23 @@ size_t otk_solve_workspace_bytes(const otk_solve_args *args);
 /* Fixed-support barycenter (otkit/barycenter.py:96-133, solve_barycenter; the
  * reference's per-iteration 3K apply_lse_kernel calls, barycenter.py:116-128)
  * as ONE persistent cooperative kernel over a materialised square support
- * cost: cost/cost_t [n, n] fp32 (otk_dense_cost / otk_dense_transpose),
- * log2_hists [K, n] fp32 (log2 of the histograms, -inf for zeros), weights
- * [K] f64.  Workspaces F, G, B: [K, n] fp32 each; part: otk_barycenter_part_len
- * doubles.  Outputs: log2_p [n] f64 (log2 of the unnormalised barycenter of
- * the last iteration), errors [max_iters] f64 (max_k marginal L1 error per
- * iteration), state[4] = {iterations, converged, nan_iteration (0 = none),
- * grid}.  Stops after the first iteration whose error <= threshold, on NaN in
- * log p (DivergedError at that iteration, barycenter.py:120-121) or at
- * max_iters. */
+ * cost.  Layout: cost_p / cost_tp [n, ld] fp32 row-major, ld =
+ * otk_barycenter_ld(n) (multiple of 4), columns n..ld-1 = +inf, written by
+ * otk_barycenter_pad from a contiguous [n, n] cost.  log2_hists [K, n] fp32
+ * (log2 of the histograms, -inf for zeros), weights [K] f64.  Workspaces
+ * F, G, B: [K, ld] fp32 each; part: otk_barycenter_part_len doubles.
+ * Outputs: log2_p [n] f64 (log2 of the unnormalised barycenter of the last
+ * iteration), errors [max_iters] f64 (max_k marginal L1 error per iteration),
+ * state[8] = {iterations, converged, nan_iteration (0 = none), grid, 4 x
+ * scratch (task counters)}.  Stops
+ * after the first iteration whose error <= threshold, on NaN in log p
+ * (DivergedError at that iteration, barycenter.py:120-121) or at max_iters. */
+int64_t otk_barycenter_ld(int64_t n);
 int64_t otk_barycenter_part_len(int64_t n, int32_t K);
-int otk_solve_barycenter(const float *cost, const float *cost_t, int64_t n, int32_t K,
-                         const float *log2_hists, const double *weights, double eps,
+int otk_barycenter_pad(const float *cost, int64_t n, int64_t ld, float *cost_p, float *cost_tp,
+                       void *stream);
+int otk_solve_barycenter(const float *cost_p, const float *cost_tp, int64_t n, int64_t ld,
+                         int32_t K, const float *log2_hists, const double *weights, double eps,
                          double threshold, int32_t max_iters, float *F, float *G, float *B,
                          double *log2_p, double *errors, int32_t *state, double *part,
                          void *stream);

@@ -73,8 +73,11 @@ SIGNATURES = {
     "otk_dense_cost_reduce": (C.c_int, [P, I64, I64, I64, P, P, P, P, P]),
     "otk_bench_pipes": (C.c_int, [P, P, P]),
     "otk_bench_read": (C.c_int, [P, I64, P, P]),
+    "otk_barycenter_ld": (I64, [I64]),
     "otk_barycenter_part_len": (I64, [I64, I32]),
-    "otk_solve_barycenter": (C.c_int, [P, P, I64, I32, P, P, F64, F64, I32, P, P, P, P, P, P, P, P]),
+    "otk_barycenter_pad": (C.c_int, [P, I64, I64, P, P, P]),
+    "otk_solve_barycenter": (C.c_int, [P, P, I64, I64, I32, P, P, F64, F64, I32, P, P, P, P, P, P,
+                                       P, P]),
     "otk_solve_workspace_bytes": (SZ, [C.POINTER(SolveArgs)]),
     "otk_solve_pointcloud": (C.c_int, [C.POINTER(SolveArgs)]),
 }

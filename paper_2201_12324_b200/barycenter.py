@@ -6,7 +6,7 @@ Drop-in for reference otkit/barycenter.py: same names (``BarycenterProblem``,
 ``DivergedError`` (barycenter.py:107-133).  The K histograms share one
 square support geometry; the solve is ONE cooperative kernel launch
 (csrc/bary.cu, ``otk_solve_barycenter``) over the support cost materialised
-once on the device (C and C^T, 8 N^2 bytes).  ``PointCloudGeometry``
+once on the device (C and C^T, 8 N^2 bytes, padded rows).  ``PointCloudGeometry``
 (sqeucl / cosine) and ``DenseGeometry`` supports are accepted;
 ``GridGeometry`` (separable grids) is not part of this build.
 """
@@ -82,28 +82,34 @@ class BarycenterOutput:
 
 
 def _support_costs(geom):
-    """(C, C^T) of the square support on the device, fp32 row-major."""
+    """(C_p, C^T_p) of the square support on the device: fp32 row-major with the
+    leading dimension padded to a multiple of 4 by +inf costs (otk_barycenter_pad)."""
     import torch
+    lib = N.lib()
+    n = geom.shape[0]
     if isinstance(geom, DenseGeometry):
-        return geom._c_ct()
-    if isinstance(geom, PointCloudGeometry):
-        n = geom.shape[0]
-        dev = device()
+        C = geom._c()
+    elif isinstance(geom, PointCloudGeometry):
         px = as_device_f32(geom._kernel_points(geom.x)).contiguous()
         py = px if geom._same_points else as_device_f32(geom._kernel_points(geom.y)).contiguous()
-        C = torch.empty((n, n), dtype=torch.float32, device=dev)
-        CT = torch.empty_like(C)
-        N.check(N.lib().otk_dense_cost(N.ptr(px), N.ptr(py), 1, n, n, px.shape[1],
-                                       N.OTK_SAME_POINTS if geom._same_points else 0, N.ptr(C),
-                                       N.ptr(CT), stream()), "barycenter support cost")
-        return C, CT
-    raise TypeError(f"solve_barycenter supports PointCloudGeometry and DenseGeometry, "
-                    f"got {type(geom).__name__}")
+        C = torch.empty((n, n), dtype=torch.float32, device=px.device)
+        N.check(lib.otk_dense_cost(N.ptr(px), N.ptr(py), 1, n, n, px.shape[1],
+                                   N.OTK_SAME_POINTS if geom._same_points else 0, N.ptr(C),
+                                   None, stream()), "barycenter support cost")
+    else:
+        raise TypeError(f"solve_barycenter supports PointCloudGeometry and DenseGeometry, "
+                        f"got {type(geom).__name__}")
+    ld = int(lib.otk_barycenter_ld(n))
+    Cp = torch.empty((n, ld), dtype=torch.float32, device=C.device)
+    CTp = torch.empty_like(Cp)
+    N.check(lib.otk_barycenter_pad(N.ptr(C), n, ld, N.ptr(Cp), N.ptr(CTp), stream()),
+            "barycenter_pad")
+    return Cp, CTp, ld
 
 
 def _check_memory(n: int, k: int) -> None:
     import torch
-    need = 8 * n * n + 12 * k * n + 64 * n
+    need = 12 * n * (n + 4) + 12 * k * (n + 4) + 64 * n
     free, _ = torch.cuda.mem_get_info()
     if need > 0.9 * free:
         raise ValueError(f"barycenter support of {n} points needs {need / 2**30:.1f} GiB of "
@@ -136,7 +142,7 @@ def solve_barycenter(bp: BarycenterProblem, eps: float | None = None, *,
     k, n = bp.histograms.shape
     dev = device()
     _check_memory(n, k)
-    C, CT = _support_costs(geom)
+    C, CT, ld = _support_costs(geom)
     with np.errstate(divide="ignore"):
         log2h = torch.as_tensor(np.ascontiguousarray(np.log2(bp.histograms), dtype=np.float32),
                                 device=dev)
@@ -145,18 +151,18 @@ def solve_barycenter(bp: BarycenterProblem, eps: float | None = None, *,
     plen = int(lib.otk_barycenter_part_len(n, k))
     if plen <= 0:
         raise RuntimeError("otk_barycenter_part_len failed")
-    F = torch.empty((k, n), dtype=torch.float32, device=dev)
+    F = torch.empty((k, ld), dtype=torch.float32, device=dev)
     G = torch.empty_like(F)
     B = torch.empty_like(F)
     lp2 = torch.empty(n, dtype=torch.float64, device=dev)
     errors = torch.full((max_iters,), float("nan"), dtype=torch.float64, device=dev)
-    state = torch.zeros(4, dtype=torch.int32, device=dev)
+    state = torch.zeros(8, dtype=torch.int32, device=dev)
     part = torch.empty(plen, dtype=torch.float64, device=dev)
-    N.check(lib.otk_solve_barycenter(N.ptr(C), N.ptr(CT), n, k, N.ptr(log2h), N.ptr(w), eps,
+    N.check(lib.otk_solve_barycenter(N.ptr(C), N.ptr(CT), n, ld, k, N.ptr(log2h), N.ptr(w), eps,
                                      float(threshold), int(max_iters), N.ptr(F), N.ptr(G),
                                      N.ptr(B), N.ptr(lp2), N.ptr(errors), N.ptr(state),
                                      N.ptr(part), stream()), "solve_barycenter")
-    iters, converged, nan_iter, _grid = (int(v) for v in state.cpu().numpy())
+    iters, converged, nan_iter, _grid = (int(v) for v in state.cpu().numpy()[:4])
     if nan_iter:
         raise DivergedError("NaN in barycenter iterations; eps is likely too small",
                             iteration=nan_iter)

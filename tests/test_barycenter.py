@@ -67,7 +67,8 @@ def test_problem_validation():
 
 def test_barycenter_symbols_exported():
     lib = N.lib()
-    for name in ("otk_solve_barycenter", "otk_barycenter_part_len"):
+    for name in ("otk_solve_barycenter", "otk_barycenter_part_len", "otk_barycenter_pad",
+                 "otk_barycenter_ld"):
         assert hasattr(lib, name)
 
 
