@@ -44,6 +44,7 @@ enum otk_status {
 /* flags for otk_lse_partial / otk_cost_partial */
 #define OTK_SAME_POINTS 0x1 /* x and y are the same set: exact-zero diagonal (geometry.py:259-261) */
 #define OTK_CLAMP 0x2       /* clamp C >= 0 (geometry.py:273)                                      */
+#define OTK_COST_EUCL 0x4   /* cost_fn "eucl": C = sqrt(max(|p|^2+|q|^2-2<p,q>, 0)) (geometry.py:274-275) */
 #define OTK_IMPL_SIMT 0x10  /* force the FP32 FMA kernel                                           */
 #define OTK_IMPL_TC 0x20    /* force the tcgen05 split-fp16 kernel                                 */
 #define OTK_IMPL_NOPERSIST 0x40 /* otk_solve_pointcloud: never use the one-kernel small-problem solve */
@@ -234,7 +235,7 @@ typedef struct otk_solve_args {
   double threshold;
   int32_t max_iters, inner_iters;
   const float *g_init;       /* nullable warm start (sinkhorn.py:166)         */
-  int32_t flags;             /* OTK_IMPL_* / OTK_CLAMP                        */
+  int32_t flags;             /* OTK_IMPL_* / OTK_CLAMP / OTK_COST_EUCL        */
   int32_t use_graphs;        /* capture constant-eps check periods            */
   /* outputs */
   float *f_out, *g_out;      /* device [n], [m]                               */

@@ -71,9 +71,13 @@ class EpsilonScheduleOracle:
 
 
 class PointCloudOracle:
-    """Streamed squared-Euclidean point-cloud geometry in float64."""
+    """Streamed point-cloud geometry in float64: sqeucl (default), eucl, cosine
+    (geometry.py:263-276)."""
 
-    def __init__(self, x, y, block_size=BLOCK):
+    def __init__(self, x, y, block_size=BLOCK, cost_fn="sqeucl"):
+        if cost_fn not in ("sqeucl", "eucl", "cosine"):
+            raise OracleValueError(f"unknown cost_fn {cost_fn!r}")
+        self.cost_fn = cost_fn
         self.x = np.asarray(x, dtype=np.float64)
         self.y = np.asarray(y, dtype=np.float64)
         self.shape = (self.x.shape[0], self.y.shape[0])
@@ -82,12 +86,17 @@ class PointCloudOracle:
             self.x.shape == self.y.shape and np.array_equal(self.x, self.y))
 
     # --- cost blocks (geometry.py:263-292) ---
-    @staticmethod
-    def _sq_block(xs, ys):
+    def _sq_block(self, xs, ys):
+        if self.cost_fn == "cosine":
+            xn = xs / np.linalg.norm(xs, axis=1, keepdims=True)
+            yn = ys / np.linalg.norm(ys, axis=1, keepdims=True)
+            return 1.0 - xn @ yn.T
         nx = np.einsum("id,id->i", xs, xs)
         ny = np.einsum("jd,jd->j", ys, ys)
         blk = nx[:, None] + ny[None, :] - 2.0 * (xs @ ys.T)
         np.maximum(blk, 0.0, out=blk)
+        if self.cost_fn == "eucl":
+            return np.sqrt(blk)
         return blk
 
     def cost_rows(self, lo, hi):
@@ -115,8 +124,15 @@ class PointCloudOracle:
         rng = np.random.default_rng(0)
         i = rng.integers(0, n, size=MEAN_COST_SAMPLES)
         j = rng.integers(0, m, size=MEAN_COST_SAMPLES)
-        diff = self.x[i] - self.y[j]
-        vals = np.maximum(np.einsum("kd,kd->k", diff, diff), 0.0)
+        if self.cost_fn == "cosine":
+            xn = self.x[i] / np.linalg.norm(self.x[i], axis=1, keepdims=True)
+            yn = self.y[j] / np.linalg.norm(self.y[j], axis=1, keepdims=True)
+            vals = 1.0 - np.einsum("kd,kd->k", xn, yn)
+        else:
+            diff = self.x[i] - self.y[j]
+            vals = np.maximum(np.einsum("kd,kd->k", diff, diff), 0.0)
+            if self.cost_fn == "eucl":
+                vals = np.sqrt(vals)
         if self.same_points:
             vals = np.where(i == j, 0.0, vals)
         return float(vals.mean())

@@ -20,6 +20,7 @@ OTK_OK, OTK_EINVAL, OTK_ECUDA, OTK_ENOTSUP, OTK_ENCCL = 0, -1, -2, -3, -4
 OTK_DIVERGED, OTK_BAD_POTENTIAL = 1, 2
 OTK_SAME_POINTS, OTK_CLAMP, OTK_IMPL_SIMT, OTK_IMPL_TC = 0x1, 0x2, 0x10, 0x20
 OTK_IMPL_NOPERSIST = 0x40
+OTK_COST_EUCL = 0x4
 OTK_FIN_SOLVER, OTK_FIN_APPLY, OTK_FIN_LOG2 = 0, 1, 2
 ABI_VERSION = 3
 

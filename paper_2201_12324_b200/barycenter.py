@@ -7,7 +7,7 @@ Drop-in for reference otkit/barycenter.py: same names (``BarycenterProblem``,
 square support geometry; the solve is ONE cooperative kernel launch
 (csrc/bary.cu, ``otk_solve_barycenter``) over the support cost materialised
 once on the device (C and C^T, 8 N^2 bytes, padded rows).  ``PointCloudGeometry``
-(sqeucl / cosine) and ``DenseGeometry`` supports are accepted;
+(sqeucl / eucl / cosine) and ``DenseGeometry`` supports are accepted;
 ``GridGeometry`` (separable grids) is not part of this build.
 """
 
@@ -94,7 +94,7 @@ def _support_costs(geom):
         py = px if geom._same_points else as_device_f32(geom._kernel_points(geom.y)).contiguous()
         C = torch.empty((n, n), dtype=torch.float32, device=px.device)
         N.check(lib.otk_dense_cost(N.ptr(px), N.ptr(py), 1, n, n, px.shape[1],
-                                   N.OTK_SAME_POINTS if geom._same_points else 0, N.ptr(C),
+                                   geom._cost_flags, N.ptr(C),
                                    None, stream()), "barycenter support cost")
     else:
         raise TypeError(f"solve_barycenter supports PointCloudGeometry and DenseGeometry, "

@@ -13,12 +13,12 @@ atomic writes.  Differences, all on the side of doing more: the regularised
 cost is computed online (no 4e6-entry cap), and the n x m coupling is only
 materialised when --coupling-out asks for it (the reference always builds
 it, cli.py:157, so it refuses every problem above the cap).  The low-rank
-solver, the LP ``--verify`` oracle, the eucl cost and the other
-subcommands (quad, softsort, gmm) are outside this build's hot path and exit
+solver, the LP ``--verify`` oracle and the other subcommands (quad,
+softsort, gmm) are outside this build's hot path and exit
 with an input error.
 
     python -m paper_2201_12324_b200 barycenter --support S.csv --hist H1.csv
-        --hist H2.csv [--weights 0.3,0.7 | --weights W.csv] [--cost sqeucl|cosine]
+        --hist H2.csv [--weights 0.3,0.7 | --weights W.csv] [--cost sqeucl|eucl|cosine]
         [--eps E | --eps-rel R] [--threshold T] [--max-iters N]
         [--barycenter-out P.csv] [--out summary.json]
 
@@ -135,8 +135,6 @@ def _cmd_lin(args) -> int:
         raise _InputError("--solver lr (low-rank Sinkhorn) is outside this build's hot path")
     if args.verify:
         raise _InputError("--verify (exact LP oracle) is outside this build's hot path")
-    if args.cost == "eucl":
-        raise _InputError("--cost eucl is outside this build's hot path (sqeucl, cosine)")
     if args.cost_matrix is not None:
         geom = DenseGeometry(read_matrix(args.cost_matrix))
     else:
@@ -190,8 +188,6 @@ def _cmd_barycenter(args) -> int:
         raise _InputError("provide either --support or --grid")
     if args.grid is not None:
         raise _InputError("--grid (separable GridGeometry) is outside this build's hot path")
-    if args.cost == "eucl":
-        raise _InputError("--cost eucl is outside this build's hot path (sqeucl, cosine)")
     support = read_matrix(args.support)
     geom = PointCloudGeometry(support, support, args.cost)
     hists = np.stack([read_vector(p) for p in args.hist])

@@ -28,7 +28,7 @@ constexpr int DC_B = 64;   // cost tile: 64 x 64 outputs per CTA, 4 x 4 per thre
 // the row kernel instead of striding down the columns of C.
 __global__ void __launch_bounds__(256) dense_cost_kernel(const float *__restrict__ x,
                                                          const float *__restrict__ y, int64_t n,
-                                                         int64_t m, int d, int same,
+                                                         int64_t m, int d, int same, int eucl,
                                                          float *__restrict__ cost,
                                                          float *__restrict__ cost_t) {
   extern __shared__ float sm[];  // xs[64][d+1], ys[64][d+1]; reused as the [64][65] out tile
@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(256) dense_cost_kernel(const float *__restrict
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int64_t i = i0 + ty + 16 * r, j = j0 + tx + 16 * c;
+      if (eucl) acc[r][c] = sqrtf(acc[r][c]);
       if (same && i == j) acc[r][c] = 0.f;
       if (i < n && j < m) cost[((int64_t)b * n + i) * m + j] = acc[r][c];
     }
@@ -396,7 +397,8 @@ int otk_dense_cost(const float *x, const float *y, int64_t batch, int64_t n, int
                                   (int)smem));
   dim3 grid((unsigned)((m + DC_B - 1) / DC_B), (unsigned)((n + DC_B - 1) / DC_B), (unsigned)batch);
   dense_cost_kernel<<<grid, 256, smem, as_stream(stream)>>>(x, y, n, m, d,
-                                                            (flags & OTK_SAME_POINTS) ? 1 : 0, cost,
+                                                            (flags & OTK_SAME_POINTS) ? 1 : 0,
+                                                            (flags & OTK_COST_EUCL) ? 1 : 0, cost,
                                                             cost_t);
   OTK_LAUNCH_CHECK();
   return OTK_OK;

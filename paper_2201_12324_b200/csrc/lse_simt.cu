@@ -23,7 +23,7 @@ namespace otk {
 
 constexpr int SB_M = 64, SB_N = 64, SB_T = 256;
 
-template <int KC, bool CLAMP, bool SAME>
+template <int KC, bool CLAMP, bool SAME, bool EU>
 __global__ void __launch_bounds__(SB_T) lse_simt_kernel(
     const float *__restrict__ P, const float *__restrict__ psq, int64_t np,
     const float *__restrict__ Q, const float *__restrict__ qsq, int64_t nq, int d,
@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(SB_T) lse_simt_kernel(
   const int64_t c_begin = (int64_t)split * cols_per_split;
   const int64_t c_end = min(nq, c_begin + cols_per_split);
   const float two_kappa = 2.f * kappa;
+  const float sk = sqrtf(kappa);
   const bool p_resident = (d <= KC);
 
   float cp[4];
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(SB_T) lse_simt_kernel(
       int64_t j = col0 + tx * 4 + c;
       ok[c] = j < c_end;
       cq[c] = ok[c] ? qbias[j] : 0.f;
-      hb[c] = ok[c] ? fmaf(-kappa, qsq[j], cq[c]) : 0.f;
+      hb[c] = ok[c] ? fmaf(-kappa, qsq[j], EU ? 0.f : cq[c]) : 0.f;
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -102,7 +103,10 @@ __global__ void __launch_bounds__(SB_T) lse_simt_kernel(
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float v = fmaf(acc[r][c], two_kappa, hb[c]);
-        if (CLAMP) {
+        if (EU) {  // kappa*sqrt(C) = sqrt(kappa) * sqrt(kappa*C), kappa*C = cp - v
+          v = (SAME && row == col0 + tx * 4 + c) ? cq[c]
+                                                  : fmaf(-sk, sqrt_approx(fmaxf(cp[r] - v, 0.f)), cq[c]);
+        } else if (CLAMP) {
           float ub = cq[c] + cp[r];
           v = fminf(v, ub);
           if (SAME && row == col0 + tx * 4 + c) v = ub;
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(SB_T) lse_simt_kernel(
       st[r].merge(m2, s2);
     }
     int64_t row = row0 + ty * 4 + r;
-    if (tx == 0 && row < np) partial[(int64_t)split * np + row] = st[r].value() - cp[r];
+    if (tx == 0 && row < np) partial[(int64_t)split * np + row] = st[r].value() - (EU ? 0.f : cp[r]);
   }
 }
 
@@ -144,7 +148,7 @@ __global__ void __launch_bounds__(SB_T) lse_simt_kernel(
 // with a per-row online log2-sum-exp2 and merge with a fixed butterfly.
 constexpr int LD_T = 256, LD_WARPS = LD_T / 32, LD_R = 4, LD_CH = 512, LD_CB = 4;
 
-template <int NV, bool CLAMP, bool SAME>
+template <int NV, bool CLAMP, bool SAME, bool EU>
 __global__ void __launch_bounds__(LD_T) lse_lowd_kernel(
     const float *__restrict__ P, const float *__restrict__ psq, int64_t np,
     const float *__restrict__ Q, const float *__restrict__ qsq, int64_t nq, int d,
@@ -158,6 +162,7 @@ __global__ void __launch_bounds__(LD_T) lse_lowd_kernel(
   const int64_t c_begin = (int64_t)split * cols_per_split;
   const int64_t c_end = min(nq, c_begin + cols_per_split);
   const float two_k = 2.f * kappa;
+  const float sk = sqrtf(kappa);
   // query vectors, two rows per float2 (rows 2t and 2t+1)
   float2 pv[LD_R / 2][4 * NV];
   float cp[LD_R], mx[LD_R], sm[LD_R];
@@ -211,14 +216,24 @@ __global__ void __launch_bounds__(LD_T) lse_lowd_kernel(
           for (int k = 0; k < 4 * NV; ++k)
             if (k <= d || k < 4) acc = __ffma2_rn(pv[t][k], make_float2(qv[k], qv[k]), acc);
           float v0 = acc.x, v1 = acc.y;
-          if (CLAMP) {
-            v0 = fminf(v0, cp[2 * t]);
-            v1 = fminf(v1, cp[2 * t + 1]);
-          }
-          if (SAME) {
-            const int64_t j = j0 + c;
-            if (j == row0 + 2 * t) v0 = cp[2 * t];
-            if (j == row0 + 2 * t + 1) v1 = cp[2 * t + 1];
+          if (EU) {  // u = b - sqrt(kappa) sqrt(kappa C), kappa C = cp - v
+            v0 = -sk * sqrt_approx(fmaxf(cp[2 * t] - v0, 0.f));
+            v1 = -sk * sqrt_approx(fmaxf(cp[2 * t + 1] - v1, 0.f));
+            if (SAME) {
+              const int64_t j = j0 + c;
+              if (j == row0 + 2 * t) v0 = 0.f;
+              if (j == row0 + 2 * t + 1) v1 = 0.f;
+            }
+          } else {
+            if (CLAMP) {
+              v0 = fminf(v0, cp[2 * t]);
+              v1 = fminf(v1, cp[2 * t + 1]);
+            }
+            if (SAME) {
+              const int64_t j = j0 + c;
+              if (j == row0 + 2 * t) v0 = cp[2 * t];
+              if (j == row0 + 2 * t + 1) v1 = cp[2 * t + 1];
+            }
           }
           u[cb][2 * t] = v0 + b;
           u[cb][2 * t + 1] = v1 + b;
@@ -253,14 +268,14 @@ __global__ void __launch_bounds__(LD_T) lse_lowd_kernel(
       st.merge(m2, s2);
     }
     const int64_t i = row0 + r;
-    if (lane == 0 && i < np) partial[(int64_t)split * np + i] = st.value() - cp[r];
+    if (lane == 0 && i < np) partial[(int64_t)split * np + i] = st.value() - (EU ? 0.f : cp[r]);
   }
 }
 
 // ---------------------------------------------------------------- K6 cost
 // Per (split,row): m = max u, s = sum 2^(u-m), t = sum C*2^(u-m),
 // u = (f_i + g_j - C_ij)*kappa with C clamped at 0 (and zero diagonal).
-template <int KC, bool SAME>
+template <int KC, bool SAME, bool EU>
 __global__ void __launch_bounds__(SB_T) cost_simt_kernel(
     const float *__restrict__ P, const float *__restrict__ psq, int64_t np,
     const float *__restrict__ Q, const float *__restrict__ qsq, int64_t nq, int d,
@@ -325,6 +340,7 @@ __global__ void __launch_bounds__(SB_T) cost_simt_kernel(
       for (int r = 0; r < 4; ++r) {
         int64_t row = row0 + ty * 4 + r;
         float cij = fmaxf(pr[r] + qj - 2.f * acc[r][c], 0.f);
+        if (EU) cij = sqrtf(cij);
         if (SAME && row == j) cij = 0.f;
         float u = (fr[r] + gj - cij) * kappa;
         if (u > m[r]) {
@@ -397,13 +413,14 @@ __global__ void __launch_bounds__(1024) cost_reduce_kernel(const float *__restri
 __global__ void plan_kernel(const float *__restrict__ P, const float *__restrict__ psq, int64_t np,
                             const float *__restrict__ Q, const float *__restrict__ qsq, int64_t nq,
                             int d, const float *__restrict__ f, const float *__restrict__ g,
-                            double inv_eps, int same, float *__restrict__ plan) {
+                            double inv_eps, int same, int eucl, float *__restrict__ plan) {
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= np * nq) return;
   int64_t i = idx / nq, j = idx % nq;
   float dot = 0.f;
   for (int k = 0; k < d; ++k) dot = fmaf(P[i * d + k], Q[j * d + k], dot);
   float c = fmaxf(psq[i] + qsq[j] - 2.f * dot, 0.f);
+  if (eucl) c = sqrtf(c);
   if (same && i == j) c = 0.f;
   plan[idx] = (float)exp(((double)f[i] + (double)g[j] - (double)c) * inv_eps);
 }
@@ -415,46 +432,56 @@ int lse_simt_launch(const float *p, const float *p_sq, int64_t np, const float *
                     int flags, int nsplit, float *partial, cudaStream_t st) {
   int64_t cps = (nq + nsplit - 1) / nsplit;
   cps = (cps + SB_N - 1) / SB_N * SB_N;
-  const bool clamp = flags & OTK_CLAMP, same = flags & OTK_SAME_POINTS;
+  const bool clamp = flags & OTK_CLAMP, same = flags & OTK_SAME_POINTS, eu = flags & OTK_COST_EUCL;
   if (d <= 7 && !getenv("OTK_SIMT_TILED")) {
     dim3 g2((unsigned)((np + LD_WARPS * LD_R - 1) / (LD_WARPS * LD_R)), (unsigned)nsplit);
-#define OTK_LOWD_CASE(NV, CL, SA)                                                         \
-    if ((d <= 3) == (NV == 1) && clamp == CL && same == SA) {                             \
-      lse_lowd_kernel<NV, CL, SA><<<g2, LD_T, 0, st>>>(p, p_sq, np, q, q_sq, nq, d, q_bias, \
-                                                       kappa, cps, partial);              \
+#define OTK_LOWD_CASE(NV, CL, SA, EU)                                                     \
+    if ((d <= 3) == (NV == 1) && clamp == CL && same == SA && eu == EU) {                 \
+      lse_lowd_kernel<NV, CL, SA, EU><<<g2, LD_T, 0, st>>>(p, p_sq, np, q, q_sq, nq, d,     \
+                                                           q_bias, kappa, cps, partial);  \
       cudaError_t e = cudaGetLastError();                                                 \
       return e == cudaSuccess ? OTK_OK : cuda_status(e, "lse_lowd_kernel");               \
     }
-    OTK_LOWD_CASE(1, false, false)
-    OTK_LOWD_CASE(1, true, false)
-    OTK_LOWD_CASE(1, true, true)
-    OTK_LOWD_CASE(2, false, false)
-    OTK_LOWD_CASE(2, true, false)
-    OTK_LOWD_CASE(2, true, true)
+    OTK_LOWD_CASE(1, false, false, false)
+    OTK_LOWD_CASE(1, true, false, false)
+    OTK_LOWD_CASE(1, true, true, false)
+    OTK_LOWD_CASE(2, false, false, false)
+    OTK_LOWD_CASE(2, true, false, false)
+    OTK_LOWD_CASE(2, true, true, false)
+    OTK_LOWD_CASE(1, true, false, true)
+    OTK_LOWD_CASE(1, true, true, true)
+    OTK_LOWD_CASE(2, true, false, true)
+    OTK_LOWD_CASE(2, true, true, true)
 #undef OTK_LOWD_CASE
-    set_error("lse_simt: OTK_SAME_POINTS requires OTK_CLAMP");
+    set_error("lse_simt: OTK_SAME_POINTS / OTK_COST_EUCL require OTK_CLAMP");
     return OTK_EINVAL;
   }
   dim3 grid((unsigned)((np + SB_M - 1) / SB_M), (unsigned)nsplit);
   const int kc = pick_kc(d);
-#define OTK_SIMT_CASE(KC, CL, SA)                                                          \
-  if (kc == KC && clamp == CL && same == SA) {                                             \
-    lse_simt_kernel<KC, CL, SA><<<grid, SB_T, 0, st>>>(p, p_sq, np, q, q_sq, nq, d, q_bias, \
-                                                        kappa, cps, partial);              \
+#define OTK_SIMT_CASE(KC, CL, SA, EU)                                                      \
+  if (kc == KC && clamp == CL && same == SA && eu == EU) {                                 \
+    lse_simt_kernel<KC, CL, SA, EU><<<grid, SB_T, 0, st>>>(p, p_sq, np, q, q_sq, nq, d,     \
+                                                            q_bias, kappa, cps, partial);  \
     cudaError_t e = cudaGetLastError();                                                    \
     return e == cudaSuccess ? OTK_OK : cuda_status(e, "lse_simt_kernel");                  \
   }
-  OTK_SIMT_CASE(4, false, false)
-  OTK_SIMT_CASE(4, true, false)
-  OTK_SIMT_CASE(4, true, true)
-  OTK_SIMT_CASE(8, false, false)
-  OTK_SIMT_CASE(8, true, false)
-  OTK_SIMT_CASE(8, true, true)
-  OTK_SIMT_CASE(16, false, false)
-  OTK_SIMT_CASE(16, true, false)
-  OTK_SIMT_CASE(16, true, true)
+  OTK_SIMT_CASE(4, false, false, false)
+  OTK_SIMT_CASE(4, true, false, false)
+  OTK_SIMT_CASE(4, true, true, false)
+  OTK_SIMT_CASE(8, false, false, false)
+  OTK_SIMT_CASE(8, true, false, false)
+  OTK_SIMT_CASE(8, true, true, false)
+  OTK_SIMT_CASE(16, false, false, false)
+  OTK_SIMT_CASE(16, true, false, false)
+  OTK_SIMT_CASE(16, true, true, false)
+  OTK_SIMT_CASE(4, true, false, true)
+  OTK_SIMT_CASE(4, true, true, true)
+  OTK_SIMT_CASE(8, true, false, true)
+  OTK_SIMT_CASE(8, true, true, true)
+  OTK_SIMT_CASE(16, true, false, true)
+  OTK_SIMT_CASE(16, true, true, true)
 #undef OTK_SIMT_CASE
-  set_error("lse_simt: OTK_SAME_POINTS requires OTK_CLAMP");
+  set_error("lse_simt: OTK_SAME_POINTS / OTK_COST_EUCL require OTK_CLAMP");
   return OTK_EINVAL;
 }
 
@@ -485,19 +512,23 @@ int otk_cost_partial(const float *p, const float *p_sq, int64_t np, const float 
   const float kappa = (float)(1.4426950408889634 / eps);
   const int kc = pick_kc(d);
   cudaStream_t st = as_stream(stream);
-  const bool same = flags & OTK_SAME_POINTS;
-#define OTK_COST_CASE(KC)                                                                     \
-  if (kc == KC) {                                                                             \
-    if (same)                                                                                 \
-      cost_simt_kernel<KC, true><<<grid, SB_T, 0, st>>>(p, p_sq, np, q, q_sq, nq, d, f, g,     \
-                                                        kappa, cps, rec);                     \
-    else                                                                                      \
-      cost_simt_kernel<KC, false><<<grid, SB_T, 0, st>>>(p, p_sq, np, q, q_sq, nq, d, f, g,    \
-                                                         kappa, cps, rec);                    \
-  }
-  OTK_COST_CASE(4)
-  OTK_COST_CASE(8)
-  OTK_COST_CASE(16)
+  const bool same = flags & OTK_SAME_POINTS, eu = flags & OTK_COST_EUCL;
+#define OTK_COST_CASE(KC, SA, EU)                                                             \
+  if (kc == KC && same == SA && eu == EU)                                                     \
+    cost_simt_kernel<KC, SA, EU><<<grid, SB_T, 0, st>>>(p, p_sq, np, q, q_sq, nq, d, f, g,     \
+                                                        kappa, cps, rec);
+  OTK_COST_CASE(4, false, false)
+  OTK_COST_CASE(4, true, false)
+  OTK_COST_CASE(4, false, true)
+  OTK_COST_CASE(4, true, true)
+  OTK_COST_CASE(8, false, false)
+  OTK_COST_CASE(8, true, false)
+  OTK_COST_CASE(8, false, true)
+  OTK_COST_CASE(8, true, true)
+  OTK_COST_CASE(16, false, false)
+  OTK_COST_CASE(16, true, false)
+  OTK_COST_CASE(16, false, true)
+  OTK_COST_CASE(16, true, true)
 #undef OTK_COST_CASE
   OTK_LAUNCH_CHECK();
   cost_reduce_kernel<<<1, 1024, 0, st>>>(rec, (int64_t)nsplit * np, out);
@@ -513,7 +544,8 @@ int otk_transport_matrix(const float *p, const float *p_sq, int64_t np, const fl
   OTK_CHECK_ARG(eps > 0, "otk_transport_matrix: eps must be positive");
   int64_t cells = np * nq;
   plan_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, as_stream(stream)>>>(
-      p, p_sq, np, q, q_sq, nq, d, f, g, 1.0 / eps, (flags & OTK_SAME_POINTS) ? 1 : 0, plan);
+      p, p_sq, np, q, q_sq, nq, d, f, g, 1.0 / eps, (flags & OTK_SAME_POINTS) ? 1 : 0,
+      (flags & OTK_COST_EUCL) ? 1 : 0, plan);
   OTK_LAUNCH_CHECK();
   return OTK_OK;
 }

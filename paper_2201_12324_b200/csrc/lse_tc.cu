@@ -238,7 +238,8 @@ struct Params {
   int64_t np, nq;
   int kb;                 // K-blocks (dpad / 64)
   int row_tiles, ntiles, tps, nsplit, num_units;
-  float c2k;              // 2*kappa/s^2
+  float c2k;              // 2*kappa/s^2 (sqeucl) or -kappa*sqrt(2)/s (eucl)
+  int same;               // identical point sets (eucl: exact-zero diagonal)
   float *partial;         // [nsplit][np]
   int probe;              // pipeline probe (OTK_TC_PROBE, timing experiments only):
                           // 1 = epilogue skips the math, 2 = sums without exp,
@@ -287,6 +288,25 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 // Packed f32x2 arithmetic (FFMA2 / FADD2) halves the issue slots of the
 // per-cell work; EP of every 8 column pairs take their exps from the FMA-pipe
 // polynomial instead of MUFU.
+//
+// eucl cost (OTK_COST_EUCL, geometry.py:274-275): the accumulator holds
+// -s^2 C / 2; replace it by sqrt(max(-acc, 0)) = s sqrt(C / 2) so that the
+// same single FFMA with c2k = -kappa sqrt(2) / s gives kappa (g - sqrt C).
+// Identical point sets: the diagonal is forced to an exact zero (the split
+// products leave |C_ii| ~ 1e-6 |p|^2, whose square root would not be small).
+template <int CH>
+__device__ __forceinline__ void eucl_transform(float *acc, int64_t row, int64_t col0, int same) {
+  const int64_t dd = row - col0;
+  // bit i set <=> column i of this chunk is the diagonal (a bit test per
+  // register keeps the chunk in registers; no dynamically indexed store)
+  const uint32_t diag = (same && dd >= 0 && dd < CH) ? (1u << (int)dd) : 0u;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    const float r = sqrt_approx(fmaxf(-acc[i], 0.f));
+    acc[i] = ((diag >> i) & 1u) ? 0.f : r;
+  }
+}
+
 template <int CH, bool MASK, int EP>
 __device__ __forceinline__ void lse_chunk(const float *acc, const float *bias, float c2k, int valid,
                                           float &m, float &s) {
@@ -326,7 +346,7 @@ __device__ __forceinline__ void lse_chunk(const float *acc, const float *bias, f
   s += t2.x + t2.y;
 }
 
-template <int V, bool A_RES, int NS, int ABUF, int EP, int NG>
+template <int V, bool A_RES, int NS, int ABUF, int EP, int NG, bool EU>
 __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
     lse_tc_kernel(const __grid_constant__ CUtensorMap tm_phi, const __grid_constant__ CUtensorMap tm_plo,
                   const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo,
@@ -581,6 +601,7 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
             bv[4 * i + 2] = q.z;
             bv[4 * i + 3] = q.w;
           }
+          if constexpr (EU) eucl_transform<C::CH>(accv, (int64_t)rt * BM + row_local, j0 + c * C::CH, prm.same);
           if (prm.probe == 1) {
             s += accv[0];
           } else if (prm.probe == 2) {
@@ -724,7 +745,7 @@ struct Plan2 {
                               2 * (NG - 1) * 2 * BM * (int)sizeof(float);
 };
 
-template <int KB>
+template <int KB, bool EU>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     lse_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_phi, const __grid_constant__ CUtensorMap tm_plo,
                        const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo,
@@ -918,6 +939,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           float accv[CH], bv[CH];
 #pragma unroll
           for (int i = 0; i < CH; ++i) accv[i] = __uint_as_float(v[i]);
+          if constexpr (EU) eucl_transform<CH>(accv, (int64_t)rt * BM + row_local, j0 + c * CH, prm.same);
           const float4 *bp = reinterpret_cast<const float4 *>(bias + c * CH);
 #pragma unroll
           for (int i = 0; i < CH / 4; ++i) {
@@ -1058,11 +1080,11 @@ static int emu_pairs(int v) {
   return 0;  // measured: the split-column epilogue is no longer MUFU-bound at d = 64
 }
 
-template <int V, bool A_RES, int NS, int ABUF, int EP, int NG>
+template <int V, bool A_RES, int NS, int ABUF, int EP, int NG, bool EU = false>
 static int launch_one(const CUtensorMap (&maps)[7], const Params &prm, cudaStream_t st) {
   using L = Plan<V, A_RES, NS, ABUF, NG>;
   const int smem = L::smem_bytes(prm.kb);
-  auto kern = lse_tc_kernel<V, A_RES, NS, ABUF, EP, NG>;
+  auto kern = lse_tc_kernel<V, A_RES, NS, ABUF, EP, NG, EU>;
   static bool attr_set = false;
   if (smem > 227 * 1024) {
     set_error("lse_tc: shared memory plan too large (%d B, kb=%d)", smem, prm.kb);
@@ -1086,7 +1108,8 @@ static int epi_groups() {
 }
 
 template <int V, bool A_RES, int NS, int ABUF>
-static int launch_variant(const CUtensorMap (&maps)[7], const Params &prm, cudaStream_t st) {
+static int launch_variant(const CUtensorMap (&maps)[7], const Params &prm, bool eucl, cudaStream_t st) {
+  if (eucl) return launch_one<V, A_RES, NS, ABUF, 0, 4, true>(maps, prm, st);  // default knobs only
   const bool g4 = epi_groups() == 4;
   if constexpr (V == 1) {
     switch (emu_pairs(V)) {
@@ -1108,10 +1131,10 @@ static bool use_pair_kernel(int kb) {
   return kb == 2;
 }
 
-template <int KB>
+template <int KB, bool EU>
 static int launch_pair(const CUtensorMap (&maps)[7], const Params &prm, cudaStream_t st) {
   using L = pair::Plan2<KB>;
-  auto kern = pair::lse_tc_pair_kernel<KB>;
+  auto kern = pair::lse_tc_pair_kernel<KB, EU>;
   static bool attr_set = false;
   static_assert(L::SMEM <= 227 * 1024, "pair kernel shared memory plan too large");
   if (!attr_set) {
@@ -1155,7 +1178,7 @@ int tc_tile_cols(int dpad) { return tc::variant_for(dpad / tc::BK) == 1 ? 256 : 
 int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
                   const uint16_t *q_hi, const uint16_t *q_lo, const uint16_t *q_ext, int64_t nq,
                   int dpad, float two_kappa_scaled, const float *q_bias, int nsplit,
-                  int /*same: see the file header*/, float *partial, cudaStream_t st) {
+                  int same, int eucl, float *partial, cudaStream_t st) {
   using namespace tc;
   if (np > (int64_t)INT32_MAX || nq > (int64_t)INT32_MAX) {
     set_error("lse_tc: too many points");
@@ -1191,20 +1214,25 @@ int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_
   prm.tps = (prm.ntiles + nsplit - 1) / nsplit;
   prm.num_units = prm.row_tiles * nsplit;
   prm.c2k = two_kappa_scaled;
+  prm.same = same;  // used by the eucl epilogue only (see the file header)
   prm.partial = partial;
   prm.probe = getenv("OTK_TC_PROBE") ? atoi(getenv("OTK_TC_PROBE")) : 0;
-  if (use_pair) return kb == 1 ? launch_pair<1>(maps, prm, st) : launch_pair<2>(maps, prm, st);
+  const bool eu = eucl != 0;
+  if (use_pair) {
+    if (eu) return kb == 1 ? launch_pair<1, true>(maps, prm, st) : launch_pair<2, true>(maps, prm, st);
+    return kb == 1 ? launch_pair<1, false>(maps, prm, st) : launch_pair<2, false>(maps, prm, st);
+  }
   if (v == 1) {
-    if (kb == 1) return launch_variant<1, true, 2, 2>(maps, prm, st);
-    if (kb == 2) return launch_variant<1, true, 2, 1>(maps, prm, st);
-    return launch_variant<1, false, 2, 1>(maps, prm, st);
+    if (kb == 1) return launch_variant<1, true, 2, 2>(maps, prm, eu, st);
+    if (kb == 2) return launch_variant<1, true, 2, 1>(maps, prm, eu, st);
+    return launch_variant<1, false, 2, 1>(maps, prm, eu, st);
   }
   if (v == 2) {
-    if (kb <= 2) return launch_variant<2, true, 4, 1>(maps, prm, st);
-    if (kb <= 4) return launch_variant<2, true, 2, 1>(maps, prm, st);
-    return launch_variant<2, false, 3, 1>(maps, prm, st);
+    if (kb <= 2) return launch_variant<2, true, 4, 1>(maps, prm, eu, st);
+    if (kb <= 4) return launch_variant<2, true, 2, 1>(maps, prm, eu, st);
+    return launch_variant<2, false, 3, 1>(maps, prm, eu, st);
   }
-  return launch_variant<4, false, 3, 1>(maps, prm, st);
+  return launch_variant<4, false, 3, 1>(maps, prm, eu, st);
 }
 
 }  // namespace otk

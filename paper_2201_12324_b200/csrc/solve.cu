@@ -30,7 +30,7 @@ int lse_simt_launch(const float *p, const float *p_sq, int64_t np, const float *
 int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
                   const uint16_t *q_hi, const uint16_t *q_lo, const uint16_t *q_ext, int64_t nq,
                   int dpad, float two_kappa_scaled, const float *q_bias, int nsplit, int same,
-                  float *partial, cudaStream_t st);
+                  int eucl, float *partial, cudaStream_t st);
 bool tc_available();
 int tc_tile_cols(int dpad);
 namespace small {
@@ -49,7 +49,7 @@ struct Args {
 };
 }  // namespace small
 bool small_solve_fits(int64_t n, int64_t m, int d);
-int small_solve_launch(const small::Args &A, bool same, cudaStream_t st);
+int small_solve_launch(const small::Args &A, bool same, bool eucl, cudaStream_t st);
 }  // namespace otk
 
 using namespace otk;
@@ -101,9 +101,12 @@ extern "C" int otk_lse_partial(const float *p, const float *p_sq, const uint16_t
       set_error("otk_lse_partial: tcgen05 path requires an sm_100 device");
       return OTK_ENOTSUP;
     }
-    return lse_tc_launch(p_hi, p_lo, p_ext, np, q_hi, q_lo, q_ext, nq, dpad,
-                         2.f * kappa * split_inv, q_bias, nsplit, (flags & OTK_SAME_POINTS) ? 1 : 0,
-                         partial, as_stream(stream));
+    // sqeucl: u = (2 kappa / s^2) acc + bias with acc = -s^2 C / 2;
+    // eucl:   u = -(kappa sqrt(2) / s) sqrt(max(-acc, 0)) + bias
+    const bool eu = flags & OTK_COST_EUCL;
+    const float scale = eu ? -kappa * sqrtf(2.f * split_inv) : 2.f * kappa * split_inv;
+    return lse_tc_launch(p_hi, p_lo, p_ext, np, q_hi, q_lo, q_ext, nq, dpad, scale, q_bias, nsplit,
+                         (flags & OTK_SAME_POINTS) ? 1 : 0, eu ? 1 : 0, partial, as_stream(stream));
   }
   OTK_CHECK_ARG(p && q && p_sq && q_sq, "otk_lse_partial: FP32 path needs points and squared norms");
   return lse_simt_launch(p, p_sq, np, q, q_sq, nq, d, q_bias, kappa, flags, nsplit, partial,
@@ -299,7 +302,7 @@ static int solve_small(otk_solve_args *A, Layout &L, cudaStream_t st) {
   S.state = L.state;
   S.probe = getenv("OTK_SMALL_PROBE") ? atoi(getenv("OTK_SMALL_PROBE")) : 0;
   OTK_CUDA(cudaMemsetAsync(L.first_bad, 0x7f, sizeof(int), st));
-  OTK_TRY(small_solve_launch(S, A->same_points != 0, st));
+  OTK_TRY(small_solve_launch(S, A->same_points != 0, (A->flags & OTK_COST_EUCL) != 0, st));
   int state[8];
   OTK_CUDA(cudaMemcpyAsync(state, L.state, 5 * sizeof(int), cudaMemcpyDeviceToHost, st));
   OTK_CUDA(cudaStreamSynchronize(st));
@@ -340,7 +343,7 @@ static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st) {
   OTK_CUDA(cudaMemsetAsync(L.chk_ws, 0, otk_check_workspace_bytes(), st));
 
   HalfStep H{A, &L, st, 1.f / (s * s),
-             (A->flags & (OTK_IMPL_SIMT | OTK_IMPL_TC)) | OTK_CLAMP |
+             (A->flags & (OTK_IMPL_SIMT | OTK_IMPL_TC | OTK_COST_EUCL)) | OTK_CLAMP |
                  (A->same_points ? OTK_SAME_POINTS : 0)};
 
   // ---- initial g (zeros or warm start) and its bias for h = 1

@@ -96,7 +96,7 @@ __device__ __forceinline__ float dot_q(const float (&p)[4 * NV], const float4 *q
 constexpr int SL = 4;
 constexpr int PAIRS = WARPS / SL;
 
-template <int NV, bool SAME, bool CHECK>
+template <int NV, bool SAME, bool CHECK, bool EU>
 __device__ void half_step(const Args &A, const float4 *P, int np, const float4 *Q, int nq,
                           const float *qbias, const float *logw, float *out_pot, float *out_bias,
                           int step, const float *f_prev, double (&chk)[NVALS]) {
@@ -106,6 +106,7 @@ __device__ void half_step(const Args &A, const float4 *P, int np, const float4 *
   const int per = (nq + SL - 1) / SL;
   const int c_lo = slice * per, c_hi = min(nq, c_lo + per);
   const float two_k = 2.f * A.kappa;
+  const float sk = sqrtf(A.kappa);
   const int n_pairs = (A.probe == 1) ? 0 : (np + R - 1) / R;
   for (int base = blockIdx.x * PAIRS; base < n_pairs; base += gridDim.x * PAIRS) {
     const int r0 = (base + pair) * R;
@@ -132,8 +133,14 @@ __device__ void half_step(const Args &A, const float4 *P, int np, const float4 *
             const float bj = qbias[j];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-              float v = fminf(dot_q<NV>(p[r], Q + j * NV), cp[r]);
-              if (SAME && j == r0 + r) v = cp[r];
+              float v;
+              if (EU) {  // kappa sqrt(C) = sqrt(kappa) sqrt(kappa C), kappa C = cp - dot
+                v = -sk * sqrt_approx(fmaxf(cp[r] - dot_q<NV>(p[r], Q + j * NV), 0.f));
+                if (SAME && j == r0 + r) v = 0.f;
+              } else {
+                v = fminf(dot_q<NV>(p[r], Q + j * NV), cp[r]);
+                if (SAME && j == r0 + r) v = cp[r];
+              }
               u[c][r] = v + bj;
             }
           } else {
@@ -183,7 +190,7 @@ __device__ void half_step(const Args &A, const float4 *P, int np, const float4 *
         st.s = part[pair][r][0][1];
 #pragma unroll
         for (int q = 1; q < SL; ++q) st.merge(part[pair][r][q][0], part[pair][r][q][1]);
-        const float L = st.value() - (-reinterpret_cast<const float *>(P + i * NV)[A.d]);
+        const float L = st.value() - (EU ? 0.f : -reinterpret_cast<const float *>(P + i * NV)[A.d]);
         const float v = A.eps * logw[i] - A.eps * kLn2 * L;
         out_pot[i] = v;
         out_bias[i] = v * A.kappa;
@@ -207,7 +214,7 @@ __device__ void load_bias(float *dst, const float *src, int count) {
   for (int j = threadIdx.x; j < count; j += blockDim.x) dst[j] = src[j];
 }
 
-template <int NV, bool SAME>
+template <int NV, bool SAME, bool EU>
 __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ float4 sh4[];
@@ -237,13 +244,13 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
     if (!f_ready) {
       load_bias(bias_s, A.bias_y, A.m);
       __syncthreads();
-      half_step<NV, SAME, false>(A, xs, A.n, ys, A.m, bias_s, A.la, f, A.bias_x, 2 * t, nullptr, chk);
+      half_step<NV, SAME, false, EU>(A, xs, A.n, ys, A.m, bias_s, A.la, f, A.bias_x, 2 * t, nullptr, chk);
       grid.sync();
     }
     f_ready = false;
     load_bias(bias_s, A.bias_x, A.n);
     __syncthreads();
-    half_step<NV, SAME, false>(A, ys, A.m, xs, A.n, bias_s, A.lb, A.g, A.bias_y, 2 * t + 1, nullptr, chk);
+    half_step<NV, SAME, false, EU>(A, ys, A.m, xs, A.n, bias_s, A.lb, A.g, A.bias_y, 2 * t + 1, nullptr, chk);
     grid.sync();
     if (t % A.inner_iters == 0 || t == A.max_iters) {
       // f_{t+1} into fn, with the check of (f_t, g_t) fused in
@@ -251,7 +258,7 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
       for (int k = 0; k < NVALS; ++k) chk[k] = 0.0;
       load_bias(bias_s, A.bias_y, A.m);
       __syncthreads();
-      half_step<NV, SAME, true>(A, xs, A.n, ys, A.m, bias_s, A.la, fn, A.bias_x, 2 * t + 2, f, chk);
+      half_step<NV, SAME, true, EU>(A, xs, A.n, ys, A.m, bias_s, A.la, fn, A.bias_x, 2 * t + 2, f, chk);
       for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.m; j += gridDim.x * blockDim.x) {
         const double gj = A.g[j], bj = A.b[j];
         if (bj > 0.0) chk[3] += bj * gj;
@@ -348,13 +355,18 @@ bool small_solve_fits(int64_t n, int64_t m, int d) {
   return coop && small::smem_bytes((int)n, (int)m, nv) + 4096 <= (size_t)max_smem;
 }
 
-int small_solve_launch(const small::Args &A, bool same, cudaStream_t st) {
+int small_solve_launch(const small::Args &A, bool same, bool eucl, cudaStream_t st) {
   using namespace small;
   const int nv = (A.d + 1 + 3) / 4;
   const size_t smem = smem_bytes(A.n, A.m, nv);
   void *kern = nullptr;
-  if (nv == 1) kern = same ? (void *)solve_small_kernel<1, true> : (void *)solve_small_kernel<1, false>;
-  else kern = same ? (void *)solve_small_kernel<2, true> : (void *)solve_small_kernel<2, false>;
+  if (eucl) {
+    if (nv == 1) kern = same ? (void *)solve_small_kernel<1, true, true> : (void *)solve_small_kernel<1, false, true>;
+    else kern = same ? (void *)solve_small_kernel<2, true, true> : (void *)solve_small_kernel<2, false, true>;
+  } else {
+    if (nv == 1) kern = same ? (void *)solve_small_kernel<1, true, false> : (void *)solve_small_kernel<1, false, false>;
+    else kern = same ? (void *)solve_small_kernel<2, true, false> : (void *)solve_small_kernel<2, false, false>;
+  }
   OTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   OTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));

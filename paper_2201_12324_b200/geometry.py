@@ -7,12 +7,12 @@ inputs may be numpy arrays (results come back as float64 numpy, like the
 reference) or CUDA torch tensors (results stay on the device).
 
 Implemented: ``PointCloudGeometry`` with the squared-Euclidean cost (never
-materialised: the online kernels of csrc/lse_simt.cu and csrc/lse_tc.cu) and
-the cosine cost (1 - <x^,y^> = |x^/sqrt2 - y^/sqrt2|^2: the same kernels on
-normalised, 1/sqrt(2)-scaled points), ``DenseGeometry`` (stored cost,
+materialised: the online kernels of csrc/lse_simt.cu and csrc/lse_tc.cu), the
+Euclidean cost (the same kernels with a square root per cell, OTK_COST_EUCL)
+and the cosine cost (1 - <x^,y^> = |x^/sqrt2 - y^/sqrt2|^2: the sqeucl kernels
+on normalised, 1/sqrt(2)-scaled points), ``DenseGeometry`` (stored cost,
 csrc/dense.cu), ``EpsilonSchedule`` and the non-log ``apply_kernel`` (built on
-the log-domain kernels).  Out of scope: the ``eucl``
-cost (a square root per cell in every kernel) and ``GridGeometry``.
+the log-domain kernels).  Out of scope: ``GridGeometry``.
 """
 
 from __future__ import annotations
@@ -37,7 +37,7 @@ DEFAULT_EPSILON_SCALE = 0.05        # geometry.py:40
 _MEAN_COST_SAMPLES = 1000           # geometry.py:42
 DEFAULT_BLOCK_SIZE = 256            # geometry.py:44 (accepted, performance-only)
 DEFAULT_DENSE_CAP = 4_000_000       # geometry.py:46
-COST_FNS = ("sqeucl", "cosine")     # reference: ("sqeucl", "eucl", "cosine"); see module doc
+COST_FNS = ("sqeucl", "eucl", "cosine")  # geometry.py:35
 _REFERENCE_COST_FNS = ("sqeucl", "eucl", "cosine")
 _LOG2E = 1.4426950408889634
 
@@ -213,6 +213,24 @@ class _Cloud:
         return self
 
 
+def kernel_points(p, cost_fn: str):
+    """Points the kernels see: cosine -> x/|x|/sqrt(2) (float64 math), so that
+    |x'-y'|^2 = 1 - <x^, y^> (geometry.py:264-267); sqeucl / eucl -> x."""
+    if cost_fn != "cosine":
+        return p
+    if is_torch(p):
+        q = as_device_f32(p).double()
+        return (q / q.norm(dim=1, keepdim=True) / np.sqrt(2.0)).float().contiguous()
+    q = np.asarray(p, dtype=np.float64)
+    return q / np.linalg.norm(q, axis=1, keepdims=True) / np.sqrt(2.0)
+
+
+def cost_fn_flags(cost_fn: str) -> int:
+    if cost_fn not in COST_FNS:
+        raise ValueError(f"cost_fn must be one of {COST_FNS}, got {cost_fn!r}")
+    return N.OTK_COST_EUCL if cost_fn == "eucl" else 0
+
+
 class PointCloudGeometry(Geometry):
     """Squared-Euclidean costs between two point sets, never materialised.
 
@@ -232,9 +250,6 @@ class PointCloudGeometry(Geometry):
             raise ValueError("points contain non-finite entries")
         if cost_fn not in _REFERENCE_COST_FNS:
             raise ValueError(f"cost_fn must be one of {_REFERENCE_COST_FNS}, got {cost_fn!r}")
-        if cost_fn not in COST_FNS:
-            raise NotImplementedError(
-                f"cost_fn {cost_fn!r} is outside this build's hot path (sqeucl, cosine)")
         if cost_fn == "cosine" and (_has_zero_row(x) or (not same_obj and _has_zero_row(y))):
             raise ValueError("cosine cost is undefined for zero vectors")
         if epsilon_default is not None and not (epsilon_default > 0):
@@ -260,14 +275,7 @@ class PointCloudGeometry(Geometry):
 
     # ---- device state (lazy: construction and validation need no GPU)
     def _kernel_points(self, p):
-        """Points the sqeucl kernels see: cosine -> x/|x|/sqrt(2) (float64 math)."""
-        if self.cost_fn != "cosine":
-            return p
-        if is_torch(p):
-            q = as_device_f32(p).double()
-            return (q / q.norm(dim=1, keepdim=True) / np.sqrt(2.0)).float().contiguous()
-        q = np.asarray(p, dtype=np.float64)
-        return q / np.linalg.norm(q, axis=1, keepdims=True) / np.sqrt(2.0)
+        return kernel_points(p, self.cost_fn)
 
     def _clouds(self):
         if self._dev is None:
@@ -286,8 +294,14 @@ class PointCloudGeometry(Geometry):
         return self._dev
 
     @property
+    def _cost_flags(self):
+        """OTK_SAME_POINTS / OTK_COST_EUCL for every kernel that forms a cost."""
+        return ((N.OTK_SAME_POINTS if self._same_points else 0) |
+                (N.OTK_COST_EUCL if self.cost_fn == "eucl" else 0))
+
+    @property
     def _flags(self):
-        return N.OTK_CLAMP | (N.OTK_SAME_POINTS if self._same_points else 0) | self.impl_flags
+        return N.OTK_CLAMP | self._cost_flags | self.impl_flags
 
     def mean_cost(self) -> float:
         """0.05 * this is epsilon_default; subsampled like geometry.py:294-312."""
@@ -304,6 +318,8 @@ class PointCloudGeometry(Geometry):
         jj = torch.as_tensor(j, device=cx.p.device)
         diff = cx.p[ii].double() - cy.p[jj].double()
         vals = torch.clamp((diff * diff).sum(dim=1), min=0.0)
+        if self.cost_fn == "eucl":
+            vals = torch.sqrt(vals)
         if self._same_points:
             vals = torch.where(ii == jj, torch.zeros_like(vals), vals)
         return float(vals.mean().item())
@@ -316,7 +332,7 @@ class PointCloudGeometry(Geometry):
         n, m = self.shape
         out = torch.empty((n, m), dtype=torch.float32, device=cx.p.device)
         N.check(N.lib().otk_dense_cost(N.ptr(cx.p), N.ptr(cy.p), 1, n, m, cx.d,
-                                       N.OTK_SAME_POINTS if self._same_points else 0, N.ptr(out),
+                                       self._cost_flags, N.ptr(out),
                                        None, stream()), "cost_matrix")
         return to_output(out, self.x)
 

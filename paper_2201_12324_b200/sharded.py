@@ -179,7 +179,7 @@ class CudaShardEngine:
         self.cx.prepare(scale, planes)
         self.cy.prepare(scale, planes)
         self.sinv = 1.0 / (scale * scale)
-        self.flags = (flags & (N.OTK_IMPL_SIMT | N.OTK_IMPL_TC)) | N.OTK_CLAMP
+        self.flags = (flags & (N.OTK_IMPL_SIMT | N.OTK_IMPL_TC | N.OTK_COST_EUCL)) | N.OTK_CLAMP
         dev = self.cx.p.device
         with np.errstate(divide="ignore"):
             la, lb = np.log(np.asarray(a_local, dtype=np.float64)), np.log(np.asarray(b, dtype=np.float64))
@@ -347,8 +347,11 @@ class ShardedProblem:
     """
 
     def __init__(self, x, y, a=None, b=None, *, comm=None, x_is_local: bool = False,
-                 n_total: int | None = None, impl: str = "auto"):
+                 n_total: int | None = None, impl: str = "auto", cost_fn: str = "sqeucl"):
+        from .geometry import cost_fn_flags, kernel_points
         from .sinkhorn import _impl_flags
+        cflags = cost_fn_flags(cost_fn)
+        self.cost_fn = cost_fn
         self.comm = comm = comm or TorchComm()
         dev = _dev_of(x)
         if x_is_local:
@@ -374,7 +377,8 @@ class ShardedProblem:
         def amax_reduce(v):  # one common split scale on every rank
             return float(comm.all_gather_host(np.array([v]), dev)[:, 0].max())
 
-        self.engine = CudaShardEngine(x_local, y, a_loc, b_w, flags=_impl_flags(impl),
+        self.engine = CudaShardEngine(kernel_points(x_local, cost_fn), kernel_points(y, cost_fn),
+                                      a_loc, b_w, flags=_impl_flags(impl) | cflags,
                                       amax_reduce=amax_reduce)
         self.lo, self.hi, self.n_total, self.m = lo, hi, n_total, m
 
@@ -414,7 +418,8 @@ class ShardedProblem:
 def solve_sinkhorn_sharded(x, y, eps, a=None, b=None, *, threshold: float = 1e-3,
                            max_iters: int = 2000, inner_iters: int = 10, g_init=None,
                            comm=None, x_is_local: bool = False, n_total: int | None = None,
-                           impl: str = "auto", gather_f: bool = False) -> ShardedSinkhornOutput:
+                           impl: str = "auto", gather_f: bool = False,
+                           cost_fn: str = "sqeucl") -> ShardedSinkhornOutput:
     """Row-sharded ``solve_sinkhorn`` on a point cloud (one rank per GPU):
     ``ShardedProblem(x, y, a, b, ...).solve(eps, ...)``."""
     if max_iters < 1 or inner_iters < 1:
@@ -422,7 +427,7 @@ def solve_sinkhorn_sharded(x, y, eps, a=None, b=None, *, threshold: float = 1e-3
     if not (threshold > 0):
         raise ValueError("threshold must be positive")
     prob = ShardedProblem(x, y, a, b, comm=comm, x_is_local=x_is_local, n_total=n_total,
-                          impl=impl)
+                          impl=impl, cost_fn=cost_fn)
     return prob.solve(eps, threshold=threshold, max_iters=max_iters, inner_iters=inner_iters,
                       g_init=g_init, gather_f=gather_f)
 
@@ -434,12 +439,14 @@ def _dev_of(x):
     return device()
 
 
-def reg_ot_cost_sharded(out: ShardedSinkhornOutput, x_local, y, a_local, b, comm=None):
+def reg_ot_cost_sharded(out: ShardedSinkhornOutput, x_local, y, a_local, b, comm=None,
+                        cost_fn: str = "sqeucl"):
     """reg_ot_cost (sinkhorn.py:210-216) over row shards: online local sums + rank-order total."""
     import torch
-    from .geometry import _Cloud
+    from .geometry import _Cloud, cost_fn_flags, kernel_points
     comm = comm or TorchComm()
-    cx, cy = _Cloud(x_local), _Cloud(y)
+    cflags = cost_fn_flags(cost_fn)
+    cx, cy = _Cloud(kernel_points(x_local, cost_fn)), _Cloud(kernel_points(y, cost_fn))
     cx.prepare(1.0, False)
     cy.prepare(1.0, False)
     lib = N.lib()
@@ -448,7 +455,7 @@ def reg_ot_cost_sharded(out: ShardedSinkhornOutput, x_local, y, a_local, b, comm
     f_d = as_device_f32(out.f_device if out.f_device is not None else out.f_local)
     g_d = as_device_f32(out.g_device if out.g_device is not None else out.g)
     N.check(lib.otk_cost_partial(N.ptr(cx.p), N.ptr(cx.sq), cx.n, N.ptr(cy.p), N.ptr(cy.sq), cy.n,
-                                 cx.d, N.ptr(f_d), N.ptr(g_d), float(out.eps), 0, N.ptr(res),
+                                 cx.d, N.ptr(f_d), N.ptr(g_d), float(out.eps), cflags, N.ptr(res),
                                  N.ptr(ws), stream()), "reg_ot_cost")
     a_local = np.asarray(a_local, dtype=float)
     b = np.asarray(b, dtype=float)

@@ -268,7 +268,7 @@ def _solve_pointcloud(prob, sched, threshold, max_iters, inner_iters, g_init, im
     A.eps_target, A.eps_init_scale, A.eps_decay = sched.target, sched.init_scale, sched.decay
     A.threshold, A.max_iters, A.inner_iters = float(threshold), int(max_iters), int(inner_iters)
     A.g_init = N.ptr(gi)
-    A.flags = _impl_flags(impl) | geom.impl_flags
+    A.flags = _impl_flags(impl) | geom.impl_flags | (geom._cost_flags & N.OTK_COST_EUCL)
     A.use_graphs = 1 if use_graphs else 0
     A.f_out, A.g_out = N.ptr(f_out), N.ptr(g_out)
     A.errors = errs.ctypes.data_as(ctypes.c_void_p)
@@ -558,8 +558,8 @@ def transport_matrix(out: SinkhornOutput, prob: LinearProblem) -> Coupling:
         plan = torch.empty((n, m), dtype=torch.float32, device=cx.p.device)
         N.check(N.lib().otk_transport_matrix(N.ptr(cx.p), N.ptr(cx.sq), n, N.ptr(cy.p), N.ptr(cy.sq),
                                              m, cx.d, N.ptr(f), N.ptr(g), float(out.eps),
-                                             N.OTK_SAME_POINTS if geom._same_points else 0,
-                                             N.ptr(plan), stream()), "transport_matrix")
+                                             geom._cost_flags, N.ptr(plan), stream()),
+                "transport_matrix")
     elif isinstance(geom, DenseGeometry):
         C = geom._c()
         plan = torch.empty((n, m), dtype=torch.float32, device=C.device)
@@ -583,9 +583,8 @@ def reg_ot_cost(out: SinkhornOutput, prob: LinearProblem) -> RegOTCost:
         ws = torch.empty(lib.otk_cost_workspace_bytes(n, m), dtype=torch.uint8, device=cx.p.device)
         res = torch.zeros(2, dtype=torch.float64, device=cx.p.device)
         N.check(lib.otk_cost_partial(N.ptr(cx.p), N.ptr(cx.sq), n, N.ptr(cy.p), N.ptr(cy.sq), m,
-                                     cx.d, N.ptr(f), N.ptr(g), float(out.eps),
-                                     N.OTK_SAME_POINTS if geom._same_points else 0, N.ptr(res),
-                                     N.ptr(ws), stream()), "reg_ot_cost")
+                                     cx.d, N.ptr(f), N.ptr(g), float(out.eps), geom._cost_flags,
+                                     N.ptr(res), N.ptr(ws), stream()), "reg_ot_cost")
         transport, mass = (float(v) for v in res.cpu().numpy())
     elif isinstance(geom, DenseGeometry):
         C = geom._c()

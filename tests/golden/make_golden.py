@@ -260,6 +260,45 @@ def spot_checks():
              f=fpot.astype(np.float32), rows_g0=rows_g0, rows_g=rows_g, cols_f=cols_f)
 
 
+def eucl_cases():
+    """cost_fn="eucl" (geometry.py:274-275): apply_lse_kernel rows/cols and full
+    solves by the reference, incl. identical point sets and -inf potentials."""
+    rng = np.random.default_rng(2201)
+    res = {}
+    for k, (n, m, d, same) in enumerate([(97, 130, 2, False), (200, 200, 3, True),
+                                         (150, 90, 16, False), (128, 128, 64, True),
+                                         (96, 140, 100, False), (64, 70, 300, False)]):
+        x = rng.standard_normal((n, d)).astype(np.float32)
+        y = x if same else (rng.standard_normal((m, d)) + 0.4).astype(np.float32)
+        x64 = x.astype(np.float64)
+        y64 = x64 if same else y.astype(np.float64)
+        geom = otkit.PointCloudGeometry(x64, y64, "eucl")
+        eps = float(0.2 * geom.mean_cost())
+        f = (rng.standard_normal(n) * eps).astype(np.float32).astype(np.float64)
+        g = (rng.standard_normal(m) * eps).astype(np.float32).astype(np.float64)
+        if k % 2 == 1:
+            g[rng.random(m) < 0.2] = -np.inf
+        rows = geom.apply_lse_kernel(f, g, eps, "rows")
+        cols = geom.apply_lse_kernel(f, g, eps, "cols")
+        solve_eps = float(0.05 * geom.mean_cost())
+        prob = otkit.LinearProblem(geom)
+        out = otkit.solve_sinkhorn(prob, solve_eps, threshold=1e-3, max_iters=2000)
+        old = ogeo.DEFAULT_DENSE_CAP
+        ogeo.DEFAULT_DENSE_CAP = max(old, n * m)
+        try:
+            cost = otkit.reg_ot_cost(out, prob)
+        finally:
+            ogeo.DEFAULT_DENSE_CAP = old
+        for key, v in dict(x=x, y=y, same=same, eps=eps, f=f, g=g, rows=rows, cols=cols,
+                           solve_eps=solve_eps, sol_f=out.f, sol_g=out.g,
+                           iterations=out.iterations, converged=out.converged,
+                           errors=out.errors, transport=cost.transport_cost,
+                           dual=cost.dual_objective, mean_cost=geom.mean_cost()).items():
+            res[f"e{k}__{key}"] = np.asarray(v)
+        print(f"eucl e{k}: n={n} m={m} d={d} same={same} iters={out.iterations}")
+    save("eucl", **res)
+
+
 def barycenter_cases():
     """Fixed-support barycenters (otkit/barycenter.py:73-133), SURVEY.md §8f row 4.
 
@@ -328,7 +367,7 @@ def barycenter_cases():
 
 
 def main():
-    which = sys.argv[1:] or ["lse", "known", "solve", "fixed", "dense", "spot", "bary"]
+    which = sys.argv[1:] or ["lse", "known", "solve", "fixed", "dense", "spot", "bary", "eucl"]
     meta = dict(reference="/root/reference/pkg (otkit 0.1.0)", numpy=np.__version__,
                 scipy=scipy.__version__, python=platform.python_version(),
                 generated_by="tests/golden/make_golden.py", when=time.strftime("%Y-%m-%d"))
@@ -346,6 +385,8 @@ def main():
         spot_checks()
     if "bary" in which:
         barycenter_cases()
+    if "eucl" in which:
+        eucl_cases()
     with open(os.path.join(OUT, "MANIFEST.json"), "w") as fh:
         json.dump(meta, fh, indent=1)
 

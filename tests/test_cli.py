@@ -31,7 +31,6 @@ def test_input_errors_exit_1(tmp_path, capsys):
     y = _write(tmp_path / "y.csv", np.zeros((4, 2)))
     assert cli.main(["lin", "--x", x, "--y", y, "--eps", "1", "--eps-rel", "1"]) == 1
     assert cli.main(["lin", "--x", x, "--y", y, "--solver", "lr"]) == 1
-    assert cli.main(["lin", "--x", x, "--y", y, "--cost", "eucl"]) == 1
     bad = _write(tmp_path / "a.csv", np.array([0.5, 0.6, 0.1]))
     assert cli.main(["lin", "--x", x, "--y", y, "--a", bad]) == 1    # sums to 1.2
     assert cli.main(["lin", "--x", str(tmp_path / "missing.csv"), "--y", y]) == 1
@@ -101,7 +100,6 @@ def test_barycenter_input_errors_exit_1(tmp_path, capsys):
                      "--weights", "0.5,x"]) == 1
     assert cli.main(["barycenter", "--support", s, "--hist", h, "--hist", h,
                      "--weights", "0.5,0.6"]) == 1
-    assert cli.main(["barycenter", "--support", s, "--hist", h, "--cost", "eucl"]) == 1
     assert cli.main(["barycenter", "--support", s, "--hist", h, "--eps", "1",
                      "--eps-rel", "1"]) == 1
     assert "error:" in capsys.readouterr().err

@@ -135,8 +135,9 @@ def test_cosine_and_apply_kernel_validation_like_reference():
     import paper_2201_12324_b200 as otk
     with pytest.raises(ValueError):
         otk.PointCloudGeometry(np.array([[0.0, 0.0]]), np.array([[1.0, 0.0]]), "cosine")
-    with pytest.raises(NotImplementedError):
-        otk.PointCloudGeometry(np.ones((2, 2)), np.ones((2, 2)), "eucl")
+    with pytest.raises(ValueError):
+        otk.PointCloudGeometry(np.ones((2, 2)), np.ones((2, 2)), "manhattan")
+    assert otk.PointCloudGeometry(np.ones((2, 2)), np.ones((2, 2)), "eucl").cost_fn == "eucl"
     geom = otk.DenseGeometry(np.zeros((2, 3)))
     with pytest.raises(ValueError):
         geom.apply_kernel(np.ones(3), 1.0, "diagonal")

@@ -153,3 +153,30 @@ def test_barycenter_oracle_validation():
         solve_barycenter(oracle.DenseOracle(np.zeros((2, 3))), good, None, 0.1)
     with pytest.raises(ValueError):
         solve_barycenter(geom, good, None, -1.0)
+
+
+def eucl_cases():
+    fx = load_golden("eucl")
+    names = sorted({k.split("__")[0] for k in fx})
+    return [(nm, {k.split("__")[1]: v for k, v in fx.items() if k.startswith(nm + "__")})
+            for nm in names]
+
+
+def test_eucl_oracle_matches_reference():
+    """cost_fn="eucl" (geometry.py:274-275): oracle LSE, solve and mean cost vs the reference."""
+    cases = eucl_cases()
+    assert len(cases) == 6
+    for name, c in cases:
+        x = c["x"].astype(np.float64)
+        y = x if bool(c["same"]) else c["y"].astype(np.float64)
+        geom = oracle.PointCloudOracle(x, y, cost_fn="eucl")
+        eps = float(c["eps"])
+        np.testing.assert_allclose(geom.apply_lse_kernel(c["f"], c["g"], eps, "rows"), c["rows"],
+                                   rtol=1e-12, atol=1e-12, err_msg=name)
+        np.testing.assert_allclose(geom.apply_lse_kernel(c["f"], c["g"], eps, "cols"), c["cols"],
+                                   rtol=1e-12, atol=1e-12, err_msg=name)
+        assert geom.mean_cost() == pytest.approx(float(c["mean_cost"]), rel=1e-12)
+        ref = oracle.sinkhorn(geom, None, None, float(c["solve_eps"]), threshold=1e-3,
+                              max_iters=2000)
+        assert ref["iterations"] == int(c["iterations"]), name
+        np.testing.assert_allclose(ref["f"], c["sol_f"], rtol=1e-9, atol=1e-12, err_msg=name)
