@@ -233,9 +233,12 @@ def pipes():
 
 
 def online_roofline(geom, wl, reps=10):
-    """Dominant kernel of the online path: one rows half-step (otk_lse_partial),
-    timed with CUDA events on its stream.  Algorithmic work per cell (SURVEY.md
-    §8d): 2d dot-product flops + 8 epilogue flops + 1 exp."""
+    """Dominant kernel of the online path: one rows half-step as the solver runs
+    it in steady state -- otk_lse_step with the row anchors of the previous
+    half-step (anchored tcgen05 kernel + finalize + the idle repair check), or
+    otk_lse_partial + finalize on the FP32 path -- timed with CUDA events on its
+    stream.  Algorithmic work per cell: 2d dot-product flops +
+    8 epilogue flops + 1 exp."""
     import torch
     from paper_2201_12324_b200 import _native as N
     from paper_2201_12324_b200._device import stream
@@ -243,18 +246,31 @@ def online_roofline(geom, wl, reps=10):
     n, m = geom.shape
     lib = N.lib()
     kappa = float(np.float32(1.4426950408889634 / wl.eps))
-    bias = torch.zeros(m, dtype=torch.float32, device=cx.p.device)
+    dev = cx.p.device
+    bias = torch.zeros(m, dtype=torch.float32, device=dev)
     flags = geom._flags
     nsplit = lib.otk_lse_suggest_nsplit(n, m, cx.d, flags)
-    part = torch.empty(nsplit * n, dtype=torch.float32, device=cx.p.device)
+    part = torch.empty(nsplit * n, dtype=torch.float32, device=dev)
     sinv = 1.0 / (cx.scale * cx.scale)
     tc = cx.hi is not None and not (flags & N.OTK_IMPL_SIMT)
+    anchored = bool(lib.otk_lse_step_anchored(cx.d, flags))
+    base = torch.full((n,), float(np.log(1.0 / n)), dtype=torch.float32, device=dev)
+    out = torch.empty(n, dtype=torch.float32, device=dev)
+    anchor = torch.empty(n, dtype=torch.float32, device=dev)
+    rep = torch.empty(lib.otk_lse_step_workspace_bytes(n), dtype=torch.uint8, device=dev)
+
+    def step(fl):
+        N.check(lib.otk_lse_step(N.ptr(cx.p), N.ptr(cx.sq), N.ptr(cx.hi), N.ptr(cx.lo),
+                                 N.ptr(cx.ext_a), n, N.ptr(cy.p), N.ptr(cy.sq), N.ptr(cy.hi),
+                                 N.ptr(cy.lo), N.ptr(cy.ext_b), m, cx.d, cx.dpad, sinv,
+                                 N.ptr(bias), kappa, fl, nsplit, N.ptr(part), N.ptr(base),
+                                 N.OTK_FIN_SOLVER, float(wl.eps), kappa, N.ptr(out), None, None, 0,
+                                 N.ptr(anchor), N.ptr(rep), stream()))
+
+    step(flags | N.OTK_ANCHOR_INIT)  # anchors of the "previous" half-step
 
     def launch():
-        N.check(lib.otk_lse_partial(N.ptr(cx.p), N.ptr(cx.sq), N.ptr(cx.hi), N.ptr(cx.lo),
-                                    N.ptr(cx.ext_a), n, N.ptr(cy.p), N.ptr(cy.sq), N.ptr(cy.hi),
-                                    N.ptr(cy.lo), N.ptr(cy.ext_b), m, cx.d, cx.dpad, sinv,
-                                    N.ptr(bias), kappa, flags, nsplit, N.ptr(part), stream()))
+        step(flags)
     for _ in range(3):
         launch()
     sec = event_time(launch, reps)
@@ -278,7 +294,9 @@ def online_roofline(geom, wl, reps=10):
         roof = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "peak_note": "FP32 FFMA rate measured on this GPU x 2"}
     roof.update({
-        "traffic": traffic_for(wl.name), "kernel": "otk_lse_partial (rows half-step)",
+        "traffic": traffic_for(wl.name),
+        "kernel": ("otk_lse_step, anchored (lse_tc FIX kernel + finalize + idle repair check)"
+                   if anchored else "otk_lse_step (rows half-step: partial + finalize)"),
         "kernel_ms": sec * 1e3, "cells_per_launch": cells,
         "algorithmic_flops_per_launch": (2.0 * d + 8.0) * cells,
         "pipes": {"ex2_per_s": ex2, "ffma_per_s": ffma, "cells_per_s": cps,

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define OTK_ABI_VERSION 3
+#define OTK_ABI_VERSION 4
 
 enum otk_status {
   OTK_OK = 0,
@@ -48,6 +48,8 @@ enum otk_status {
 #define OTK_IMPL_SIMT 0x10  /* force the FP32 FMA kernel                                           */
 #define OTK_IMPL_TC 0x20    /* force the tcgen05 split-fp16 kernel                                 */
 #define OTK_IMPL_NOPERSIST 0x40 /* otk_solve_pointcloud: never use the one-kernel small-problem solve */
+#define OTK_ANCHOR_INIT 0x80    /* otk_lse_step: the anchor holds no result yet (running-max kernel; anchor written) */
+#define OTK_IMPL_NOANCHOR 0x100 /* otk_solve_pointcloud: never use the anchored half-step              */
 
 /* finalize modes */
 #define OTK_FIN_SOLVER 0 /* out = eps*logw - eps*ln2*L   (sinkhorn.py:173-174)                     */
@@ -123,6 +125,32 @@ int otk_lse_finalize(const float *partial, int32_t nsplit, int64_t np,
                      const float *base, int32_t mode, float eps, float kappa_next,
                      float *out_pot, float *out_bias, int32_t *first_bad,
                      int32_t step, void *stream);
+
+/* One whole half-step = otk_lse_partial + otk_lse_finalize (same arguments,
+ * same results to fp32 rounding), with an optional per-row ANCHOR that
+ * replaces the running max of the streaming log-sum-exp.  anchor[np] holds
+ * the log2 result L_i of this role's previous half-step (NaN = unknown) and
+ * is overwritten with the new L_i.  On the tcgen05 sqeucl path
+ * (otk_lse_step_anchored) each row sums 2^(u_ij - anchor_i) directly -- no
+ * max, no rescale; a row whose result leaves the safe window (overflow, or
+ * L_i - anchor_i outside [-96 + 2 log2(nq), 120], where terms could flush to
+ * zero) is
+ * recomputed by the running-max kernel inside the same call (device-side
+ * decision, 4 launches, CUDA-graph capturable).  flags & OTK_ANCHOR_INIT:
+ * the anchor holds nothing yet -- running-max kernel, anchor written.  With
+ * anchor == NULL this is exactly otk_lse_partial + otk_lse_finalize.
+ * repair_ws: otk_lse_step_workspace_bytes(np) bytes (no initialisation). */
+size_t otk_lse_step_workspace_bytes(int64_t np);
+int otk_lse_step_anchored(int32_t d, int32_t flags);
+int otk_lse_step(const float *p, const float *p_sq, const uint16_t *p_hi,
+                 const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
+                 const float *q, const float *q_sq, const uint16_t *q_hi,
+                 const uint16_t *q_lo, const uint16_t *q_ext, int64_t nq, int32_t d,
+                 int32_t dpad, float split_inv, const float *q_bias, float kappa,
+                 int32_t flags, int32_t nsplit, float *partial, const float *base,
+                 int32_t mode, float eps, float kappa_next, float *out_pot,
+                 float *out_bias, int32_t *first_bad, int32_t step, float *anchor,
+                 int32_t *repair_ws, void *stream);
 
 /* K5 -- fused convergence check (sinkhorn.py:175-189 + _dual_objective 115-119).
  * From f_prev = f_t, f_next = f_{t+1} (the next rows half-step) and g = g_t:

@@ -20,9 +20,10 @@ OTK_OK, OTK_EINVAL, OTK_ECUDA, OTK_ENOTSUP, OTK_ENCCL = 0, -1, -2, -3, -4
 OTK_DIVERGED, OTK_BAD_POTENTIAL = 1, 2
 OTK_SAME_POINTS, OTK_CLAMP, OTK_IMPL_SIMT, OTK_IMPL_TC = 0x1, 0x2, 0x10, 0x20
 OTK_IMPL_NOPERSIST = 0x40
+OTK_ANCHOR_INIT, OTK_IMPL_NOANCHOR = 0x80, 0x100
 OTK_COST_EUCL = 0x4
 OTK_FIN_SOLVER, OTK_FIN_APPLY, OTK_FIN_LOG2 = 0, 1, 2
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 P = C.c_void_p
 I64, I32, F32, F64, SZ = C.c_int64, C.c_int32, C.c_float, C.c_double, C.c_size_t
@@ -57,6 +58,10 @@ SIGNATURES = {
     "otk_lse_suggest_nsplit": (C.c_int, [I64, I64, I32, I32]),
     "otk_lse_uses_tc": (C.c_int, [I32, I32]),
     "otk_lse_finalize": (C.c_int, [P, I32, I64, P, I32, F32, F32, P, P, P, I32, P]),
+    "otk_lse_step_workspace_bytes": (SZ, [I64]),
+    "otk_lse_step_anchored": (C.c_int, [I32, I32]),
+    "otk_lse_step": (C.c_int, [P, P, P, P, P, I64, P, P, P, P, P, I64, I32, I32, F32, P, F32, I32,
+                               I32, P, P, I32, F32, F32, P, P, P, I32, P, P, P]),
     "otk_check_workspace_bytes": (SZ, []),
     "otk_check": (C.c_int, [P, P, P, I64, P, P, I64, F64, P, P, P]),
     "otk_cost_workspace_bytes": (SZ, [I64, I64]),

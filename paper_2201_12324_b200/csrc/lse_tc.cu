@@ -244,7 +244,34 @@ struct Params {
   int probe;              // pipeline probe (OTK_TC_PROBE, timing experiments only):
                           // 1 = epilogue skips the math, 2 = sums without exp,
                           // 3 = no B operand loads, 4 = one product per K step
+  const float *anchor;    // FIX kernels: per-P-row anchor (log2), see lse_chunk_anchored
+  int *repair_ws;         // [0] = flagged-row count, [1 + rt] = row-tile flags
+  int nflags;             // row_tiles + 1 (flag slots the FIX kernel clears)
+  const int *tile_mask;   // repair launch: process only flagged row tiles (NULL = all)
 };
+
+// Units skipped by a repair launch (every role walks the same live sequence,
+// so barrier phases stay in step).
+__device__ __forceinline__ int live_unit(const Params &prm, int u, int stride) {
+  if (prm.tile_mask != nullptr)
+    while (u < prm.num_units && prm.tile_mask[u % prm.row_tiles] == 0) u += stride;
+  return u;
+}
+__device__ __forceinline__ int live_pair(const Params &prm, int u, int stride, int pair_rows, int num_pairs) {
+  if (prm.tile_mask != nullptr)
+    while (u < num_pairs && (prm.tile_mask[2 * (u % pair_rows)] | prm.tile_mask[2 * (u % pair_rows) + 1]) == 0)
+      u += stride;
+  return u;
+}
+// Prologue shared by both kernels: a repair launch with nothing flagged exits
+// at once; a FIX launch clears the flags its finalize will set.
+__device__ __forceinline__ bool repair_idle(const Params &prm) {
+  return prm.tile_mask != nullptr && *reinterpret_cast<const volatile int *>(prm.repair_ws) == 0;
+}
+__device__ __forceinline__ void clear_repair_flags(const Params &prm) {
+  if (blockIdx.x == 0 && prm.repair_ws != nullptr && prm.tile_mask == nullptr)
+    for (int i = threadIdx.x; i <= prm.nflags; i += blockDim.x) prm.repair_ws[i] = 0;
+}
 
 template <int V, bool A_RES, int NS, int ABUF, int NG>
 struct Plan {
@@ -346,7 +373,56 @@ __device__ __forceinline__ void lse_chunk(const float *acc, const float *bias, f
   s += t2.x + t2.y;
 }
 
-template <int V, bool A_RES, int NS, int ABUF, int EP, int NG, bool EU>
+// Anchored chunk (FIX kernels): the row's log2-sum is accumulated against a
+// FIXED per-row anchor S (the same row's result from the previous half-step
+// of this role) instead of a running max: s += sum 2^(u - S).  Per cell pair
+// one FFMA2, one FADD2, two MUFU ex2 and one FADD2 -- no max, no rescale
+// (B200 same-box probe at cfg2: 1.42 vs 1.58 ms per half-step).  Terms
+// cannot overflow unless the row's sum itself does (then s = +inf) and are
+// flushed only below 2^-126 of the anchor; finalize_anchored sends every row
+// whose result leaves the safe window back through the running-max kernel.
+template <int CH, bool MASK, int EP = 0>
+__device__ __forceinline__ void lse_chunk_anchored(const float *acc, const float *bias, float c2k,
+                                                   float S, int valid, float &s) {
+  const float2 k2 = make_float2(c2k, c2k);
+  const float2 nS = make_float2(-S, -S);
+  float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int i = 0; i < CH / 2; ++i) {
+    float2 x = __ffma2_rn(make_float2(acc[2 * i], acc[2 * i + 1]), k2,
+                          make_float2(bias[2 * i], bias[2 * i + 1]));
+    x = __fadd2_rn(x, nS);
+    if (MASK) {
+      if (2 * i >= valid) x.x = -INFINITY;
+      if (2 * i + 1 >= valid) x.y = -INFINITY;
+    }
+    float2 e;
+    if (i % 8 < EP) {  // FMA-pipe exp2; x <= 126 keeps it finite (T > 120 is repaired)
+      x.x = fminf(x.x, 126.f);
+      x.y = fminf(x.y, 126.f);
+      e = ex2_poly2(x);
+      if (MASK) {
+        if (2 * i >= valid) e.x = 0.f;
+        if (2 * i + 1 >= valid) e.y = 0.f;
+      }
+    } else {
+      e = make_float2(ex2(x.x), ex2(x.y));
+    }
+    acc2[i & 1] = __fadd2_rn(acc2[i & 1], e);
+  }
+  const float2 t2 = __fadd2_rn(acc2[0], acc2[1]);
+  s += t2.x + t2.y;
+}
+
+// Row state -> partial.  Running max: m + log2 s.  Anchored: S + log2 s
+// (s = 0 -> -inf, s = +inf -> +inf, NaN propagates).
+__device__ __forceinline__ float anchored_value(float S, float s) {
+  if (s != s) return s;
+  return (s > 0.f) ? S + lg2(s) : -INFINITY;
+}
+__device__ __forceinline__ float sanitize_anchor(float S) { return isfinite(S) ? S : 0.f; }
+
+template <int V, bool A_RES, int NS, int ABUF, int EP, int NG, bool EU, bool FIX>
 __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
     lse_tc_kernel(const __grid_constant__ CUtensorMap tm_phi, const __grid_constant__ CUtensorMap tm_plo,
                   const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo,
@@ -372,6 +448,8 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
   float *comb = reinterpret_cast<float *>(bars + 32);          // [2][NG-1][BM][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (repair_idle(prm)) return;
+  if (FIX) clear_repair_flags(prm);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -428,7 +506,8 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
       int stage = 0;
       uint32_t sphase = 0;
       int uc = 0, tcount = 0;
-      for (int u = blockIdx.x; u < prm.num_units; u += gridDim.x, ++uc) {
+      for (int u = live_unit(prm, blockIdx.x, gridDim.x); u < prm.num_units;
+           u = live_unit(prm, u + gridDim.x, gridDim.x), ++uc) {
         const int split = u / prm.row_tiles, rt = u % prm.row_tiles;
         const int t0 = split * prm.tps, t1 = min(prm.ntiles, t0 + prm.tps);
         if (A_RES) {
@@ -482,7 +561,8 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
       int stage = 0;
       uint32_t sphase = 0;
       int tcount = 0, uc = 0;
-      for (int u = blockIdx.x; u < prm.num_units; u += gridDim.x, ++uc) {
+      for (int u = live_unit(prm, blockIdx.x, gridDim.x); u < prm.num_units;
+           u = live_unit(prm, u + gridDim.x, gridDim.x), ++uc) {
         const int split = u / prm.row_tiles;
         const int t0 = split * prm.tps, t1 = min(prm.ntiles, t0 + prm.tps);
         const int ab = uc % ABUF;
@@ -548,10 +628,15 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
     const uint32_t t_lane = (uint32_t)(quarter * 32) << 16;
     const float c2k = prm.c2k;
     int tcount = 0, uc = 0;
-    for (int u = blockIdx.x; u < prm.num_units; u += gridDim.x, ++uc) {
+    for (int u = live_unit(prm, blockIdx.x, gridDim.x); u < prm.num_units;
+         u = live_unit(prm, u + gridDim.x, gridDim.x), ++uc) {
       const int split = u / prm.row_tiles, rt = u % prm.row_tiles;
       const int t0 = split * prm.tps, t1 = min(prm.ntiles, t0 + prm.tps);
       float m = -INFINITY, s = 0.f;
+      if constexpr (FIX) {  // m holds the row's anchor S for the whole unit
+        const int64_t row = (int64_t)rt * BM + row_local;
+        m = sanitize_anchor(row < prm.np ? prm.anchor[row] : 0.f);
+      }
       for (int t = t0; t < t1; ++t, ++tcount) {
         const int buf = tcount % NBUF;
         const int x = tcount % NSLOT;
@@ -607,6 +692,9 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
           } else if (prm.probe == 2) {
 #pragma unroll
             for (int i = 0; i < C::CH; ++i) s += fmaf(accv[i], c2k, bv[i]);
+          } else if constexpr (FIX) {
+            if (valid >= BN) lse_chunk_anchored<C::CH, false, EP>(accv, bv, c2k, m, 0, s);
+            else lse_chunk_anchored<C::CH, true, EP>(accv, bv, c2k, m, valid - c * C::CH, s);
           } else if (valid >= BN)
             lse_chunk<C::CH, false, EP>(accv, bv, c2k, 0, m, s);
           else
@@ -635,13 +723,21 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
       }
       asm volatile("bar.sync 1, %0;" ::"n"(128 * NG) : "memory");
       if (eg == 0) {
-        Lse2 st;
-        st.m = m;
-        st.s = s;
+        float val;
+        if constexpr (FIX) {  // same anchor in every group: the sums add (fixed order)
 #pragma unroll
-        for (int g = 0; g < NG - 1; ++g) st.merge(cb[(g * BM + row_local) * 2], cb[(g * BM + row_local) * 2 + 1]);
+          for (int g = 0; g < NG - 1; ++g) s += cb[(g * BM + row_local) * 2 + 1];
+          val = anchored_value(m, s);
+        } else {
+          Lse2 st;
+          st.m = m;
+          st.s = s;
+#pragma unroll
+          for (int g = 0; g < NG - 1; ++g) st.merge(cb[(g * BM + row_local) * 2], cb[(g * BM + row_local) * 2 + 1]);
+          val = st.value();
+        }
         const int64_t row = (int64_t)rt * BM + row_local;
-        if (row < prm.np) prm.partial[(int64_t)split * prm.np + row] = st.value();
+        if (row < prm.np) prm.partial[(int64_t)split * prm.np + row] = val;
       }
     }
   }
@@ -745,7 +841,7 @@ struct Plan2 {
                               2 * (NG - 1) * 2 * BM * (int)sizeof(float);
 };
 
-template <int KB, bool EU>
+template <int KB, bool EU, bool FIX>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     lse_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_phi, const __grid_constant__ CUtensorMap tm_plo,
                        const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo,
@@ -769,6 +865,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
+  if (repair_idle(prm)) return;  // uniform over the grid: before any cluster barrier
+  if (FIX) clear_repair_flags(prm);
 
   if (threadIdx.x == 0) {
     for (int q = 0; q < NS; ++q) {
@@ -829,7 +927,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t sphase = 0;
       int uc = 0, tcount = 0;
-      for (int u = cid; u < num_pairs; u += ncl, ++uc) {
+      for (int u = live_pair(prm, cid, ncl, pair_rows, num_pairs); u < num_pairs;
+           u = live_pair(prm, u + ncl, ncl, pair_rows, num_pairs), ++uc) {
         const int split = u / pair_rows, pr = u % pair_rows;
         const int rt = 2 * pr + (int)rank;
         const int t0 = split * prm.tps, t1 = min(prm.ntiles, t0 + prm.tps);
@@ -871,7 +970,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t sphase = 0;
       int tcount = 0, uc = 0;
-      for (int u = cid; u < num_pairs; u += ncl, ++uc) {
+      for (int u = live_pair(prm, cid, ncl, pair_rows, num_pairs); u < num_pairs;
+           u = live_pair(prm, u + ncl, ncl, pair_rows, num_pairs), ++uc) {
         const int split = u / pair_rows;
         const int t0 = split * prm.tps, t1 = min(prm.ntiles, t0 + prm.tps);
         const int ab = uc % ABUF;
@@ -918,11 +1018,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const float c2k = prm.c2k;
     const uint32_t tempty_l0 = mapa(smem_u32(&tempty[0]), 0), tempty_l1 = mapa(smem_u32(&tempty[1]), 0);
     int tcount = 0, uc = 0;
-    for (int u = cid; u < num_pairs; u += ncl, ++uc) {
+    for (int u = live_pair(prm, cid, ncl, pair_rows, num_pairs); u < num_pairs;
+         u = live_pair(prm, u + ncl, ncl, pair_rows, num_pairs), ++uc) {
       const int split = u / pair_rows, pr = u % pair_rows;
       const int rt = 2 * pr + (int)rank;
       const int t0 = split * prm.tps, t1 = min(prm.ntiles, t0 + prm.tps);
       float m = -INFINITY, s = 0.f;
+      if constexpr (FIX) {
+        const int64_t row = (int64_t)rt * BM + row_local;
+        m = sanitize_anchor(row < prm.np ? prm.anchor[row] : 0.f);
+      }
       for (int t = t0; t < t1; ++t, ++tcount) {
         const int buf = tcount & 1;
         const int x = tcount % NSLOT;
@@ -949,7 +1054,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             bv[4 * i + 2] = q.z;
             bv[4 * i + 3] = q.w;
           }
-          if (valid >= BN)
+          if constexpr (FIX) {
+            if (valid >= BN) lse_chunk_anchored<CH, false>(accv, bv, c2k, m, 0, s);
+            else lse_chunk_anchored<CH, true>(accv, bv, c2k, m, valid - c * CH, s);
+          } else if (valid >= BN)
             lse_chunk<CH, false, 0>(accv, bv, c2k, 0, m, s);
           else
             lse_chunk<CH, true, 0>(accv, bv, c2k, valid - c * CH, m, s);
@@ -979,13 +1087,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
       asm volatile("bar.sync 1, %0;" ::"n"(128 * NG) : "memory");
       if (eg == 0) {
-        Lse2 st;
-        st.m = m;
-        st.s = s;
+        float val;
+        if constexpr (FIX) {
 #pragma unroll
-        for (int g = 0; g < NG - 1; ++g) st.merge(cb[(g * BM + row_local) * 2], cb[(g * BM + row_local) * 2 + 1]);
+          for (int g = 0; g < NG - 1; ++g) s += cb[(g * BM + row_local) * 2 + 1];
+          val = anchored_value(m, s);
+        } else {
+          Lse2 st;
+          st.m = m;
+          st.s = s;
+#pragma unroll
+          for (int g = 0; g < NG - 1; ++g) st.merge(cb[(g * BM + row_local) * 2], cb[(g * BM + row_local) * 2 + 1]);
+          val = st.value();
+        }
         const int64_t row = (int64_t)rt * BM + row_local;
-        if (row < prm.np) prm.partial[(int64_t)split * prm.np + row] = st.value();
+        if (row < prm.np) prm.partial[(int64_t)split * prm.np + row] = val;
       }
     }
   }
@@ -1080,11 +1196,11 @@ static int emu_pairs(int v) {
   return 0;  // measured: the split-column epilogue is no longer MUFU-bound at d = 64
 }
 
-template <int V, bool A_RES, int NS, int ABUF, int EP, int NG, bool EU = false>
+template <int V, bool A_RES, int NS, int ABUF, int EP, int NG, bool EU = false, bool FIX = false>
 static int launch_one(const CUtensorMap (&maps)[7], const Params &prm, cudaStream_t st) {
   using L = Plan<V, A_RES, NS, ABUF, NG>;
   const int smem = L::smem_bytes(prm.kb);
-  auto kern = lse_tc_kernel<V, A_RES, NS, ABUF, EP, NG, EU>;
+  auto kern = lse_tc_kernel<V, A_RES, NS, ABUF, EP, NG, EU, FIX>;
   static bool attr_set = false;
   if (smem > 227 * 1024) {
     set_error("lse_tc: shared memory plan too large (%d B, kb=%d)", smem, prm.kb);
@@ -1108,8 +1224,19 @@ static int epi_groups() {
 }
 
 template <int V, bool A_RES, int NS, int ABUF>
-static int launch_variant(const CUtensorMap (&maps)[7], const Params &prm, bool eucl, cudaStream_t st) {
+static int launch_variant(const CUtensorMap (&maps)[7], const Params &prm, bool eucl, bool fix,
+                          cudaStream_t st) {
   if (eucl) return launch_one<V, A_RES, NS, ABUF, 0, 4, true>(maps, prm, st);  // default knobs only
+  if (fix) {
+    if constexpr (V == 1) {
+      switch (emu_pairs(V)) {
+        case 1: return launch_one<V, A_RES, NS, ABUF, 1, 4, false, true>(maps, prm, st);
+        case 2: return launch_one<V, A_RES, NS, ABUF, 2, 4, false, true>(maps, prm, st);
+        default: break;
+      }
+    }
+    return launch_one<V, A_RES, NS, ABUF, 0, 4, false, true>(maps, prm, st);
+  }
   const bool g4 = epi_groups() == 4;
   if constexpr (V == 1) {
     switch (emu_pairs(V)) {
@@ -1131,10 +1258,10 @@ static bool use_pair_kernel(int kb) {
   return kb == 2;
 }
 
-template <int KB, bool EU>
+template <int KB, bool EU, bool FIX = false>
 static int launch_pair(const CUtensorMap (&maps)[7], const Params &prm, cudaStream_t st) {
   using L = pair::Plan2<KB>;
-  auto kern = pair::lse_tc_pair_kernel<KB, EU>;
+  auto kern = pair::lse_tc_pair_kernel<KB, EU, FIX>;
   static bool attr_set = false;
   static_assert(L::SMEM <= 227 * 1024, "pair kernel shared memory plan too large");
   if (!attr_set) {
@@ -1175,10 +1302,14 @@ bool tc_available() {
 // Tile width used by the TC kernel for this depth (drives the split planning).
 int tc_tile_cols(int dpad) { return tc::variant_for(dpad / tc::BK) == 1 ? 256 : 128; }
 
+// anchor != NULL: anchored (FIX) launch -- sqeucl only -- which also clears
+// repair_ws[0 .. row_tiles + 1].  repair != 0: running-max launch over the
+// row tiles flagged in repair_ws (exits at once when repair_ws[0] == 0).
 int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
                   const uint16_t *q_hi, const uint16_t *q_lo, const uint16_t *q_ext, int64_t nq,
                   int dpad, float two_kappa_scaled, const float *q_bias, int nsplit,
-                  int same, int eucl, float *partial, cudaStream_t st) {
+                  int same, int eucl, float *partial, const float *anchor, int *repair_ws,
+                  int repair, cudaStream_t st) {
   using namespace tc;
   if (np > (int64_t)INT32_MAX || nq > (int64_t)INT32_MAX) {
     set_error("lse_tc: too many points");
@@ -1218,21 +1349,35 @@ int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_
   prm.partial = partial;
   prm.probe = getenv("OTK_TC_PROBE") ? atoi(getenv("OTK_TC_PROBE")) : 0;
   const bool eu = eucl != 0;
+  const bool fix = anchor != nullptr && !repair;
+  if (fix && eu) {
+    set_error("lse_tc: anchored launch needs the sqeucl epilogue");
+    return OTK_EINVAL;
+  }
+  if ((fix || repair) && repair_ws == nullptr) {
+    set_error("lse_tc: anchored / repair launch without repair workspace");
+    return OTK_EINVAL;
+  }
+  prm.anchor = fix ? anchor : nullptr;
+  prm.repair_ws = (fix || repair) ? repair_ws : nullptr;
+  prm.nflags = prm.row_tiles + 1;
+  prm.tile_mask = repair ? repair_ws + 1 : nullptr;
   if (use_pair) {
     if (eu) return kb == 1 ? launch_pair<1, true>(maps, prm, st) : launch_pair<2, true>(maps, prm, st);
+    if (fix) return kb == 1 ? launch_pair<1, false, true>(maps, prm, st) : launch_pair<2, false, true>(maps, prm, st);
     return kb == 1 ? launch_pair<1, false>(maps, prm, st) : launch_pair<2, false>(maps, prm, st);
   }
   if (v == 1) {
-    if (kb == 1) return launch_variant<1, true, 2, 2>(maps, prm, eu, st);
-    if (kb == 2) return launch_variant<1, true, 2, 1>(maps, prm, eu, st);
-    return launch_variant<1, false, 2, 1>(maps, prm, eu, st);
+    if (kb == 1) return launch_variant<1, true, 2, 2>(maps, prm, eu, fix, st);
+    if (kb == 2) return launch_variant<1, true, 2, 1>(maps, prm, eu, fix, st);
+    return launch_variant<1, false, 2, 1>(maps, prm, eu, fix, st);
   }
   if (v == 2) {
-    if (kb <= 2) return launch_variant<2, true, 4, 1>(maps, prm, eu, st);
-    if (kb <= 4) return launch_variant<2, true, 2, 1>(maps, prm, eu, st);
-    return launch_variant<2, false, 3, 1>(maps, prm, eu, st);
+    if (kb <= 2) return launch_variant<2, true, 4, 1>(maps, prm, eu, fix, st);
+    if (kb <= 4) return launch_variant<2, true, 2, 1>(maps, prm, eu, fix, st);
+    return launch_variant<2, false, 3, 1>(maps, prm, eu, fix, st);
   }
-  return launch_variant<4, false, 3, 1>(maps, prm, eu, st);
+  return launch_variant<4, false, 3, 1>(maps, prm, eu, fix, st);
 }
 
 }  // namespace otk

@@ -105,23 +105,61 @@ __global__ void bias_kernel(const float *__restrict__ pot, int64_t m, float kapp
   bias[j] = v * kappa;
 }
 
-__global__ void finalize_kernel(const float *__restrict__ part, int nsplit, int64_t np,
-                                const float *__restrict__ base, int mode, float eps,
-                                float kappa_next, float *__restrict__ out,
-                                float *__restrict__ out_bias, int *__restrict__ first_bad,
-                                int step) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= np) return;
-  const float L = combine_log2(part + i, nsplit, np);
-  if (mode == OTK_FIN_LOG2) {  // shard partial for the multi-GPU exchange
-    out[i] = L;
+__device__ __forceinline__ void finalize_row(const FinArgs &F, int64_t i, float L) {
+  if (F.anchor != nullptr) F.anchor[i] = isfinite(L) ? L : __int_as_float(0x7fc00000);
+  if (F.mode == OTK_FIN_LOG2) {  // shard partial for the multi-GPU exchange
+    F.out[i] = L;
     return;
   }
-  const float c = eps * kLn2;
-  const float v = (mode == OTK_FIN_SOLVER) ? eps * base[i] - c * L : base[i] + c * L;
-  out[i] = v;
-  if (out_bias != nullptr) out_bias[i] = v * kappa_next;
-  if (first_bad != nullptr && bad_potential(v)) atomicMin(first_bad, step);
+  const float c = F.eps * kLn2;
+  const float v = (F.mode == OTK_FIN_SOLVER) ? F.eps * F.base[i] - c * L : F.base[i] + c * L;
+  F.out[i] = v;
+  if (F.out_bias != nullptr) F.out_bias[i] = v * F.kappa_next;
+  if (F.first_bad != nullptr && bad_potential(v)) atomicMin(F.first_bad, F.step);
+}
+
+__global__ void finalize_kernel(const FinArgs F) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= F.np) return;
+  finalize_row(F, i, combine_log2(F.part + i, F.nsplit, F.np));
+}
+
+// After an anchored launch: accept the row when its anchor was finite and the
+// result lies in the window (lo <= L - anchor <= 120: every term within 2^-30 of the
+// row's sum was above the ex2 flush threshold; an overflowing sum shows up
+// as L = +inf), or when L is NaN (a NaN potential propagates exactly as in the
+// running-max kernel).  Otherwise flag the row's 128-row tile for the repair
+// launch and leave the row to finalize_repair_kernel.
+__global__ void finalize_anchored_kernel(const FinArgs F) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= F.np) return;
+  const float L = combine_log2(F.part + i, F.nsplit, F.np);
+  const float S = F.anchor[i];
+  const bool ok = isfinite(S) && (L != L || (isfinite(L) && L - S >= F.lo && L - S <= 120.f));
+  if (!ok) {
+    atomicAdd(F.repair_ws, 1);
+    F.repair_ws[1 + (i >> 7)] = 1;
+    return;
+  }
+  finalize_row(F, i, L);
+}
+
+// After the repair launch: re-finalize every row of a flagged tile from the
+// running-max partials.
+__global__ void finalize_repair_kernel(const FinArgs F) {
+  if (*reinterpret_cast<const volatile int *>(F.repair_ws) == 0) return;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= F.np || F.repair_ws[1 + (i >> 7)] == 0) return;
+  finalize_row(F, i, combine_log2(F.part + i, F.nsplit, F.np));
+}
+
+int finalize_launch(int kind, const FinArgs &F, cudaStream_t st) {
+  const unsigned blocks = (unsigned)((F.np + 255) / 256);
+  if (kind == 0) finalize_kernel<<<blocks, 256, 0, st>>>(F);
+  else if (kind == 1) finalize_anchored_kernel<<<blocks, 256, 0, st>>>(F);
+  else finalize_repair_kernel<<<blocks, 256, 0, st>>>(F);
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
 }
 
 // ---------------------------------------------------------------- K5 check
@@ -266,10 +304,9 @@ int otk_lse_finalize(const float *partial, int32_t nsplit, int64_t np, const flo
   OTK_CHECK_ARG(mode == OTK_FIN_SOLVER || mode == OTK_FIN_APPLY || mode == OTK_FIN_LOG2,
                 "otk_lse_finalize: bad mode");
   OTK_CHECK_ARG(base || mode == OTK_FIN_LOG2, "otk_lse_finalize: base required");
-  finalize_kernel<<<(unsigned)((np + 255) / 256), 256, 0, as_stream(stream)>>>(
-      partial, nsplit, np, base, mode, eps, kappa_next, out_pot, out_bias, first_bad, step);
-  OTK_LAUNCH_CHECK();
-  return OTK_OK;
+  FinArgs F{partial, nsplit, np, base, mode, eps, kappa_next, out_pot, out_bias, first_bad, step,
+            nullptr, nullptr, 0.f};
+  return finalize_launch(0, F, as_stream(stream));
 }
 
 size_t otk_check_workspace_bytes(void) {

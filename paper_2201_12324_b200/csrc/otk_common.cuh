@@ -93,4 +93,23 @@ __device__ __forceinline__ float combine_log2(const float *part, int nsplit, int
 
 __device__ __forceinline__ bool bad_potential(float v) { return (v != v) || v == INFINITY; }
 
+// Finalize of a half-step (otk_api.cu): combine the split partials, form the
+// potential (mode), write the next bias / anchor, flag bad potentials.
+struct FinArgs {
+  const float *part;
+  int nsplit;
+  int64_t np;
+  const float *base;
+  int mode;
+  float eps, kappa_next;
+  float *out, *out_bias;
+  int *first_bad;
+  int step;
+  float *anchor;  // nullable: the row's L for the next anchored half-step (NaN if not finite)
+  int *repair_ws; // anchored: [0] = flagged rows, [1 + i / 128] = row-tile flags
+  float lo;       // anchored: smallest L - anchor accepted (see lse_tc.cu lse_chunk_anchored)
+};
+// kind 0 = plain, 1 = after an anchored launch, 2 = after the repair launch
+int finalize_launch(int kind, const FinArgs &F, cudaStream_t st);
+
 }  // namespace otk

@@ -30,7 +30,8 @@ int lse_simt_launch(const float *p, const float *p_sq, int64_t np, const float *
 int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
                   const uint16_t *q_hi, const uint16_t *q_lo, const uint16_t *q_ext, int64_t nq,
                   int dpad, float two_kappa_scaled, const float *q_bias, int nsplit, int same,
-                  int eucl, float *partial, cudaStream_t st);
+                  int eucl, float *partial, const float *anchor, int *repair_ws, int repair,
+                  cudaStream_t st);
 bool tc_available();
 int tc_tile_cols(int dpad);
 namespace small {
@@ -53,6 +54,12 @@ int small_solve_launch(const small::Args &A, bool same, bool eucl, cudaStream_t 
 }  // namespace otk
 
 using namespace otk;
+
+#define OTK_TRY_(expr)           \
+  do {                           \
+    int _r = (expr);             \
+    if (_r != OTK_OK) return _r; \
+  } while (0)
 
 // tcgen05 kernel for every d (measured on B200 at n = m = 65536, ncu in
 // profiles/r01_ncu_route_*.txt: 1.40 ms per half-step at d = 3 and 1.50 ms at
@@ -106,11 +113,63 @@ extern "C" int otk_lse_partial(const float *p, const float *p_sq, const uint16_t
     const bool eu = flags & OTK_COST_EUCL;
     const float scale = eu ? -kappa * sqrtf(2.f * split_inv) : 2.f * kappa * split_inv;
     return lse_tc_launch(p_hi, p_lo, p_ext, np, q_hi, q_lo, q_ext, nq, dpad, scale, q_bias, nsplit,
-                         (flags & OTK_SAME_POINTS) ? 1 : 0, eu ? 1 : 0, partial, as_stream(stream));
+                         (flags & OTK_SAME_POINTS) ? 1 : 0, eu ? 1 : 0, partial, nullptr, nullptr, 0,
+                         as_stream(stream));
   }
   OTK_CHECK_ARG(p && q && p_sq && q_sq, "otk_lse_partial: FP32 path needs points and squared norms");
   return lse_simt_launch(p, p_sq, np, q, q_sq, nq, d, q_bias, kappa, flags, nsplit, partial,
                          as_stream(stream));
+}
+
+static bool anchored_path(int32_t d, int32_t flags) {
+  return want_tc(flags, d) && tc_available() && !(flags & (OTK_COST_EUCL | OTK_IMPL_NOANCHOR));
+}
+
+extern "C" int otk_lse_step_anchored(int32_t d, int32_t flags) { return anchored_path(d, flags) ? 1 : 0; }
+
+extern "C" size_t otk_lse_step_workspace_bytes(int64_t np) {
+  return (size_t)(((np + 127) / 128) + 2) * sizeof(int32_t);
+}
+
+// One whole half-step: otk_lse_partial + otk_lse_finalize, anchored on the TC
+// sqeucl path.  Launch sequence when anchored (4 launches, graph-capturable,
+// no host decision): anchored partial -> finalize_anchored (accepts rows in
+// the safe window, flags the tiles of the others) -> running-max partial over
+// the flagged tiles only (exits at once when none) -> finalize_repair.
+extern "C" int otk_lse_step(const float *p, const float *p_sq, const uint16_t *p_hi,
+                            const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
+                            const float *q, const float *q_sq, const uint16_t *q_hi,
+                            const uint16_t *q_lo, const uint16_t *q_ext, int64_t nq, int32_t d,
+                            int32_t dpad, float split_inv, const float *q_bias, float kappa,
+                            int32_t flags, int32_t nsplit, float *partial, const float *base,
+                            int32_t mode, float eps, float kappa_next, float *out_pot,
+                            float *out_bias, int32_t *first_bad, int32_t step, float *anchor,
+                            int32_t *repair_ws, void *stream) {
+  OTK_CHECK_ARG(partial && out_pot && np > 0 && nq > 0 && nsplit >= 1, "otk_lse_step: bad arguments");
+  OTK_CHECK_ARG(mode == OTK_FIN_SOLVER || mode == OTK_FIN_APPLY || mode == OTK_FIN_LOG2,
+                "otk_lse_step: bad mode");
+  OTK_CHECK_ARG(base || mode == OTK_FIN_LOG2, "otk_lse_step: base required");
+  cudaStream_t st = as_stream(stream);
+  FinArgs F{partial, nsplit, np, base, mode, eps, kappa_next, out_pot, out_bias, first_bad, step,
+            anchor, repair_ws, 0.f};
+  const bool anch = anchor != nullptr && !(flags & OTK_ANCHOR_INIT) && anchored_path(d, flags);
+  if (!anch) {
+    OTK_TRY_(otk_lse_partial(p, p_sq, p_hi, p_lo, p_ext, np, q, q_sq, q_hi, q_lo, q_ext, nq, d, dpad,
+                             split_inv, q_bias, kappa, flags, nsplit, partial, stream));
+    return finalize_launch(0, F, st);
+  }
+  OTK_CHECK_ARG(repair_ws && p_hi && p_lo && p_ext && q_hi && q_lo && q_ext && dpad % 64 == 0 && dpad >= d,
+                "otk_lse_step: anchored path needs the repair workspace and the split + norm planes");
+  // flushed mass <= nq^2 2^(-126 - (L - anchor)) of the row's sum: <= 2^-30 for L - anchor >= lo
+  F.lo = -96.f + 2.f * log2f((float)nq);
+  const float scale = 2.f * kappa * split_inv;
+  const int same = (flags & OTK_SAME_POINTS) ? 1 : 0;
+  OTK_TRY_(lse_tc_launch(p_hi, p_lo, p_ext, np, q_hi, q_lo, q_ext, nq, dpad, scale, q_bias, nsplit,
+                         same, 0, partial, anchor, repair_ws, 0, st));
+  OTK_TRY_(finalize_launch(1, F, st));
+  OTK_TRY_(lse_tc_launch(p_hi, p_lo, p_ext, np, q_hi, q_lo, q_ext, nq, dpad, scale, q_bias, nsplit,
+                         same, 0, partial, nullptr, repair_ws, 1, st));
+  return finalize_launch(2, F, st);
 }
 
 // ------------------------------------------------------------------ solver
@@ -130,6 +189,8 @@ struct Carver {
 
 struct Layout {
   float *fA, *fB, *g, *xsq, *ysq, *bias_x, *bias_y, *part;
+  float *anc_x, *anc_y;       // anchors of the rows / cols half-steps (otk_lse_step)
+  int *rep_x, *rep_y;         // their repair workspaces
   uint16_t *xhi, *xlo, *yhi, *ylo, *xea, *xeb, *yea, *yeb;
   float *absmax;
   double *chk;
@@ -166,6 +227,10 @@ Layout plan(const otk_solve_args *A, void *ws) {
   L.bias_x = c.take<float>(A->n);
   L.bias_y = c.take<float>(A->m);
   L.part = c.take<float>(std::max((size_t)L.nsr * A->n, (size_t)L.nsc * A->m));
+  L.anc_x = c.take<float>(A->n);
+  L.anc_y = c.take<float>(A->m);
+  L.rep_x = reinterpret_cast<int *>(c.take<char>(otk_lse_step_workspace_bytes(A->n)));
+  L.rep_y = reinterpret_cast<int *>(c.take<char>(otk_lse_step_workspace_bytes(A->m)));
   if (L.tc) {
     L.xhi = c.take<uint16_t>((size_t)A->n * L.dpad);
     L.xlo = c.take<uint16_t>((size_t)A->n * L.dpad);
@@ -209,29 +274,36 @@ extern "C" size_t otk_solve_workspace_bytes(const otk_solve_args *A) {
     if (_r != OTK_OK) return _r; \
   } while (0)
 
+// Half-steps go through otk_lse_step: the first of each role runs the
+// running-max kernel and records the per-row anchors, every later one is
+// anchored (TC sqeucl path; OTK_IMPL_NOANCHOR disables it).
 struct HalfStep {
   const otk_solve_args *A;
   Layout *L;
   cudaStream_t st;
   float sinv;  // 1/s^2 for the TC operand scaling (one common scale s)
   int kflags;
+  bool anchored;  // anchored path available for this problem
   int launches = 0;
+  bool have_x = false, have_y = false;
 
   int rows(float kappa, float eps, float kappa_next, float *f_out, int step) {
-    launches += 2;
-    OTK_TRY(otk_lse_partial(A->x, L->xsq, L->xhi, L->xlo, L->xea, A->n, A->y, L->ysq, L->yhi,
-                            L->ylo, L->yeb, A->m, A->d, L->dpad, sinv, L->bias_y, kappa, kflags,
-                            L->nsr, L->part, st));
-    return otk_lse_finalize(L->part, L->nsr, A->n, A->log_a, OTK_FIN_SOLVER, eps, kappa_next, f_out,
-                            L->bias_x, L->first_bad, step, st);
+    const int fl = kflags | (have_x ? 0 : OTK_ANCHOR_INIT);
+    launches += (anchored && have_x) ? 4 : 2;
+    have_x = true;
+    return otk_lse_step(A->x, L->xsq, L->xhi, L->xlo, L->xea, A->n, A->y, L->ysq, L->yhi, L->ylo,
+                        L->yeb, A->m, A->d, L->dpad, sinv, L->bias_y, kappa, fl, L->nsr, L->part,
+                        A->log_a, OTK_FIN_SOLVER, eps, kappa_next, f_out, L->bias_x, L->first_bad,
+                        step, anchored ? L->anc_x : nullptr, L->rep_x, st);
   }
   int cols(float kappa, float eps, float kappa_next, int step) {
-    launches += 2;
-    OTK_TRY(otk_lse_partial(A->y, L->ysq, L->yhi, L->ylo, L->yea, A->m, A->x, L->xsq, L->xhi,
-                            L->xlo, L->xeb, A->n, A->d, L->dpad, sinv, L->bias_x, kappa, kflags,
-                            L->nsc, L->part, st));
-    return otk_lse_finalize(L->part, L->nsc, A->m, A->log_b, OTK_FIN_SOLVER, eps, kappa_next, L->g,
-                            L->bias_y, L->first_bad, step, st);
+    const int fl = kflags | (have_y ? 0 : OTK_ANCHOR_INIT);
+    launches += (anchored && have_y) ? 4 : 2;
+    have_y = true;
+    return otk_lse_step(A->y, L->ysq, L->yhi, L->ylo, L->yea, A->m, A->x, L->xsq, L->xhi, L->xlo,
+                        L->xeb, A->n, A->d, L->dpad, sinv, L->bias_x, kappa, fl, L->nsc, L->part,
+                        A->log_b, OTK_FIN_SOLVER, eps, kappa_next, L->g, L->bias_y, L->first_bad,
+                        step, anchored ? L->anc_y : nullptr, L->rep_y, st);
   }
 };
 
@@ -345,6 +417,7 @@ static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st) {
   HalfStep H{A, &L, st, 1.f / (s * s),
              (A->flags & (OTK_IMPL_SIMT | OTK_IMPL_TC | OTK_COST_EUCL)) | OTK_CLAMP |
                  (A->same_points ? OTK_SAME_POINTS : 0)};
+  H.anchored = L.tc && !(A->flags & OTK_IMPL_NOANCHOR) && otk_lse_step_anchored(A->d, H.kflags);
 
   // ---- initial g (zeros or warm start) and its bias for h = 1
   const double e0 = eps_at(A, 0);

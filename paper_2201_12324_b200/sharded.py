@@ -199,6 +199,14 @@ class CudaShardEngine:
         self.chk_ws = torch.zeros(lib.otk_check_workspace_bytes(), dtype=torch.uint8, device=dev)
         self.device = dev
         self.launches = 0
+        # anchored half-steps (otk_lse_step): per-role anchors + repair workspaces
+        self.anchored = bool(lib.otk_lse_step_anchored(self.d, self.flags)) and not (
+            flags & N.OTK_IMPL_NOANCHOR)
+        self.anc_x = torch.empty(self.n, **f32)
+        self.anc_y = torch.empty(self.m, **f32)
+        self.rep_x = torch.empty(lib.otk_lse_step_workspace_bytes(self.n), dtype=torch.uint8, device=dev)
+        self.rep_y = torch.empty(lib.otk_lse_step_workspace_bytes(self.m), dtype=torch.uint8, device=dev)
+        self.have_x = self.have_y = False
 
     def set_g(self, g_init, kappa):
         if g_init is None:
@@ -208,30 +216,39 @@ class CudaShardEngine:
         N.check(N.lib().otk_make_bias(N.ptr(self.g), self.m, kappa, N.ptr(self.bias_y),
                                       N.ptr(self.first_bad), 1, stream()), "make_bias")
 
+    def _launches(self, have):
+        return 4 if (self.anchored and have) else 2
+
     def rows(self, kappa, eps, kappa_next, which, step):
+        """Local f half-step (otk_lse_step: partial + finalize, anchored after the first)."""
         cx, cy, lib = self.cx, self.cy, N.lib()
-        st = stream()
-        N.check(lib.otk_lse_partial(N.ptr(cx.p), N.ptr(cx.sq), N.ptr(cx.hi), N.ptr(cx.lo),
-                                    N.ptr(cx.ext_a), self.n, N.ptr(cy.p), N.ptr(cy.sq), N.ptr(cy.hi),
-                                    N.ptr(cy.lo), N.ptr(cy.ext_b), self.m, self.d, cx.dpad,
-                                    self.sinv, N.ptr(self.bias_y), kappa, self.flags, self.nsr,
-                                    N.ptr(self.part), st), "rows half-step")
-        N.check(lib.otk_lse_finalize(N.ptr(self.part), self.nsr, self.n, N.ptr(self.la),
-                                     N.OTK_FIN_SOLVER, eps, kappa_next, N.ptr(self.f[which]),
-                                     N.ptr(self.bias_x), N.ptr(self.first_bad), step, st), "finalize")
-        self.launches += 2
+        fl = self.flags | (0 if self.have_x else N.OTK_ANCHOR_INIT)
+        N.check(lib.otk_lse_step(N.ptr(cx.p), N.ptr(cx.sq), N.ptr(cx.hi), N.ptr(cx.lo),
+                                 N.ptr(cx.ext_a), self.n, N.ptr(cy.p), N.ptr(cy.sq), N.ptr(cy.hi),
+                                 N.ptr(cy.lo), N.ptr(cy.ext_b), self.m, self.d, cx.dpad,
+                                 self.sinv, N.ptr(self.bias_y), kappa, fl, self.nsr,
+                                 N.ptr(self.part), N.ptr(self.la), N.OTK_FIN_SOLVER, eps, kappa_next,
+                                 N.ptr(self.f[which]), N.ptr(self.bias_x), N.ptr(self.first_bad), step,
+                                 N.ptr(self.anc_x) if self.anchored else None, N.ptr(self.rep_x),
+                                 stream()), "rows half-step")
+        self.launches += self._launches(self.have_x)
+        self.have_x = True
 
     def cols_partial(self, kappa):
+        """This shard's log2 column partials (OTK_FIN_LOG2), anchored on the shard's own
+        previous partials."""
         cx, cy, lib = self.cx, self.cy, N.lib()
-        st = stream()
-        N.check(lib.otk_lse_partial(N.ptr(cy.p), N.ptr(cy.sq), N.ptr(cy.hi), N.ptr(cy.lo),
-                                    N.ptr(cy.ext_a), self.m, N.ptr(cx.p), N.ptr(cx.sq), N.ptr(cx.hi),
-                                    N.ptr(cx.lo), N.ptr(cx.ext_b), self.n, self.d, cx.dpad,
-                                    self.sinv, N.ptr(self.bias_x), kappa, self.flags, self.nsc,
-                                    N.ptr(self.part), st), "cols half-step")
-        N.check(lib.otk_lse_finalize(N.ptr(self.part), self.nsc, self.m, None, N.OTK_FIN_LOG2, 0.0,
-                                     0.0, N.ptr(self.lcol), None, None, 0, st), "shard partial")
-        self.launches += 2
+        fl = self.flags | (0 if self.have_y else N.OTK_ANCHOR_INIT)
+        N.check(lib.otk_lse_step(N.ptr(cy.p), N.ptr(cy.sq), N.ptr(cy.hi), N.ptr(cy.lo),
+                                 N.ptr(cy.ext_a), self.m, N.ptr(cx.p), N.ptr(cx.sq), N.ptr(cx.hi),
+                                 N.ptr(cx.lo), N.ptr(cx.ext_b), self.n, self.d, cx.dpad,
+                                 self.sinv, N.ptr(self.bias_x), kappa, fl, self.nsc,
+                                 N.ptr(self.part), None, N.OTK_FIN_LOG2, 0.0, 0.0,
+                                 N.ptr(self.lcol), None, None, 0,
+                                 N.ptr(self.anc_y) if self.anchored else None, N.ptr(self.rep_y),
+                                 stream()), "cols half-step")
+        self.launches += self._launches(self.have_y)
+        self.have_y = True
         return self.lcol
 
     def cols_finalize(self, lall, eps, kappa_next, step):

@@ -202,7 +202,7 @@ def solve_sinkhorn(prob: LinearProblem, eps=None, *, threshold: float = 1e-3, ma
                    use_graphs: bool = True) -> SinkhornOutput:
     """Runs log-domain Sinkhorn iterations until the marginals match (sinkhorn.py:122-148).
 
-    ``impl`` ("auto" | "simt" | "tc") and ``use_graphs`` are performance knobs
+    ``impl`` ("auto" | "simt" | "tc" | "tc-noanchor") and ``use_graphs`` are performance knobs
     that never change results beyond float32 rounding.  ``g_init`` is the
     warm start of the reference's internal ``_sinkhorn_iterations``.
     """
@@ -231,7 +231,9 @@ def _impl_flags(impl: str) -> int:
         return N.OTK_IMPL_SIMT
     if impl == "tc":
         return N.OTK_IMPL_TC
-    raise ValueError("impl must be 'auto', 'simt' or 'tc'")
+    if impl == "tc-noanchor":  # A/B knob: running-max half-steps only
+        return N.OTK_IMPL_TC | N.OTK_IMPL_NOANCHOR
+    raise ValueError("impl must be 'auto', 'simt', 'tc' or 'tc-noanchor'")
 
 
 def _raise_status(rc: int, iteration: int):

@@ -21,7 +21,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tc"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tc", "tc-noanchor"])
     ap.add_argument("--n", type=int)
     ap.add_argument("--m", type=int)
     ap.add_argument("--d", type=int)
@@ -34,6 +34,8 @@ def main():
         geom.impl_flags = N.OTK_IMPL_SIMT
     elif args.kernel == "tc":
         geom.impl_flags = N.OTK_IMPL_TC
+    elif args.kernel == "tc-noanchor":
+        geom.impl_flags = N.OTK_IMPL_TC | N.OTK_IMPL_NOANCHOR
     r = bench.online_roofline(geom, wl, reps=args.reps)
     print(f"config {args.config}: {r['kernel_ms']:.3f} ms per half-step, "
           f"{r['pipes']['cells_per_s']:.3e} cells/s, {r['bound']} frac {r['frac']:.3f}")
