@@ -566,6 +566,7 @@ def run_e2e(otk, wl, args, dev, world, rank):
         def step():
             outs = otk.solve_sinkhorn_batched(xh, yh, wl.eps, threshold=wl.threshold,
                                               max_iters=wl.max_iters)
+            assert outs.f.shape[0] == outs.g.shape[0]  # the potentials read back (D2H)
             return int(np.sum(outs.iterations))
         h2d = wl.x.nbytes + wl.y.nbytes
         d2h = 4 * (n + m) * wl.x.shape[0]

@@ -118,11 +118,37 @@ class BatchedSinkhornOutput(Sequence):
 
     def __init__(self, f, g, err_tab, dual_tab, n_rec, iterations, converged, eps, f_device,
                  g_device):
-        self.f, self.g = f, g
-        self._err, self._dual, self._n = err_tab, dual_tab, n_rec
+        # f / g / the trace tables may be device tensors: copied to the host on
+        # first access (a batch whose potentials stay on the GPU never pays it)
+        self._f, self._g = f, g
+        self._err_src, self._dual_src, self._n = err_tab, dual_tab, n_rec
         self.iterations, self.converged, self.eps = iterations, converged, eps
         self.f_device, self.g_device = f_device, g_device
         self._cache = {}
+
+    @staticmethod
+    def _host(v, dtype):
+        return v if isinstance(v, np.ndarray) else v.cpu().numpy().astype(dtype)
+
+    @property
+    def f(self):
+        self._f = self._host(self._f, np.float64)
+        return self._f
+
+    @property
+    def g(self):
+        self._g = self._host(self._g, np.float64)
+        return self._g
+
+    @property
+    def _err(self):
+        self._err_src = self._host(self._err_src, np.float64)
+        return self._err_src
+
+    @property
+    def _dual(self):
+        self._dual_src = self._host(self._dual_src, np.float64)
+        return self._dual_src
 
     def __len__(self):
         return len(self.iterations)
@@ -470,10 +496,21 @@ def _dense_persistent(C, weights, eps, threshold, max_iters, inner_iters, g_init
             raise ValueError(f"problem {k}: g contains NaN or +inf entries")
         raise DivergedError("NaN in Sinkhorn potentials; eps is likely too small for the cost scale",
                             iteration=int(st[k, 4]))
-    return BatchedSinkhornOutput(f_out.cpu().numpy().astype(np.float64),
-                                 g_out.cpu().numpy().astype(np.float64), errs.cpu().numpy(),
-                                 duals.cpu().numpy(), st[:, 0].copy(), st[:, 1].copy(),
+    return BatchedSinkhornOutput(f_out, g_out, errs, duals, st[:, 0].copy(), st[:, 1].copy(),
                                  st[:, 2].astype(bool), np.asarray(eps, dtype=float), f_out, g_out)
+
+
+_UNIFORM_CACHE: dict = {}
+
+
+class _LazyUniform:
+    """Host view of uniform batched weights, built only if a caller needs it."""
+
+    def __init__(self, B, size):
+        self.B, self.size = B, size
+
+    def __getitem__(self, k):
+        return np.full(self.size, 1.0 / self.size)
 
 
 def solve_sinkhorn_batched(x, y, eps, a=None, b=None, *, threshold: float = 1e-3,
@@ -502,14 +539,18 @@ def solve_sinkhorn_batched(x, y, eps, a=None, b=None, *, threshold: float = 1e-3
     eps = np.broadcast_to(np.asarray(eps, dtype=float), (B,))
     if not np.all(eps > 0):
         raise ValueError("eps must be positive")
-    scheds = [EpsilonSchedule(float(e)) for e in eps]
     _fp32_guard(EpsilonSchedule(float(eps.min())), inner_iters, max_iters)
     dev = xd.device
 
     def weights_of(w, size, name):
-        if w is None:  # uniform: built on the device
-            u = torch.full((B, size), 1.0 / size, dtype=torch.float32, device=dev)
-            return np.full((B, size), 1.0 / size), u, torch.full_like(u, float(-np.log(size)))
+        if w is None:  # uniform: built on the device once per shape (read-only)
+            key = (B, size, str(dev))
+            if key not in _UNIFORM_CACHE:
+                u = torch.full((B, size), 1.0 / size, dtype=torch.float32, device=dev)
+                _UNIFORM_CACHE.clear()
+                _UNIFORM_CACHE[key] = (u, torch.full_like(u, float(-np.log(size))))
+            u, lu = _UNIFORM_CACHE[key]
+            return _LazyUniform(B, size), u, lu
         ww = np.stack([_as_weights(w[k], size, name) for k in range(B)])
         with np.errstate(divide="ignore"):
             return ww, as_device_f32(ww), as_device_f32(np.log(ww))
@@ -524,6 +565,7 @@ def solve_sinkhorn_batched(x, y, eps, a=None, b=None, *, threshold: float = 1e-3
         outs = _dense_persistent(C, (a_d, b_d, la_d, lb_d), np.asarray(eps, dtype=float), threshold,
                                  max_iters, inner_iters, g_init)
     else:
+        scheds = [EpsilonSchedule(float(e)) for e in eps]
         outs = _dense_loop(C, CT, (a_d, b_d, la_d, lb_d), scheds, threshold, max_iters,
                            inner_iters, g_init=g_init)
     if not return_cost:
