@@ -1301,6 +1301,11 @@ bool tc_available() {
 
 // Tile width used by the TC kernel for this depth (drives the split planning).
 int tc_tile_cols(int dpad) { return tc::variant_for(dpad / tc::BK) == 1 ? 256 : 128; }
+// 1 if this depth runs the CTA-pair kernel (work units are pairs of row tiles).
+int tc_uses_pair(int dpad) {
+  const int kb = dpad / tc::BK;
+  return (tc::variant_for(kb) == 1 && kb <= 2 && tc::use_pair_kernel(kb)) ? 1 : 0;
+}
 
 // anchor != NULL: anchored (FIX) launch -- sqeucl only -- which also clears
 // repair_ws[0 .. row_tiles + 1].  repair != 0: running-max launch over the

@@ -16,6 +16,9 @@
 // full pass of the reference is folded into the next iteration's work.
 // Constant-eps check periods are captured once as CUDA graphs and replayed.
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdlib>
 #include <climits>
 #include <cstring>
@@ -34,6 +37,7 @@ int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_
                   cudaStream_t st);
 bool tc_available();
 int tc_tile_cols(int dpad);
+int tc_uses_pair(int dpad);
 namespace small {
 struct Args {
   const float *x, *y, *a, *b, *la, *lb, *g_init;
@@ -76,15 +80,55 @@ static bool want_tc(int flags, int d) {
 
 extern "C" int otk_lse_uses_tc(int32_t d, int32_t flags) { return want_tc(flags, d) ? 1 : 0; }
 
+// Column-split count for the persistent TC kernel.  Its work units are
+// (row tile [pair]) x (column split), dealt round-robin to min(units, SMs
+// [/2]) CTAs [clusters]; the slowest CTA sets the half-step time.  Pick the
+// split count (1..16) with the best modelled makespan: tiles of the busiest
+// CTA plus a per-unit switch cost of ~0.4 tile (measured on B200 at cfg2:
+// nsplit 1 / 2 / 3 / 4 / 8 -> 1.53 / 1.38 / 1.43 / 1.39 / 1.39 ms, i.e. 86 /
+// 99 / 94 / 99 / 99 % balance).  Ties go to fewer splits (smaller partials).
+static int tc_balanced_nsplit(int64_t np, int64_t nq, int dpad) {
+  static std::mutex mu;
+  static std::map<std::tuple<int64_t, int64_t, int>, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(np, nq, dpad);
+  if (auto it = cache.find(key); it != cache.end()) return it->second;
+  const int bn = tc_tile_cols(dpad);
+  const bool pair = tc_uses_pair(dpad) != 0;
+  const int64_t row_tiles = (np + 127) / 128;
+  const int64_t rows_units = pair ? (row_tiles + 1) / 2 : row_tiles;
+  const int64_t ntiles = (nq + bn - 1) / bn;
+  const int64_t slots = pair ? num_sms() / 2 : num_sms();
+  int best = 1;
+  double best_cost = 1e300;
+  for (int ns = 1; ns <= 16 && ns <= ntiles; ++ns) {
+    const int64_t tps = (ntiles + ns - 1) / ns;
+    if ((ns - 1) * tps >= ntiles) continue;  // an empty split
+    const int64_t units = rows_units * ns;
+    const int64_t G = std::min<int64_t>(units, slots);
+    double worst = 0.0;
+    for (int64_t c = 0; c < G; ++c) {  // CTA c takes units c, c + G, ...
+      double t = 0.0;
+      for (int64_t u = c; u < units; u += G) {
+        const int64_t split = u / rows_units;
+        t += (double)(std::min(ntiles, (split + 1) * tps) - split * tps) + 0.4;
+      }
+      worst = std::max(worst, t);
+    }
+    if (worst < best_cost * (1.0 - 1e-9)) {
+      best_cost = worst;
+      best = ns;
+    }
+  }
+  cache.emplace(key, best);
+  return best;
+}
+
 extern "C" int otk_lse_suggest_nsplit(int64_t np, int64_t nq, int32_t d, int32_t flags) {
   const int sms = num_sms();
   if (want_tc(flags, d)) {
-    // TC kernel: 128-row tiles, 256- or 128-column tiles; aim for >= 8 work units per SM.
-    const int bn = tc_tile_cols((d + 63) / 64 * 64);
-    int64_t row_tiles = (np + 127) / 128;
-    int64_t col_tiles = (nq + bn - 1) / bn;
-    int64_t want = (8LL * sms + row_tiles - 1) / row_tiles;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(want, col_tiles));
+    if (const char *e = getenv("OTK_TC_NSPLIT")) return std::max(1, atoi(e));  // A/B knob
+    return tc_balanced_nsplit(np, nq, (d + 63) / 64 * 64);
   }
   int64_t row_tiles = (np + 63) / 64;
   int64_t col_tiles = (nq + 63) / 64;
