@@ -444,8 +444,14 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
   uint64_t *afull = bars + 2 * NS, *aempty = afull + 2;
   uint64_t *tfull = aempty + 2, *tempty = tfull + 2;
   uint64_t *xfull = tempty + 2, *xempty = xfull + NSLOT;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(xempty + NSLOT);
+  // V4 (one tile buffer): the epilogue releases the accumulator slices one by
+  // one in the order the next tile first writes them -- hi*hi slice 0 on
+  // tempty[0], slice 1 on s1empty, slice 2 on s2empty, cross on tempty[1] --
+  // so the next tile's MMAs start after one slice has been read, not four
+  uint64_t *s1empty = xempty + NSLOT, *s2empty = s1empty + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(s2empty + 1);
   float *comb = reinterpret_cast<float *>(bars + 32);          // [2][NG-1][BM][2]
+  static_assert(2 * NS + 8 + 2 * NSLOT + 3 <= 32, "barrier region");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (repair_idle(prm)) return;
@@ -466,6 +472,8 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
       mbar_init(&xfull[b], 1);
       mbar_init(&xempty[b], C::EPI_ARRIVE);
     }
+    mbar_init(s1empty, C::EPI_ARRIVE);
+    mbar_init(s2empty, C::EPI_ARRIVE);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -572,11 +580,25 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
         }
         for (int t = t0; t < t1; ++t, ++tcount) {
           const int buf = tcount % NBUF;
-          mbar_wait(&tempty[buf], ((tcount / NBUF) & 1) ^ 1);
-          tc_fence_after();
+          const uint32_t tpar = ((tcount / NBUF) & 1) ^ 1;
+          if (NACC != 4) {
+            mbar_wait(&tempty[buf], tpar);
+            tc_fence_after();
+          }
           const uint32_t d0 = tmem_base + (uint32_t)(buf * NACC * BN);
           const uint32_t d_cross = d0 + (uint32_t)((NACC - 1) * BN);
           for (int k = 0; k < kb; ++k) {
+            // V4 layout: hi*hi over three slices round-robin (slice = k % 3);
+            // the cross terms of K-blocks 0-2 go into those hi*hi slices, later
+            // ones into the cross accumulator -- so K-block k < 3 of the next
+            // tile needs only slice k released, and the cross slice (read last)
+            // is first written at k = 3
+            const int slice = (NACC == 4) ? k % 3 : 0;
+            const bool main_first = (NACC == 4) ? k < 3 : (k == 0);
+            if (NACC == 4 && k < 4) {  // first write of a slice in this tile: wait for its release
+              mbar_wait(k == 0 ? &tempty[0] : k == 1 ? s1empty : k == 2 ? s2empty : &tempty[1], tpar);
+              tc_fence_after();
+            }
             mbar_wait(&full[stage], sphase);
             tc_fence_after();
             // descriptors of the K-block; +2 (32 B >> 4) per 16-deep K step
@@ -584,24 +606,20 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
             const uint64_t dal = sw128_desc(smem_u32(A_RES ? a_tile(ab, k, 1) : st_a(stage, 1)));
             const uint64_t dbh = sw128_desc(smem_u32(st_b(stage, 0)));
             const uint64_t dbl = sw128_desc(smem_u32(st_b(stage, 1)));
-            // hi*hi accumulator of this K-block (V4: three slices round-robin)
-            const int slice = (NACC == 4) ? (k % 3) : 0;
             const uint32_t d_main = d0 + (uint32_t)(slice * BN);
-            const bool main_first = (NACC == 4) ? (k < 3) : (k == 0);
+            // cross-term target and its first write (V4: the hi*hi slice for k < 3)
+            const bool cross_in_main = (NACC == 1) || (NACC == 4 && k < 3);
+            const uint32_t d_cx = cross_in_main ? d_main : d_cross;
+            const int cross_k0 = (NACC == 4) ? 3 : 0;
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
               const uint64_t o = (uint64_t)(2 * kk);
               const uint32_t acc_main = (main_first && kk == 0) ? 0u : 1u;
-              const uint32_t acc_cross = (k == 0 && kk == 0) ? 0u : 1u;
+              const uint32_t acc_cross = (!cross_in_main && k == cross_k0 && kk == 0) ? 0u : 1u;
               umma_f16_w<C::IDESC>(d_main, dah + o, dbh + o, acc_main);
               if (prm.probe == 4) continue;  // timing probe: hi*hi only
-              if (NACC == 1) {
-                umma_f16_w<C::IDESC>(d_main, dah + o, dbl + o, 1u);
-                umma_f16_w<C::IDESC>(d_main, dal + o, dbh + o, 1u);
-              } else {
-                umma_f16_w<C::IDESC>(d_cross, dah + o, dbl + o, acc_cross);
-                umma_f16_w<C::IDESC>(d_cross, dal + o, dbh + o, 1u);
-              }
+              umma_f16_w<C::IDESC>(d_cx, dah + o, dbl + o, acc_cross);
+              umma_f16_w<C::IDESC>(d_cx, dal + o, dbh + o, 1u);
             }
             umma_commit_w(&empty[stage]);  // smem stage free once these MMAs retire
             if (++stage == NS) {
@@ -700,6 +718,66 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
           else
             lse_chunk<C::CH, true, EP>(accv, bv, c2k, valid - c * C::CH, m, s);
         };
+        if constexpr (NACC == 4) {
+          // V4: read this group's 32 columns of every slice first, releasing
+          // each slice to the MMA as soon as it is read (order 0, 1, 2, cross =
+          // the order the next tile's K-blocks first write them), then run the
+          // math on registers while the next tile's MMAs proceed.
+          constexpr int GC = C::NCH_G * C::CH;
+          static_assert(GC == 32, "V4 epilogue: 32 columns per group");
+          const int col0 = cfirst * C::CH;
+          float tot[GC];
+          uint32_t v[GC];
+          tmem_ld_x32(tbase + col0, v);
+          tmem_wait(v);
+#pragma unroll
+          for (int i = 0; i < GC; ++i) tot[i] = __uint_as_float(v[i]);
+          tc_fence_before();
+          mbar_arrive(&tempty[0]);
+          tmem_ld_x32(tbase + BN + col0, v);
+          tmem_wait(v);
+#pragma unroll
+          for (int i = 0; i < GC; ++i) tot[i] += __uint_as_float(v[i]);
+          tc_fence_before();
+          mbar_arrive(s1empty);
+          tmem_ld_x32(tbase + 2 * BN + col0, v);
+          tmem_wait(v);
+#pragma unroll
+          for (int i = 0; i < GC; ++i) tot[i] += __uint_as_float(v[i]);
+          tc_fence_before();
+          mbar_arrive(s2empty);
+          tmem_ld_x32(tbase + 3 * BN + col0, v);
+          tmem_wait(v);
+#pragma unroll
+          for (int i = 0; i < GC; ++i) tot[i] += __uint_as_float(v[i]);
+          tc_fence_before();
+          mbar_arrive(&tempty[1]);
+#pragma unroll
+          for (int h = 0; h < GC; h += 16) {
+            float *accv = tot + h;
+            const float4 *bp = reinterpret_cast<const float4 *>(bias + col0 + h);
+            float bv[16];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float4 q = bp[i];
+              bv[4 * i] = q.x;
+              bv[4 * i + 1] = q.y;
+              bv[4 * i + 2] = q.z;
+              bv[4 * i + 3] = q.w;
+            }
+            if constexpr (EU) eucl_transform<16>(accv, (int64_t)rt * BM + row_local, j0 + col0 + h, prm.same);
+            const int vh = valid - col0 - h;
+            if constexpr (FIX) {
+              if (vh >= 16) lse_chunk_anchored<16, false>(accv, bv, c2k, m, 0, s);
+              else lse_chunk_anchored<16, true>(accv, bv, c2k, m, vh, s);
+            } else if (vh >= 16) {
+              lse_chunk<16, false, 0>(accv, bv, c2k, 0, m, s);
+            } else {
+              lse_chunk<16, true, 0>(accv, bv, c2k, vh, m, s);
+            }
+          }
+          mbar_arrive(&xempty[x]);
+        } else {
         issue(cfirst, va);
         wait(va);
 #pragma unroll
@@ -714,6 +792,7 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
         tc_fence_before();
         mbar_arrive(&tempty[buf]);
         mbar_arrive(&xempty[x]);
+        }
       }
       // merge the groups' row states in a fixed order (0, 1, .., NG-1): deterministic
       float *cb = comb + (uc & 1) * ((NG - 1) * 2 * BM);
@@ -1237,6 +1316,9 @@ static int launch_variant(const CUtensorMap (&maps)[7], const Params &prm, bool 
     }
     return launch_one<V, A_RES, NS, ABUF, 0, 4, false, true>(maps, prm, st);
   }
+  if constexpr (V == 4) {  // the V4 slice-release epilogue is written for 4 groups
+    return launch_one<V, A_RES, NS, ABUF, 0, 4>(maps, prm, st);
+  } else {
   const bool g4 = epi_groups() == 4;
   if constexpr (V == 1) {
     switch (emu_pairs(V)) {
@@ -1247,6 +1329,7 @@ static int launch_variant(const CUtensorMap (&maps)[7], const Params &prm, bool 
   }
   return g4 ? launch_one<V, A_RES, NS, ABUF, 0, 4>(maps, prm, st)
             : launch_one<V, A_RES, NS, ABUF, 0, 2>(maps, prm, st);
+  }
 }
 
 // Same-box A/B (B200): cfg2 (d = 64, one K-block) 1.81 vs 1.50 ms per half-step
