@@ -30,14 +30,18 @@ def stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
-def as_device_f32(v):
-    """numpy / torch -> contiguous float32 CUDA tensor (no copy if already one)."""
+def as_device_f32(v, async_pinned: bool = False):
+    """numpy / torch -> contiguous float32 CUDA tensor (no copy if already one).
+    ``async_pinned``: copy pinned host tensors asynchronously on the current
+    stream -- only for callers that synchronise before returning to the user
+    (the geometry's validation reads back a flag right after)."""
     import torch
     dev = device()
     if is_torch(v):
         if v.device.type == "cuda" and v.dtype == torch.float32 and v.is_contiguous():
             return v
-        return v.to(device=dev, dtype=torch.float32).contiguous()
+        nb = async_pinned and v.device.type == "cpu" and v.is_pinned()
+        return v.to(device=dev, dtype=torch.float32, non_blocking=nb).contiguous()
     arr = np.ascontiguousarray(np.asarray(v), dtype=np.float32)
     return torch.from_numpy(arr).to(dev, non_blocking=False)
 

@@ -164,6 +164,11 @@ def _validate_points(p, name):
     return p
 
 
+def _cuda_available() -> bool:
+    import torch
+    return torch.cuda.is_available()
+
+
 def _has_zero_row(p) -> bool:
     if is_torch(p):
         import torch
@@ -246,11 +251,18 @@ class PointCloudGeometry(Geometry):
         y = x if same_obj else _validate_points(y, "y")
         if x.shape[1] != y.shape[1]:
             raise ValueError(f"dimension mismatch: x has d={x.shape[1]}, y has d={y.shape[1]}")
-        if not (_all_finite(x) and (same_obj or _all_finite(y))):
+        # torch inputs (host or device) are moved to the GPU once and validated
+        # there; the device copies are the ones the kernels use (_clouds)
+        self._dev_pts = None
+        if (is_torch(x) or is_torch(y)) and _cuda_available():
+            xd = as_device_f32(x, async_pinned=True)
+            self._dev_pts = (xd, xd if same_obj else as_device_f32(y, async_pinned=True))
+        vx, vy = self._dev_pts if self._dev_pts is not None else (x, y)
+        if not (_all_finite(vx) and (same_obj or _all_finite(vy))):
             raise ValueError("points contain non-finite entries")
         if cost_fn not in _REFERENCE_COST_FNS:
             raise ValueError(f"cost_fn must be one of {_REFERENCE_COST_FNS}, got {cost_fn!r}")
-        if cost_fn == "cosine" and (_has_zero_row(x) or (not same_obj and _has_zero_row(y))):
+        if cost_fn == "cosine" and (_has_zero_row(vx) or (not same_obj and _has_zero_row(vy))):
             raise ValueError("cosine cost is undefined for zero vectors")
         if epsilon_default is not None and not (epsilon_default > 0):
             raise ValueError("epsilon_default must be positive")
@@ -264,10 +276,9 @@ class PointCloudGeometry(Geometry):
         self._epsilon_default = epsilon_default
         if same_obj:
             self._same_points = True
-        elif is_torch(x) or is_torch(y):
+        elif self._dev_pts is not None:
             import torch
-            self._same_points = bool(x.shape == y.shape and torch.equal(
-                as_device_f32(x), as_device_f32(y)))
+            self._same_points = bool(x.shape == y.shape and torch.equal(*self._dev_pts))
         else:
             self._same_points = bool(x.shape == y.shape and np.array_equal(x, y))
         self._dev = None
@@ -280,8 +291,9 @@ class PointCloudGeometry(Geometry):
     def _clouds(self):
         if self._dev is None:
             device()
-            cx = _Cloud(self._kernel_points(self.x))
-            cy = cx if self._same_points else _Cloud(self._kernel_points(self.y))
+            px, py = self._dev_pts if self._dev_pts is not None else (self.x, self.y)
+            cx = _Cloud(self._kernel_points(px))
+            cy = cx if self._same_points else _Cloud(self._kernel_points(py))
             planes = bool(N.lib().otk_lse_uses_tc(cx.d, self.impl_flags))
             scale = 1.0
             if planes:
