@@ -283,7 +283,7 @@ def online_roofline(geom, wl, reps=10):
                                  N.ptr(cy.lo), N.ptr(cy.ext_b), m, cx.d, cx.dpad, sinv,
                                  N.ptr(bias), kappa, fl, nsplit, N.ptr(part), N.ptr(base),
                                  N.OTK_FIN_SOLVER, float(wl.eps), kappa, N.ptr(out), None, None, 0,
-                                 N.ptr(anchor), N.ptr(rep), stream()))
+                                 N.ptr(anchor), N.ptr(rep), None, stream()))
 
     step(flags | N.OTK_ANCHOR_INIT)  # anchors of the "previous" half-step
 

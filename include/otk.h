@@ -140,8 +140,42 @@ int otk_lse_finalize(const float *partial, int32_t nsplit, int64_t np,
  * the anchor holds nothing yet -- running-max kernel, anchor written.  With
  * anchor == NULL this is exactly otk_lse_partial + otk_lse_finalize.
  * repair_ws: otk_lse_step_workspace_bytes(np) bytes (no initialisation). */
+/* Multi-GPU exchange over NVLink peer memory (row-sharded solve, the g
+ * half-step).  Every rank owns one exchange buffer of
+ * otk_exchange_bytes(world, m) bytes (otk_exchange_alloc: cudaMalloc, zeroed,
+ * IPC-exportable), exports it (otk_ipc_handle, 64 bytes), opens the peers'
+ * (otk_ipc_open) and stores the W base pointers -- its own at [rank] -- in its
+ * buffer (otk_exchange_set_peers).  otk_lse_step with an otk_exchange in
+ * OTK_FIN_LOG2 mode then pushes every row's log2 partial into slot
+ * (epoch & 1, rank) of every peer from its last finalize kernel and releases
+ * one flag per 256-row block on every peer; otk_exchange_finalize waits for
+ * the W flags of each block (acquire), combines the W partials in rank order
+ * and applies the finalize mode -- g bitwise equal on all ranks and to the
+ * all-gather + otk_lse_finalize path.  epoch >= 1 grows by one per exchange,
+ * identical on all ranks.  A wait longer than timeout_ms (0 = 10 s) sets the
+ * buffer's error word (otk_exchange_status != 0) instead of hanging. */
+typedef struct otk_exchange {
+  void *local;         /* this rank's exchange buffer (device) */
+  int32_t world, rank;
+  uint32_t epoch;
+} otk_exchange;
+size_t otk_exchange_bytes(int32_t world, int64_t m);
+int otk_exchange_alloc(size_t bytes, void **ptr);
+int otk_exchange_free(void *ptr);
+int otk_ipc_handle(void *ptr, void *handle);
+int otk_ipc_open(const void *handle, void **ptr);
+int otk_ipc_close(void *ptr);
+int otk_exchange_set_peers(void *local, int32_t world, int64_t m, void *const *peers,
+                           void *stream);
+int otk_exchange_finalize(void *local, int32_t world, int64_t m, uint32_t epoch,
+                          const float *base, int32_t mode, float eps, float kappa_next,
+                          float *out_pot, float *out_bias, int32_t *first_bad, int32_t step,
+                          uint32_t timeout_ms /* 0 = 10 s */, void *stream);
+int otk_exchange_status(void *local, int32_t *status, void *stream);
+
 size_t otk_lse_step_workspace_bytes(int64_t np);
 int otk_lse_step_anchored(int32_t d, int32_t flags);
+/* xchg (nullable, OTK_FIN_LOG2 only): push the rows to every rank (above). */
 int otk_lse_step(const float *p, const float *p_sq, const uint16_t *p_hi,
                  const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,
                  const float *q, const float *q_sq, const uint16_t *q_hi,
@@ -150,7 +184,7 @@ int otk_lse_step(const float *p, const float *p_sq, const uint16_t *p_hi,
                  int32_t flags, int32_t nsplit, float *partial, const float *base,
                  int32_t mode, float eps, float kappa_next, float *out_pot,
                  float *out_bias, int32_t *first_bad, int32_t step, float *anchor,
-                 int32_t *repair_ws, void *stream);
+                 int32_t *repair_ws, const otk_exchange *xchg, void *stream);
 
 /* K5 -- fused convergence check (sinkhorn.py:175-189 + _dual_objective 115-119).
  * From f_prev = f_t, f_next = f_{t+1} (the next rows half-step) and g = g_t:

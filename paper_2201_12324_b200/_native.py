@@ -44,6 +44,12 @@ class SolveArgs(C.Structure):
     ]
 
 
+class Exchange(C.Structure):
+    """Mirror of ``otk_exchange`` (include/otk.h): multi-GPU exchange over peer memory."""
+
+    _fields_ = [("local", P), ("world", I32), ("rank", I32), ("epoch", C.c_uint32)]
+
+
 # name -> (restype, argtypes); every symbol declared in include/otk.h
 SIGNATURES = {
     "otk_abi_version": (C.c_int, []),
@@ -61,7 +67,17 @@ SIGNATURES = {
     "otk_lse_step_workspace_bytes": (SZ, [I64]),
     "otk_lse_step_anchored": (C.c_int, [I32, I32]),
     "otk_lse_step": (C.c_int, [P, P, P, P, P, I64, P, P, P, P, P, I64, I32, I32, F32, P, F32, I32,
-                               I32, P, P, I32, F32, F32, P, P, P, I32, P, P, P]),
+                               I32, P, P, I32, F32, F32, P, P, P, I32, P, P, C.POINTER(Exchange), P]),
+    "otk_exchange_bytes": (SZ, [I32, I64]),
+    "otk_exchange_alloc": (C.c_int, [SZ, C.POINTER(P)]),
+    "otk_exchange_free": (C.c_int, [P]),
+    "otk_ipc_handle": (C.c_int, [P, P]),
+    "otk_ipc_open": (C.c_int, [P, C.POINTER(P)]),
+    "otk_ipc_close": (C.c_int, [P]),
+    "otk_exchange_set_peers": (C.c_int, [P, I32, I64, P, P]),
+    "otk_exchange_finalize": (C.c_int, [P, I32, I64, C.c_uint32, P, I32, F32, F32, P, P, P, I32,
+                                        C.c_uint32, P]),
+    "otk_exchange_status": (C.c_int, [P, P, P]),
     "otk_check_workspace_bytes": (SZ, []),
     "otk_check": (C.c_int, [P, P, P, I64, P, P, I64, F64, P, P, P]),
     "otk_cost_workspace_bytes": (SZ, [I64, I64]),

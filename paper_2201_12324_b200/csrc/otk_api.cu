@@ -105,8 +105,31 @@ __global__ void bias_kernel(const float *__restrict__ pot, int64_t m, float kapp
   bias[j] = v * kappa;
 }
 
+// Multi-GPU exchange: row i's L into slot (epoch & 1, rank) of every peer.
+__device__ __forceinline__ void push_row(const FinArgs &F, int64_t i, float L) {
+  const XLayout X(F.xworld, F.np);
+  char *const *peers = reinterpret_cast<char *const *>(F.xlocal + X.table);
+  const int64_t off = ((int64_t)(F.xepoch & 1u) * F.xworld + F.xrank) * X.m_pad + i;
+  for (int s = 0; s < F.xworld; ++s) reinterpret_cast<float *>(peers[s] + X.data)[off] = L;
+}
+// After every thread of the block has pushed its rows: one release per peer
+// (bar.sync orders the block's stores before thread 0's system-scope fence).
+__device__ __forceinline__ void signal_block(const FinArgs &F) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const XLayout X(F.xworld, F.np);
+    char *const *peers = reinterpret_cast<char *const *>(F.xlocal + X.table);
+    __threadfence_system();
+    for (int s = 0; s < F.xworld; ++s) {
+      unsigned *flag = reinterpret_cast<unsigned *>(peers[s] + X.flags) + (size_t)F.xrank * X.nblk + blockIdx.x;
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(F.xepoch) : "memory");
+    }
+  }
+}
+
 __device__ __forceinline__ void finalize_row(const FinArgs &F, int64_t i, float L) {
   if (F.anchor != nullptr) F.anchor[i] = isfinite(L) ? L : __int_as_float(0x7fc00000);
+  if (F.xlocal != nullptr) push_row(F, i, L);
   if (F.mode == OTK_FIN_LOG2) {  // shard partial for the multi-GPU exchange
     F.out[i] = L;
     return;
@@ -120,8 +143,8 @@ __device__ __forceinline__ void finalize_row(const FinArgs &F, int64_t i, float 
 
 __global__ void finalize_kernel(const FinArgs F) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= F.np) return;
-  finalize_row(F, i, combine_log2(F.part + i, F.nsplit, F.np));
+  if (i < F.np) finalize_row(F, i, combine_log2(F.part + i, F.nsplit, F.np));
+  if (F.xlocal != nullptr) signal_block(F);
 }
 
 // After an anchored launch: accept the row when its anchor was finite and the
@@ -145,12 +168,18 @@ __global__ void finalize_anchored_kernel(const FinArgs F) {
 }
 
 // After the repair launch: re-finalize every row of a flagged tile from the
-// running-max partials.
+// running-max partials.  With a multi-GPU exchange this is the half-step's
+// last kernel: it also pushes the rows finalize_anchored accepted (LOG2 mode:
+// their L is already in out) and signals every block.
 __global__ void finalize_repair_kernel(const FinArgs F) {
-  if (*reinterpret_cast<const volatile int *>(F.repair_ws) == 0) return;
+  const bool any = *reinterpret_cast<const volatile int *>(F.repair_ws) != 0;
+  if (!any && F.xlocal == nullptr) return;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= F.np || F.repair_ws[1 + (i >> 7)] == 0) return;
-  finalize_row(F, i, combine_log2(F.part + i, F.nsplit, F.np));
+  if (i < F.np) {
+    if (any && F.repair_ws[1 + (i >> 7)] != 0) finalize_row(F, i, combine_log2(F.part + i, F.nsplit, F.np));
+    else if (F.xlocal != nullptr) push_row(F, i, F.out[i]);
+  }
+  if (F.xlocal != nullptr) signal_block(F);
 }
 
 int finalize_launch(int kind, const FinArgs &F, cudaStream_t st) {
@@ -305,7 +334,7 @@ int otk_lse_finalize(const float *partial, int32_t nsplit, int64_t np, const flo
                 "otk_lse_finalize: bad mode");
   OTK_CHECK_ARG(base || mode == OTK_FIN_LOG2, "otk_lse_finalize: base required");
   FinArgs F{partial, nsplit, np, base, mode, eps, kappa_next, out_pot, out_bias, first_bad, step,
-            nullptr, nullptr, 0.f};
+            nullptr, nullptr, 0.f, nullptr, 0, 0, 0u};
   return finalize_launch(0, F, as_stream(stream));
 }
 

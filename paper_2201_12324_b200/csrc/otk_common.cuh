@@ -108,6 +108,29 @@ struct FinArgs {
   float *anchor;  // nullable: the row's L for the next anchored half-step (NaN if not finite)
   int *repair_ws; // anchored: [0] = flagged rows, [1 + i / 128] = row-tile flags
   float lo;       // anchored: smallest L - anchor accepted (see lse_tc.cu lse_chunk_anchored)
+  // multi-GPU exchange (p2p.cu): push every row's L into slot (epoch & 1, rank)
+  // of every peer's exchange buffer, then flag this block on every peer
+  char *xlocal;   // this rank's exchange buffer (NULL = no push)
+  int xworld, xrank;
+  unsigned xepoch;
+};
+
+// Exchange-buffer layout (p2p.cu, include/otk.h otk_exchange_*): header with
+// the error word, the peer pointer table, the partials [2][world][m_pad]
+// float, and the per-block flags [world][nblk] uint32 (nblk = ceil(m / 256),
+// the finalize kernels' block size).
+struct XLayout {
+  size_t table, data, flags, total;
+  int64_t m_pad;
+  int nblk;
+  __host__ __device__ XLayout(int world, int64_t m) {
+    m_pad = (m + 3) & ~(int64_t)3;
+    nblk = (int)((m + 255) / 256);
+    table = 256;
+    data = table + (((size_t)world * 8 + 255) / 256) * 256;
+    flags = data + (((size_t)2 * world * m_pad * 4 + 255) / 256) * 256;
+    total = flags + (((size_t)world * nblk * 4 + 255) / 256) * 256;
+  }
 };
 // kind 0 = plain, 1 = after an anchored launch, 2 = after the repair launch
 int finalize_launch(int kind, const FinArgs &F, cudaStream_t st);

@@ -188,19 +188,29 @@ extern "C" int otk_lse_step(const float *p, const float *p_sq, const uint16_t *p
                             int32_t flags, int32_t nsplit, float *partial, const float *base,
                             int32_t mode, float eps, float kappa_next, float *out_pot,
                             float *out_bias, int32_t *first_bad, int32_t step, float *anchor,
-                            int32_t *repair_ws, void *stream) {
+                            int32_t *repair_ws, const otk_exchange *xchg, void *stream) {
   OTK_CHECK_ARG(partial && out_pot && np > 0 && nq > 0 && nsplit >= 1, "otk_lse_step: bad arguments");
+  OTK_CHECK_ARG(!xchg || (xchg->local && xchg->world >= 1 && xchg->rank >= 0 &&
+                          xchg->rank < xchg->world && xchg->epoch >= 1 && mode == OTK_FIN_LOG2),
+                "otk_lse_step: the exchange needs OTK_FIN_LOG2 and a valid otk_exchange");
   OTK_CHECK_ARG(mode == OTK_FIN_SOLVER || mode == OTK_FIN_APPLY || mode == OTK_FIN_LOG2,
                 "otk_lse_step: bad mode");
   OTK_CHECK_ARG(base || mode == OTK_FIN_LOG2, "otk_lse_step: base required");
   cudaStream_t st = as_stream(stream);
   FinArgs F{partial, nsplit, np, base, mode, eps, kappa_next, out_pot, out_bias, first_bad, step,
-            anchor, repair_ws, 0.f};
+            anchor, repair_ws, 0.f, nullptr, 0, 0, 0u};
+  FinArgs Fx = F;  // the half-step's LAST finalize also pushes to the peers
+  if (xchg) {
+    Fx.xlocal = static_cast<char *>(xchg->local);
+    Fx.xworld = xchg->world;
+    Fx.xrank = xchg->rank;
+    Fx.xepoch = xchg->epoch;
+  }
   const bool anch = anchor != nullptr && !(flags & OTK_ANCHOR_INIT) && anchored_path(d, flags);
   if (!anch) {
     OTK_TRY_(otk_lse_partial(p, p_sq, p_hi, p_lo, p_ext, np, q, q_sq, q_hi, q_lo, q_ext, nq, d, dpad,
                              split_inv, q_bias, kappa, flags, nsplit, partial, stream));
-    return finalize_launch(0, F, st);
+    return finalize_launch(0, Fx, st);
   }
   OTK_CHECK_ARG(repair_ws && p_hi && p_lo && p_ext && q_hi && q_lo && q_ext && dpad % 64 == 0 && dpad >= d,
                 "otk_lse_step: anchored path needs the repair workspace and the split + norm planes");
@@ -213,7 +223,7 @@ extern "C" int otk_lse_step(const float *p, const float *p_sq, const uint16_t *p
   OTK_TRY_(finalize_launch(1, F, st));
   OTK_TRY_(lse_tc_launch(p_hi, p_lo, p_ext, np, q_hi, q_lo, q_ext, nq, dpad, scale, q_bias, nsplit,
                          same, 0, partial, nullptr, repair_ws, 1, st));
-  return finalize_launch(2, F, st);
+  return finalize_launch(2, Fx, st);
 }
 
 // ------------------------------------------------------------------ solver
@@ -338,7 +348,7 @@ struct HalfStep {
     return otk_lse_step(A->x, L->xsq, L->xhi, L->xlo, L->xea, A->n, A->y, L->ysq, L->yhi, L->ylo,
                         L->yeb, A->m, A->d, L->dpad, sinv, L->bias_y, kappa, fl, L->nsr, L->part,
                         A->log_a, OTK_FIN_SOLVER, eps, kappa_next, f_out, L->bias_x, L->first_bad,
-                        step, anchored ? L->anc_x : nullptr, L->rep_x, st);
+                        step, anchored ? L->anc_x : nullptr, L->rep_x, nullptr, st);
   }
   int cols(float kappa, float eps, float kappa_next, int step) {
     const int fl = kflags | (have_y ? 0 : OTK_ANCHOR_INIT);
@@ -347,7 +357,7 @@ struct HalfStep {
     return otk_lse_step(A->y, L->ysq, L->yhi, L->ylo, L->yea, A->m, A->x, L->xsq, L->xhi, L->xlo,
                         L->xeb, A->n, A->d, L->dpad, sinv, L->bias_x, kappa, fl, L->nsc, L->part,
                         A->log_b, OTK_FIN_SOLVER, eps, kappa_next, L->g, L->bias_y, L->first_bad,
-                        step, anchored ? L->anc_y : nullptr, L->rep_y, st);
+                        step, anchored ? L->anc_y : nullptr, L->rep_y, nullptr, st);
   }
 };
 

@@ -43,6 +43,7 @@ __all__ = [
     "CudaShardEngine",
     "sharded_loop",
     "ShardedProblem",
+    "PeerExchange",
     "solve_sinkhorn_sharded",
     "reg_ot_cost_sharded",
 ]
@@ -105,6 +106,14 @@ class TorchComm:
         t = self._host(vec, device)
         return self.all_gather_rows(t).cpu().numpy()
 
+    def all_gather_objects(self, obj) -> list:
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def all_gather_bytes(self, b: bytes) -> list:
+        return [bytes(x) for x in self.all_gather_objects(bytes(b))]
+
 
 class ThreadComm:
     """W ranks emulated by W threads of one process (shared device, host barrier).
@@ -151,6 +160,92 @@ class ThreadComm:
 
     def all_gather_host(self, vec: np.ndarray, device=None) -> np.ndarray:
         return np.stack(self._exchange(np.asarray(vec, dtype=np.float64).copy()))
+
+
+# ---------------------------------------------------------------- peer-memory exchange
+class PeerExchange:
+    """The g half-step's exchange over NVLink peer memory (csrc/p2p.cu).
+
+    Every rank allocates one exchange buffer, exports it as a CUDA IPC handle,
+    opens the other ranks' handles (handles travel through ``comm``'s host
+    all-gather) and writes the W base pointers into its own buffer.  Each g
+    half-step then pushes its column partials from the half-step's last
+    kernel and combines the W partials after per-block acquire flags (see
+    include/otk.h, otk_exchange).  One process per GPU only: ranks that share
+    a GPU (``ThreadComm``) must not run kernels that wait on each other.
+    """
+
+    def __init__(self, comm, m: int):
+        import ctypes
+        lib = N.lib()
+        self.world, self.rank, self.m = comm.world, comm.rank, int(m)
+        self.bytes = lib.otk_exchange_bytes(self.world, self.m)
+        buf = ctypes.c_void_p()
+        N.check(lib.otk_exchange_alloc(self.bytes, ctypes.byref(buf)), "exchange alloc")
+        self.local = buf.value
+        self.opened = []
+        try:
+            handle = (ctypes.c_uint8 * 64)()
+            N.check(lib.otk_ipc_handle(self.local, handle), "ipc handle")
+            handles = comm.all_gather_bytes(bytes(handle))
+            ptrs = []
+            for r, h in enumerate(handles):
+                if r == self.rank:
+                    ptrs.append(self.local)
+                    continue
+                peer = ctypes.c_void_p()
+                N.check(lib.otk_ipc_open((ctypes.c_uint8 * 64).from_buffer_copy(h),
+                                         ctypes.byref(peer)), f"ipc open (rank {r})")
+                self.opened.append(peer.value)
+                ptrs.append(peer.value)
+            table = (ctypes.c_void_p * self.world)(*ptrs)
+            N.check(lib.otk_exchange_set_peers(self.local, self.world, self.m, table, stream()),
+                    "exchange peers")
+        except Exception:
+            self.close()
+            raise
+        self.epoch = 0
+
+    def next(self):
+        """Arguments of the next exchange (epochs 1, 2, ... on every rank alike)."""
+        self.epoch += 1
+        return N.Exchange(self.local, self.world, self.rank, self.epoch)
+
+    def status(self) -> int:
+        import ctypes
+        v = ctypes.c_int32()
+        N.check(N.lib().otk_exchange_status(self.local, ctypes.byref(v), stream()), "exchange status")
+        return int(v.value)
+
+    def close(self):
+        lib = N.lib()
+        for p in self.opened:
+            lib.otk_ipc_close(p)
+        self.opened = []
+        if getattr(self, "local", None):
+            lib.otk_exchange_free(self.local)
+            self.local = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
+
+
+def p2p_exchange_supported(comm) -> bool:
+    """True when every rank is a separate process on its own GPU of one host and
+    every pair of those GPUs can access each other's memory (NVLink / NVSwitch)."""
+    import socket
+    import torch
+    if not isinstance(comm, TorchComm) or comm.dist.get_backend(comm.group) != "nccl":
+        return False
+    me = (socket.gethostname(), torch.cuda.current_device())
+    everyone = comm.all_gather_objects(me)
+    if len({h for h, _ in everyone}) != 1 or len({d for _, d in everyone}) != len(everyone):
+        return False
+    dev = me[1]
+    return all(d == dev or torch.cuda.can_device_access_peer(dev, d) for _, d in everyone)
 
 
 # ---------------------------------------------------------------- device engine
@@ -230,13 +325,15 @@ class CudaShardEngine:
                                  N.ptr(self.part), N.ptr(self.la), N.OTK_FIN_SOLVER, eps, kappa_next,
                                  N.ptr(self.f[which]), N.ptr(self.bias_x), N.ptr(self.first_bad), step,
                                  N.ptr(self.anc_x) if self.anchored else None, N.ptr(self.rep_x),
-                                 stream()), "rows half-step")
+                                 None, stream()), "rows half-step")
         self.launches += self._launches(self.have_x)
         self.have_x = True
 
-    def cols_partial(self, kappa):
+    def cols_partial(self, kappa, xchg=None):
         """This shard's log2 column partials (OTK_FIN_LOG2), anchored on the shard's own
-        previous partials."""
+        previous partials; with ``xchg`` (an ``N.Exchange``) the last finalize kernel
+        also pushes them into every rank's exchange buffer over peer memory."""
+        import ctypes
         cx, cy, lib = self.cx, self.cy, N.lib()
         fl = self.flags | (0 if self.have_y else N.OTK_ANCHOR_INIT)
         N.check(lib.otk_lse_step(N.ptr(cy.p), N.ptr(cy.sq), N.ptr(cy.hi), N.ptr(cy.lo),
@@ -246,10 +343,22 @@ class CudaShardEngine:
                                  N.ptr(self.part), None, N.OTK_FIN_LOG2, 0.0, 0.0,
                                  N.ptr(self.lcol), None, None, 0,
                                  N.ptr(self.anc_y) if self.anchored else None, N.ptr(self.rep_y),
-                                 stream()), "cols half-step")
+                                 ctypes.byref(xchg) if xchg is not None else None, stream()),
+                "cols half-step")
         self.launches += self._launches(self.have_y)
         self.have_y = True
         return self.lcol
+
+    def cols_exchange(self, p2p, kappa, eps, kappa_next, step):
+        """g half-step over peer memory: local partials pushed to every rank by the
+        half-step's last kernel, then the W partials combined in rank order."""
+        x = p2p.next()
+        self.cols_partial(kappa, x)
+        N.check(N.lib().otk_exchange_finalize(x.local, x.world, self.m, x.epoch, N.ptr(self.lb),
+                                              N.OTK_FIN_SOLVER, eps, kappa_next, N.ptr(self.g),
+                                              N.ptr(self.bias_y), N.ptr(self.first_bad), step, 0,
+                                              stream()), "exchange combine")
+        self.launches += 1
 
     def cols_finalize(self, lall, eps, kappa_next, step):
         W = lall.shape[0]
@@ -281,8 +390,12 @@ class CudaShardEngine:
 
 # ---------------------------------------------------------------- the loop
 def sharded_loop(engine, comm, sched: EpsilonSchedule, threshold: float, max_iters: int,
-                 inner_iters: int, g_init=None):
+                 inner_iters: int, g_init=None, p2p=None):
     """The reference loop (sinkhorn.py:151-200) over row shards.
+
+    The g half-step's exchange goes through ``comm`` (all-gather of the column
+    partials, e.g. NCCL) or, with ``p2p`` (a ``PeerExchange``), over peer
+    memory from the half-step's own last kernel.
 
     Returns (which_f, iterations, converged, errors, duals).  Raises
     DivergedError / ValueError at the same iteration the single-GPU solver
@@ -302,14 +415,19 @@ def sharded_loop(engine, comm, sched: EpsilonSchedule, threshold: float, max_ite
         if not f_ready:
             engine.rows(kap, e, kap, which, 2 * t)
         f_ready = False
-        lall = comm.all_gather_rows(engine.cols_partial(kap))
-        engine.cols_finalize(lall, e, kap_next, 2 * t + 1)
+        if p2p is not None:  # fused push (last kernel of the half-step) + combine
+            engine.cols_exchange(p2p, kap, e, kap_next, 2 * t + 1)
+        else:
+            lall = comm.all_gather_rows(engine.cols_partial(kap))
+            engine.cols_finalize(lall, e, kap_next, 2 * t + 1)
         if t % inner_iters == 0 or t == max_iters:
             measure = not (e > target)
             if measure:
                 engine.rows(kap, e, kap, 1 - which, 2 * t + 2)
             local = engine.check(which, measure, e)
             fb = engine.read_first_bad()
+            if p2p is not None and p2p.status() != 0:
+                raise RuntimeError("peer-memory exchange timed out waiting for another rank")
             rows = comm.all_gather_host(np.append(local, float(fb)), engine.device)
             tot = np.zeros(8)
             for r in range(rows.shape[0]):          # fixed rank order: deterministic
@@ -335,6 +453,8 @@ def sharded_loop(engine, comm, sched: EpsilonSchedule, threshold: float, max_ite
                 break
             if t < max_iters:
                 which, f_ready = 1 - which, True
+    if p2p is not None and p2p.status() != 0:
+        raise RuntimeError("peer-memory exchange timed out waiting for another rank")
     return which, min(t, max_iters), converged, np.asarray(errors), np.asarray(duals)
 
 
@@ -364,7 +484,8 @@ class ShardedProblem:
     """
 
     def __init__(self, x, y, a=None, b=None, *, comm=None, x_is_local: bool = False,
-                 n_total: int | None = None, impl: str = "auto", cost_fn: str = "sqeucl"):
+                 n_total: int | None = None, impl: str = "auto", cost_fn: str = "sqeucl",
+                 exchange: str = "auto"):
         from .geometry import cost_fn_flags, kernel_points
         from .sinkhorn import _impl_flags
         cflags = cost_fn_flags(cost_fn)
@@ -398,6 +519,23 @@ class ShardedProblem:
                                       a_loc, b_w, flags=_impl_flags(impl) | cflags,
                                       amax_reduce=amax_reduce)
         self.lo, self.hi, self.n_total, self.m = lo, hi, n_total, m
+        # g half-step exchange: "p2p" = pushed over NVLink peer memory by the
+        # half-step's last kernel (csrc/p2p.cu); "collective" = comm all-gather
+        # (NCCL) + combine; "auto" = p2p whenever every rank is its own process
+        # on its own peer-accessible GPU of one host (OTK_EXCHANGE overrides)
+        import os
+        exchange = os.environ.get("OTK_EXCHANGE", exchange)
+        if exchange not in ("auto", "p2p", "collective"):
+            raise ValueError("exchange must be 'auto', 'p2p' or 'collective'")
+        self.p2p = None
+        if exchange != "collective":
+            ok = p2p_exchange_supported(comm)
+            if exchange == "p2p" and not ok:
+                raise ValueError("peer-memory exchange needs one process per GPU of one host "
+                                 "(TorchComm over NCCL) with peer access between all GPUs")
+            if ok:
+                self.p2p = PeerExchange(comm, m)
+        self.exchange = "p2p" if self.p2p is not None else "collective"
 
     def solve(self, eps, *, threshold: float = 1e-3, max_iters: int = 2000,
               inner_iters: int = 10, g_init=None, gather_f: bool = False) -> ShardedSinkhornOutput:
@@ -413,7 +551,7 @@ class ShardedProblem:
         comm, eng = self.comm, self.engine
         eng.reset_first_bad()
         which, iters, conv, errs, duals = sharded_loop(eng, comm, sched, threshold, max_iters,
-                                                       inner_iters, g_init)
+                                                       inner_iters, g_init, p2p=self.p2p)
         f_dev, g_dev = eng.f_result(which).clone(), eng.g_result().clone()
         f_full = None
         if gather_f:
@@ -436,7 +574,7 @@ def solve_sinkhorn_sharded(x, y, eps, a=None, b=None, *, threshold: float = 1e-3
                            max_iters: int = 2000, inner_iters: int = 10, g_init=None,
                            comm=None, x_is_local: bool = False, n_total: int | None = None,
                            impl: str = "auto", gather_f: bool = False,
-                           cost_fn: str = "sqeucl") -> ShardedSinkhornOutput:
+                           cost_fn: str = "sqeucl", exchange: str = "auto") -> ShardedSinkhornOutput:
     """Row-sharded ``solve_sinkhorn`` on a point cloud (one rank per GPU):
     ``ShardedProblem(x, y, a, b, ...).solve(eps, ...)``."""
     if max_iters < 1 or inner_iters < 1:
@@ -444,7 +582,7 @@ def solve_sinkhorn_sharded(x, y, eps, a=None, b=None, *, threshold: float = 1e-3
     if not (threshold > 0):
         raise ValueError("threshold must be positive")
     prob = ShardedProblem(x, y, a, b, comm=comm, x_is_local=x_is_local, n_total=n_total,
-                          impl=impl, cost_fn=cost_fn)
+                          impl=impl, cost_fn=cost_fn, exchange=exchange)
     return prob.solve(eps, threshold=threshold, max_iters=max_iters, inner_iters=inner_iters,
                       g_init=g_init, gather_f=gather_f)
 

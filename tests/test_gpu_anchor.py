@@ -63,7 +63,8 @@ def _step(env, geom, cx, cy, g, eps, anchor=None, init=False, mode=None, rep=Non
                              N.ptr(cy.p), N.ptr(cy.sq), N.ptr(cy.hi), N.ptr(cy.lo), N.ptr(cy.ext_b), m,
                              cx.d, cx.dpad, 1.0 / (cx.scale * cx.scale), N.ptr(bias), kappa, flags,
                              nsplit, N.ptr(part), N.ptr(base), mode, float(eps), kappa, N.ptr(out),
-                             None, None, 0, N.ptr(anchor), N.ptr(rep), stream()), "otk_lse_step")
+                             None, None, 0, N.ptr(anchor), N.ptr(rep), None, stream()),
+            "otk_lse_step")
     torch.cuda.synchronize()
     return out.cpu().numpy(), rep
 

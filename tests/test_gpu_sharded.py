@@ -135,3 +135,44 @@ def test_thread_ranks_converge_like_the_reference(otk):
     ref = oracle.sinkhorn(geom64, a, b, wl.eps, threshold=wl.threshold, max_iters=wl.max_iters)
     assert outs[0].iterations == ref["iterations"] and outs[0].converged == ref["converged"]
     assert len(outs[0].errors) == len(ref["errors"])
+
+
+@pytest.mark.parametrize("d,gen", [(3, "cfg1"), (64, "cfg2")])
+def test_world1_peer_exchange_is_bitwise_the_collective(otk, nccl_world1, d, gen):
+    """The g half-step pushed over peer memory by its own last kernel (csrc/p2p.cu)
+    gives the same bits as the NCCL all-gather + combine path (world 1: the
+    rank is its own peer; no kernel waits on another process)."""
+    from paper_2201_12324_b200.sharded import ShardedProblem
+    kw = dict(n=700, m=515) if gen != "cfg2" else dict(n=700, m=515, d=d)
+    wl = getattr(workloads, gen)(**kw)
+    p2p = ShardedProblem(wl.x, wl.y, wl.a, wl.b, exchange="p2p")
+    col = ShardedProblem(wl.x, wl.y, wl.a, wl.b, exchange="collective")
+    assert p2p.exchange == "p2p" and col.exchange == "collective"
+    for thr, its in ((wl.threshold, 60), (1e-300, 23)):
+        a = p2p.solve(wl.eps, threshold=thr, max_iters=its)
+        b = col.solve(wl.eps, threshold=thr, max_iters=its)
+        assert a.iterations == b.iterations and a.converged == b.converged
+        assert np.array_equal(a.f_local, b.f_local)
+        assert np.array_equal(a.g, b.g)
+        np.testing.assert_array_equal(a.errors, b.errors)
+    assert p2p.p2p.status() == 0
+    assert p2p.p2p.epoch > 0
+
+
+def test_peer_exchange_wait_times_out_instead_of_hanging(otk, nccl_world1):
+    """A combine whose peers never signal (epoch far ahead) gives up after its
+    timeout, reports it through the status word and yields NaN, not a hang."""
+    import torch
+    from paper_2201_12324_b200 import _native as N
+    from paper_2201_12324_b200._device import stream
+    from paper_2201_12324_b200.sharded import PeerExchange, TorchComm
+    m = 300
+    px = PeerExchange(TorchComm(), m)
+    out = torch.empty(m, dtype=torch.float32, device="cuda")
+    base = torch.zeros(m, dtype=torch.float32, device="cuda")
+    N.check(N.lib().otk_exchange_finalize(px.local, 1, m, 1000, N.ptr(base), N.OTK_FIN_SOLVER, 1.0,
+                                          1.0, N.ptr(out), None, None, 0, 50, stream()))
+    torch.cuda.synchronize()
+    assert px.status() == 1
+    assert torch.isnan(out).all()
+    px.close()

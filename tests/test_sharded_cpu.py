@@ -274,3 +274,79 @@ def test_shard_rows_partition():
             assert all(spans[i][1] == spans[i + 1][0] for i in range(w - 1))
             sizes = [hi - lo for lo, hi in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+# ------------------------------------------------ peer-memory exchange protocol
+def _gloo_exchange_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2201_12324_b200.sharded import p2p_exchange_supported
+        comm = TorchComm()
+        handles = comm.all_gather_bytes(bytes([rank]) * 64)   # IPC handles are 64 bytes
+        objs = comm.all_gather_objects(("host", rank))
+        q.put((rank, handles, objs, p2p_exchange_supported(comm)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_exchange_handshake_host_logic():
+    """The handle exchange of PeerExchange (64-byte CUDA IPC handles through the
+    process group, in rank order) and the transport choice: gloo -> collective."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_exchange_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (h, o, s)) for r, h, o, s in (q.get(timeout=300) for _ in procs))
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    for r in range(2):
+        handles, objs, supported = res[r]
+        assert handles == [bytes([0]) * 64, bytes([1]) * 64]
+        assert objs == [("host", 0), ("host", 1)]
+        assert supported is False
+
+
+def test_exchange_protocol_model_never_reads_a_stale_or_overwritten_slot():
+    """Host model of csrc/p2p.cu's protocol (W ranks as threads with random
+    delays): each epoch e every rank writes its tagged partial into slot
+    (e & 1, rank) of every peer, then releases flag[rank] = e on every peer;
+    the combine waits for all flags >= e and reads slot (e & 1).  Two slots
+    must suffice: no rank may ever read a partial of the wrong epoch."""
+    import random
+    import threading as th
+    W, E = 4, 200
+    slots = [[[None] * W for _ in range(2)] for _ in range(W)]   # [owner][slot][writer]
+    flags = [[0] * W for _ in range(W)]                             # [owner][writer]
+    cv = th.Condition()
+    errors = []
+
+    def rank(r):
+        rng = random.Random(r)
+        for e in range(1, E + 1):
+            for s in rng.sample(range(W), W):           # push in any order
+                slots[s][e & 1][r] = (r, e)
+                if rng.random() < 0.3:
+                    th.Event().wait(0.0001)
+            with cv:                                     # release after all stores
+                for s in range(W):
+                    flags[s][r] = e
+                cv.notify_all()
+            with cv:                                     # acquire: wait for every writer
+                cv.wait_for(lambda: all(flags[r][w] >= e for w in range(W)))
+            got = [slots[r][e & 1][w] for w in range(W)]
+            if got != [(w, e) for w in range(W)]:
+                errors.append((r, e, got))
+            if rng.random() < 0.3:
+                th.Event().wait(0.0002)
+
+    ts = [th.Thread(target=rank, args=(r,)) for r in range(W)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(120)
+    assert not errors, errors[:3]
