@@ -15,7 +15,8 @@ L2 is flushed (512 MiB write) before every timed step.
 
 N > 1 (torchrun, one rank per GPU, NCCL): the row-sharded solver
 (paper_2201_12324_b200/sharded.py) on the SAME problem --
-x split in N row shards, one NCCL all-gather of m floats per g half-step --
+x split in N row shards, the g half-step's m partials per rank pushed to every
+rank over NVLink peer memory (csrc/p2p.cu; NCCL all-gather as fallback) --
 so the scaling is strong; value = n*m*iters / max-over-ranks step time.
 --config 3 runs the batched materialised path (512 problems of 512^2).
 
@@ -430,7 +431,9 @@ def run_ours(args, wl, rank, world):
 
         def cells_of(out):
             return float(n) * m * out.iterations
-        parallelism = f"row-sharded x{world} (NCCL all-gather per g half-step)"
+        parallelism = (f"row-sharded x{world} (g half-step partials pushed over NVLink peer memory "
+                       "by the half-step's last kernel)" if sprob.exchange == "p2p" else
+                       f"row-sharded x{world} (all-gather per g half-step)")
     else:
         xd = torch.from_numpy(wl.x).to(dev)
         yd = torch.from_numpy(wl.y).to(dev)
