@@ -15,7 +15,11 @@
 // The fused check computes f_{t+1} and r_i = a_i exp((f_t - f_{t+1})/eps).
 // Failure semantics follow the lock-step loop (sinkhorn._dense_loop): the
 // first half-step to emit NaN/+inf is recorded by step number.
+#include <cooperative_groups.h>
+
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "otk_common.cuh"
 
@@ -314,6 +318,412 @@ __global__ void __launch_bounds__(THREADS, 1) dense_solve_kernel(Args A) {
   }
 }
 
+// ---------------------------------------------------------------- K3c
+// The same per-problem loop with the problem's cost RESIDENT ON CHIP: a
+// cluster of CL CTAs owns one problem at a time, each CTA keeping a slice of
+// ceil(n / CL) rows of C (cfg3: 64 rows x 512 columns = 128 KB) in shared
+// memory, loaded once per problem with bulk copies.  C is then read from HBM
+// once per solve instead of once per half-step, and the loop is bound by
+// the exps (MUFU), not HBM.
+//   rows half-step: local (each CTA finalizes its own rows; g replicated)
+//   cols half-step: every CTA reduces its rows into one log2 partial per
+//     column, publishes it in its shared memory (double-buffered by parity),
+//     one cluster barrier, then EVERY CTA combines the CL partials of every
+//     column from distributed shared memory in rank order -> g is computed
+//     identically (bitwise) in every CTA of the cluster
+//   check: per-CTA sums (the g terms counted by rank 0 only) and the
+//     first-bad step are published the same way and reduced in rank order,
+//     so every CTA takes the same decision at the same iteration.
+// Parity buffers make one barrier per exchange enough: a CTA rewrites a
+// parity buffer only after passing the NEXT exchange's barrier, which every
+// reader of the previous use has reached after reading.
+constexpr int CL_MAX = 8;
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+// Rows half-step on the CTA's resident rows: a group of RG = 8 threads per
+// row (each LDS.128 phase of 8 threads reads one row's 128 consecutive bytes:
+// no bank conflicts), each thread streaming every 8th float4 of the row with
+// an online (max, sum), then a 3-level shuffle merge in fixed order.
+constexpr int RG = 8;
+constexpr int RCH = 4 * RG * 4;  // columns per chunk
+template <bool CHECK>
+__device__ void rows_local(const float *Cs, int rows, int m, const float *by, const float *lw,
+                           float eps, float kappa, float *out, float *bx, int *fbad, int step,
+                           const float *fprev, const float *a, double eps_d, double (&chk)[NV]) {
+  const int gi = threadIdx.x / RG, gl = threadIdx.x % RG;
+  constexpr int GROUPS = THREADS / RG;
+  for (int i0 = 0; i0 < rows; i0 += GROUPS) {
+    const int i = i0 + gi;
+    Lse2 st;
+    st.init();
+    if (i < rows) {
+      const float *row = Cs + (int64_t)i * m;
+      for (int j0 = gl * 4; j0 < m; j0 += RCH) {  // 4 float4 per chunk
+        float u[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = j0 + q * 4 * RG;
+          if (j < m) {
+            const float4 c = *reinterpret_cast<const float4 *>(row + j);
+            const float4 h = *reinterpret_cast<const float4 *>(by + j);
+            u[4 * q + 0] = fmaf(-kappa, c.x, h.x);
+            u[4 * q + 1] = fmaf(-kappa, c.y, h.y);
+            u[4 * q + 2] = fmaf(-kappa, c.z, h.z);
+            u[4 * q + 3] = fmaf(-kappa, c.w, h.w);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) u[4 * q + e] = -INFINITY;
+          }
+        }
+        float cm = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) cm = fmaxf(cm, u[e]);
+        if (cm > st.m) {
+          st.s *= ex2(st.m - cm);
+          st.m = cm;
+        }
+        const float ms = (st.m == -INFINITY) ? 0.f : st.m;
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          a0 += ex2(u[e] - ms);
+          a1 += ex2(u[e + 1] - ms);
+        }
+        st.s += a0 + a1;
+      }
+    }
+#pragma unroll
+    for (int o = RG / 2; o > 0; o >>= 1) {  // within the row's group of 8 lanes
+      const float m2 = __shfl_xor_sync(0xffffffffu, st.m, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, st.s, o);
+      st.merge(m2, s2);
+    }
+    if (gl == 0 && i < rows) {
+      const float v = eps * lw[i] - eps * kLn2 * st.value();
+      out[i] = v;
+      bx[i] = v * kappa;
+      if (bad_potential(v)) atomicMin(fbad, step);
+      if (CHECK) {
+        const double fp = fprev[i], ai = a[i];
+        const double rr = (ai > 0.0) ? ai * exp((fp - (double)v) / eps_d) : 0.0;
+        chk[0] += fabs(rr - ai);
+        chk[1] += rr;
+        if (ai > 0.0) chk[2] += ai * fp;
+        chk[4] += (fp != fp) ? 1.0 : 0.0;
+        chk[6] += (fp == INFINITY) ? 1.0 : 0.0;
+      }
+    }
+  }
+}
+
+// this CTA's log2 partial of every column over its rows -> part[j]
+// (16-row chunks: max first, then one rescale at most, sums in two chains)
+__device__ void cols_partial_local(const float *Cs, int rows, int m, const float *bx, float kappa,
+                                   float *part) {
+  for (int j = threadIdx.x; j < m; j += THREADS) {
+    float mx = -INFINITY, sm = 0.f;
+    const float *cp = Cs + j;
+    int i0 = 0;
+    for (; i0 + 16 <= rows; i0 += 16, cp += 16 * m) {
+      float u[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) u[k] = fmaf(-kappa, cp[k * m], bx[i0 + k]);
+      float c0 = fmaxf(fmaxf(u[0], u[1]), fmaxf(u[2], u[3]));
+      float c1 = fmaxf(fmaxf(u[4], u[5]), fmaxf(u[6], u[7]));
+      float c2 = fmaxf(fmaxf(u[8], u[9]), fmaxf(u[10], u[11]));
+      float c3 = fmaxf(fmaxf(u[12], u[13]), fmaxf(u[14], u[15]));
+      const float cm = fmaxf(fmaxf(c0, c1), fmaxf(c2, c3));
+      if (cm > mx) {
+        sm *= ex2(mx - cm);
+        mx = cm;
+      }
+      const float ms = (mx == -INFINITY) ? 0.f : mx;
+      float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; k += 2) {
+        a0 += ex2(u[k] - ms);
+        a1 += ex2(u[k + 1] - ms);
+      }
+      sm += a0 + a1;
+    }
+    if (i0 < rows) {  // last partial chunk, masked
+      float u[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) u[k] = (i0 + k < rows) ? fmaf(-kappa, cp[k * m], bx[i0 + k]) : -INFINITY;
+      float cm = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) cm = fmaxf(cm, u[k]);
+      if (cm > mx) {
+        sm *= ex2(mx - cm);
+        mx = cm;
+      }
+      const float ms = (mx == -INFINITY) ? 0.f : mx;
+      float a0 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) a0 += ex2(u[k] - ms);
+      sm += a0;
+    }
+    Lse2 st;
+    st.m = mx;
+    st.s = sm;
+    part[j] = st.value();
+  }
+}
+
+template <int CL>
+__global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  extern __shared__ __align__(16) float shc[];
+  const int n = A.n, m = A.m;
+  const int rows_per = (n + CL - 1) / CL;
+  const int rp4 = (rows_per + 3) & ~3, m4 = (m + 3) & ~3;
+  float *Cs = shc;                                    // [rows_per][m]
+  float *f0 = Cs + (size_t)rows_per * m, *f1 = f0 + rp4, *bx = f1 + rp4;
+  float *g = bx + rp4, *by = g + m4;
+  float *part = by + m4;                              // [2][m4] log2 column partials
+  double *slot = reinterpret_cast<double *>(part + 2 * m4);  // [2][NV + 1]
+  __shared__ double red[NV * WARPS];
+  __shared__ int fbad;
+  __shared__ __align__(8) uint64_t lbar;
+  const int r0 = min(n, rank * rows_per), r1 = min(n, r0 + rows_per), rows = r1 - r0;
+  const int ncl = (int)(gridDim.x / CL), cid = (int)(blockIdx.x / CL);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&lbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t lphase = 0;
+  int xpar = 0;  // parity of the next exchange (column partials or check slots)
+  for (int64_t b = cid; b < A.batch; b += ncl) {
+    const float *Cb = A.C + b * (int64_t)n * m;
+    const float *a = A.a + b * n + r0, *bw = A.b + b * m;
+    const float *la = A.la + b * n + r0, *lb = A.lb + b * m;
+    const float eps = A.eps[b];
+    const double eps_d = A.eps_d[b];
+    const float kappa = kLog2e / eps;
+    // this CTA's rows of C -> shared memory (bulk copies, 32 KB pieces)
+    if (threadIdx.x == 0 && rows > 0) {
+      const size_t bytes = (size_t)rows * m * sizeof(float);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(&lbar)),
+                   "r"((uint32_t)bytes)
+                   : "memory");
+      const char *src = reinterpret_cast<const char *>(Cb + (int64_t)r0 * m);
+      for (size_t off = 0; off < bytes; off += 32768)
+        bulk_g2s(reinterpret_cast<char *>(Cs) + off, src + off, (uint32_t)min((size_t)32768, bytes - off),
+                 &lbar);
+    }
+    if (threadIdx.x == 0) fbad = 0x7fffffff;
+    for (int j = threadIdx.x; j < m; j += THREADS) {
+      const float g0 = A.g_init ? A.g_init[b * m + j] : 0.f;
+      g[j] = g0;
+      by[j] = g0 * kappa;
+      if (bad_potential(g0)) atomicMin(&fbad, 1);
+    }
+    if (rows > 0) {  // wait for the cost slice
+      asm volatile(
+          "{\n\t.reg .pred p;\nW_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+          "@!p bra W_%=;\n\t}" ::"r"((uint32_t)__cvta_generic_to_shared(&lbar)),
+          "r"(lphase)
+          : "memory");
+      lphase ^= 1;
+    }
+    __syncthreads();
+    float *f = f0, *fn = f1;
+    bool f_ready = false;
+    int n_checks = 0, status = OTK_OK, fail_iter = 0, converged = 0, t;
+    double chk[NV];
+    for (t = 1; t <= A.max_iters; ++t) {
+      if (!f_ready) {
+        rows_local<false>(Cs, rows, m, by, la, eps, kappa, f, bx, &fbad, 2 * t, nullptr, a, eps_d, chk);
+        __syncthreads();
+      }
+      f_ready = false;
+      // ---- columns: local partials -> cluster exchange -> every CTA forms g
+      float *mypart = part + xpar * m4;
+      cols_partial_local(Cs, rows, m, bx, kappa, mypart);
+      cluster.sync();
+      for (int j = threadIdx.x; j < m; j += THREADS) {
+        float v[CL];
+#pragma unroll
+        for (int r = 0; r < CL; ++r) v[r] = cluster.map_shared_rank(mypart, r)[j];
+        float mx = -INFINITY;
+        bool nan = false;
+#pragma unroll
+        for (int r = 0; r < CL; ++r) {
+          nan |= (v[r] != v[r]);
+          mx = fmaxf(mx, v[r]);
+        }
+        float L;
+        if (nan) {
+          L = __int_as_float(0x7fc00000);
+        } else if (mx == -INFINITY || mx == INFINITY) {
+          L = mx;
+        } else {
+          float acc = 0.f;
+#pragma unroll
+          for (int r = 0; r < CL; ++r) acc += ex2(v[r] - mx);
+          L = mx + lg2(acc);
+        }
+        const float gv = eps * lb[j] - eps * kLn2 * L;
+        g[j] = gv;
+        by[j] = gv * kappa;
+        if (bad_potential(gv)) atomicMin(&fbad, 2 * t + 1);
+      }
+      xpar ^= 1;
+      __syncthreads();
+      if (t % A.inner_iters == 0 || t == A.max_iters) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) chk[k] = 0.0;
+        rows_local<true>(Cs, rows, m, by, la, eps, kappa, fn, bx, &fbad, 2 * t + 2, f, a, eps_d, chk);
+        if (rank == 0) {  // g is replicated: its terms are counted once
+          for (int j = threadIdx.x; j < m; j += THREADS) {
+            const double gj = g[j], bj = bw[j];
+            if (bj > 0.0) chk[3] += bj * gj;
+            chk[5] += (gj != gj) ? 1.0 : 0.0;
+            chk[7] += (gj == INFINITY) ? 1.0 : 0.0;
+          }
+        }
+        block_sum(chk, red);  // ends with every thread holding the CTA totals
+        double *myslot = slot + xpar * (NV + 1);
+        __syncthreads();      // fbad final for this CTA
+        if (threadIdx.x == 0) {
+#pragma unroll
+          for (int k = 0; k < NV; ++k) myslot[k] = chk[k];
+          myslot[NV] = (double)fbad;
+        }
+        cluster.sync();
+        double tot[NV];
+        double fb = 2147483647.0;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) tot[k] = 0.0;
+        for (int r = 0; r < CL; ++r) {  // rank order: identical in every CTA
+          const double *ps = cluster.map_shared_rank(myslot, r);
+#pragma unroll
+          for (int k = 0; k < NV; ++k) tot[k] += ps[k];
+          fb = fmin(fb, ps[NV]);
+        }
+        xpar ^= 1;
+        const int fbi = (int)fb;
+        int d = 0;  // 0 continue, 1 converged, 2 bad potential, 3 diverged
+        if (fbi <= 2 * t) {
+          d = 2;
+          fail_iter = (fbi + 1) / 2;
+        } else if (tot[4] > 0 || tot[5] > 0) {
+          d = 3;
+          fail_iter = t;
+        } else if (fbi == 2 * t + 1) {
+          d = 2;
+          fail_iter = t;
+        } else {
+          if (rank == 0 && threadIdx.x == 0 && n_checks < A.max_checks) {
+            A.errors[b * A.max_checks + n_checks] = tot[0];
+            A.duals[b * A.max_checks + n_checks] = tot[2] + tot[3] - eps_d * (tot[1] - 1.0);
+          }
+          if (tot[0] <= A.threshold) d = 1;
+        }
+        if (d == 2 || d == 3) {
+          status = (d == 2) ? OTK_BAD_POTENTIAL : OTK_DIVERGED;
+          break;
+        }
+        ++n_checks;
+        if (d == 1) {
+          converged = 1;
+          break;
+        }
+        if (t < A.max_iters) {
+          float *tmp = f;
+          f = fn;
+          fn = tmp;
+          f_ready = true;
+        }
+      }
+    }
+    for (int i = threadIdx.x; i < rows; i += THREADS) A.f_out[b * n + r0 + i] = f[i];
+    if (rank == 0) {
+      for (int j = threadIdx.x; j < m; j += THREADS) A.g_out[b * m + j] = g[j];
+      if (threadIdx.x == 0) {
+        int *st = A.state + b * 5;
+        st[0] = min(n_checks, A.max_checks);
+        st[1] = min(t, A.max_iters);
+        st[2] = converged;
+        st[3] = status;
+        st[4] = fail_iter;
+      }
+    }
+    // no CTA may overwrite its cost slice / partials while a peer still reads them
+    cluster.sync();
+  }
+}
+
+size_t cluster_smem_bytes(int n, int m, int CL) {
+  const size_t rows_per = (n + CL - 1) / CL;
+  const size_t rp4 = (rows_per + 3) & ~(size_t)3, m4 = (m + 3) & ~3;
+  return rows_per * m * sizeof(float) + (3 * rp4 + 2 * m4 + 2 * m4) * sizeof(float) +
+         2 * (NV + 1) * sizeof(double) + 64;
+}
+
+template <int CL>
+static int cluster_try(const Args &A, int n, int m, int64_t batch, int grid, cudaStream_t st,
+                       bool launch, int *sms_used) {
+  int dev = 0, max_smem = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t smem = cluster_smem_bytes(n, m, CL);
+  if (smem + 2048 > (size_t)max_smem) return OTK_ENOTSUP;
+  auto kern = dense_cluster_solve_kernel<CL>;
+  OTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL * 64);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = CL;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl <= 0) {
+    cudaGetLastError();
+    return OTK_ENOTSUP;
+  }
+  if (grid > 0) ncl = std::min(ncl, std::max(1, grid / CL));
+  ncl = (int)std::min<int64_t>(ncl, batch);
+  *sms_used = ncl * CL;
+  if (!launch) return OTK_OK;
+  cfg.gridDim = dim3(CL * ncl);
+  OTK_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
+  return OTK_OK;
+}
+
+// Cluster size with the most SMs in use (clusters live inside one GPC: 8 x k
+// may leave SMs idle where 6 x k does not); OTK_DENSE_CL forces 6 or 8.
+int launch_cluster_solve(const Args &A, int n, int m, int64_t batch, int grid, int want_cl,
+                         cudaStream_t st) {
+  int used6 = 0, used8 = 0;
+  const bool ok6 = (want_cl == 0 || want_cl == 6) &&
+                   cluster_try<6>(A, n, m, batch, grid, st, false, &used6) == OTK_OK;
+  const bool ok8 = (want_cl == 0 || want_cl == 8) &&
+                   cluster_try<8>(A, n, m, batch, grid, st, false, &used8) == OTK_OK;
+  if (!ok6 && !ok8) return OTK_ENOTSUP;
+  int dummy = 0;
+  if (ok8 && (!ok6 || used8 >= used6)) return cluster_try<8>(A, n, m, batch, grid, st, true, &dummy);
+  return cluster_try<6>(A, n, m, batch, grid, st, true, &dummy);
+}
+
 size_t smem_bytes(int n, int m) {
   const size_t n4 = (n + 3) & ~3, m4 = (m + 3) & ~3;
   return (3 * n4 + 2 * m4) * sizeof(float) + (size_t)WARPS * 128 * 2 * sizeof(float);
@@ -347,6 +757,14 @@ extern "C" int otk_solve_dense_batched(const float *cost, int64_t batch, int64_t
                 "otk_solve_dense_batched: bad loop parameters");
   dsolve::Args A{cost, batch, (int)n, (int)m, a, b, log_a, log_b, eps, g_init, eps_d, threshold,
                  max_iters, inner_iters, max_checks, f_out, g_out, errors, duals, state};
+  // K3c (cost resident in a cluster's shared memory) whenever a slice fits;
+  // OTK_DENSE_KERNEL=cta forces the one-CTA-per-problem streaming kernel K3p
+  const char *kind = getenv("OTK_DENSE_KERNEL");
+  if (!(kind && strcmp(kind, "cta") == 0)) {
+    const int want_cl = getenv("OTK_DENSE_CL") ? atoi(getenv("OTK_DENSE_CL")) : 0;
+    int rc = dsolve::launch_cluster_solve(A, (int)n, (int)m, batch, grid, want_cl, as_stream(stream));
+    if (rc != OTK_ENOTSUP) return rc;
+  }
   const size_t smem = dsolve::smem_bytes((int)n, (int)m);
   OTK_CUDA(cudaFuncSetAttribute(dsolve::dense_solve_kernel,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -256,7 +256,11 @@ def test_dense_geometry_solves_match_reference(otk):
         np.testing.assert_allclose(rc, fx[f"p{k}_cost"], rtol=COST_TOL)
 
 
-def test_batched_cfg3_matches_reference(otk):
+@pytest.mark.parametrize("kernel", ["cluster", "cta"])
+def test_batched_cfg3_matches_reference(otk, kernel, monkeypatch):
+    """Both one-launch batched solvers: K3c (cost resident in a cluster's shared
+    memory, the default) and K3p (one CTA per problem streaming C from HBM)."""
+    monkeypatch.setenv("OTK_DENSE_KERNEL", kernel)
     fx = load_golden("dense_cfg3")
     wl = workloads.cfg3(batch=6)
     outs, costs = otk.solve_sinkhorn_batched(wl.x, wl.y, wl.eps, threshold=wl.threshold,
@@ -481,3 +485,30 @@ def test_apply_kernel_matches_dense_gibbs_product(otk, cost_fn):
         np.array([1.0]), 1.0, "rows"), [1.0], rtol=1e-6)
     np.testing.assert_allclose(otk.DenseGeometry(np.zeros((2, 2))).apply_kernel(
         np.array([1.0, 1.0]), 1.0, "rows"), [2.0, 2.0], rtol=1e-6)
+
+
+@pytest.mark.parametrize("n,m,cl", [(512, 512, "6"), (512, 512, "8"), (130, 68, "0"), (37, 1024, "0"),
+                                    (700, 300, "0")])
+def test_batched_cluster_solver_matches_streaming_solver(otk, monkeypatch, n, m, cl):
+    """K3c vs K3p on ragged shapes (rows not a multiple of the cluster, CTAs with no
+    rows, several column chunks), warm start, fixed iterations and tolerance runs:
+    same iteration counts and convergence, potentials within fp32 rounding."""
+    rng = np.random.default_rng(n + m)
+    B, d = 20, 5
+    x = rng.standard_normal((B, n, d)).astype(np.float32)
+    y = (rng.standard_normal((B, m, d)) + rng.uniform(-1, 1, (B, 1, d))).astype(np.float32)
+    eps = np.array([0.05 * np.mean(np.sum((x[k, :64, None] - y[k, None, :64]) ** 2, -1))
+                    for k in range(B)])
+    g0 = (rng.standard_normal((B, m)) * eps[:, None]).astype(np.float32)
+    monkeypatch.setenv("OTK_DENSE_CL", cl)
+    for kw in (dict(threshold=1e-3, max_iters=500), dict(threshold=1e-300, max_iters=37),
+               dict(threshold=1e-3, max_iters=500, g_init=g0)):
+        monkeypatch.setenv("OTK_DENSE_KERNEL", "cluster")
+        a = otk.solve_sinkhorn_batched(x, y, eps, **kw)
+        monkeypatch.setenv("OTK_DENSE_KERNEL", "cta")
+        b = otk.solve_sinkhorn_batched(x, y, eps, **kw)
+        assert np.array_equal(a.iterations, b.iterations)
+        assert np.array_equal(a.converged, b.converged)
+        for k in range(B):
+            assert rel_inf(a.f[k], b.f[k]) <= 2e-6
+            assert rel_inf(a.g[k], b.g[k]) <= 2e-6
