@@ -342,6 +342,7 @@ struct HalfStep {
   bool have_x = false, have_y = false;
 
   int rows(float kappa, float eps, float kappa_next, float *f_out, int step) {
+    NvtxRange r("otk f half-step");
     const int fl = kflags | (have_x ? 0 : OTK_ANCHOR_INIT);
     launches += (anchored && have_x) ? 4 : 2;
     have_x = true;
@@ -351,6 +352,7 @@ struct HalfStep {
                         step, anchored ? L->anc_x : nullptr, L->rep_x, nullptr, st);
   }
   int cols(float kappa, float eps, float kappa_next, int step) {
+    NvtxRange r("otk g half-step");
     const int fl = kflags | (have_y ? 0 : OTK_ANCHOR_INIT);
     launches += (anchored && have_y) ? 4 : 2;
     have_y = true;
@@ -447,6 +449,7 @@ static int solve_small(otk_solve_args *A, Layout &L, cudaStream_t st) {
 }
 
 static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st) {
+  NvtxRange range("otk_solve_pointcloud");
   A->n_checks = 0;
   A->iterations = 0;
   A->converged = 0;
