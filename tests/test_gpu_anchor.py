@@ -170,3 +170,35 @@ def test_solver_anchored_graph_periods(env):
     for name in ("f", "g"):
         u, v = getattr(a, name), getattr(b, name)
         assert np.max(np.abs(u - v)) / np.max(np.abs(v)) <= 1e-5, name
+
+
+def test_anchored_solver_zero_weights_and_small_eps(env):
+    """Zero weights on both sides (-inf potentials, empty plan rows/columns) and a
+    small eps (most terms far below each row's maximum) on the anchored tcgen05
+    path: same trajectory as the running-max path and the float64 oracle."""
+    otk, N, torch = env
+    rng = np.random.default_rng(17)
+    n, m, d = 700, 900, 64
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    y = (1.5 * rng.standard_normal((m, d))).astype(np.float32)
+    a = rng.uniform(0.5, 1.5, n)
+    b = rng.uniform(0.5, 1.5, m)
+    a[rng.choice(n, 40, replace=False)] = 0.0
+    b[rng.choice(m, 55, replace=False)] = 0.0
+    a /= a.sum()
+    b /= b.sum()
+    mean_c = float(np.mean(np.sum((x[:64, None, :] - y[None, :64, :]) ** 2, axis=-1)))
+    geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64))
+    for scale, its in ((0.05, 30), (0.005, 40)):
+        eps = scale * mean_c
+        prob = otk.LinearProblem(otk.PointCloudGeometry(x, y), a, b)
+        out = otk.solve_sinkhorn(prob, eps, threshold=1e-300, max_iters=its, impl="tc")
+        ref_rm = otk.solve_sinkhorn(prob, eps, threshold=1e-300, max_iters=its, impl="tc-noanchor")
+        ref = oracle.sinkhorn(geom64, a, b, eps, threshold=1e-300, max_iters=its)
+        assert np.array_equal(np.isneginf(out.f), a == 0) and np.array_equal(np.isneginf(out.g), b == 0)
+        for name in ("f", "g"):
+            got, rm, want = getattr(out, name), getattr(ref_rm, name), ref[name]
+            fin = np.isfinite(want)
+            scale_ = np.max(np.abs(want[fin]))
+            assert np.max(np.abs(got[fin] - rm[fin])) / scale_ <= 2e-6, (scale, name)
+            assert np.max(np.abs(got[fin] - want[fin])) / scale_ <= 1e-4, (scale, name)
