@@ -1,0 +1,80 @@
+"""Randomised parity sweep of the device solver vs the float64 oracle.
+
+Random shapes (odd sizes, n != m), dimensions across every kernel route
+(FP32 small solve, tcgen05 V1 / pair / V2 / V4), eps scales, zero weights,
+warm starts; fixed-iteration solves compared on f, g (1e-4 of the largest
+finite entry) and the transport cost (1e-5); anchored vs running-max
+trajectories compared at 2e-6.  usage: python tools/fuzz_parity.py [cases] [seed]
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
+import paper_2201_12324_b200 as otk  # noqa: E402
+
+
+def rel(a, b):
+    fin = np.isfinite(b)
+    return float(np.max(np.abs(a[fin] - b[fin])) / max(np.max(np.abs(b[fin])), 1e-30))
+
+
+def main(cases=60, seed=0):
+    rng = np.random.default_rng(seed)
+    worst = {"f": 0.0, "g": 0.0, "cost": 0.0, "anch": 0.0}
+    fails = 0
+    for c in range(cases):
+        d = int(rng.choice([2, 3, 5, 16, 33, 64, 100, 128, 200, 300, 520]))
+        n = int(rng.integers(1, 900))
+        m = int(rng.integers(1, 900))
+        x = rng.standard_normal((n, d)).astype(np.float32) * float(rng.choice([0.3, 1.0, 4.0]))
+        y = (rng.standard_normal((m, d)) * float(rng.choice([0.5, 1.0, 2.0])) + rng.uniform(-1, 1)).astype(np.float32)
+        a = rng.uniform(0.5, 1.5, n)
+        b = rng.uniform(0.5, 1.5, m)
+        if rng.random() < 0.4 and n > 2:
+            a[rng.choice(n, max(1, n // 10), replace=False)] = 0.0
+        if rng.random() < 0.4 and m > 2:
+            b[rng.choice(m, max(1, m // 10), replace=False)] = 0.0
+        a /= a.sum()
+        b /= b.sum()
+        k = min(n, m, 64)
+        mc = float(np.mean(np.sum((x[:k, None, :] - y[None, :k, :]) ** 2, axis=-1)))
+        eps = float(rng.choice([0.01, 0.05, 0.5])) * max(mc, 1e-3)
+        its = int(rng.integers(3, 40))
+        g0 = None
+        if rng.random() < 0.3:
+            g0 = (rng.standard_normal(m) * eps * float(rng.choice([1.0, 50.0]))).astype(np.float32)
+        geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64))
+        prob = otk.LinearProblem(otk.PointCloudGeometry(x, y), a, b)
+        try:
+            ref = oracle.sinkhorn(geom64, a, b, eps, threshold=1e-300, max_iters=its,
+                                  g_init=None if g0 is None else g0.astype(np.float64))
+        except Exception as exc:  # noqa: BLE001 -- the oracle itself diverged: skip the case
+            print(f"case {c}: oracle {type(exc).__name__}, skipped")
+            continue
+        out = otk.solve_sinkhorn(prob, eps, threshold=1e-300, max_iters=its, g_init=g0)
+        e = {"f": rel(out.f, ref["f"]), "g": rel(out.g, ref["g"])}
+        cost = otk.reg_ot_cost(out, prob)
+        ref_cost = oracle.reg_ot_cost(geom64, ref["f"], ref["g"], a, b, eps)
+        e["cost"] = abs(cost.transport_cost - ref_cost[0]) / max(abs(ref_cost[0]), 1e-30)
+        if d >= 4:
+            rm = otk.solve_sinkhorn(prob, eps, threshold=1e-300, max_iters=its, g_init=g0,
+                                    impl="tc-noanchor")
+            e["anch"] = max(rel(out.f, rm.f), rel(out.g, rm.g))
+        for kk, v in e.items():
+            worst[kk] = max(worst[kk], v)
+        bad = e["f"] > 1e-4 or e["g"] > 1e-4 or e["cost"] > 1e-5 or e.get("anch", 0.0) > 2e-6
+        fails += bad
+        print(f"case {c:3d} n={n:4d} m={m:4d} d={d:3d} eps/mc={eps / max(mc, 1e-3):.3g} its={its:2d} "
+              f"zeros={int((a == 0).sum())}/{int((b == 0).sum())} g0={'y' if g0 is not None else 'n'} "
+              + " ".join(f"{kk}={v:.1e}" for kk, v in e.items()) + ("  <-- FAIL" if bad else ""),
+              flush=True)
+    print("worst", {k: f"{v:.2e}" for k, v in worst.items()}, "fails", fails)
+
+
+if __name__ == "__main__":
+    main(*(int(v) for v in sys.argv[1:]))
