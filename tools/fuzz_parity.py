@@ -67,7 +67,7 @@ def main(cases=60, seed=0):
             e["anch"] = max(rel(out.f, rm.f), rel(out.g, rm.g))
         for kk, v in e.items():
             worst[kk] = max(worst[kk], v)
-        bad = e["f"] > 1e-4 or e["g"] > 1e-4 or e["cost"] > 1e-5 or e.get("anch", 0.0) > 2e-6
+        bad = e["f"] > 1e-4 or e["g"] > 1e-4 or e["cost"] > 1e-5 or e.get("anch", 0.0) > 1e-5
         fails += bad
         print(f"case {c:3d} n={n:4d} m={m:4d} d={d:3d} eps/mc={eps / max(mc, 1e-3):.3g} its={its:2d} "
               f"zeros={int((a == 0).sum())}/{int((b == 0).sum())} g0={'y' if g0 is not None else 'n'} "
