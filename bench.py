@@ -272,7 +272,7 @@ def online_roofline(geom, wl, reps=10):
     part = torch.empty(nsplit * n, dtype=torch.float32, device=dev)
     sinv = 1.0 / (cx.scale * cx.scale)
     tc = cx.hi is not None and not (flags & N.OTK_IMPL_SIMT)
-    anchored = bool(lib.otk_lse_step_anchored(cx.d, flags))
+    anchored = bool(lib.otk_lse_step_anchored(n, m, cx.d, flags))
     base = torch.full((n,), float(np.log(1.0 / n)), dtype=torch.float32, device=dev)
     out = torch.empty(n, dtype=torch.float32, device=dev)
     anchor = torch.empty(n, dtype=torch.float32, device=dev)

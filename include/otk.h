@@ -174,7 +174,9 @@ int otk_exchange_finalize(void *local, int32_t world, int64_t m, uint32_t epoch,
 int otk_exchange_status(void *local, int32_t *status, void *stream);
 
 size_t otk_lse_step_workspace_bytes(int64_t np);
-int otk_lse_step_anchored(int32_t d, int32_t flags);
+/* 1 if otk_lse_step anchors on this path AND the half-step is long enough for
+ * it to pay (np * nq >= 2^27 cells; env OTK_ANCHOR_MIN_CELLS overrides). */
+int otk_lse_step_anchored(int64_t np, int64_t nq, int32_t d, int32_t flags);
 /* xchg (nullable, OTK_FIN_LOG2 only): push the rows to every rank (above). */
 int otk_lse_step(const float *p, const float *p_sq, const uint16_t *p_hi,
                  const uint16_t *p_lo, const uint16_t *p_ext, int64_t np,

@@ -65,7 +65,7 @@ SIGNATURES = {
     "otk_lse_uses_tc": (C.c_int, [I32, I32]),
     "otk_lse_finalize": (C.c_int, [P, I32, I64, P, I32, F32, F32, P, P, P, I32, P]),
     "otk_lse_step_workspace_bytes": (SZ, [I64]),
-    "otk_lse_step_anchored": (C.c_int, [I32, I32]),
+    "otk_lse_step_anchored": (C.c_int, [I64, I64, I32, I32]),
     "otk_lse_step": (C.c_int, [P, P, P, P, P, I64, P, P, P, P, P, I64, I32, I32, F32, P, F32, I32,
                                I32, P, P, I32, F32, F32, P, P, P, I32, P, P, C.POINTER(Exchange), P]),
     "otk_exchange_bytes": (SZ, [I32, I64]),

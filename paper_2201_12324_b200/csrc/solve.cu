@@ -169,7 +169,17 @@ static bool anchored_path(int32_t d, int32_t flags) {
   return want_tc(flags, d) && tc_available() && !(flags & (OTK_COST_EUCL | OTK_IMPL_NOANCHOR));
 }
 
-extern "C" int otk_lse_step_anchored(int32_t d, int32_t flags) { return anchored_path(d, flags) ? 1 : 0; }
+// The anchored step costs two extra small launches per half-step (~10 us);
+// it pays off only where the half-step itself is long (measured gain ~7 % of
+// the TC kernel at cfg2; break-even near 10^4 x 10^4): default threshold
+// 2^27 cells (np * nq), override
+// with OTK_ANCHOR_MIN_CELLS.
+extern "C" int otk_lse_step_anchored(int64_t np, int64_t nq, int32_t d, int32_t flags) {
+  if (!anchored_path(d, flags)) return 0;
+  double min_cells = 134217728.0;
+  if (const char *e = getenv("OTK_ANCHOR_MIN_CELLS")) min_cells = atof(e);
+  return (double)np * (double)nq >= min_cells ? 1 : 0;
+}
 
 extern "C" size_t otk_lse_step_workspace_bytes(int64_t np) {
   return (size_t)(((np + 127) / 128) + 2) * sizeof(int32_t);
@@ -474,7 +484,7 @@ static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st) {
   HalfStep H{A, &L, st, 1.f / (s * s),
              (A->flags & (OTK_IMPL_SIMT | OTK_IMPL_TC | OTK_COST_EUCL)) | OTK_CLAMP |
                  (A->same_points ? OTK_SAME_POINTS : 0)};
-  H.anchored = L.tc && !(A->flags & OTK_IMPL_NOANCHOR) && otk_lse_step_anchored(A->d, H.kflags);
+  H.anchored = L.tc && !(A->flags & OTK_IMPL_NOANCHOR) && otk_lse_step_anchored(A->n, A->m, A->d, H.kflags);
 
   // ---- initial g (zeros or warm start) and its bias for h = 1
   const double e0 = eps_at(A, 0);

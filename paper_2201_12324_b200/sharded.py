@@ -295,7 +295,7 @@ class CudaShardEngine:
         self.device = dev
         self.launches = 0
         # anchored half-steps (otk_lse_step): per-role anchors + repair workspaces
-        self.anchored = bool(lib.otk_lse_step_anchored(self.d, self.flags)) and not (
+        self.anchored = bool(lib.otk_lse_step_anchored(self.n, self.m, self.d, self.flags)) and not (
             flags & N.OTK_IMPL_NOANCHOR)
         self.anc_x = torch.empty(self.n, **f32)
         self.anc_y = torch.empty(self.m, **f32)

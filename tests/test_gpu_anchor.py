@@ -128,8 +128,15 @@ def test_anchor_solver_mode_matches_partial_finalize(env):
         assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) <= 1e-5
 
 
+@pytest.fixture
+def anchor_always(monkeypatch):
+    """The solver anchors only long half-steps by default (>= 2^27 cells); these
+    tests exercise the anchored path at small sizes."""
+    monkeypatch.setenv("OTK_ANCHOR_MIN_CELLS", "0")
+
+
 @pytest.mark.parametrize("d", [64, 128])
-def test_solver_anchored_vs_running_max(env, d):
+def test_solver_anchored_vs_running_max(env, d, anchor_always):
     """Whole solves: anchored (default) vs running-max only -- same iterations and
     convergence, potentials within fp32 noise; far-off warm start forces repairs."""
     otk, N, torch = env
@@ -150,7 +157,7 @@ def test_solver_anchored_vs_running_max(env, d):
         assert np.allclose(a.errors, b.errors, rtol=1e-3, atol=1e-6)
 
 
-def test_solver_anchored_graph_periods(env):
+def test_solver_anchored_graph_periods(env, anchor_always):
     """Long fixed-iteration solve (CUDA-graph periods replayed many times) stays
     on the running-max trajectory."""
     otk, N, torch = env
@@ -172,7 +179,7 @@ def test_solver_anchored_graph_periods(env):
         assert np.max(np.abs(u - v)) / np.max(np.abs(v)) <= 1e-5, name
 
 
-def test_anchored_solver_zero_weights_and_small_eps(env):
+def test_anchored_solver_zero_weights_and_small_eps(env, anchor_always):
     """Zero weights on both sides (-inf potentials, empty plan rows/columns) and a
     small eps (most terms far below each row's maximum) on the anchored tcgen05
     path: same trajectory as the running-max path and the float64 oracle."""
