@@ -51,6 +51,8 @@ struct Args {
   double *errors, *duals;
   int *state;
   int probe;
+  unsigned long long *xch_x, *xch_y;
+  int variant;
 };
 }  // namespace small
 bool small_solve_fits(int64_t n, int64_t m, int d);
@@ -261,6 +263,7 @@ struct Layout {
   void *chk_ws;
   int *first_bad;
   double *slots, *d_errors, *d_duals;  // persistent small-problem kernel
+  unsigned long long *xch;
   int *state;
   int nsr, nsc, dpad;
   bool tc, small;
@@ -316,6 +319,7 @@ Layout plan(const otk_solve_args *A, void *ws) {
     L.d_errors = c.take<double>(A->max_checks);
     L.d_duals = c.take<double>(A->max_checks);
     L.state = c.take<int>(8);
+    L.xch = c.take<unsigned long long>(2 * (size_t)(A->n + A->m));
   }
   L.bytes = c.off + 256;
   return L;
@@ -439,6 +443,9 @@ static int solve_small(otk_solve_args *A, Layout &L, cudaStream_t st) {
   S.duals = L.d_duals;
   S.state = L.state;
   S.probe = getenv("OTK_SMALL_PROBE") ? atoi(getenv("OTK_SMALL_PROBE")) : 0;
+  S.xch_x = L.xch;
+  S.xch_y = L.xch + 2 * A->n;
+  S.variant = getenv("OTK_SMALL_V1") ? atoi(getenv("OTK_SMALL_V1")) : 0;
   OTK_CUDA(cudaMemsetAsync(L.first_bad, 0x7f, sizeof(int), st));
   OTK_TRY(small_solve_launch(S, A->same_points != 0, (A->flags & OTK_COST_EUCL) != 0, st));
   int state[8];

@@ -47,7 +47,10 @@ struct Args {
   int *first_bad;
   double *errors, *duals;    // [max_checks]
   int *state;                // n_checks, iterations, converged, status, fail_iter
-  int probe;                 // timing probe (OTK_SMALL_PROBE): 1 = skip the half-step math
+  int probe;                 // timing probe (OTK_SMALL_PROBE): 1 = skip the half-step math, 2 = skip the
+                             // passes over the cells (row-chunk variant); probes never converge
+  unsigned long long *xch_x, *xch_y;  // row-chunk exchange words, 2 buffers per role ([2n], [2m])
+  int variant;               // 0 = row-chunk half-step (default), 1 = column-sliced (OTK_SMALL_V1)
 };
 
 __device__ __forceinline__ void load_points(const float *src, int count, int d, float kappa,
@@ -210,11 +213,270 @@ __device__ void half_step(const Args &A, const float4 *P, int np, const float4 *
   }
 }
 
+// ---- row-chunk half-step (default) ----
+//
+// A CTA takes a chunk of RC <= 16 consecutive rows (rc = ceil(np / grid) rows
+// when that is <= 16, so a 2048-row half-step is one chunk per SM) and ALL its
+// columns: thread t holds columns t, t + THREADS, ... (CPT per group) in
+// registers, reads each row's query vector as a shared-memory broadcast and
+// accumulates one partial per row.  Partials leave a warp through a
+// shuffle reduce-scatter (16 rows -> one row per lane pair in 16 shuffles, not
+// 16 x 5), meet across warps in shared memory and are folded in warp order:
+// deterministic.  The chunks of a role stay with one CTA for the whole solve,
+// so their query vectors p' and anchors live in that CTA's shared memory.
+//
+// Rows are summed against an anchor instead of a running max: the row's own
+// log2 result of the previous half-step of this role.  A row is accepted when
+// its anchor was finite and -96 + 2 log2(nq) <= L - anchor <= 120 (every term
+// within 2^-30 of the row's sum stayed above the ex2 flush threshold and
+// nothing overflowed; the same window as the tcgen05 anchored epilogue) or
+// when L is NaN; a chunk with any other row (or the first half-step of each
+// role, which has no anchors) is redone exactly: one pass for the row maxima,
+// then the sum against them.  The decision is local to the CTA.
+//
+// No grid barrier between half-steps: each output row is published as ONE
+// 64-bit word {kappa * potential, half-step index} (relaxed gpu-scope store),
+// double-buffered per role, and a consumer spins on its columns' words until
+// the tag is the half-step it needs.  Value and tag travel in one single-copy
+// atomic access, so no fence is needed.  A buffer is rewritten two half-steps
+// of its role later, which every reader of it has provably finished: its
+// writer first consumed the other role's words, whose writers consumed this
+// buffer.  Check iterations keep their grid barriers (global sums).
+constexpr int RC = 16;    // rows per chunk (the reduce-scatter width)
+constexpr int CPT = 4;    // columns per thread per register group
+constexpr int KMAX = 8;   // chunks per CTA per role (n <= 8 * 16 * #SMs)
+
+typedef unsigned long long xword;
+
+__device__ __forceinline__ xword ld_relaxed(const xword *p) {
+  xword v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(xword *p, xword v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ xword xpack(float v, int tag) {
+  return ((xword)(unsigned)tag << 32) | (xword)__float_as_uint(v);
+}
+
+template <bool MAXP>
+__device__ __forceinline__ float rs_op(float a, float b) { return MAXP ? fmaxf(a, b) : a + b; }
+
+// 16 per-lane row partials -> the warp's total of row rs16_row(lane) on lanes
+// with bit 0 clear (fixed tree: deterministic, and + / max are commutative).
+template <bool MAXP>
+__device__ __forceinline__ float rs16(float (&v)[RC], int lane) {
+#pragma unroll
+  for (int w = 8; w >= 1; w >>= 1) {
+    const bool up = lane & (2 * w);
+#pragma unroll
+    for (int k = 0; k < w; ++k) {
+      const float send = up ? v[k] : v[k + w];
+      const float keep = up ? v[k + w] : v[k];
+      v[k] = rs_op<MAXP>(keep, __shfl_xor_sync(0xffffffffu, send, 2 * w));
+    }
+  }
+  return rs_op<MAXP>(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
+}
+__device__ __forceinline__ int rs16_row(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+
+// One pass over the chunk's rc rows and all nq columns: per row the max of
+// u_ij (MAXP) or sum_j 2^(u_ij - shift_r).  Result for row r in tot[r].
+// Column j's kappa * potential comes from its exchange word (tag `need`).
+template <int NV, bool SAME, bool EU, bool MAXP>
+__device__ __forceinline__ void chunk_pass(const Args &A, const float4 *Q, int nq, const xword *qx,
+                                           int need, int r0, int rc, const float4 (*prow)[NV],
+                                           const float2 *rowc, float (*red)[RC], float *tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float sk = sqrtf(A.kappa);
+  float acc[RC];
+#pragma unroll
+  for (int r = 0; r < RC; ++r) acc[r] = MAXP ? -INFINITY : 0.f;
+  for (int j0 = threadIdx.x; j0 < nq; j0 += THREADS * CPT) {
+    float4 q[CPT][NV];
+    float bj[CPT];
+    int jj[CPT];
+    xword w[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int j = j0 + c * THREADS;
+      jj[c] = j;
+      w[c] = (j < nq) ? ld_relaxed(qx + j) : xpack(-INFINITY, need);
+    }
+    for (int spins = 0;; ++spins) {  // spin until every column word carries the half-step we need
+      bool ready = true;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) ready &= (int)(w[c] >> 32) == need;
+      if (ready) break;
+      if (spins > (1 << 23)) __trap();  // a protocol bug must fail the launch, not hang the GPU
+#pragma unroll
+      for (int c = 0; c < CPT; ++c)
+        if ((int)(w[c] >> 32) != need) w[c] = ld_relaxed(qx + jj[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const bool ok = jj[c] < nq;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) q[c][v] = ok ? Q[jj[c] * NV + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+      bj[c] = __uint_as_float((unsigned)w[c]);
+    }
+#pragma unroll
+    for (int r = 0; r < RC; ++r) {
+      if (r < rc) {
+        asm volatile("" ::: "memory");  // re-read the row from shared memory (no hoisting of 16 rows)
+        float p[4 * NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const float4 pv = prow[r][v];
+          p[4 * v] = pv.x;
+          p[4 * v + 1] = pv.y;
+          p[4 * v + 2] = pv.z;
+          p[4 * v + 3] = pv.w;
+        }
+        const float2 rcw = rowc[r];  // (kappa |p|^2, shift)
+        float e[CPT];
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          float v;
+          if (EU) {
+            v = -sk * sqrt_approx(fmaxf(rcw.x - dot_q<NV>(p, q[c]), 0.f));
+            if (SAME && jj[c] == r0 + r) v = 0.f;
+          } else {
+            v = fminf(dot_q<NV>(p, q[c]), rcw.x);
+            if (SAME && jj[c] == r0 + r) v = rcw.x;
+          }
+          e[c] = MAXP ? v + bj[c] : ex2(v + (bj[c] - rcw.y));
+        }
+        if (MAXP) acc[r] = fmaxf(acc[r], fmaxf(fmaxf(e[0], e[1]), fmaxf(e[2], e[3])));
+        else acc[r] += (e[0] + e[1]) + (e[2] + e[3]);
+      }
+    }
+  }
+  const float v = rs16<MAXP>(acc, lane);
+  if (!(lane & 1)) red[warp][rs16_row(lane)] = v;
+  __syncthreads();
+  if (threadIdx.x < rc) {
+    float t = red[0][threadIdx.x];
+#pragma unroll
+    for (int w = 1; w < WARPS; ++w) t = rs_op<MAXP>(t, red[w][threadIdx.x]);
+    tot[threadIdx.x] = t;
+  }
+  __syncthreads();
+}
+
+// Per-role state a CTA keeps for the rows it owns (chunks blockIdx.x + k*G).
+template <int NV>
+struct RoleRows {
+  float4 prow[KMAX * RC][NV];  // p' = (2 kappa p, 1, 0..)
+  float2 rowc[KMAX * RC];      // (kappa |p|^2, anchor)
+};
+
+template <int NV>
+__device__ void init_role_rows(const Args &A, const float4 *P, int np, RoleRows<NV> &S) {
+  const int G = gridDim.x;
+  const int rc = min(RC, (np + G - 1) / G);
+  const int n_chunks = (np + rc - 1) / rc;
+  const float two_k = 2.f * A.kappa;
+  for (int idx = threadIdx.x; idx < KMAX * RC; idx += blockDim.x) {
+    const int k = idx / RC, r = idx % RC;
+    const int ch = blockIdx.x + k * G;
+    const int i = min(ch * rc + r, np - 1);
+    if (ch >= n_chunks) continue;
+    const float *pv = reinterpret_cast<const float *>(P + i * NV);
+    float p[4 * NV];
+#pragma unroll
+    for (int kk = 0; kk < 4 * NV; ++kk) p[kk] = (kk < A.d) ? two_k * pv[kk] : (kk == A.d ? 1.f : 0.f);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) S.prow[idx][v] = make_float4(p[4 * v], p[4 * v + 1], p[4 * v + 2], p[4 * v + 3]);
+    S.rowc[idx] = make_float2(-pv[A.d], -INFINITY);
+  }
+}
+
+// One half-step of a role: rows P (np) against the columns' exchange words
+// qx (tag step - 1).  Publishes {kappa * out_pot, step} into px and writes
+// out_pot (own rows).  CHECK: the f-side check sums (f_prev = previous f,
+// weights A.a); CHECKG: the g-side sums (weights A.b) of this g half-step.
+template <int NV, bool SAME, bool CHECK, bool CHECKG, bool EU>
+__device__ void half_step_rows(const Args &A, const float4 *P, int np, const float4 *Q, int nq,
+                               const xword *qx, xword *px, const float *logw, float *out_pot,
+                               RoleRows<NV> &S, bool anchored, int step, const float *f_prev,
+                               double (&chk)[NVALS]) {
+  static_assert(CPT == 4, "chunk_pass folds 4 columns per group");
+  __shared__ float red[WARPS][RC];
+  __shared__ float tot[RC];
+  __shared__ int redo;
+  const int G = gridDim.x;
+  const int rc = min(RC, (np + G - 1) / G);
+  const int n_chunks = (np + rc - 1) / rc;
+  const float lo = -96.f + 2.f * log2f((float)nq);
+  const int need = step - 1;
+  for (int ch = blockIdx.x, k = 0; ch < n_chunks; ch += G, ++k) {
+    const int r0 = ch * rc, rn = min(rc, np - r0);
+    const float4 (*prow)[NV] = S.prow + k * RC;
+    float2 *rowc = S.rowc + k * RC;
+    if (threadIdx.x == 0) redo = 0;
+    __syncthreads();
+    if (threadIdx.x < rn && !(anchored && fabsf(rowc[threadIdx.x].y) <= 3.0e38f)) redo = 1;
+    __syncthreads();
+    float L = 0.f;  // log2 sum (before the -kappa|p|^2 shift), row threadIdx.x
+    if (A.probe != 0) {  // timing probe: everything but the passes over the cells
+      if (threadIdx.x < rn) L = rowc[threadIdx.x].x;
+    } else if (!redo) {
+      chunk_pass<NV, SAME, EU, false>(A, Q, nq, qx, need, r0, rn, prow, rowc, red, tot);
+      if (threadIdx.x < rn) {
+        const float an = rowc[threadIdx.x].y;
+        L = an + lg2(tot[threadIdx.x]);
+        const float dl = L - an;
+        if (!(L != L) && !(dl >= lo && dl <= 120.f)) redo = 1;
+      }
+      __syncthreads();
+    }
+    if (redo && A.probe == 0) {  // exact: row maxima, then the sum against them
+      chunk_pass<NV, SAME, EU, true>(A, Q, nq, qx, need, r0, rn, prow, rowc, red, tot);
+      if (threadIdx.x < rn) {
+        const float mx = tot[threadIdx.x];
+        rowc[threadIdx.x].y = (mx == -INFINITY) ? 0.f : mx;  // all -inf -> sum 0 -> -inf; NaN survives
+      }
+      __syncthreads();
+      chunk_pass<NV, SAME, EU, false>(A, Q, nq, qx, need, r0, rn, prow, rowc, red, tot);
+      if (threadIdx.x < rn) L = rowc[threadIdx.x].y + lg2(tot[threadIdx.x]);
+    }
+    if (threadIdx.x < rn) {
+      const int i = r0 + threadIdx.x;
+      const float Lf = L - (EU ? 0.f : rowc[threadIdx.x].x);
+      rowc[threadIdx.x].y = L;
+      const float v = A.eps * logw[i] - A.eps * kLn2 * Lf;
+      st_relaxed(px + i, xpack(v * A.kappa, step));
+      out_pot[i] = v;
+      if (bad_potential(v)) atomicMin(A.first_bad, step);
+      if (CHECK) {
+        const double fp = f_prev[i], ai = A.a[i];
+        const double rr = (ai > 0.0) ? ai * exp((fp - (double)v) / A.eps_d) : 0.0;
+        chk[0] += fabs(rr - ai);
+        chk[1] += rr;
+        if (ai > 0.0) chk[2] += ai * fp;
+        chk[4] += (fp != fp) ? 1.0 : 0.0;
+        chk[6] += (fp == INFINITY) ? 1.0 : 0.0;
+      }
+      if (CHECKG) {
+        const double gj = v, bj = A.b[i];
+        if (bj > 0.0) chk[3] += bj * gj;
+        chk[5] += (gj != gj) ? 1.0 : 0.0;
+        chk[7] += (gj == INFINITY) ? 1.0 : 0.0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __device__ void load_bias(float *dst, const float *src, int count) {
   for (int j = threadIdx.x; j < count; j += blockDim.x) dst[j] = src[j];
 }
 
-template <int NV, bool SAME, bool EU>
+template <int NV, bool SAME, bool EU, int V1>
 __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ float4 sh4[];
@@ -226,44 +488,84 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
 
   load_points(A.x, A.n, A.d, A.kappa, xs, NV);
   load_points(A.y, A.m, A.d, A.kappa, ys, NV);
-  // initial g and its bias (h = 1 marks a bad warm start)
+  // initial g and its bias (h = 1 marks a bad warm start); the row-chunk
+  // variant publishes it as the y-words of half-step 1 and clears every other
+  // exchange word (a previous solve's tags must not match)
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.m; j += gridDim.x * blockDim.x) {
     const float g0 = A.g_init ? A.g_init[j] : 0.f;
     A.g[j] = g0;
     A.bias_y[j] = g0 * A.kappa;
+    if (!V1) {
+      A.xch_y[j] = xpack(g0 * A.kappa, 1);
+      A.xch_y[A.m + j] = xpack(0.f, -1);
+    }
     if (bad_potential(g0)) atomicMin(A.first_bad, 1);
+  }
+  if (!V1)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * A.n; i += gridDim.x * blockDim.x)
+      A.xch_x[i] = xpack(0.f, -1);
+  __shared__ RoleRows<NV> rows_x, rows_y;
+  if (!V1) {
+    __syncthreads();
+    init_role_rows<NV>(A, xs, A.n, rows_x);
+    init_role_rows<NV>(A, ys, A.m, rows_y);
   }
   __syncthreads();
   grid.sync();
 
+  // exchange buffer of the words tagged T: (T >> 1) & 1
+  auto xb = [&](unsigned long long *base, int len, int tag) { return base + ((tag >> 1) & 1) * (size_t)len; };
   float *f = A.f0, *fn = A.f1;
   bool f_ready = false;
   int n_checks = 0, status = OTK_OK, fail_iter = 0, converged = 0, t;
   double chk[NVALS];
   for (t = 1; t <= A.max_iters; ++t) {
+    const bool check = (t % A.inner_iters == 0 || t == A.max_iters);
+#pragma unroll
+    for (int k = 0; k < NVALS; ++k) chk[k] = 0.0;
     if (!f_ready) {
-      load_bias(bias_s, A.bias_y, A.m);
-      __syncthreads();
-      half_step<NV, SAME, false, EU>(A, xs, A.n, ys, A.m, bias_s, A.la, f, A.bias_x, 2 * t, nullptr, chk);
-      grid.sync();
+      if (V1) {
+        load_bias(bias_s, A.bias_y, A.m);
+        __syncthreads();
+        half_step<NV, SAME, false, EU>(A, xs, A.n, ys, A.m, bias_s, A.la, f, A.bias_x, 2 * t, nullptr, chk);
+        grid.sync();
+      } else {
+        half_step_rows<NV, SAME, false, false, EU>(A, xs, A.n, ys, A.m, xb(A.xch_y, A.m, 2 * t - 1),
+                                                   xb(A.xch_x, A.n, 2 * t), A.la, f, rows_x, t > 1, 2 * t,
+                                                   nullptr, chk);
+      }
     }
     f_ready = false;
-    load_bias(bias_s, A.bias_x, A.n);
-    __syncthreads();
-    half_step<NV, SAME, false, EU>(A, ys, A.m, xs, A.n, bias_s, A.lb, A.g, A.bias_y, 2 * t + 1, nullptr, chk);
-    grid.sync();
-    if (t % A.inner_iters == 0 || t == A.max_iters) {
-      // f_{t+1} into fn, with the check of (f_t, g_t) fused in
-#pragma unroll
-      for (int k = 0; k < NVALS; ++k) chk[k] = 0.0;
-      load_bias(bias_s, A.bias_y, A.m);
+    if (V1) {
+      load_bias(bias_s, A.bias_x, A.n);
       __syncthreads();
-      half_step<NV, SAME, true, EU>(A, xs, A.n, ys, A.m, bias_s, A.la, fn, A.bias_x, 2 * t + 2, f, chk);
-      for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.m; j += gridDim.x * blockDim.x) {
-        const double gj = A.g[j], bj = A.b[j];
-        if (bj > 0.0) chk[3] += bj * gj;
-        chk[5] += (gj != gj) ? 1.0 : 0.0;
-        chk[7] += (gj == INFINITY) ? 1.0 : 0.0;
+      half_step<NV, SAME, false, EU>(A, ys, A.m, xs, A.n, bias_s, A.lb, A.g, A.bias_y, 2 * t + 1, nullptr, chk);
+      grid.sync();
+    } else if (check) {
+      half_step_rows<NV, SAME, false, true, EU>(A, ys, A.m, xs, A.n, xb(A.xch_x, A.n, 2 * t),
+                                                xb(A.xch_y, A.m, 2 * t + 1), A.lb, A.g, rows_y, t > 1,
+                                                2 * t + 1, nullptr, chk);
+    } else {
+      half_step_rows<NV, SAME, false, false, EU>(A, ys, A.m, xs, A.n, xb(A.xch_x, A.n, 2 * t),
+                                                 xb(A.xch_y, A.m, 2 * t + 1), A.lb, A.g, rows_y, t > 1,
+                                                 2 * t + 1, nullptr, chk);
+    }
+    if (check) {
+      // f_{t+1} into fn, with the check of (f_t, g_t) fused in
+      if (V1) {
+        load_bias(bias_s, A.bias_y, A.m);
+        __syncthreads();
+        half_step<NV, SAME, true, EU>(A, xs, A.n, ys, A.m, bias_s, A.la, fn, A.bias_x, 2 * t + 2, f, chk);
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.m; j += gridDim.x * blockDim.x) {
+          const double gj = A.g[j], bj = A.b[j];
+          if (bj > 0.0) chk[3] += bj * gj;
+          chk[5] += (gj != gj) ? 1.0 : 0.0;
+          chk[7] += (gj == INFINITY) ? 1.0 : 0.0;
+        }
+      } else {
+        half_step_rows<NV, SAME, true, false, EU>(A, xs, A.n, ys, A.m, xb(A.xch_y, A.m, 2 * t + 1),
+                                                  xb(A.xch_x, A.n, 2 * t + 2), A.la, fn, rows_x, true,
+                                                  2 * t + 2, f, chk);
       }
       // fixed-order block reduction -> this CTA's slot
 #pragma unroll
@@ -312,7 +614,7 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
         A.duals[n_checks] = tot_s[2] + tot_s[3] - A.eps_d * (tot_s[1] - 1.0);
       }
       ++n_checks;
-      if (err <= A.threshold) {
+      if (err <= A.threshold && A.probe == 0) {
         converged = 1;
         break;
       }
@@ -352,7 +654,10 @@ bool small_solve_fits(int64_t n, int64_t m, int d) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  return coop && small::smem_bytes((int)n, (int)m, nv) + 4096 <= (size_t)max_smem;
+  const int64_t per_cta = 16LL * num_sms() * small::KMAX;  // row-chunk variant: chunks per CTA
+  if (n > per_cta || m > per_cta) return false;
+  // static shared memory: the per-role row state (<= 10 KB) + reductions
+  return coop && small::smem_bytes((int)n, (int)m, nv) + 16384 <= (size_t)max_smem;
 }
 
 int small_solve_launch(const small::Args &A, bool same, bool eucl, cudaStream_t st) {
@@ -360,13 +665,17 @@ int small_solve_launch(const small::Args &A, bool same, bool eucl, cudaStream_t 
   const int nv = (A.d + 1 + 3) / 4;
   const size_t smem = smem_bytes(A.n, A.m, nv);
   void *kern = nullptr;
-  if (eucl) {
-    if (nv == 1) kern = same ? (void *)solve_small_kernel<1, true, true> : (void *)solve_small_kernel<1, false, true>;
-    else kern = same ? (void *)solve_small_kernel<2, true, true> : (void *)solve_small_kernel<2, false, true>;
-  } else {
-    if (nv == 1) kern = same ? (void *)solve_small_kernel<1, true, false> : (void *)solve_small_kernel<1, false, false>;
-    else kern = same ? (void *)solve_small_kernel<2, true, false> : (void *)solve_small_kernel<2, false, false>;
-  }
+  const int key = (nv == 2) * 8 + same * 4 + eucl * 2 + (A.variant == 1);
+#define OTK_SMALL_K(NV_, SA_, EU_, V1_) (void *)solve_small_kernel<NV_, SA_, EU_, V1_>
+  void *const table[16] = {
+      OTK_SMALL_K(1, false, false, 0), OTK_SMALL_K(1, false, false, 1), OTK_SMALL_K(1, false, true, 0),
+      OTK_SMALL_K(1, false, true, 1),  OTK_SMALL_K(1, true, false, 0),  OTK_SMALL_K(1, true, false, 1),
+      OTK_SMALL_K(1, true, true, 0),   OTK_SMALL_K(1, true, true, 1),   OTK_SMALL_K(2, false, false, 0),
+      OTK_SMALL_K(2, false, false, 1), OTK_SMALL_K(2, false, true, 0),  OTK_SMALL_K(2, false, true, 1),
+      OTK_SMALL_K(2, true, false, 0),  OTK_SMALL_K(2, true, false, 1),  OTK_SMALL_K(2, true, true, 0),
+      OTK_SMALL_K(2, true, true, 1)};
+#undef OTK_SMALL_K
+  kern = table[key];
   OTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   OTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
