@@ -19,6 +19,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <cstdio>
 #include <cstdlib>
 #include <climits>
 #include <cstring>
@@ -39,21 +40,22 @@ bool tc_available();
 int tc_tile_cols(int dpad);
 int tc_uses_pair(int dpad);
 namespace small {
-struct Args {
+struct Args {  // solve_small.cu
   const float *x, *y, *a, *b, *la, *lb, *g_init;
   int n, m, d;
   float eps, kappa;
   double eps_d, threshold;
   int max_iters, inner_iters, max_checks;
-  float *f0, *f1, *g, *bias_x, *bias_y, *f_out, *g_out;
+  float *f0, *f1, *g, *f_out, *g_out;
   double *slots;
-  int *first_bad;
   double *errors, *duals;
   int *state;
   int probe;
   unsigned long long *xch_x, *xch_y;
-  int variant;
+  unsigned long long *trace;
+  int trace_steps;
 };
+constexpr int SLOT = 10;
 }  // namespace small
 bool small_solve_fits(int64_t n, int64_t m, int d);
 int small_solve_launch(const small::Args &A, bool same, bool eucl, cudaStream_t st);
@@ -315,7 +317,7 @@ Layout plan(const otk_solve_args *A, void *ws) {
   L.chk_ws = c.take<char>(otk_check_workspace_bytes());
   L.first_bad = c.take<int>(1);
   if (L.small) {
-    L.slots = c.take<double>((size_t)num_sms() * 8);
+    L.slots = c.take<double>((size_t)2 * num_sms() * small::SLOT);
     L.d_errors = c.take<double>(A->max_checks);
     L.d_duals = c.take<double>(A->max_checks);
     L.state = c.take<int>(8);
@@ -433,21 +435,32 @@ static int solve_small(otk_solve_args *A, Layout &L, cudaStream_t st) {
   S.f0 = L.fA;
   S.f1 = L.fB;
   S.g = L.g;
-  S.bias_x = L.bias_x;
-  S.bias_y = L.bias_y;
   S.f_out = A->f_out;
   S.g_out = A->g_out;
   S.slots = L.slots;
-  S.first_bad = L.first_bad;
   S.errors = L.d_errors;
   S.duals = L.d_duals;
   S.state = L.state;
   S.probe = getenv("OTK_SMALL_PROBE") ? atoi(getenv("OTK_SMALL_PROBE")) : 0;
   S.xch_x = L.xch;
   S.xch_y = L.xch + 2 * A->n;
-  S.variant = getenv("OTK_SMALL_V1") ? atoi(getenv("OTK_SMALL_V1")) : 0;
-  OTK_CUDA(cudaMemsetAsync(L.first_bad, 0x7f, sizeof(int), st));
+  const char *trace_path = getenv("OTK_SMALL_TRACE");  // diagnostics: per-CTA phase stamps
+  if (trace_path) {
+    S.trace_steps = 64;
+    OTK_CUDA(cudaMalloc(&S.trace, (size_t)S.trace_steps * num_sms() * 8 * sizeof(unsigned long long)));
+    OTK_CUDA(cudaMemsetAsync(S.trace, 0, (size_t)S.trace_steps * num_sms() * 8 * sizeof(unsigned long long), st));
+  }
   OTK_TRY(small_solve_launch(S, A->same_points != 0, (A->flags & OTK_COST_EUCL) != 0, st));
+  if (trace_path) {
+    std::vector<unsigned long long> h((size_t)S.trace_steps * num_sms() * 8);
+    OTK_CUDA(cudaMemcpyAsync(h.data(), S.trace, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost, st));
+    OTK_CUDA(cudaStreamSynchronize(st));
+    cudaFree(S.trace);
+    if (FILE *fp = fopen(trace_path, "wb")) {
+      fwrite(h.data(), sizeof(h[0]), h.size(), fp);
+      fclose(fp);
+    }
+  }
   int state[8];
   OTK_CUDA(cudaMemcpyAsync(state, L.state, 5 * sizeof(int), cudaMemcpyDeviceToHost, st));
   OTK_CUDA(cudaStreamSynchronize(st));

@@ -1,27 +1,28 @@
 // K1p -- the whole Sinkhorn solve of a SMALL point-cloud problem in ONE
-// persistent cooperative kernel (one CTA per SM, grid-wide barriers between
-// half-steps).  Replaces the reference loop sinkhorn._sinkhorn_iterations
-// (reference sinkhorn.py:151-200) with apply_lse_kernel (geometry.py:336-354)
-// for problems whose points fit in shared memory (BASELINE configs[0]:
-// 2048^2, d = 3), where a launch per half-step costs more than the math.
+// persistent cooperative kernel (one CTA per SM).  Replaces the reference loop
+// sinkhorn._sinkhorn_iterations (reference sinkhorn.py:151-200) with
+// apply_lse_kernel (geometry.py:336-354) for problems whose points fit in
+// shared memory (BASELINE configs[0]: 2048^2, d = 3), where a launch -- or a
+// grid barrier -- per half-step costs more than the math.
 //
 // Every CTA keeps both point sets resident in shared memory as NV float4 per
-// point: coordinates, then -kappa*|q|^2 in slot d, zeros after.  A half-step
-// gives each warp R = 2 rows; a row's query vector p' = (2 kappa p, 1, 0..)
-// turns one dot product into 2 kappa <p,q> - kappa |q|^2, clamped at
-// kappa |p|^2 (C >= 0, geometry.py:273) and shifted by the column's
-// kappa * potential.  Lanes stride the columns with an online log2-sum-exp2
-// and merge in a fixed butterfly order: deterministic.
+// point: coordinates, then -kappa*|q|^2 in slot d, zeros after.  A row's query
+// vector p' = (2 kappa p, 1, 0..) turns one dot product into
+// 2 kappa <p,q> - kappa |q|^2, clamped at kappa |p|^2 (C >= 0,
+// geometry.py:273) and shifted by the column's kappa * potential.
 //
-// The fused check (sinkhorn.py:175-189) runs inside the f_{t+1} half-step:
-// r_i = a_i exp((f_t,i - f_{t+1},i)/eps); every CTA writes 8 partial sums,
-// and after the barrier EVERY CTA adds all CTAs' slots in the same order, so
-// all CTAs take the same converged / diverged decision (one more barrier
-// keeps the first-bad marker stable while every CTA reads it).
+// Half-steps (below) exchange their outputs through tagged 64-bit words, with
+// no grid barrier.  The fused check (sinkhorn.py:175-189) runs inside the
+// f_{t+1} half-step: r_i = a_i exp((f_t,i - f_{t+1},i)/eps); each CTA
+// writes its 8 partial sums and the first half-step at which it produced a
+// NaN/+inf potential into a slot (double-buffered by check parity), and after
+// ONE grid barrier EVERY CTA adds all CTAs' slots in the same order, so all
+// take the same converged / diverged decision.
 // Constant-eps schedules only (the general loop is solve.cu).
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <climits>
 
 #include "otk_common.cuh"
 
@@ -32,9 +33,9 @@ namespace small {
 
 constexpr int THREADS = 512;
 constexpr int WARPS = THREADS / 32;
-constexpr int R = 2;     // rows per warp (register reuse of every column load)
-constexpr int CB = 8;    // columns per lane batch (online-update granularity)
 constexpr int NVALS = 8;
+constexpr int SLOT = 10;  // doubles per CTA check slot: 8 sums, first bad half-step, pad
+constexpr int MAX_GRID = 160;  // CTAs (one per SM)
 
 struct Args {
   const float *x, *y, *a, *b, *la, *lb, *g_init;
@@ -42,16 +43,24 @@ struct Args {
   float eps, kappa;          // float32 eps and kappa = log2(e)/eps
   double eps_d, threshold;
   int max_iters, inner_iters, max_checks;
-  float *f0, *f1, *g, *bias_x, *bias_y, *f_out, *g_out;
-  double *slots;             // [gridDim][8]
-  int *first_bad;
+  float *f0, *f1, *g, *f_out, *g_out;
+  double *slots;             // [2][gridDim][SLOT] check slots (by check parity)
   double *errors, *duals;    // [max_checks]
   int *state;                // n_checks, iterations, converged, status, fail_iter
-  int probe;                 // timing probe (OTK_SMALL_PROBE): 1 = skip the half-step math, 2 = skip the
-                             // passes over the cells (row-chunk variant); probes never converge
-  unsigned long long *xch_x, *xch_y;  // row-chunk exchange words, 2 buffers per role ([2n], [2m])
-  int variant;               // 0 = row-chunk half-step (default), 1 = column-sliced (OTK_SMALL_V1)
+  int probe;                 // timing probe (OTK_SMALL_PROBE): skip the passes over the cells;
+                             // a probe never converges
+  unsigned long long *xch_x, *xch_y;  // exchange words, 2 buffers per role ([2n], [2m])
+  unsigned long long *trace; // OTK_SMALL_TRACE: globaltimer stamps [trace_steps][grid][8] (thread 0)
+  int trace_steps;
 };
+
+__device__ __forceinline__ void trace_mark(const Args &A, int step, int k) {
+  if (A.trace && threadIdx.x == 0 && step < A.trace_steps) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    A.trace[((size_t)step * gridDim.x + blockIdx.x) * 8 + k] = t;
+  }
+}
 
 __device__ __forceinline__ void load_points(const float *src, int count, int d, float kappa,
                                             float4 *dst, int nv) {
@@ -69,151 +78,7 @@ __device__ __forceinline__ void load_points(const float *src, int count, int d, 
   }
 }
 
-template <int NV>
-__device__ __forceinline__ float dot_q(const float (&p)[4 * NV], const float4 *q) {
-  float4 q0 = q[0];
-  float acc = p[0] * q0.x;
-  acc = fmaf(p[1], q0.y, acc);
-  acc = fmaf(p[2], q0.z, acc);
-  acc = fmaf(p[3], q0.w, acc);
-  if (NV == 2) {
-    float4 q1 = q[1];
-    acc = fmaf(p[4], q1.x, acc);
-    acc = fmaf(p[5], q1.y, acc);
-    acc = fmaf(p[6], q1.z, acc);
-    acc = fmaf(p[7], q1.w, acc);
-  }
-  return acc;
-}
-
-// One half-step over rows P (np) against columns Q (nq) whose kappa*potential
-// is qbias (already in shared memory).  Writes out_pot = eps*logw - eps*ln2*L
-// and out_bias = kappa*out_pot for the next half-step; bad outputs mark step.
-// With CHECK, also accumulates the 8 check values of the rows handled here
-// (f_prev = the previous f, a = weights).
-//
-// Work split: a CTA round covers PAIRS = WARPS/SL row pairs; the SL warps of
-// a pair each take one contiguous slice of the columns (lanes stride it), so
-// even a 2048-row problem keeps 16 warps per SM busy.  The slices' (max, sum)
-// meet in shared memory and merge in slice order (deterministic).
-constexpr int SL = 4;
-constexpr int PAIRS = WARPS / SL;
-
-template <int NV, bool SAME, bool CHECK, bool EU>
-__device__ void half_step(const Args &A, const float4 *P, int np, const float4 *Q, int nq,
-                          const float *qbias, const float *logw, float *out_pot, float *out_bias,
-                          int step, const float *f_prev, double (&chk)[NVALS]) {
-  __shared__ float part[PAIRS][R][SL][2];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int pair = warp / SL, slice = warp % SL;
-  const int per = (nq + SL - 1) / SL;
-  const int c_lo = slice * per, c_hi = min(nq, c_lo + per);
-  const float two_k = 2.f * A.kappa;
-  const float sk = sqrtf(A.kappa);
-  const int n_pairs = (A.probe == 1) ? 0 : (np + R - 1) / R;
-  for (int base = blockIdx.x * PAIRS; base < n_pairs; base += gridDim.x * PAIRS) {
-    const int r0 = (base + pair) * R;
-    const bool live = r0 < np;
-    float p[R][4 * NV], cp[R];
-    float mx[R], sm[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = min(r0 + r, np - 1);
-      const float *pv = reinterpret_cast<const float *>(P + i * NV);
-#pragma unroll
-      for (int k = 0; k < 4 * NV; ++k) p[r][k] = (k < A.d) ? two_k * pv[k] : (k == A.d ? 1.f : 0.f);
-      cp[r] = -pv[A.d];  // kappa |p|^2
-      mx[r] = -INFINITY;
-      sm[r] = 0.f;
-    }
-    if (live) {
-      for (int j0 = c_lo + lane; j0 < c_hi; j0 += 32 * CB) {
-        float u[CB][R];
-#pragma unroll
-        for (int c = 0; c < CB; ++c) {
-          const int j = j0 + 32 * c;
-          if (j < c_hi) {
-            const float bj = qbias[j];
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              float v;
-              if (EU) {  // kappa sqrt(C) = sqrt(kappa) sqrt(kappa C), kappa C = cp - dot
-                v = -sk * sqrt_approx(fmaxf(cp[r] - dot_q<NV>(p[r], Q + j * NV), 0.f));
-                if (SAME && j == r0 + r) v = 0.f;
-              } else {
-                v = fminf(dot_q<NV>(p[r], Q + j * NV), cp[r]);
-                if (SAME && j == r0 + r) v = cp[r];
-              }
-              u[c][r] = v + bj;
-            }
-          } else {
-#pragma unroll
-            for (int r = 0; r < R; ++r) u[c][r] = -INFINITY;
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          float cm = -INFINITY;
-#pragma unroll
-          for (int c = 0; c < CB; ++c) cm = fmaxf(cm, u[c][r]);
-          if (cm > mx[r] + 8.f) {
-            sm[r] *= ex2(mx[r] - cm);
-            mx[r] = cm;
-          }
-          const float ms = (mx[r] == -INFINITY) ? 0.f : mx[r];
-          float acc = 0.f;
-#pragma unroll
-          for (int c = 0; c < CB; ++c) acc += ex2(u[c][r] - ms);
-          sm[r] += acc;
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      Lse2 st;
-      st.m = mx[r];
-      st.s = sm[r];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float m2 = __shfl_xor_sync(0xffffffffu, st.m, o);
-        const float s2 = __shfl_xor_sync(0xffffffffu, st.s, o);
-        st.merge(m2, s2);
-      }
-      if (lane == 0) {
-        part[pair][r][slice][0] = st.m;
-        part[pair][r][slice][1] = st.s;
-      }
-    }
-    __syncthreads();
-    if (slice == 0 && lane < R) {
-      const int r = lane, i = r0 + r;
-      if (i < np) {
-        Lse2 st;
-        st.m = part[pair][r][0][0];
-        st.s = part[pair][r][0][1];
-#pragma unroll
-        for (int q = 1; q < SL; ++q) st.merge(part[pair][r][q][0], part[pair][r][q][1]);
-        const float L = st.value() - (EU ? 0.f : -reinterpret_cast<const float *>(P + i * NV)[A.d]);
-        const float v = A.eps * logw[i] - A.eps * kLn2 * L;
-        out_pot[i] = v;
-        out_bias[i] = v * A.kappa;
-        if (bad_potential(v)) atomicMin(A.first_bad, step);
-        if (CHECK) {
-          const double fp = f_prev[i], ai = A.a[i];
-          const double rr = (ai > 0.0) ? ai * exp((fp - (double)v) / A.eps_d) : 0.0;
-          chk[0] += fabs(rr - ai);
-          chk[1] += rr;
-          if (ai > 0.0) chk[2] += ai * fp;
-          chk[4] += (fp != fp) ? 1.0 : 0.0;
-          chk[6] += (fp == INFINITY) ? 1.0 : 0.0;
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// ---- row-chunk half-step (default) ----
+// ---- half-step ----
 //
 // A CTA takes a chunk of RC <= 16 consecutive rows (rc = ceil(np / grid) rows
 // when that is <= 16, so a 2048-row half-step is one chunk per SM) and ALL its
@@ -283,20 +148,56 @@ __device__ __forceinline__ int rs16_row(int lane) {
   return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
 }
 
+// Per-role state a CTA keeps for the rows it owns (chunks blockIdx.x + k*G,
+// RC slots each): p' = (2 kappa p, 1, 0..) stored per ROW PAIR (component k of
+// rows 2h and 2h+1 side by side, so packed FFMA2 takes the pair from one
+// shared-memory load and the column coordinate as a broadcast scalar),
+// kappa |p|^2 and the anchor / shift of every row.
+template <int NV>
+struct RoleRows {
+  float2 p2[KMAX * RC / 2][4 * NV];
+  float cp[KMAX * RC];
+  float an[KMAX * RC];
+};
+
+template <int NV>
+__device__ void init_role_rows(const Args &A, const float4 *P, int np, RoleRows<NV> &S) {
+  const int G = gridDim.x;
+  const int rc = min(RC, (np + G - 1) / G);
+  const int n_chunks = (np + rc - 1) / rc;
+  const float two_k = 2.f * A.kappa;
+  for (int idx = threadIdx.x; idx < KMAX * RC; idx += blockDim.x) {
+    const int k = idx / RC, r = idx % RC;
+    const int ch = blockIdx.x + k * G;
+    const int i = min(ch * rc + r, np - 1);  // slots past the chunk repeat a real row (finite)
+    if (ch >= n_chunks) continue;
+    const float *pv = reinterpret_cast<const float *>(P + i * NV);
+    float *dst = reinterpret_cast<float *>(S.p2[idx / 2]) + (idx & 1);
+#pragma unroll
+    for (int kk = 0; kk < 4 * NV; ++kk) dst[2 * kk] = (kk < A.d) ? two_k * pv[kk] : (kk == A.d ? 1.f : 0.f);
+    S.cp[idx] = -pv[A.d];
+    S.an[idx] = -INFINITY;
+  }
+}
+
 // One pass over the chunk's rc rows and all nq columns: per row the max of
 // u_ij (MAXP) or sum_j 2^(u_ij - shift_r).  Result for row r in tot[r].
 // Column j's kappa * potential comes from its exchange word (tag `need`).
+// Cells of a row pair run in packed FFMA2 / FADD2, with b_j folded into the
+// norm slot of q (q_d = b_j - kappa |q|^2) and the chain started at -shift:
+//   u = min(<p', q> - shift, kappa |p|^2 + b_j - shift)   (the C >= 0 clamp)
 template <int NV, bool SAME, bool EU, bool MAXP>
 __device__ __forceinline__ void chunk_pass(const Args &A, const float4 *Q, int nq, const xword *qx,
-                                           int need, int r0, int rc, const float4 (*prow)[NV],
-                                           const float2 *rowc, float (*red)[RC], float *tot) {
+                                           int need, int r0, int rc, const float2 (*p2)[4 * NV],
+                                           const float *cp, const float *sh, float (*red)[RC],
+                                           float *tot) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float sk = sqrtf(A.kappa);
-  float acc[RC];
+  float2 acc[RC / 2];
 #pragma unroll
-  for (int r = 0; r < RC; ++r) acc[r] = MAXP ? -INFINITY : 0.f;
+  for (int h = 0; h < RC / 2; ++h) acc[h] = MAXP ? make_float2(-INFINITY, -INFINITY) : make_float2(0.f, 0.f);
   for (int j0 = threadIdx.x; j0 < nq; j0 += THREADS * CPT) {
-    float4 q[CPT][NV];
+    float q[CPT][4 * NV];
     float bj[CPT];
     int jj[CPT];
     xword w[CPT];
@@ -316,46 +217,76 @@ __device__ __forceinline__ void chunk_pass(const Args &A, const float4 *Q, int n
       for (int c = 0; c < CPT; ++c)
         if ((int)(w[c] >> 32) != need) w[c] = ld_relaxed(qx + jj[c]);
     }
+    if (!MAXP) trace_mark(A, need + 1, 1);
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       const bool ok = jj[c] < nq;
 #pragma unroll
-      for (int v = 0; v < NV; ++v) q[c][v] = ok ? Q[jj[c] * NV + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int v = 0; v < NV; ++v) {
+        const float4 qv = ok ? Q[jj[c] * NV + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+        q[c][4 * v] = qv.x;
+        q[c][4 * v + 1] = qv.y;
+        q[c][4 * v + 2] = qv.z;
+        q[c][4 * v + 3] = qv.w;
+      }
       bj[c] = __uint_as_float((unsigned)w[c]);
+      if (!EU) {  // fold kappa * potential into the norm slot: <p', q> = 2k<p,q> - k|q|^2 + b_j
+#pragma unroll
+        for (int k = 0; k < 4 * NV; ++k) q[c][k] = q[c][k] + (k == A.d ? bj[c] : 0.f);
+      }
     }
 #pragma unroll
-    for (int r = 0; r < RC; ++r) {
-      if (r < rc) {
-        asm volatile("" ::: "memory");  // re-read the row from shared memory (no hoisting of 16 rows)
-        float p[4 * NV];
+    for (int h = 0; h < RC / 2; ++h) {
+      if (2 * h < rc) {
+        asm volatile("" ::: "memory");  // re-read the rows from shared memory (no hoisting of 16 rows)
+        float2 pk[4 * NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const float4 pv = prow[r][v];
-          p[4 * v] = pv.x;
-          p[4 * v + 1] = pv.y;
-          p[4 * v + 2] = pv.z;
-          p[4 * v + 3] = pv.w;
-        }
-        const float2 rcw = rowc[r];  // (kappa |p|^2, shift)
-        float e[CPT];
+        for (int k = 0; k < 4 * NV; ++k) pk[k] = p2[h][k];
+        const float2 cp2 = *reinterpret_cast<const float2 *>(cp + 2 * h);
+        const float2 ns2 = MAXP ? make_float2(0.f, 0.f) : make_float2(-sh[2 * h], -sh[2 * h + 1]);
+        const float2 cpns = __fadd2_rn(cp2, ns2);
+        float2 e[CPT];
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
-          float v;
-          if (EU) {
-            v = -sk * sqrt_approx(fmaxf(rcw.x - dot_q<NV>(p, q[c]), 0.f));
-            if (SAME && jj[c] == r0 + r) v = 0.f;
+          float2 u;
+          if (EU) {  // kappa sqrt(C) = sqrt(kappa) sqrt(kappa C), kappa C = cp - dot
+            const float2 bs = __fadd2_rn(ns2, make_float2(bj[c], bj[c]));
+            float2 dt = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < 4 * NV; ++k) dt = __ffma2_rn(pk[k], make_float2(q[c][k], q[c][k]), dt);
+            float v0 = -sk * sqrt_approx(fmaxf(cp2.x - dt.x, 0.f));
+            float v1 = -sk * sqrt_approx(fmaxf(cp2.y - dt.y, 0.f));
+            if (SAME && jj[c] == r0 + 2 * h) v0 = 0.f;
+            if (SAME && jj[c] == r0 + 2 * h + 1) v1 = 0.f;
+            u = __fadd2_rn(make_float2(v0, v1), bs);
           } else {
-            v = fminf(dot_q<NV>(p, q[c]), rcw.x);
-            if (SAME && jj[c] == r0 + r) v = rcw.x;
+            float2 dt = ns2;  // b_j is in the norm slot of q
+#pragma unroll
+            for (int k = 0; k < 4 * NV; ++k) dt = __ffma2_rn(pk[k], make_float2(q[c][k], q[c][k]), dt);
+            const float2 lim = __fadd2_rn(cpns, make_float2(bj[c], bj[c]));
+            u = make_float2(fminf(dt.x, lim.x), fminf(dt.y, lim.y));
+            if (SAME && jj[c] == r0 + 2 * h) u.x = lim.x;
+            if (SAME && jj[c] == r0 + 2 * h + 1) u.y = lim.y;
           }
-          e[c] = MAXP ? v + bj[c] : ex2(v + (bj[c] - rcw.y));
+          e[c] = MAXP ? u : make_float2(ex2(u.x), ex2(u.y));
         }
-        if (MAXP) acc[r] = fmaxf(acc[r], fmaxf(fmaxf(e[0], e[1]), fmaxf(e[2], e[3])));
-        else acc[r] += (e[0] + e[1]) + (e[2] + e[3]);
+        if (MAXP) {
+          acc[h].x = fmaxf(acc[h].x, fmaxf(fmaxf(e[0].x, e[1].x), fmaxf(e[2].x, e[3].x)));
+          acc[h].y = fmaxf(acc[h].y, fmaxf(fmaxf(e[0].y, e[1].y), fmaxf(e[2].y, e[3].y)));
+        } else {
+          acc[h] = __fadd2_rn(acc[h], __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3])));
+        }
       }
     }
   }
-  const float v = rs16<MAXP>(acc, lane);
+  if (!MAXP) trace_mark(A, need + 1, 2);
+  float v16[RC];
+#pragma unroll
+  for (int h = 0; h < RC / 2; ++h) {
+    v16[2 * h] = acc[h].x;
+    v16[2 * h + 1] = acc[h].y;
+  }
+  const float v = rs16<MAXP>(v16, lane);
   if (!(lane & 1)) red[warp][rs16_row(lane)] = v;
   __syncthreads();
   if (threadIdx.x < rc) {
@@ -365,34 +296,7 @@ __device__ __forceinline__ void chunk_pass(const Args &A, const float4 *Q, int n
     tot[threadIdx.x] = t;
   }
   __syncthreads();
-}
-
-// Per-role state a CTA keeps for the rows it owns (chunks blockIdx.x + k*G).
-template <int NV>
-struct RoleRows {
-  float4 prow[KMAX * RC][NV];  // p' = (2 kappa p, 1, 0..)
-  float2 rowc[KMAX * RC];      // (kappa |p|^2, anchor)
-};
-
-template <int NV>
-__device__ void init_role_rows(const Args &A, const float4 *P, int np, RoleRows<NV> &S) {
-  const int G = gridDim.x;
-  const int rc = min(RC, (np + G - 1) / G);
-  const int n_chunks = (np + rc - 1) / rc;
-  const float two_k = 2.f * A.kappa;
-  for (int idx = threadIdx.x; idx < KMAX * RC; idx += blockDim.x) {
-    const int k = idx / RC, r = idx % RC;
-    const int ch = blockIdx.x + k * G;
-    const int i = min(ch * rc + r, np - 1);
-    if (ch >= n_chunks) continue;
-    const float *pv = reinterpret_cast<const float *>(P + i * NV);
-    float p[4 * NV];
-#pragma unroll
-    for (int kk = 0; kk < 4 * NV; ++kk) p[kk] = (kk < A.d) ? two_k * pv[kk] : (kk == A.d ? 1.f : 0.f);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) S.prow[idx][v] = make_float4(p[4 * v], p[4 * v + 1], p[4 * v + 2], p[4 * v + 3]);
-    S.rowc[idx] = make_float2(-pv[A.d], -INFINITY);
-  }
+  if (!MAXP) trace_mark(A, need + 1, 3);
 }
 
 // One half-step of a role: rows P (np) against the columns' exchange words
@@ -403,7 +307,7 @@ template <int NV, bool SAME, bool CHECK, bool CHECKG, bool EU>
 __device__ void half_step_rows(const Args &A, const float4 *P, int np, const float4 *Q, int nq,
                                const xword *qx, xword *px, const float *logw, float *out_pot,
                                RoleRows<NV> &S, bool anchored, int step, const float *f_prev,
-                               double (&chk)[NVALS]) {
+                               double (&chk)[NVALS], int *bad_s) {
   static_assert(CPT == 4, "chunk_pass folds 4 columns per group");
   __shared__ float red[WARPS][RC];
   __shared__ float tot[RC];
@@ -415,43 +319,45 @@ __device__ void half_step_rows(const Args &A, const float4 *P, int np, const flo
   const int need = step - 1;
   for (int ch = blockIdx.x, k = 0; ch < n_chunks; ch += G, ++k) {
     const int r0 = ch * rc, rn = min(rc, np - r0);
-    const float4 (*prow)[NV] = S.prow + k * RC;
-    float2 *rowc = S.rowc + k * RC;
+    trace_mark(A, step, 0);
+    const float2 (*p2)[4 * NV] = S.p2 + k * (RC / 2);
+    const float *cp = S.cp + k * RC;
+    float *an = S.an + k * RC;
     if (threadIdx.x == 0) redo = 0;
     __syncthreads();
-    if (threadIdx.x < rn && !(anchored && fabsf(rowc[threadIdx.x].y) <= 3.0e38f)) redo = 1;
+    if (threadIdx.x < rn && !(anchored && fabsf(an[threadIdx.x]) <= 3.0e38f)) redo = 1;
     __syncthreads();
     float L = 0.f;  // log2 sum (before the -kappa|p|^2 shift), row threadIdx.x
     if (A.probe != 0) {  // timing probe: everything but the passes over the cells
-      if (threadIdx.x < rn) L = rowc[threadIdx.x].x;
+      if (threadIdx.x < rn) L = cp[threadIdx.x];
     } else if (!redo) {
-      chunk_pass<NV, SAME, EU, false>(A, Q, nq, qx, need, r0, rn, prow, rowc, red, tot);
+      chunk_pass<NV, SAME, EU, false>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
       if (threadIdx.x < rn) {
-        const float an = rowc[threadIdx.x].y;
-        L = an + lg2(tot[threadIdx.x]);
-        const float dl = L - an;
+        const float a0 = an[threadIdx.x];
+        L = a0 + lg2(tot[threadIdx.x]);
+        const float dl = L - a0;
         if (!(L != L) && !(dl >= lo && dl <= 120.f)) redo = 1;
       }
       __syncthreads();
     }
     if (redo && A.probe == 0) {  // exact: row maxima, then the sum against them
-      chunk_pass<NV, SAME, EU, true>(A, Q, nq, qx, need, r0, rn, prow, rowc, red, tot);
+      chunk_pass<NV, SAME, EU, true>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
       if (threadIdx.x < rn) {
         const float mx = tot[threadIdx.x];
-        rowc[threadIdx.x].y = (mx == -INFINITY) ? 0.f : mx;  // all -inf -> sum 0 -> -inf; NaN survives
+        an[threadIdx.x] = (mx == -INFINITY) ? 0.f : mx;  // all -inf -> sum 0 -> -inf; NaN survives
       }
       __syncthreads();
-      chunk_pass<NV, SAME, EU, false>(A, Q, nq, qx, need, r0, rn, prow, rowc, red, tot);
-      if (threadIdx.x < rn) L = rowc[threadIdx.x].y + lg2(tot[threadIdx.x]);
+      chunk_pass<NV, SAME, EU, false>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
+      if (threadIdx.x < rn) L = an[threadIdx.x] + lg2(tot[threadIdx.x]);
     }
     if (threadIdx.x < rn) {
       const int i = r0 + threadIdx.x;
-      const float Lf = L - (EU ? 0.f : rowc[threadIdx.x].x);
-      rowc[threadIdx.x].y = L;
+      const float Lf = L - (EU ? 0.f : cp[threadIdx.x]);
+      an[threadIdx.x] = L;
       const float v = A.eps * logw[i] - A.eps * kLn2 * Lf;
       st_relaxed(px + i, xpack(v * A.kappa, step));
       out_pot[i] = v;
-      if (bad_potential(v)) atomicMin(A.first_bad, step);
+      if (bad_potential(v)) atomicMin(bad_s, step);
       if (CHECK) {
         const double fp = f_prev[i], ai = A.a[i];
         const double rr = (ai > 0.0) ? ai * exp((fp - (double)v) / A.eps_d) : 0.0;
@@ -469,52 +375,45 @@ __device__ void half_step_rows(const Args &A, const float4 *P, int np, const flo
       }
     }
     __syncthreads();
+    trace_mark(A, step, 4);
   }
 }
 
-__device__ void load_bias(float *dst, const float *src, int count) {
-  for (int j = threadIdx.x; j < count; j += blockDim.x) dst[j] = src[j];
-}
-
-template <int NV, bool SAME, bool EU, int V1>
+template <int NV, bool SAME, bool EU>
 __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ float4 sh4[];
   float4 *xs = sh4;
   float4 *ys = xs + A.n * NV;
-  float *bias_s = reinterpret_cast<float *>(ys + A.m * NV);
+  __shared__ RoleRows<NV> rows_x, rows_y;
   __shared__ double red[NVALS][WARPS];
   __shared__ double tot_s[NVALS];
+  __shared__ int bad_s, bad_all;
+  __shared__ double slot_s[MAX_GRID][NVALS + 1];
+  const int G = gridDim.x;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = G * blockDim.x;
 
+  if (threadIdx.x == 0) bad_s = INT_MAX;
   load_points(A.x, A.n, A.d, A.kappa, xs, NV);
   load_points(A.y, A.m, A.d, A.kappa, ys, NV);
-  // initial g and its bias (h = 1 marks a bad warm start); the row-chunk
-  // variant publishes it as the y-words of half-step 1 and clears every other
-  // exchange word (a previous solve's tags must not match)
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.m; j += gridDim.x * blockDim.x) {
+  __syncthreads();
+  // initial g, published as the y-words of half-step 1; every other exchange
+  // word is cleared (a previous solve's tags must not match)
+  for (int j = gtid; j < A.m; j += gstride) {
     const float g0 = A.g_init ? A.g_init[j] : 0.f;
     A.g[j] = g0;
-    A.bias_y[j] = g0 * A.kappa;
-    if (!V1) {
-      A.xch_y[j] = xpack(g0 * A.kappa, 1);
-      A.xch_y[A.m + j] = xpack(0.f, -1);
-    }
-    if (bad_potential(g0)) atomicMin(A.first_bad, 1);
+    A.xch_y[j] = xpack(g0 * A.kappa, 1);
+    A.xch_y[A.m + j] = xpack(0.f, -1);
+    if (bad_potential(g0)) atomicMin(&bad_s, 1);  // a bad warm start
   }
-  if (!V1)
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * A.n; i += gridDim.x * blockDim.x)
-      A.xch_x[i] = xpack(0.f, -1);
-  __shared__ RoleRows<NV> rows_x, rows_y;
-  if (!V1) {
-    __syncthreads();
-    init_role_rows<NV>(A, xs, A.n, rows_x);
-    init_role_rows<NV>(A, ys, A.m, rows_y);
-  }
+  for (int i = gtid; i < 2 * A.n; i += gstride) A.xch_x[i] = xpack(0.f, -1);
+  init_role_rows<NV>(A, xs, A.n, rows_x);
+  init_role_rows<NV>(A, ys, A.m, rows_y);
   __syncthreads();
   grid.sync();
 
   // exchange buffer of the words tagged T: (T >> 1) & 1
-  auto xb = [&](unsigned long long *base, int len, int tag) { return base + ((tag >> 1) & 1) * (size_t)len; };
+  auto xb = [](xword *base, int len, int tag) { return base + ((tag >> 1) & 1) * (size_t)len; };
   float *f = A.f0, *fn = A.f1;
   bool f_ready = false;
   int n_checks = 0, status = OTK_OK, fail_iter = 0, converged = 0, t;
@@ -523,114 +422,106 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
     const bool check = (t % A.inner_iters == 0 || t == A.max_iters);
 #pragma unroll
     for (int k = 0; k < NVALS; ++k) chk[k] = 0.0;
-    if (!f_ready) {
-      if (V1) {
-        load_bias(bias_s, A.bias_y, A.m);
-        __syncthreads();
-        half_step<NV, SAME, false, EU>(A, xs, A.n, ys, A.m, bias_s, A.la, f, A.bias_x, 2 * t, nullptr, chk);
-        grid.sync();
-      } else {
-        half_step_rows<NV, SAME, false, false, EU>(A, xs, A.n, ys, A.m, xb(A.xch_y, A.m, 2 * t - 1),
-                                                   xb(A.xch_x, A.n, 2 * t), A.la, f, rows_x, t > 1, 2 * t,
-                                                   nullptr, chk);
-      }
-    }
+    if (!f_ready)
+      half_step_rows<NV, SAME, false, false, EU>(A, xs, A.n, ys, A.m, xb(A.xch_y, A.m, 2 * t - 1),
+                                                 xb(A.xch_x, A.n, 2 * t), A.la, f, rows_x, t > 1, 2 * t,
+                                                 nullptr, chk, &bad_s);
     f_ready = false;
-    if (V1) {
-      load_bias(bias_s, A.bias_x, A.n);
-      __syncthreads();
-      half_step<NV, SAME, false, EU>(A, ys, A.m, xs, A.n, bias_s, A.lb, A.g, A.bias_y, 2 * t + 1, nullptr, chk);
-      grid.sync();
-    } else if (check) {
+    if (check)
       half_step_rows<NV, SAME, false, true, EU>(A, ys, A.m, xs, A.n, xb(A.xch_x, A.n, 2 * t),
                                                 xb(A.xch_y, A.m, 2 * t + 1), A.lb, A.g, rows_y, t > 1,
-                                                2 * t + 1, nullptr, chk);
-    } else {
+                                                2 * t + 1, nullptr, chk, &bad_s);
+    else
       half_step_rows<NV, SAME, false, false, EU>(A, ys, A.m, xs, A.n, xb(A.xch_x, A.n, 2 * t),
                                                  xb(A.xch_y, A.m, 2 * t + 1), A.lb, A.g, rows_y, t > 1,
-                                                 2 * t + 1, nullptr, chk);
+                                                 2 * t + 1, nullptr, chk, &bad_s);
+    if (!check) continue;
+    // f_{t+1} into fn, with the check of (f_t, g_t) fused in
+    half_step_rows<NV, SAME, true, false, EU>(A, xs, A.n, ys, A.m, xb(A.xch_y, A.m, 2 * t + 1),
+                                              xb(A.xch_x, A.n, 2 * t + 2), A.la, fn, rows_x, true,
+                                              2 * t + 2, f, chk, &bad_s);
+    // fixed-order block reduction -> this CTA's slot
+#pragma unroll
+    for (int k = 0; k < NVALS; ++k) {
+      double v = chk[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = v;
     }
-    if (check) {
-      // f_{t+1} into fn, with the check of (f_t, g_t) fused in
-      if (V1) {
-        load_bias(bias_s, A.bias_y, A.m);
-        __syncthreads();
-        half_step<NV, SAME, true, EU>(A, xs, A.n, ys, A.m, bias_s, A.la, fn, A.bias_x, 2 * t + 2, f, chk);
-        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.m; j += gridDim.x * blockDim.x) {
-          const double gj = A.g[j], bj = A.b[j];
-          if (bj > 0.0) chk[3] += bj * gj;
-          chk[5] += (gj != gj) ? 1.0 : 0.0;
-          chk[7] += (gj == INFINITY) ? 1.0 : 0.0;
+    __syncthreads();
+    // slots double-buffered by check parity: a CTA may write the next check's
+    // slot while a slower one still reads this check's
+    double *slots = A.slots + (size_t)(n_checks & 1) * G * SLOT;
+    if (threadIdx.x < NVALS) {
+      double v = 0.0;
+      for (int w = 0; w < WARPS; ++w) v += red[threadIdx.x][w];
+      slots[blockIdx.x * SLOT + threadIdx.x] = v;
+    } else if (threadIdx.x == NVALS) {
+      slots[blockIdx.x * SLOT + NVALS] = (double)bad_s;
+    }
+    grid.sync();
+    // every CTA gathers all slots (one round trip) and reduces them in the
+    // same order -> identical decisions everywhere
+    for (int k = threadIdx.x; k < G; k += blockDim.x) {
+#pragma unroll
+      for (int v = 0; v <= NVALS; ++v) slot_s[k][v] = __ldcg(slots + k * SLOT + v);
+    }
+    __syncthreads();
+    {  // warp v folds value v: lanes stride the slots, then a fixed shuffle tree
+      const int wv = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      if (wv <= NVALS) {
+        const bool mn = wv == NVALS;  // the first bad half-step: a minimum
+        double v = mn ? (double)INT_MAX : 0.0;
+        for (int bk = lane; bk < G; bk += 32) v = mn ? fmin(v, slot_s[bk][wv]) : v + slot_s[bk][wv];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double u = __shfl_xor_sync(0xffffffffu, v, o);
+          v = mn ? fmin(v, u) : v + u;
         }
-      } else {
-        half_step_rows<NV, SAME, true, false, EU>(A, xs, A.n, ys, A.m, xb(A.xch_y, A.m, 2 * t + 1),
-                                                  xb(A.xch_x, A.n, 2 * t + 2), A.la, fn, rows_x, true,
-                                                  2 * t + 2, f, chk);
+        if (lane == 0) {
+          if (mn) bad_all = (int)v;
+          else tot_s[wv] = v;
+        }
       }
-      // fixed-order block reduction -> this CTA's slot
-#pragma unroll
-      for (int k = 0; k < NVALS; ++k) {
-        double v = chk[k];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = v;
-      }
-      __syncthreads();
-      if (threadIdx.x < NVALS) {
-        double v = 0.0;
-        for (int w = 0; w < WARPS; ++w) v += red[threadIdx.x][w];
-        A.slots[blockIdx.x * NVALS + threadIdx.x] = v;
-      }
-      grid.sync();
-      // every CTA reduces all slots in the same order -> identical decisions
-      if (threadIdx.x < NVALS) {
-        double v = 0.0;
-        for (int bk = 0; bk < (int)gridDim.x; ++bk)
-          v += reinterpret_cast<volatile double *>(A.slots)[bk * NVALS + threadIdx.x];
-        tot_s[threadIdx.x] = v;
-      }
-      __syncthreads();
-      const int fb = *reinterpret_cast<volatile int *>(A.first_bad);
-      const double err = tot_s[0];
-      // no CTA may mark first_bad again (next half-step) before all have read it
-      grid.sync();
-      if (fb <= 2 * t) {
-        status = OTK_BAD_POTENTIAL;
-        fail_iter = (fb + 1) / 2;
-        break;
-      }
-      if (tot_s[4] > 0 || tot_s[5] > 0) {
-        status = OTK_DIVERGED;
-        fail_iter = t;
-        break;
-      }
-      if (fb == 2 * t + 1) {
-        status = OTK_BAD_POTENTIAL;
-        fail_iter = t;
-        break;
-      }
-      if (blockIdx.x == 0 && threadIdx.x == 0 && n_checks < A.max_checks) {
-        A.errors[n_checks] = err;
-        A.duals[n_checks] = tot_s[2] + tot_s[3] - A.eps_d * (tot_s[1] - 1.0);
-      }
-      ++n_checks;
-      if (err <= A.threshold && A.probe == 0) {
-        converged = 1;
-        break;
-      }
-      if (t < A.max_iters) {
-        float *tmp = f;
-        f = fn;
-        fn = tmp;
-        f_ready = true;
-      }
+    }
+    __syncthreads();
+    const int fb = bad_all;
+    const double err = tot_s[0];
+    if (fb <= 2 * t) {
+      status = OTK_BAD_POTENTIAL;
+      fail_iter = (fb + 1) / 2;
+      break;
+    }
+    if (tot_s[4] > 0 || tot_s[5] > 0) {
+      status = OTK_DIVERGED;
+      fail_iter = t;
+      break;
+    }
+    if (fb == 2 * t + 1) {
+      status = OTK_BAD_POTENTIAL;
+      fail_iter = t;
+      break;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && n_checks < A.max_checks) {
+      A.errors[n_checks] = err;
+      A.duals[n_checks] = tot_s[2] + tot_s[3] - A.eps_d * (tot_s[1] - 1.0);
+    }
+    ++n_checks;
+    if (err <= A.threshold && A.probe == 0) {
+      converged = 1;
+      break;
+    }
+    if (t < A.max_iters) {
+      float *tmp = f;
+      f = fn;
+      fn = tmp;
+      f_ready = true;
     }
   }
+  grid.sync();  // every CTA's rows of f and g written
   // results (f = f_t of the last completed iteration, g = g_t)
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x)
-    A.f_out[i] = f[i];
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.m; j += gridDim.x * blockDim.x)
-    A.g_out[j] = A.g[j];
+  for (int i = gtid; i < A.n; i += gstride) A.f_out[i] = f[i];
+  for (int j = gtid; j < A.m; j += gstride) A.g_out[j] = A.g[j];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.state[0] = min(n_checks, A.max_checks);
     A.state[1] = min(t, A.max_iters);
@@ -640,9 +531,7 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
   }
 }
 
-size_t smem_bytes(int n, int m, int nv) {
-  return (size_t)(n + m) * nv * sizeof(float4) + (size_t)std::max(n, m) * sizeof(float);
-}
+size_t smem_bytes(int n, int m, int nv) { return (size_t)(n + m) * nv * sizeof(float4); }
 
 }  // namespace small
 
@@ -654,28 +543,24 @@ bool small_solve_fits(int64_t n, int64_t m, int d) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const int64_t per_cta = 16LL * num_sms() * small::KMAX;  // row-chunk variant: chunks per CTA
+  const int64_t per_cta = (int64_t)small::RC * num_sms() * small::KMAX;  // chunks per CTA per role
   if (n > per_cta || m > per_cta) return false;
-  // static shared memory: the per-role row state (<= 10 KB) + reductions
-  return coop && small::smem_bytes((int)n, (int)m, nv) + 16384 <= (size_t)max_smem;
+  if (num_sms() > small::MAX_GRID) return false;
+  // static shared memory: the per-role row state (<= 10 KB), the gathered check slots (12.5 KB)
+  return coop && small::smem_bytes((int)n, (int)m, nv) + 32768 <= (size_t)max_smem;
 }
 
 int small_solve_launch(const small::Args &A, bool same, bool eucl, cudaStream_t st) {
   using namespace small;
   const int nv = (A.d + 1 + 3) / 4;
   const size_t smem = smem_bytes(A.n, A.m, nv);
-  void *kern = nullptr;
-  const int key = (nv == 2) * 8 + same * 4 + eucl * 2 + (A.variant == 1);
-#define OTK_SMALL_K(NV_, SA_, EU_, V1_) (void *)solve_small_kernel<NV_, SA_, EU_, V1_>
-  void *const table[16] = {
-      OTK_SMALL_K(1, false, false, 0), OTK_SMALL_K(1, false, false, 1), OTK_SMALL_K(1, false, true, 0),
-      OTK_SMALL_K(1, false, true, 1),  OTK_SMALL_K(1, true, false, 0),  OTK_SMALL_K(1, true, false, 1),
-      OTK_SMALL_K(1, true, true, 0),   OTK_SMALL_K(1, true, true, 1),   OTK_SMALL_K(2, false, false, 0),
-      OTK_SMALL_K(2, false, false, 1), OTK_SMALL_K(2, false, true, 0),  OTK_SMALL_K(2, false, true, 1),
-      OTK_SMALL_K(2, true, false, 0),  OTK_SMALL_K(2, true, false, 1),  OTK_SMALL_K(2, true, true, 0),
-      OTK_SMALL_K(2, true, true, 1)};
+#define OTK_SMALL_K(NV_, SA_, EU_) (void *)solve_small_kernel<NV_, SA_, EU_>
+  void *const table[8] = {OTK_SMALL_K(1, false, false), OTK_SMALL_K(1, false, true),
+                          OTK_SMALL_K(1, true, false),  OTK_SMALL_K(1, true, true),
+                          OTK_SMALL_K(2, false, false), OTK_SMALL_K(2, false, true),
+                          OTK_SMALL_K(2, true, false),  OTK_SMALL_K(2, true, true)};
 #undef OTK_SMALL_K
-  kern = table[key];
+  void *kern = table[(nv == 2) * 4 + same * 2 + eucl];
   OTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   OTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
