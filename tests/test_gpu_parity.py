@@ -512,3 +512,73 @@ def test_batched_cluster_solver_matches_streaming_solver(otk, monkeypatch, n, m,
         for k in range(B):
             assert rel_inf(a.f[k], b.f[k]) <= 2e-6
             assert rel_inf(a.g[k], b.g[k]) <= 2e-6
+
+
+def _small_vs_general(otk, x, y, a, b, eps, **kw):
+    """Run the one-kernel small solve and the launch-per-half-step loop on the
+    same problem; return (outcome, outcome) where an outcome is the result or
+    the (exception type, iteration / message) it raised."""
+    from paper_2201_12324_b200 import _native as N
+
+    def run(flags):
+        g = otk.PointCloudGeometry(x, y)
+        g.impl_flags = flags
+        try:
+            return otk.solve_sinkhorn(otk.LinearProblem(g, a, b), eps, **kw)
+        except otk.DivergedError as e:
+            return ("diverged", e.iteration)
+        except ValueError as e:
+            return ("value", str(e))
+    return run(0), run(N.OTK_IMPL_NOPERSIST)
+
+
+def test_persistent_small_solve_failure_paths_match_general_loop(otk):
+    """The persistent small solve (per-CTA first-bad markers, one grid barrier
+    per check) raises exactly what the general loop raises, at the same
+    iteration: a warm start with NaN / +inf entries (reference geometry.py:65-72
+    via apply_lse_kernel), and divergence from a zero-weight column whose
+    kernel underflows (reference tests/test_sinkhorn.py:244-250 analog)."""
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((300, 3)).astype(np.float32)
+    y = (rng.standard_normal((260, 3)) + 0.5).astype(np.float32)
+    for bad in (np.nan, np.inf):
+        g0 = np.zeros(260)
+        g0[17] = bad
+        fast, gen = _small_vs_general(otk, x, y, None, None, 0.5, g_init=g0)
+        assert fast == gen and fast[0] == "value", (fast, gen)
+    b = np.full(260, 1.0 / 259)
+    b[-1] = 0.0
+    y2 = y.copy()
+    y2[-1] = 1e4  # far away: its column's kernel underflows at small eps
+    fast, gen = _small_vs_general(otk, x, y2, None, b, 1e-3, inner_iters=1, max_iters=50)
+    if isinstance(gen, tuple):
+        assert fast == gen, (fast, gen)
+    else:
+        assert not isinstance(fast, tuple)
+        assert fast.iterations == gen.iterations and fast.converged == gen.converged
+
+
+@pytest.mark.parametrize("n,m", [(2048, 2048), (3000, 2100), (1, 7), (149, 150)])
+def test_persistent_small_solve_shapes_and_zero_weights(otk, n, m):
+    """Row-chunk shapes of the persistent small solve (one chunk per SM at the
+    cfg1 size, several chunks per SM, a single row, chunk size 1-2) with zero
+    weights on both sides (-inf potentials, empty rows / columns) against the
+    general loop and the float64 oracle."""
+    rng = np.random.default_rng(n + m)
+    x = rng.standard_normal((n, 3)).astype(np.float32)
+    y = (rng.standard_normal((m, 3)) * 1.3 + 0.2).astype(np.float32)
+    a = rng.uniform(0.5, 1.5, n)
+    b = rng.uniform(0.5, 1.5, m)
+    if n > 1:
+        a[::7] = 0.0
+    b[::5] = 0.0
+    a /= a.sum()
+    b /= b.sum()
+    geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64))
+    eps = 0.05 * float(np.mean(geom64.cost_matrix()))
+    ref = oracle.sinkhorn(geom64, a, b, eps, threshold=1e-3, max_iters=300)
+    fast, gen = _small_vs_general(otk, x, y, a, b, eps, threshold=1e-3, max_iters=300)
+    for out in (fast, gen):
+        assert out.iterations == ref["iterations"] and out.converged == ref["converged"]
+        assert rel_inf(out.f, ref["f"]) <= POT_TOL
+        assert rel_inf(out.g, ref["g"]) <= POT_TOL
