@@ -326,6 +326,25 @@ def online_roofline(geom, wl, reps=10):
     return roof
 
 
+def small_roofline(value, step_s, wl):
+    """The whole solve is ONE persistent kernel (solve_small.cu, problems that
+    fit in shared memory -- cfg1): its roof is MUFU ex2, 2 exps per
+    cell-update (one per cell per half-step; cfg1 is MUFU-bound),
+    achieved = 2 x cell-updates/s of the timed steps (one launch per step, so
+    the kernel time is the step time), peak = the ex2 rate measured on this GPU."""
+    ex2, ffma = pipes()
+    achieved = 2.0 * value
+    return {"bound": "mufu", "achieved": achieved / 1e9, "peak": ex2 / 1e9, "unit": "Gex2/s",
+            "frac": achieved / ex2, "traffic": traffic_for(wl.name),
+            "kernel": "solve_small_kernel (whole solve, one launch)", "kernel_ms": step_s * 1e3,
+            "cells_per_launch": float(wl.x.shape[0]) * wl.y.shape[0],
+            "peak_note": "MUFU ex2 rate measured on this GPU (csrc/pipes.cu)",
+            "achieved_note": "2 ex2 per cell-update x cell-updates/s of the timed steps; the "
+                             "kernel is latency-bound (the half-step exchange and reductions, "
+                             "tools/small_trace.py), not MUFU-bound",
+            "pipes": {"ex2_per_s": ex2, "ffma_per_s": ffma}}
+
+
 def dense_roofline(C, wl, reps=3):
     """Dominant kernel of the batched materialised path: the one-launch batched
     solve (otk_solve_dense_batched: K3c by default, K3p with OTK_DENSE_KERNEL=cta),
@@ -546,6 +565,8 @@ def run_ours(args, wl, rank, world):
 
     # launches of our kernels per step (native solver count / sharded engine count)
     result["gpu_launches"] = count_launches(otk, wl, args, solve, world) * args.steps
+    if rank == 0 and world == 1 and not wl.materialised and result["gpu_launches"] == args.steps:
+        roofline = small_roofline(value, total / args.steps, wl)
 
     if not args.no_e2e:
         e2e = run_e2e(otk, wl, args, dev, world, rank)
