@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -39,7 +40,18 @@ struct Args {
   float *f_out, *g_out;
   double *errors, *duals;
   int *state;  // [B][5]: n_checks, iterations, converged, status, fail_iter
+  unsigned long long *trace;  // OTK_DENSE_TRACE (trace builds): globaltimer stamps of cluster 0's first problem
 };
+
+__device__ __forceinline__ void dtrace(const Args &A, bool on, int t, int k) {
+#ifdef OTK_DENSE_TRACE_BUILD  // tools/build_variant.sh ... -DOTK_DENSE_TRACE_BUILD
+  if (on && A.trace && threadIdx.x == 0 && t < 64) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    A.trace[t * 8 + k] = v;
+  }
+#endif
+}
 
 __device__ __forceinline__ void block_sum(double (&v)[NV], double *red /* [NV][WARPS] */) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -51,12 +63,16 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double *red /* [NV][W
     if (lane == 0) red[k * WARPS + warp] = x;
   }
   __syncthreads();
+  if (warp < NV) {  // warp k folds value k over the warps in a fixed shuffle tree
+    static_assert(WARPS <= 32, "one lane per warp");
+    double x = (lane < WARPS) ? red[warp * WARPS + lane] : 0.0;
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    double x = 0.0;
-    for (int w = 0; w < WARPS; ++w) x += red[k * WARPS + w];  // fixed order
-    v[k] = x;
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) red[warp * WARPS] = x;
   }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = red[k * WARPS];
 }
 
 // rows half-step: out_i = eps log w_i - eps ln2 LSE2_j(by_j - kappa C_ij); bx_i = kappa out_i
@@ -433,8 +449,24 @@ __device__ void cols_partial_local(const float *Cs, int rows, int m, const float
     int i0 = 0;
     for (; i0 + 16 <= rows; i0 += 16, cp += 16 * m) {
       float u[16];
+#ifndef OTK_DENSE_SCALAR_BX
+      // the 16 row potentials as 4 broadcast LDS.128 (bx is 16-byte aligned, i0 % 16 == 0):
+      // the pass is bound by shared-memory instructions as much as by MUFU
+      float hb[16];
+#pragma unroll
+      for (int k = 0; k < 16; k += 4) {
+        const float4 h = *reinterpret_cast<const float4 *>(bx + i0 + k);
+        hb[k] = h.x;
+        hb[k + 1] = h.y;
+        hb[k + 2] = h.z;
+        hb[k + 3] = h.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) u[k] = fmaf(-kappa, cp[k * m], hb[k]);
+#else
 #pragma unroll
       for (int k = 0; k < 16; ++k) u[k] = fmaf(-kappa, cp[k * m], bx[i0 + k]);
+#endif
       float c0 = fmaxf(fmaxf(u[0], u[1]), fmaxf(u[2], u[3]));
       float c1 = fmaxf(fmaxf(u[4], u[5]), fmaxf(u[6], u[7]));
       float c2 = fmaxf(fmaxf(u[8], u[9]), fmaxf(u[10], u[11]));
@@ -492,6 +524,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
   float *part = by + m4;                              // [2][m4] log2 column partials
   double *slot = reinterpret_cast<double *>(part + 2 * m4);  // [2][NV + 1]
   __shared__ double red[NV * WARPS];
+  __shared__ double rsl[CL * (NV + 1)], rtot[NV + 1];
   __shared__ int fbad;
   __shared__ __align__(8) uint64_t lbar;
   const int r0 = min(n, rank * rows_per), r1 = min(n, r0 + rows_per), rows = r1 - r0;
@@ -543,16 +576,21 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
     bool f_ready = false;
     int n_checks = 0, status = OTK_OK, fail_iter = 0, converged = 0, t;
     double chk[NV];
+    const bool tr = (b == cid) && blockIdx.x == 0;
     for (t = 1; t <= A.max_iters; ++t) {
+      dtrace(A, tr, t, 0);
       if (!f_ready) {
         rows_local<false>(Cs, rows, m, by, la, eps, kappa, f, bx, &fbad, 2 * t, nullptr, a, eps_d, chk);
         __syncthreads();
       }
+      dtrace(A, tr, t, 1);
       f_ready = false;
       // ---- columns: local partials -> cluster exchange -> every CTA forms g
       float *mypart = part + xpar * m4;
       cols_partial_local(Cs, rows, m, bx, kappa, mypart);
+      dtrace(A, tr, t, 2);
       cluster.sync();
+      dtrace(A, tr, t, 3);
       for (int j = threadIdx.x; j < m; j += THREADS) {
         float v[CL];
 #pragma unroll
@@ -582,6 +620,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
       }
       xpar ^= 1;
       __syncthreads();
+      dtrace(A, tr, t, 4);
       if (t % A.inner_iters == 0 || t == A.max_iters) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) chk[k] = 0.0;
@@ -603,16 +642,24 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
           myslot[NV] = (double)fbad;
         }
         cluster.sync();
-        double tot[NV];
-        double fb = 2147483647.0;
-#pragma unroll
-        for (int k = 0; k < NV; ++k) tot[k] = 0.0;
-        for (int r = 0; r < CL; ++r) {  // rank order: identical in every CTA
-          const double *ps = cluster.map_shared_rank(myslot, r);
-#pragma unroll
-          for (int k = 0; k < NV; ++k) tot[k] += ps[k];
-          fb = fmin(fb, ps[NV]);
+        // the CL slots -> shared memory (one remote load per value), then thread
+        // k folds value k in rank order: identical in every CTA
+        for (int e = threadIdx.x; e < CL * (NV + 1); e += THREADS)
+          rsl[e] = cluster.map_shared_rank(myslot, e / (NV + 1))[e % (NV + 1)];
+        __syncthreads();
+        if (threadIdx.x <= NV) {
+          double v = rsl[threadIdx.x];
+          for (int r = 1; r < CL; ++r) {
+            const double w = rsl[r * (NV + 1) + threadIdx.x];
+            v = (threadIdx.x == NV) ? fmin(v, w) : v + w;
+          }
+          rtot[threadIdx.x] = v;
         }
+        __syncthreads();
+        double tot[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) tot[k] = rtot[k];
+        const double fb = rtot[NV];
         xpar ^= 1;
         const int fbi = (int)fb;
         int d = 0;  // 0 continue, 1 converged, 2 bad potential, 3 diverged
@@ -647,6 +694,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
           fn = tmp;
           f_ready = true;
         }
+        dtrace(A, tr, t, 5);
       }
     }
     for (int i = threadIdx.x; i < rows; i += THREADS) A.f_out[b * n + r0 + i] = f[i];
@@ -756,14 +804,31 @@ extern "C" int otk_solve_dense_batched(const float *cost, int64_t batch, int64_t
   OTK_CHECK_ARG(max_iters >= 1 && inner_iters >= 1 && max_checks >= 1 && threshold > 0,
                 "otk_solve_dense_batched: bad loop parameters");
   dsolve::Args A{cost, batch, (int)n, (int)m, a, b, log_a, log_b, eps, g_init, eps_d, threshold,
-                 max_iters, inner_iters, max_checks, f_out, g_out, errors, duals, state};
+                 max_iters, inner_iters, max_checks, f_out, g_out, errors, duals, state, nullptr};
+  const char *trace_path = getenv("OTK_DENSE_TRACE");  // diagnostics (tools/dense_trace.py)
+  if (trace_path) {
+    OTK_CUDA(cudaMalloc(&A.trace, 64 * 8 * sizeof(unsigned long long)));
+    OTK_CUDA(cudaMemsetAsync(A.trace, 0, 64 * 8 * sizeof(unsigned long long), as_stream(stream)));
+  }
   // K3c (cost resident in a cluster's shared memory) whenever a slice fits;
   // OTK_DENSE_KERNEL=cta forces the one-CTA-per-problem streaming kernel K3p
   const char *kind = getenv("OTK_DENSE_KERNEL");
   if (!(kind && strcmp(kind, "cta") == 0)) {
     const int want_cl = getenv("OTK_DENSE_CL") ? atoi(getenv("OTK_DENSE_CL")) : 0;
     int rc = dsolve::launch_cluster_solve(A, (int)n, (int)m, batch, grid, want_cl, as_stream(stream));
-    if (rc != OTK_ENOTSUP) return rc;
+    if (rc != OTK_ENOTSUP) {
+      if (trace_path) {
+        unsigned long long h[64 * 8];
+        OTK_CUDA(cudaMemcpyAsync(h, A.trace, sizeof(h), cudaMemcpyDeviceToHost, as_stream(stream)));
+        OTK_CUDA(cudaStreamSynchronize(as_stream(stream)));
+        cudaFree(A.trace);
+        if (FILE *fp = fopen(trace_path, "wb")) {
+          fwrite(h, sizeof(h[0]), 64 * 8, fp);
+          fclose(fp);
+        }
+      }
+      return rc;
+    }
   }
   const size_t smem = dsolve::smem_bytes((int)n, (int)m);
   OTK_CUDA(cudaFuncSetAttribute(dsolve::dense_solve_kernel,
