@@ -258,7 +258,19 @@ class PointCloudGeometry(Geometry):
             xd = as_device_f32(x, async_pinned=True)
             self._dev_pts = (xd, xd if same_obj else as_device_f32(y, async_pinned=True))
         vx, vy = self._dev_pts if self._dev_pts is not None else (x, y)
-        if not (_all_finite(vx) and (same_obj or _all_finite(vy))):
+        same_dev = None
+        if self._dev_pts is not None:
+            # one device->host read for both finiteness flags and the same-points test
+            import torch
+            flags = [torch.isfinite(vx).all(), torch.isfinite(vy).all()]
+            if not same_obj and x.shape == y.shape:
+                flags.append((vx == vy).all())
+            got = torch.stack(flags).cpu().tolist()
+            finite = got[0] and (same_obj or got[1])
+            same_dev = bool(got[2]) if len(got) > 2 else False
+        else:
+            finite = _all_finite(vx) and (same_obj or _all_finite(vy))
+        if not finite:
             raise ValueError("points contain non-finite entries")
         if cost_fn not in _REFERENCE_COST_FNS:
             raise ValueError(f"cost_fn must be one of {_REFERENCE_COST_FNS}, got {cost_fn!r}")
@@ -277,23 +289,33 @@ class PointCloudGeometry(Geometry):
         if same_obj:
             self._same_points = True
         elif self._dev_pts is not None:
-            import torch
-            self._same_points = bool(x.shape == y.shape and torch.equal(*self._dev_pts))
+            self._same_points = same_dev
         else:
             self._same_points = bool(x.shape == y.shape and np.array_equal(x, y))
         self._dev = None
+        self._kpts = None
         self.impl_flags = 0  # N.OTK_IMPL_SIMT / N.OTK_IMPL_TC to force a kernel
 
     # ---- device state (lazy: construction and validation need no GPU)
     def _kernel_points(self, p):
         return kernel_points(p, self.cost_fn)
 
-    def _clouds(self):
-        if self._dev is None:
+    def _points(self):
+        """fp32 device points the kernels see (cosine: normalised), cached; the
+        whole-solve entry needs only these (it prepares norms / planes itself)."""
+        if self._kpts is None:
             device()
             px, py = self._dev_pts if self._dev_pts is not None else (self.x, self.y)
-            cx = _Cloud(self._kernel_points(px))
-            cy = cx if self._same_points else _Cloud(self._kernel_points(py))
+            kx = as_device_f32(self._kernel_points(px)).contiguous()
+            ky = kx if self._same_points else as_device_f32(self._kernel_points(py)).contiguous()
+            self._kpts = (kx, ky)
+        return self._kpts
+
+    def _clouds(self):
+        if self._dev is None:
+            kx, ky = self._points()
+            cx = _Cloud(kx)
+            cy = cx if self._same_points else _Cloud(ky)
             planes = bool(N.lib().otk_lse_uses_tc(cx.d, self.impl_flags))
             scale = 1.0
             if planes:

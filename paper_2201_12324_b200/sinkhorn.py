@@ -88,7 +88,11 @@ class LinearProblem:
         if self._dev is None:
             with np.errstate(divide="ignore"):
                 la, lb = np.log(self.a), np.log(self.b)
-            object.__setattr__(self, "_dev", tuple(as_device_f32(v) for v in (self.a, self.b, la, lb)))
+            # one host->device copy for the four vectors
+            n, m = self.a.shape[0], self.b.shape[0]
+            packed = as_device_f32(np.concatenate([self.a, self.b, la, lb]))
+            object.__setattr__(self, "_dev", (packed[:n], packed[n:n + m], packed[n + m:2 * n + m],
+                                              packed[2 * n + m:]))
         return self._dev
 
 
@@ -275,10 +279,11 @@ def _raise_status(rc: int, iteration: int):
 def _solve_pointcloud(prob, sched, threshold, max_iters, inner_iters, g_init, impl, use_graphs):
     import torch
     geom: PointCloudGeometry = prob.geom
-    cx, cy = geom._clouds()
+    px, py = geom._points()  # the native solve prepares norms / operand planes itself
     a, b, la, lb = prob._weights()
     n, m = geom.shape
-    dev = cx.p.device
+    d = int(px.shape[1])
+    dev = px.device
     f_out = torch.empty(n, dtype=torch.float32, device=dev)
     g_out = torch.empty(m, dtype=torch.float32, device=dev)
     max_checks = max_iters // inner_iters + 2
@@ -290,7 +295,7 @@ def _solve_pointcloud(prob, sched, threshold, max_iters, inner_iters, g_init, im
         if tuple(gi.shape) != (m,):
             raise ValueError(f"g_init must have shape ({m},)")
     A = N.SolveArgs()
-    A.x, A.y, A.n, A.m, A.d = N.ptr(cx.p), N.ptr(cy.p), n, m, cx.d
+    A.x, A.y, A.n, A.m, A.d = N.ptr(px), N.ptr(py), n, m, d
     A.a, A.b, A.log_a, A.log_b = N.ptr(a), N.ptr(b), N.ptr(la), N.ptr(lb)
     A.same_points = 1 if geom._same_points else 0
     A.eps_target, A.eps_init_scale, A.eps_decay = sched.target, sched.init_scale, sched.decay
