@@ -369,6 +369,29 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // an online (max, sum), then a 3-level shuffle merge in fixed order.
 constexpr int RG = 8;
 constexpr int RCH = 4 * RG * 4;  // columns per chunk
+
+// sum_e 2^(u_e - ms) over 16 values in two chains (even / odd e), as packed
+// FADD2 pairs: bitwise the scalar (a0 += ..even.., a1 += ..odd..; a0 + a1)
+__device__ __forceinline__ float sum_ex2_16(const float (&u)[16], float ms) {
+#ifndef OTK_DENSE_NOPACK
+  float2 acc = make_float2(0.f, 0.f);
+  const float2 nms = make_float2(-ms, -ms);
+#pragma unroll
+  for (int e = 0; e < 16; e += 2) {
+    const float2 t = __fadd2_rn(make_float2(u[e], u[e + 1]), nms);
+    acc = __fadd2_rn(acc, make_float2(ex2(t.x), ex2(t.y)));
+  }
+  return acc.x + acc.y;
+#else
+  float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+  for (int e = 0; e < 16; e += 2) {
+    a0 += ex2(u[e] - ms);
+    a1 += ex2(u[e + 1] - ms);
+  }
+  return a0 + a1;
+#endif
+}
 template <bool CHECK>
 __device__ void rows_local(const float *Cs, int rows, int m, const float *by, const float *lw,
                            float eps, float kappa, float *out, float *bx, int *fbad, int step,
@@ -389,10 +412,20 @@ __device__ void rows_local(const float *Cs, int rows, int m, const float *by, co
           if (j < m) {
             const float4 c = *reinterpret_cast<const float4 *>(row + j);
             const float4 h = *reinterpret_cast<const float4 *>(by + j);
+#ifndef OTK_DENSE_NOPACK  // packed FFMA2 (same IEEE results as the scalar FFMAs)
+            const float2 nk = make_float2(-kappa, -kappa);
+            const float2 u01 = __ffma2_rn(nk, make_float2(c.x, c.y), make_float2(h.x, h.y));
+            const float2 u23 = __ffma2_rn(nk, make_float2(c.z, c.w), make_float2(h.z, h.w));
+            u[4 * q + 0] = u01.x;
+            u[4 * q + 1] = u01.y;
+            u[4 * q + 2] = u23.x;
+            u[4 * q + 3] = u23.y;
+#else
             u[4 * q + 0] = fmaf(-kappa, c.x, h.x);
             u[4 * q + 1] = fmaf(-kappa, c.y, h.y);
             u[4 * q + 2] = fmaf(-kappa, c.z, h.z);
             u[4 * q + 3] = fmaf(-kappa, c.w, h.w);
+#endif
           } else {
 #pragma unroll
             for (int e = 0; e < 4; ++e) u[4 * q + e] = -INFINITY;
@@ -406,13 +439,7 @@ __device__ void rows_local(const float *Cs, int rows, int m, const float *by, co
           st.m = cm;
         }
         const float ms = (st.m == -INFINITY) ? 0.f : st.m;
-        float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-        for (int e = 0; e < 16; e += 2) {
-          a0 += ex2(u[e] - ms);
-          a1 += ex2(u[e + 1] - ms);
-        }
-        st.s += a0 + a1;
+        st.s += sum_ex2_16(u, ms);
       }
     }
 #pragma unroll
@@ -461,8 +488,18 @@ __device__ void cols_partial_local(const float *Cs, int rows, int m, const float
         hb[k + 2] = h.z;
         hb[k + 3] = h.w;
       }
+#ifndef OTK_DENSE_NOPACK
+#pragma unroll
+      for (int k = 0; k < 16; k += 2) {
+        const float2 uu = __ffma2_rn(make_float2(-kappa, -kappa), make_float2(cp[k * m], cp[(k + 1) * m]),
+                                     make_float2(hb[k], hb[k + 1]));
+        u[k] = uu.x;
+        u[k + 1] = uu.y;
+      }
+#else
 #pragma unroll
       for (int k = 0; k < 16; ++k) u[k] = fmaf(-kappa, cp[k * m], hb[k]);
+#endif
 #else
 #pragma unroll
       for (int k = 0; k < 16; ++k) u[k] = fmaf(-kappa, cp[k * m], bx[i0 + k]);
@@ -477,13 +514,7 @@ __device__ void cols_partial_local(const float *Cs, int rows, int m, const float
         mx = cm;
       }
       const float ms = (mx == -INFINITY) ? 0.f : mx;
-      float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-      for (int k = 0; k < 16; k += 2) {
-        a0 += ex2(u[k] - ms);
-        a1 += ex2(u[k + 1] - ms);
-      }
-      sm += a0 + a1;
+      sm += sum_ex2_16(u, ms);
     }
     if (i0 < rows) {  // last partial chunk, masked
       float u[16];
