@@ -1,7 +1,7 @@
 """Per-iteration cost of the persistent small solve (cfg1 shape): time fixed
 100- and 300-iteration solves with CUDA events and report the difference / 200
-(launch + setup cancel).  Env knobs read by the library: OTK_SMALL_V1=1 (the
-column-sliced half-step), OTK_SMALL_PROBE=1/2 (timing probes, see solve_small.cu)."""
+(launch + setup cancel).  Env knob read by the library: OTK_SMALL_PROBE=1 (timing
+probe: skip the passes over the cells, see solve_small.cu)."""
 import os
 import sys
 
@@ -36,6 +36,6 @@ def t_solve(iters, reps=10):
 
 t1, i1 = t_solve(100)
 t3, i3 = t_solve(300)
-tag = "V1=%s PROBE=%s" % (os.environ.get("OTK_SMALL_V1", "0"), os.environ.get("OTK_SMALL_PROBE", "0"))
+tag = "PROBE=%s" % os.environ.get("OTK_SMALL_PROBE", "0")
 print("%s  100-it %.3f ms  300-it %.3f ms  per-iteration %.2f us (iters %d/%d)"
       % (tag, t1, t3, (t3 - t1) / (i3 - i1) * 1e3, i1, i3), flush=True)
