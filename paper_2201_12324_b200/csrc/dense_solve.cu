@@ -373,7 +373,6 @@ constexpr int RCH = 4 * RG * 4;  // columns per chunk
 // sum_e 2^(u_e - ms) over 16 values in two chains (even / odd e), as packed
 // FADD2 pairs: bitwise the scalar (a0 += ..even.., a1 += ..odd..; a0 + a1)
 __device__ __forceinline__ float sum_ex2_16(const float (&u)[16], float ms) {
-#ifndef OTK_DENSE_NOPACK
   float2 acc = make_float2(0.f, 0.f);
   const float2 nms = make_float2(-ms, -ms);
 #pragma unroll
@@ -382,15 +381,6 @@ __device__ __forceinline__ float sum_ex2_16(const float (&u)[16], float ms) {
     acc = __fadd2_rn(acc, make_float2(ex2(t.x), ex2(t.y)));
   }
   return acc.x + acc.y;
-#else
-  float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-  for (int e = 0; e < 16; e += 2) {
-    a0 += ex2(u[e] - ms);
-    a1 += ex2(u[e + 1] - ms);
-  }
-  return a0 + a1;
-#endif
 }
 template <bool CHECK>
 __device__ void rows_local(const float *Cs, int rows, int m, const float *by, const float *lw,
@@ -412,7 +402,7 @@ __device__ void rows_local(const float *Cs, int rows, int m, const float *by, co
           if (j < m) {
             const float4 c = *reinterpret_cast<const float4 *>(row + j);
             const float4 h = *reinterpret_cast<const float4 *>(by + j);
-#ifndef OTK_DENSE_NOPACK  // packed FFMA2 (same IEEE results as the scalar FFMAs)
+            // packed FFMA2: the same IEEE results as four scalar FFMAs
             const float2 nk = make_float2(-kappa, -kappa);
             const float2 u01 = __ffma2_rn(nk, make_float2(c.x, c.y), make_float2(h.x, h.y));
             const float2 u23 = __ffma2_rn(nk, make_float2(c.z, c.w), make_float2(h.z, h.w));
@@ -420,12 +410,6 @@ __device__ void rows_local(const float *Cs, int rows, int m, const float *by, co
             u[4 * q + 1] = u01.y;
             u[4 * q + 2] = u23.x;
             u[4 * q + 3] = u23.y;
-#else
-            u[4 * q + 0] = fmaf(-kappa, c.x, h.x);
-            u[4 * q + 1] = fmaf(-kappa, c.y, h.y);
-            u[4 * q + 2] = fmaf(-kappa, c.z, h.z);
-            u[4 * q + 3] = fmaf(-kappa, c.w, h.w);
-#endif
           } else {
 #pragma unroll
             for (int e = 0; e < 4; ++e) u[4 * q + e] = -INFINITY;
@@ -476,9 +460,8 @@ __device__ void cols_partial_local(const float *Cs, int rows, int m, const float
     int i0 = 0;
     for (; i0 + 16 <= rows; i0 += 16, cp += 16 * m) {
       float u[16];
-#ifndef OTK_DENSE_SCALAR_BX
       // the 16 row potentials as 4 broadcast LDS.128 (bx is 16-byte aligned, i0 % 16 == 0):
-      // the pass is bound by shared-memory instructions as much as by MUFU
+      // a quarter of the shared-memory instructions (column pass 2.8 -> 2.5 us per iteration)
       float hb[16];
 #pragma unroll
       for (int k = 0; k < 16; k += 4) {
@@ -488,7 +471,6 @@ __device__ void cols_partial_local(const float *Cs, int rows, int m, const float
         hb[k + 2] = h.z;
         hb[k + 3] = h.w;
       }
-#ifndef OTK_DENSE_NOPACK
 #pragma unroll
       for (int k = 0; k < 16; k += 2) {
         const float2 uu = __ffma2_rn(make_float2(-kappa, -kappa), make_float2(cp[k * m], cp[(k + 1) * m]),
@@ -496,14 +478,6 @@ __device__ void cols_partial_local(const float *Cs, int rows, int m, const float
         u[k] = uu.x;
         u[k + 1] = uu.y;
       }
-#else
-#pragma unroll
-      for (int k = 0; k < 16; ++k) u[k] = fmaf(-kappa, cp[k * m], hb[k]);
-#endif
-#else
-#pragma unroll
-      for (int k = 0; k < 16; ++k) u[k] = fmaf(-kappa, cp[k * m], bx[i0 + k]);
-#endif
       float c0 = fmaxf(fmaxf(u[0], u[1]), fmaxf(u[2], u[3]));
       float c1 = fmaxf(fmaxf(u[4], u[5]), fmaxf(u[6], u[7]));
       float c2 = fmaxf(fmaxf(u[8], u[9]), fmaxf(u[10], u[11]));
