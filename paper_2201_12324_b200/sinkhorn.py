@@ -284,8 +284,11 @@ def _solve_pointcloud(prob, sched, threshold, max_iters, inner_iters, g_init, im
     n, m = geom.shape
     d = int(px.shape[1])
     dev = px.device
-    f_out = torch.empty(n, dtype=torch.float32, device=dev)
-    g_out = torch.empty(m, dtype=torch.float32, device=dev)
+    # f and g in one buffer (one device->host read at the end); g starts on a
+    # 256-byte boundary, as every separately allocated potential does
+    n_pad = (n + 63) // 64 * 64
+    fg = torch.empty(n_pad + m, dtype=torch.float32, device=dev)
+    f_out, g_out = fg[:n], fg[n_pad:]
     max_checks = max_iters // inner_iters + 2
     errs = np.zeros(max_checks)
     duals = np.zeros(max_checks)
@@ -318,8 +321,9 @@ def _solve_pointcloud(prob, sched, threshold, max_iters, inner_iters, g_init, im
     if not A.converged:
         logger.info("sinkhorn: no convergence after %d iterations (last error %s)", A.iterations,
                     errs[k - 1] if k else None)
+    fg_host = fg.cpu().numpy().astype(np.float64)
     return SinkhornOutput(
-        f=f_out.cpu().numpy().astype(np.float64), g=g_out.cpu().numpy().astype(np.float64),
+        f=fg_host[:n], g=fg_host[n_pad:],
         errors=errs[:k].copy(), dual_trace=duals[:k].copy(), iterations=int(A.iterations),
         converged=bool(A.converged), eps=sched.target, f_device=f_out, g_device=g_out)
 
