@@ -52,6 +52,7 @@ struct Args {  // solve_small.cu
   int *state;
   int probe;
   unsigned long long *xch_x, *xch_y;
+  float4 *pts;
   unsigned long long *trace;
   int trace_steps;
 };
@@ -266,6 +267,7 @@ struct Layout {
   int *first_bad;
   double *slots, *d_errors, *d_duals;  // persistent small-problem kernel
   unsigned long long *xch;
+  float4 *pts;
   int *state;
   int nsr, nsc, dpad;
   bool tc, small;
@@ -322,6 +324,7 @@ Layout plan(const otk_solve_args *A, void *ws) {
     L.d_duals = c.take<double>(A->max_checks);
     L.state = c.take<int>(8);
     L.xch = c.take<unsigned long long>(2 * (size_t)(A->n + A->m));
+    L.pts = c.take<float4>((size_t)(A->n + A->m) * 5);  // d >= 8: staged points (<= 5 float4 each)
   }
   L.bytes = c.off + 256;
   return L;
@@ -444,6 +447,7 @@ static int solve_small(otk_solve_args *A, Layout &L, cudaStream_t st) {
   S.probe = getenv("OTK_SMALL_PROBE") ? atoi(getenv("OTK_SMALL_PROBE")) : 0;
   S.xch_x = L.xch;
   S.xch_y = L.xch + 2 * A->n;
+  S.pts = L.pts;
   const char *trace_path = getenv("OTK_SMALL_TRACE");  // diagnostics: per-CTA phase stamps
   if (trace_path) {
     S.trace_steps = 64;

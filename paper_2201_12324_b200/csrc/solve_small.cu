@@ -3,7 +3,9 @@
 // sinkhorn._sinkhorn_iterations (reference sinkhorn.py:151-200) with
 // apply_lse_kernel (geometry.py:336-354) for problems whose points fit in
 // shared memory (BASELINE configs[0]: 2048^2, d = 3), where a launch -- or a
-// grid barrier -- per half-step costs more than the math.
+// grid barrier -- per half-step costs more than the math.  d <= 19: up to
+// d = 7 both point sets live in every CTA's shared memory; beyond, they are
+// staged once in global memory (L2-resident) and read per column group.
 //
 // Every CTA keeps both point sets resident in shared memory as NV float4 per
 // point: coordinates, then -kappa*|q|^2 in slot d, zeros after.  A row's query
@@ -50,6 +52,7 @@ struct Args {
   int probe;                 // timing probe (OTK_SMALL_PROBE): skip the passes over the cells;
                              // a probe never converges
   unsigned long long *xch_x, *xch_y;  // exchange words, 2 buffers per role ([2n], [2m])
+  float4 *pts;               // d >= 8: both point sets as NV float4 in global memory (L2-resident)
   unsigned long long *trace; // OTK_SMALL_TRACE: globaltimer stamps [trace_steps][grid][8] (thread 0)
   int trace_steps;
 };
@@ -62,19 +65,28 @@ __device__ __forceinline__ void trace_mark(const Args &A, int step, int k) {
   }
 }
 
+// Points as NV float4: coordinates, -kappa |q|^2 in slot d, zeros after.
+// Threads [first, first + stride) of the grid (or of the CTA) share the rows.
+template <int NV>
 __device__ __forceinline__ void load_points(const float *src, int count, int d, float kappa,
-                                            float4 *dst, int nv) {
-  for (int i = threadIdx.x; i < count; i += blockDim.x) {
-    float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                                            float4 *dst, int first, int stride) {
+  for (int i = first; i < count; i += stride) {
+    float v[4 * NV];
+#pragma unroll
+    for (int k = 0; k < 4 * NV; ++k) v[k] = 0.f;
     double sq = 0.0;
-    for (int k = 0; k < d; ++k) {
-      const float c = src[(int64_t)i * d + k];
-      v[k] = c;
-      sq = fma((double)c, (double)c, sq);
-    }
-    v[d] = -kappa * (float)sq;
-    dst[i * nv] = make_float4(v[0], v[1], v[2], v[3]);
-    if (nv == 2) dst[i * nv + 1] = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+    for (int k = 0; k < 4 * NV; ++k)
+      if (k < d) {
+        const float c = src[(int64_t)i * d + k];
+        v[k] = c;
+        sq = fma((double)c, (double)c, sq);
+      }
+#pragma unroll
+    for (int k = 0; k < 4 * NV; ++k)
+      if (k == d) v[k] = -kappa * (float)sq;
+#pragma unroll
+    for (int w = 0; w < NV; ++w) dst[i * NV + w] = make_float4(v[4 * w], v[4 * w + 1], v[4 * w + 2], v[4 * w + 3]);
   }
 }
 
@@ -108,7 +120,10 @@ __device__ __forceinline__ void load_points(const float *src, int count, int d, 
 // writer first consumed the other role's words, whose writers consumed this
 // buffer.  Check iterations keep their grid barriers (global sums).
 constexpr int RC = 16;    // rows per chunk (the reduce-scatter width)
-constexpr int CPT = 4;    // columns per thread per register group
+// columns per thread per register group: 4 while a point is <= 2 float4 (d <= 7),
+// 2 beyond (the q vectors of the group live in registers)
+template <int NV>
+struct Cols { static constexpr int CPT = NV <= 2 ? 4 : 2; };
 constexpr int KMAX = 8;   // chunks per CTA per role (n <= 8 * 16 * #SMs)
 
 typedef unsigned long long xword;
@@ -191,6 +206,8 @@ __device__ __forceinline__ void chunk_pass(const Args &A, const float4 *Q, int n
                                            int need, int r0, int rc, const float2 (*p2)[4 * NV],
                                            const float *cp, const float *sh, float (*red)[RC],
                                            float *tot) {
+  constexpr int CPT = Cols<NV>::CPT;
+  static_assert(CPT == 2 || CPT == 4, "column groups of 2 or 4");
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float sk = sqrtf(A.kappa);
   float2 acc[RC / 2];
@@ -270,11 +287,20 @@ __device__ __forceinline__ void chunk_pass(const Args &A, const float4 *Q, int n
           }
           e[c] = MAXP ? u : make_float2(ex2(u.x), ex2(u.y));
         }
-        if (MAXP) {
-          acc[h].x = fmaxf(acc[h].x, fmaxf(fmaxf(e[0].x, e[1].x), fmaxf(e[2].x, e[3].x)));
-          acc[h].y = fmaxf(acc[h].y, fmaxf(fmaxf(e[0].y, e[1].y), fmaxf(e[2].y, e[3].y)));
+        if constexpr (CPT == 4) {
+          if (MAXP) {
+            acc[h].x = fmaxf(acc[h].x, fmaxf(fmaxf(e[0].x, e[1].x), fmaxf(e[2].x, e[3].x)));
+            acc[h].y = fmaxf(acc[h].y, fmaxf(fmaxf(e[0].y, e[1].y), fmaxf(e[2].y, e[3].y)));
+          } else {
+            acc[h] = __fadd2_rn(acc[h], __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3])));
+          }
         } else {
-          acc[h] = __fadd2_rn(acc[h], __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3])));
+          if (MAXP) {
+            acc[h].x = fmaxf(acc[h].x, fmaxf(e[0].x, e[1].x));
+            acc[h].y = fmaxf(acc[h].y, fmaxf(e[0].y, e[1].y));
+          } else {
+            acc[h] = __fadd2_rn(acc[h], __fadd2_rn(e[0], e[1]));
+          }
         }
       }
     }
@@ -308,7 +334,6 @@ __device__ void half_step_rows(const Args &A, const float4 *P, int np, const flo
                                const xword *qx, xword *px, const float *logw, float *out_pot,
                                RoleRows<NV> &S, bool anchored, int step, const float *f_prev,
                                double (&chk)[NVALS], int *bad_s) {
-  static_assert(CPT == 4, "chunk_pass folds 4 columns per group");
   __shared__ float red[WARPS][RC];
   __shared__ float tot[RC];
   __shared__ int redo;
@@ -383,8 +408,6 @@ template <int NV, bool SAME, bool EU>
 __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ float4 sh4[];
-  float4 *xs = sh4;
-  float4 *ys = xs + A.n * NV;
   __shared__ RoleRows<NV> rows_x, rows_y;
   __shared__ double red[NVALS][WARPS];
   __shared__ double tot_s[NVALS];
@@ -394,8 +417,20 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = G * blockDim.x;
 
   if (threadIdx.x == 0) bad_s = INT_MAX;
-  load_points(A.x, A.n, A.d, A.kappa, xs, NV);
-  load_points(A.y, A.m, A.d, A.kappa, ys, NV);
+  // d <= 7: both point sets resident in every CTA's shared memory; d >= 8:
+  // staged once in global memory (L2-resident), each CTA writing a share
+  float4 *xs, *ys;
+  if constexpr (NV <= 2) {
+    xs = sh4;
+    ys = xs + A.n * NV;
+    load_points<NV>(A.x, A.n, A.d, A.kappa, xs, threadIdx.x, blockDim.x);
+    load_points<NV>(A.y, A.m, A.d, A.kappa, ys, threadIdx.x, blockDim.x);
+  } else {
+    xs = A.pts;
+    ys = xs + A.n * NV;
+    load_points<NV>(A.x, A.n, A.d, A.kappa, xs, gtid, gstride);
+    load_points<NV>(A.y, A.m, A.d, A.kappa, ys, gtid, gstride);
+  }
   __syncthreads();
   // initial g, published as the y-words of half-step 1; every other exchange
   // word is cleared (a previous solve's tags must not match)
@@ -407,10 +442,11 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
     if (bad_potential(g0)) atomicMin(&bad_s, 1);  // a bad warm start
   }
   for (int i = gtid; i < 2 * A.n; i += gstride) A.xch_x[i] = xpack(0.f, -1);
-  init_role_rows<NV>(A, xs, A.n, rows_x);
-  init_role_rows<NV>(A, ys, A.m, rows_y);
   __syncthreads();
   grid.sync();
+  init_role_rows<NV>(A, xs, A.n, rows_x);  // after the barrier: global points are complete
+  init_role_rows<NV>(A, ys, A.m, rows_y);
+  __syncthreads();
 
   // exchange buffer of the words tagged T: (T >> 1) & 1
   auto xb = [](xword *base, int len, int tag) { return base + ((tag >> 1) & 1) * (size_t)len; };
@@ -531,14 +567,23 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
   }
 }
 
-size_t smem_bytes(int n, int m, int nv) { return (size_t)(n + m) * nv * sizeof(float4); }
+// dynamic shared memory: the resident point sets (d <= 7 only)
+size_t smem_bytes(int n, int m, int nv) { return nv <= 2 ? (size_t)(n + m) * nv * sizeof(float4) : 0; }
+inline int nv_of(int d) {
+  const int nv = (d + 1 + 3) / 4;
+  return nv <= 3 ? nv : 5;  // instantiated: 1, 2, 3, 5 float4 per point
+}
 
 }  // namespace small
 
 // Can this problem run as one persistent kernel on this device?
 bool small_solve_fits(int64_t n, int64_t m, int d) {
-  if (d > 7 || n > (1 << 20) || m > (1 << 20)) return false;
-  const int nv = (d + 1 + 3) / 4;
+  if (d > 19 || n > (1 << 20) || m > (1 << 20)) return false;
+  const int nv = small::nv_of(d);
+  // d >= 8: the FP32 cells grow with d; beyond ~2^27 cell-dimensions per
+  // half-step the tcgen05 loop is faster despite its launches (measured:
+  // 2048^2 d = 16 17.4 vs 24.7 us per iteration; 512^2 d = 16 6.5 vs 24.7)
+  if (nv >= 3 && (double)n * (double)m * (d + 1) > (double)(1 << 27)) return false;
   int dev = 0, coop = 0, max_smem = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
@@ -546,21 +591,22 @@ bool small_solve_fits(int64_t n, int64_t m, int d) {
   const int64_t per_cta = (int64_t)small::RC * num_sms() * small::KMAX;  // chunks per CTA per role
   if (n > per_cta || m > per_cta) return false;
   if (num_sms() > small::MAX_GRID) return false;
-  // static shared memory: the per-role row state (<= 10 KB), the gathered check slots (12.5 KB)
-  return coop && small::smem_bytes((int)n, (int)m, nv) + 32768 <= (size_t)max_smem;
+  // static shared memory: the per-role row state (<= 21 KB at NV = 5), the gathered check slots (12.5 KB)
+  return coop && small::smem_bytes((int)n, (int)m, nv) + 40960 <= (size_t)max_smem;
 }
 
 int small_solve_launch(const small::Args &A, bool same, bool eucl, cudaStream_t st) {
   using namespace small;
-  const int nv = (A.d + 1 + 3) / 4;
+  const int nv = nv_of(A.d);
   const size_t smem = smem_bytes(A.n, A.m, nv);
 #define OTK_SMALL_K(NV_, SA_, EU_) (void *)solve_small_kernel<NV_, SA_, EU_>
-  void *const table[8] = {OTK_SMALL_K(1, false, false), OTK_SMALL_K(1, false, true),
-                          OTK_SMALL_K(1, true, false),  OTK_SMALL_K(1, true, true),
-                          OTK_SMALL_K(2, false, false), OTK_SMALL_K(2, false, true),
-                          OTK_SMALL_K(2, true, false),  OTK_SMALL_K(2, true, true)};
+#define OTK_SMALL_K4(NV_) OTK_SMALL_K(NV_, false, false), OTK_SMALL_K(NV_, false, true), \
+                          OTK_SMALL_K(NV_, true, false), OTK_SMALL_K(NV_, true, true)
+  void *const table[16] = {OTK_SMALL_K4(1), OTK_SMALL_K4(2), OTK_SMALL_K4(3), OTK_SMALL_K4(5)};
+#undef OTK_SMALL_K4
 #undef OTK_SMALL_K
-  void *kern = table[(nv == 2) * 4 + same * 2 + eucl];
+  const int slot = nv == 5 ? 3 : nv - 1;
+  void *kern = table[slot * 4 + same * 2 + eucl];
   OTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   OTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));

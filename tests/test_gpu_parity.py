@@ -330,7 +330,8 @@ def test_reference_loop_drives_the_drop_in_geometry(otk):
 
 
 @pytest.mark.parametrize("d,same,nonuniform", [(3, False, False), (1, False, True), (5, False, False),
-                                               (3, True, False), (7, False, True)])
+                                               (3, True, False), (7, False, True), (8, False, False),
+                                               (11, True, False), (16, False, True), (19, False, False)])
 def test_persistent_small_solve_matches_general_loop_and_oracle(otk, d, same, nonuniform):
     """The one-kernel small-problem solve (csrc/solve_small.cu) against the
     general launch-per-half-step loop (OTK_IMPL_NOPERSIST) and the oracle:
