@@ -176,7 +176,7 @@ struct RoleRows {
 };
 
 template <int NV>
-__device__ void init_role_rows(const Args &A, const float4 *P, int np, RoleRows<NV> &S) {
+__device__ __forceinline__ void init_role_rows(const Args &A, const float4 *P, int np, RoleRows<NV> &S) {
   const int G = gridDim.x;
   const int rc = min(RC, (np + G - 1) / G);
   const int n_chunks = (np + rc - 1) / rc;
@@ -330,7 +330,7 @@ __device__ __forceinline__ void chunk_pass(const Args &A, const float4 *Q, int n
 // out_pot (own rows).  CHECK: the f-side check sums (f_prev = previous f,
 // weights A.a); CHECKG: the g-side sums (weights A.b) of this g half-step.
 template <int NV, bool SAME, bool CHECK, bool CHECKG, bool EU>
-__device__ void half_step_rows(const Args &A, const float4 *P, int np, const float4 *Q, int nq,
+__device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, int np, const float4 *Q, int nq,
                                const xword *qx, xword *px, const float *logw, float *out_pot,
                                RoleRows<NV> &S, bool anchored, int step, const float *f_prev,
                                double (&chk)[NVALS], int *bad_s) {
