@@ -1,28 +1,33 @@
 """Benchmark: Sinkhorn cell-updates/s (n*m*iters/s) and time-to-tolerance.
 
-Default workload = BASELINE.json configs[1] (cfg2: n = m = 65536, d = 64,
-fp32, eps = 0.05 x subsample mean, tolerance 1e-3, checks every 10).  One
-STEP = one fixed-iteration solve (--iters, default 100: threshold 1e-300, the
-reference's check every 10 iterations still runs) on inputs already resident
-in HBM; value = n*m*iterations / step time -- SURVEY.md §8d: "throughput
-comes from fixed-iteration runs".  The time-to-tolerance (the workload's own
-threshold and max_iters; cfg2 converges at its first check, iteration 10) is
-timed separately under the same rules and reported as
-config.time_to_tolerance_ms; --iters 0 makes the tolerance solve the step.
-L2 is flushed (512 MiB write) before every timed step.
+Default workload = BASELINE.json configs[3] (cfg4: n = 262144, m = 131072,
+d = 128, non-uniform weights, eps = 0.05 x subsample mean, tolerance 1e-3):
+the largest configuration that fits one GPU, the one the north star's
+8-GPU scaling target names.  One STEP = one fixed-iteration solve (--iters,
+default 100: threshold 1e-300, the reference's check every 10 iterations
+still runs) on inputs already resident in HBM; value = n*m*iterations / step
+time -- SURVEY.md §8d: "throughput comes from fixed-iteration runs".  The
+time-to-tolerance (the workload's own threshold and max_iters) is timed
+separately under the same rules, INCLUDING the prep of the geometry (norms,
+split planes) and the on-device eps estimate (config.time_to_tolerance_ms);
+--iters 0 makes the tolerance solve the step.  L2 is flushed (512 MiB write)
+before every timed step.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config k]
 
-N > 1 (torchrun, one rank per GPU, NCCL): the row-sharded solver
-(paper_2201_12324_b200/sharded.py) on the SAME problem --
-x split in N row shards, the g half-step's m partials per rank pushed to every
-rank over NVLink peer memory (csrc/p2p.cu; NCCL all-gather as fallback) --
-so the scaling is strong; value = n*m*iters / max-over-ranks step time.
---config 3 runs the batched materialised path (512 problems of 512^2).
+--gpus N > 1 without torchrun: bench.py re-launches itself under
+``torch.distributed.run`` with N ranks (127.0.0.1) and asserts the world size.
+N > 1 (one rank per GPU, NCCL): the row-sharded solver
+(paper_2201_12324_b200/sharded.py) on the SAME problem -- x
+split in N row shards, the g half-step's m partials per rank pushed to every
+rank over NVLink peer memory (csrc/p2p.cu) -- so the scaling is strong;
+value = n*m*iters / max-over-ranks step time.  --config 3 runs the batched
+materialised path (512 problems of 512^2).
 
 ``--impl reference`` times the reference's CPU algorithm (the float64 numpy
 restatement under oracle/; the reference itself is pure Python/numpy) on a
-bounded sample of the same workload on rank 0's host cores.
+bounded sample of the same workload on rank 0's host cores.  Both arms print
+the same ``config`` object; run-specific facts go under ``run``.
 """
 
 from __future__ import annotations
@@ -53,10 +58,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tc"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--plumbing", action="store_true",
+                    help="(test) launch N ranks over gloo, check the world size, print it and exit")
     ap.add_argument("--iters", type=int, default=100,
                     help="timed step = a fixed-iteration solve of this many iterations "
                          "(SURVEY.md §8d: throughput from fixed-iteration runs); 0 = the "
@@ -100,7 +107,7 @@ class ClockSampler:
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, index=0, period=0.02):
+    def __init__(self, index=0, period=0.002):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self.period = period
         self._stop = threading.Event()
@@ -205,7 +212,9 @@ def run_reference(args, wl, rank):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
-        "config": workload_config(wl, "cpu (oracle port of the reference, rank 0)"),
+        "config": workload_config(wl),
+        "run": {"parallelism": "cpu (oracle port of the reference, rank 0's host cores)",
+                "iters_per_sample": "see cpu_baseline.sample"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
                          "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -213,11 +222,13 @@ def run_reference(args, wl, rank):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(wl, parallelism):
+def workload_config(wl):
+    """The workload only -- identical in both arms (the driver compares them)."""
     n, m = wl.shape
     cfg = {"workload": wl.name, "n": n, "m": m, "d": wl.d, "threshold": wl.threshold,
-           "max_iters": wl.max_iters, "parallelism": parallelism,
-           "l2": "flushed (512 MiB write) before every timed step"}
+           "max_iters": wl.max_iters, "inner_iters": wl.inner_iters,
+           "weights": "uniform" if wl.a is None else "non-uniform (U(0.5,1.5), normalised)",
+           "l2": "flushed (512 MiB write) before every timed step (GPU arm)"}
     if wl.materialised:
         cfg["batch"] = int(wl.x.shape[0])
         cfg["eps"] = "per problem: 0.05 x exact mean cost"
@@ -423,6 +434,7 @@ def run_ours(args, wl, rank, world):
     import torch
     import paper_2201_12324_b200 as otk
     from paper_2201_12324_b200 import _native as N
+    from paper_2201_12324_b200 import workloads
     dev = torch.device("cuda", local_device())
     torch.cuda.set_device(dev)
     N.lib()
@@ -431,12 +443,16 @@ def run_ours(args, wl, rank, world):
 
     kw_step = solve_kw(wl, args.iters)
     kw_tol = solve_kw(wl, 0)
+    tol_note = "one tolerance solve from device-resident points"
     if wl.materialised:
         xd = torch.from_numpy(wl.x).to(dev)
         yd = torch.from_numpy(wl.y).to(dev)
 
         def make_solve(kw):
             return lambda: otk.solve_sinkhorn_batched(xd, yd, wl.eps, **kw)
+
+        solve_tol = make_solve(kw_tol)
+        tol_note += " (cost build included; per-problem eps given)"
 
         def cells_of(outs):
             return float(n) * m * float(np.sum(outs.iterations))
@@ -448,15 +464,29 @@ def run_ours(args, wl, rank, world):
         xd = torch.from_numpy(wl.x[lo:hi]).to(dev)
         yd = torch.from_numpy(wl.y).to(dev)
         a_loc = None if wl.a is None else wl.a[lo:hi]
+        ix, iy = workloads.subsample_rows(n, m, wl.eps_subsample_seed or 0)
+        x_sub = torch.from_numpy(wl.x[ix] if wl.eps_subsample_seed is not None else wl.x).to(dev)
 
-        sprob = otk.ShardedProblem(xd, yd, a_loc, wl.b, x_is_local=True, n_total=n, comm=comm,
-                                   impl=args.kernel)
+        def new_problem():
+            return otk.ShardedProblem(xd, yd, a_loc, wl.b, x_is_local=True, n_total=n, comm=comm,
+                                      impl=args.kernel)
+        sprob = new_problem()
 
         def make_solve(kw):
             def solve():
                 return sprob.solve(wl.eps, **kw)
             solve.sharded_problem = sprob
             return solve
+
+        def solve_tol():
+            sp = new_problem()
+            sub = wl if wl.eps_subsample_seed is None else \
+                workloads.Workload(wl.name, wl.x, wl.y, None, None, wl.eps, wl.threshold,
+                                   wl.max_iters, eps_scale=wl.eps_scale)
+            e = workloads.estimate_eps_device(sub, x_sub, yd[torch.as_tensor(iy, device=dev)]
+                                              if wl.eps_subsample_seed is not None else yd)
+            return sp.solve(e, **kw_tol)
+        tol_note += " (shard prep + on-device eps estimate included)"
 
         def cells_of(out):
             return float(n) * m * out.iterations
@@ -472,11 +502,17 @@ def run_ours(args, wl, rank, world):
         def make_solve(kw):
             return lambda: otk.solve_sinkhorn(prob, wl.eps, impl=args.kernel, **kw)
 
+        def solve_tol():
+            g2 = otk.PointCloudGeometry(xd, yd)
+            e = workloads.estimate_eps_device(wl, xd, yd)
+            return otk.solve_sinkhorn(otk.LinearProblem(g2, wl.a, wl.b), e, impl=args.kernel,
+                                      **kw_tol)
+        tol_note += " (geometry prep + on-device eps estimate included)"
+
         def cells_of(out):
             return float(n) * m * out.iterations
         parallelism = "single GPU"
     solve = make_solve(kw_step)
-    solve_tol = make_solve(kw_tol)
 
     # the dominant kernel, timed alone BEFORE the long timed region (the burst
     # peak applies; after minutes of solves the part sits at its power cap)
@@ -529,38 +565,38 @@ def run_ours(args, wl, rank, world):
     def summary(o):
         its = int(np.max(o.iterations)) if wl.materialised else o.iterations
         cv = bool(np.all(o.converged)) if wl.materialised else bool(o.converged)
-        return its, cv
-    iters, conv = summary(outs[-1])
-    # time-to-tolerance: the workload's own threshold / max_iters, same timing rules
-    if kw_step == kw_tol:
-        tol_ms, tol_iters, tol_conv = 1e3 * total / args.steps, iters, conv
-    else:
-        for _ in range(2):
-            solve_tol()
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        t_tol, o_tol = timed_steps(solve_tol, args.steps, dev, flush)
-        tt = sum(t_tol)
-        if world > 1:
-            t = torch.tensor([tt], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            tt = float(t.item())
-        tol_ms = 1e3 * tt / args.steps
-        tol_iters, tol_conv = summary(o_tol[-1])
-    config = workload_config(wl, parallelism)
+        nchk = int(np.max([len(o[k].errors) for k in range(len(o.iterations))])) \
+            if wl.materialised else len(o.errors)
+        return its, cv, nchk
+    iters, conv, _ = summary(outs[-1])
+    # time-to-tolerance: the workload's own threshold / max_iters, same timing rules,
+    # prep and eps estimate inside the timed call
+    for _ in range(2):
+        solve_tol()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t_tol, o_tol = timed_steps(solve_tol, args.steps, dev, flush)
+    tt = sum(t_tol)
+    if world > 1:
+        t = torch.tensor([tt], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tt = float(t.item())
+    tol_ms = 1e3 * tt / args.steps
+    tol_iters, tol_conv, tol_checks = summary(o_tol[-1])
     step_desc = (f"one fixed {kw_step['max_iters']}-iteration solve (threshold 1e-300, checks every "
                  f"{wl.inner_iters} as in the reference; SURVEY.md §8d: throughput from "
                  "fixed-iteration runs), inputs resident in HBM" if args.iters
                  else "one complete solve to tolerance (inputs resident in HBM)")
-    config.update({"iterations_per_step": iters, "converged": conv, "step": step_desc,
-                   "time_to_tolerance_ms": tol_ms, "tolerance_iterations": tol_iters,
-                   "tolerance_converged": tol_conv, "kernel": args.kernel})
+    run = {"parallelism": parallelism, "iterations_per_step": iters, "converged": conv,
+           "step": step_desc, "time_to_tolerance_ms": tol_ms, "tolerance_iterations": tol_iters,
+           "tolerance_converged": tol_conv, "tolerance_checks": tol_checks,
+           "time_to_tolerance_note": tol_note, "kernel": args.kernel}
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": n_w, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": DATA, "config": config,
-        "clocks": clocks.summary(),
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": DATA,
+        "config": workload_config(wl), "run": run, "clocks": clocks.summary(),
     }
 
     # launches of our kernels per step (native solver count / sharded engine count)
@@ -576,8 +612,17 @@ def run_ours(args, wl, rank, world):
         result["roofline"] = roofline
         if not args.no_cpu and world == 1:
             v, dt, desc = cpu_sample_rate(wl)
-            result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cpu_cores(),
-                                      "kind": "port", "sample": f"{desc}, {dt:.1f} s"}
+            # the reference's time for the same tolerance solve: its half-steps
+            # (2 per iteration + 1 per check) at the measured CPU rate
+            half_steps = 2.0 * tol_iters + tol_checks
+            cpu_ttt = half_steps * 0.5 * float(n) * m * (wl.x.shape[0] if wl.materialised else 1) / v
+            result["cpu_baseline"] = {
+                "value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+                "sample": f"{desc}, {dt:.1f} s",
+                "time_to_tolerance_s_extrapolated": cpu_ttt,
+                "time_to_tolerance_note": (f"extrapolated: the GPU tolerance solve's {tol_iters} "
+                                           f"iterations + {tol_checks} checks = {half_steps:.0f} "
+                                           "half-steps at the sampled CPU rate")}
         print(json.dumps(result), flush=True)
 
 
@@ -705,10 +750,47 @@ def local_device() -> int:
     return int(os.environ.get("LOCAL_RANK", 0))
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: run this same command as N ranks of
+    ``torch.distributed.run`` (one node, 127.0.0.1) and return its exit code."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def plumbing(args, rank, world):
+    """(test) the multi-rank launch: gloo ranks agree on the world size."""
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    t = torch.tensor([float(rank)])
+    dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"plumbing": True, "n_gpus": world, "gpus_arg": args.gpus,
+                          "rank_sum": float(t.item())}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        sys.exit(relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.impl != "reference" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.plumbing:
+        plumbing(args, rank, world)
+        return
     from paper_2201_12324_b200 import workloads
     if args.impl == "reference":
         if rank != 0:

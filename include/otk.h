@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define OTK_ABI_VERSION 4
+#define OTK_ABI_VERSION 5
 
 enum otk_status {
   OTK_OK = 0,
@@ -75,6 +75,18 @@ int otk_device_query(int device, int *sm_count, int *cc_major, int *cc_minor);
 int otk_prep_points(const float *pts, int64_t n, int32_t d, float *sqnorm,
                     uint16_t *hi, uint16_t *lo, uint16_t *ext_a, uint16_t *ext_b,
                     int32_t dpad, float split_scale, void *stream);
+
+/* Translation (before K0).  The cost is translation-invariant; the reference
+ * forms _cost_block (geometry.py:268-273) in float64, where a common offset of
+ * the clouds costs nothing, but float32 |p|^2 + |q|^2 - 2<p,q> loses
+ * ~ulp(|p|^2) to cancellation.  Both sets are therefore shifted by one common
+ * centre before prep: otk_column_mean writes mean[k] = (1/m) sum_j q_jk in
+ * float64 (fixed-order, deterministic; ws of otk_center_workspace_bytes(m, d)
+ * bytes), otk_shift_points writes out = fp32(p - center) (out may not alias p). */
+size_t otk_center_workspace_bytes(int64_t m, int32_t d);
+int otk_column_mean(const float *q, int64_t m, int32_t d, double *mean, void *ws, void *stream);
+int otk_shift_points(const float *p, int64_t n, int32_t d, const double *center, float *out,
+                     void *stream);
 
 /* max |p_ik| over the array (for choosing split_scale); out is one float. */
 int otk_absmax(const float *pts, int64_t count, float *out, void *stream);
@@ -151,9 +163,13 @@ int otk_lse_finalize(const float *partial, int32_t nsplit, int64_t np,
  * one flag per 256-row block on every peer; otk_exchange_finalize waits for
  * the W flags of each block (acquire), combines the W partials in rank order
  * and applies the finalize mode -- g bitwise equal on all ranks and to the
- * all-gather + otk_lse_finalize path.  epoch >= 1 grows by one per exchange,
- * identical on all ranks.  A wait longer than timeout_ms (0 = 10 s) sets the
- * buffer's error word (otk_exchange_status != 0) instead of hanging. */
+ * all-gather + otk_lse_finalize path.  epoch: 0 = device-counted (the push
+ * and the combine use one past the buffer's count of completed combines; the
+ * combine advances it -- replayable inside CUDA graphs; what every caller of
+ * this library uses), or an explicit epoch >= 1 growing by one per exchange,
+ * identical on all ranks (the two must not be mixed on one buffer).  A wait
+ * longer than timeout_ms (0 = 10 s) sets the buffer's error word
+ * (otk_exchange_status != 0) instead of hanging. */
 typedef struct otk_exchange {
   void *local;         /* this rank's exchange buffer (device) */
   int32_t world, rank;
@@ -172,6 +188,14 @@ int otk_exchange_finalize(void *local, int32_t world, int64_t m, uint32_t epoch,
                           float *out_pot, float *out_bias, int32_t *first_bad, int32_t step,
                           uint32_t timeout_ms /* 0 = 10 s */, void *stream);
 int otk_exchange_status(void *local, int32_t *status, void *stream);
+/* Check-sum exchange of a sharded solve (sinkhorn.py:175-189 over row
+ * shards): sums[0..7] = this rank's otk_check output, *first_bad = its first
+ * bad step; out[0..7] = the rank-order totals every rank computes alike
+ * ([3], [5], [7] -- the replicated g terms -- from rank 0), out[8] = min
+ * first-bad step over ranks, out[9] = nonzero if any rank's exchange timed
+ * out.  One single-block launch; epochs device-counted. */
+int otk_exchange_check(void *local, int32_t world, int32_t rank, int64_t m, const double *sums,
+                       const int32_t *first_bad, double *out, uint32_t timeout_ms, void *stream);
 
 size_t otk_lse_step_workspace_bytes(int64_t np);
 /* 1 if otk_lse_step anchors on this path AND the half-step is long enough for
@@ -355,6 +379,19 @@ int otk_bench_read(const float *buf, int64_t bytes, double *gbs, void *stream);
  * (grid-wide barriers between half-steps, fused check, launches = 1);
  * everything else runs the general loop (CUDA graphs per check period). */
 int otk_solve_pointcloud(otk_solve_args *args);
+
+/* Row-sharded whole solve, one rank per GPU: args describes
+ * THIS rank's rows (x, n, a, log_a: the shard; y, b, log_b, g_init:
+ * replicated; flags must include OTK_IMPL_NOPERSIST).  The g half-step's
+ * column partials and the check sums travel through xchg (epoch 0) -- the
+ * same loop, outputs and error outcomes as otk_solve_pointcloud, identical g
+ * and check trace on every rank, no host collective, one host sync per
+ * check, CUDA-graph check periods.  split_scale: the common operand scale
+ * (otk_split_scale of the max |coordinate| over ALL ranks; <= 0 = this
+ * rank's own).  Returns OTK_ENCCL when a peer did not answer within
+ * timeout_ms (0 = 10 s) -- on every rank at the same check. */
+int otk_solve_pointcloud_sharded(otk_solve_args *args, const otk_exchange *xchg,
+                                 float split_scale, uint32_t timeout_ms);
 
 #ifdef __cplusplus
 }

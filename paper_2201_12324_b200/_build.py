@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import glob
+import hashlib
 import os
 import shutil
 import subprocess
@@ -30,6 +31,34 @@ def nvcc() -> str:
         if cand and os.path.exists(cand):
             return cand
     raise RuntimeError("nvcc not found: cannot build the sm_100a library")
+
+
+HASH_FILE = LIB + ".srchash"
+
+
+def source_hash() -> str:
+    """sha256 over every source the library is built from (csrc/*.cu, *.cuh,
+    include/*.h) and the compile flags."""
+    h = hashlib.sha256(" ".join(ARCH + FLAGS[:4]).encode())
+    files = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+                   + glob.glob(os.path.join(ROOT, "include", "*.h")))
+    for f in files:
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
+def stale_reason() -> str | None:
+    """Why the in-tree library does not match the sources (None = it does).
+    The built .so travels to the GPU box with the sources; a library built
+    from other sources must not be loaded silently."""
+    if not os.path.exists(HASH_FILE):
+        return "no source hash recorded next to the library"
+    with open(HASH_FILE) as fh:
+        if fh.read().strip() != source_hash():
+            return "built from different sources"
+    return None
 
 
 def _deps_mtime() -> float:
@@ -67,6 +96,10 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if res.returncode != 0:
             raise RuntimeError(f"nvcc link failed:\n{res.stderr}")
         os.replace(tmp, LIB)
+    digest = source_hash()
+    if stale_reason() is not None:
+        with open(HASH_FILE, "w") as fh:
+            fh.write(digest + "\n")
     return LIB
 
 

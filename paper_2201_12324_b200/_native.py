@@ -23,7 +23,7 @@ OTK_IMPL_NOPERSIST = 0x40
 OTK_ANCHOR_INIT, OTK_IMPL_NOANCHOR = 0x80, 0x100
 OTK_COST_EUCL = 0x4
 OTK_FIN_SOLVER, OTK_FIN_APPLY, OTK_FIN_LOG2 = 0, 1, 2
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 P = C.c_void_p
 I64, I32, F32, F64, SZ = C.c_int64, C.c_int32, C.c_float, C.c_double, C.c_size_t
@@ -58,6 +58,9 @@ SIGNATURES = {
     "otk_prep_points": (C.c_int, [P, I64, I32, P, P, P, P, P, I32, F32, P]),
     "otk_split_scale": (F32, [F32, I32]),
     "otk_absmax": (C.c_int, [P, I64, P, P]),
+    "otk_center_workspace_bytes": (SZ, [I64, I32]),
+    "otk_column_mean": (C.c_int, [P, I64, I32, P, P, P]),
+    "otk_shift_points": (C.c_int, [P, I64, I32, P, P, P]),
     "otk_make_bias": (C.c_int, [P, I64, F32, P, P, I32, P]),
     "otk_lse_partial": (C.c_int, [P, P, P, P, P, I64, P, P, P, P, P, I64, I32, I32, F32, P, F32,
                                   I32, I32, P, P]),
@@ -78,6 +81,7 @@ SIGNATURES = {
     "otk_exchange_finalize": (C.c_int, [P, I32, I64, C.c_uint32, P, I32, F32, F32, P, P, P, I32,
                                         C.c_uint32, P]),
     "otk_exchange_status": (C.c_int, [P, P, P]),
+    "otk_exchange_check": (C.c_int, [P, I32, I32, I64, P, P, P, C.c_uint32, P]),
     "otk_check_workspace_bytes": (SZ, []),
     "otk_check": (C.c_int, [P, P, P, I64, P, P, I64, F64, P, P, P]),
     "otk_cost_workspace_bytes": (SZ, [I64, I64]),
@@ -102,6 +106,8 @@ SIGNATURES = {
                                        P, P]),
     "otk_solve_workspace_bytes": (SZ, [C.POINTER(SolveArgs)]),
     "otk_solve_pointcloud": (C.c_int, [C.POINTER(SolveArgs)]),
+    "otk_solve_pointcloud_sharded": (C.c_int, [C.POINTER(SolveArgs), C.POINTER(Exchange), F32,
+                                               C.c_uint32]),
 }
 
 
@@ -117,6 +123,12 @@ def lib():
             raise RuntimeError(
                 f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
                 "g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+        if not os.environ.get("OTK_LIB"):
+            from . import _build
+            stale = _build.stale_reason()
+            if stale:
+                raise RuntimeError(f"{_LIB_PATH} is stale ({stale}): rebuild it with "
+                                   "`python -c 'import __graft_entry__ as g; g.build()'`")
         handle = C.CDLL(_LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(handle, name)

@@ -90,9 +90,7 @@ def _support_costs(geom):
     if isinstance(geom, DenseGeometry):
         C = geom._c()
     elif isinstance(geom, PointCloudGeometry):
-        gx, gy = geom._dev_pts if getattr(geom, "_dev_pts", None) is not None else (geom.x, geom.y)
-        px = as_device_f32(geom._kernel_points(gx)).contiguous()
-        py = px if geom._same_points else as_device_f32(geom._kernel_points(gy)).contiguous()
+        px, py = geom._points()  # centred kernel points (geometry.centered_points)
         C = torch.empty((n, n), dtype=torch.float32, device=px.device)
         N.check(lib.otk_dense_cost(N.ptr(px), N.ptr(py), 1, n, n, px.shape[1],
                                    geom._cost_flags, N.ptr(C),

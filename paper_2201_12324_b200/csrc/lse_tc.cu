@@ -3,10 +3,11 @@
 // streaming log2-sum-exp2 epilogue read straight out of TMEM.
 //
 // Replaces PointCloudGeometry.apply_lse_kernel (reference geometry.py:336-354)
-// for d >= 4 (solve.cu: want_tc).  Identical point sets: C_ii comes out of the
-// split products as 0 up to fp32 rounding (|C_ii| <~ 1e-6 |p_i|^2), not
-// forced to an exact zero as the FP32 kernels do (geometry.py:278-292); the
-// effect on the potentials is far below the 1e-4 parity tolerance (tested).  Contract (include/otk.h, otk_lse_partial):
+// for every d (solve.cu: want_tc).  Identical point sets: the split products
+// leave C_ii at 0 only up to fp32 rounding (|C_ii| <~ 1e-6 |p_i|^2), so the
+// same-points instantiation (epilogue mode EU == 2) forces the diagonal to an
+// exact zero like the reference (geometry.py:278-292) with a per-register bit
+// test; the default instantiation carries no such test.  Contract (include/otk.h, otk_lse_partial):
 //     partial_i = log2 sum_j 2^(kappa*g_j - kappa*C_ij),  C_ij = |p_i|^2+|q_j|^2-2<p_i,q_j>
 // The dot products run on the tensor cores in split-fp16 ("3xFP16"): every
 // fp32 coordinate is pre-split (K0, otk_prep_points) into hi = fp16(s*x),
@@ -334,6 +335,24 @@ __device__ __forceinline__ void eucl_transform(float *acc, int64_t row, int64_t 
   }
 }
 
+// sqeucl, identical point sets (epilogue mode 2): acc = -s^2 C / 2 -> exactly 0
+// on the diagonal (geometry.py:278-292), same bit test as eucl_transform.
+template <int CH>
+__device__ __forceinline__ void diag_zero(float *acc, int64_t row, int64_t col0) {
+  const int64_t dd = row - col0;
+  const uint32_t diag = (dd >= 0 && dd < CH) ? (1u << (int)dd) : 0u;
+  if (diag == 0u) return;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) acc[i] = ((diag >> i) & 1u) ? 0.f : acc[i];
+}
+
+// Epilogue cost transform: EU 0 = sqeucl, 1 = eucl, 2 = sqeucl with an exact-zero diagonal.
+template <int EU, int CH>
+__device__ __forceinline__ void cost_transform(float *acc, int64_t row, int64_t col0, int same) {
+  if constexpr (EU == 1) eucl_transform<CH>(acc, row, col0, same);
+  else if constexpr (EU == 2) diag_zero<CH>(acc, row, col0);
+}
+
 template <int CH, bool MASK, int EP>
 __device__ __forceinline__ void lse_chunk(const float *acc, const float *bias, float c2k, int valid,
                                           float &m, float &s) {
@@ -422,7 +441,7 @@ __device__ __forceinline__ float anchored_value(float S, float s) {
 }
 __device__ __forceinline__ float sanitize_anchor(float S) { return isfinite(S) ? S : 0.f; }
 
-template <int V, bool A_RES, int NS, int ABUF, int EP, int NG, bool EU, bool FIX>
+template <int V, bool A_RES, int NS, int ABUF, int EP, int NG, int EU, bool FIX>
 __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
     lse_tc_kernel(const __grid_constant__ CUtensorMap tm_phi, const __grid_constant__ CUtensorMap tm_plo,
                   const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo,
@@ -704,7 +723,7 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
             bv[4 * i + 2] = q.z;
             bv[4 * i + 3] = q.w;
           }
-          if constexpr (EU) eucl_transform<C::CH>(accv, (int64_t)rt * BM + row_local, j0 + c * C::CH, prm.same);
+          if constexpr (EU != 0) cost_transform<EU, C::CH>(accv, (int64_t)rt * BM + row_local, j0 + c * C::CH, prm.same);
           if (prm.probe == 1) {
             s += accv[0];
           } else if (prm.probe == 2) {
@@ -765,7 +784,7 @@ __global__ void __launch_bounds__(Cfg<V, NG>::THREADS, 1)
               bv[4 * i + 2] = q.z;
               bv[4 * i + 3] = q.w;
             }
-            if constexpr (EU) eucl_transform<16>(accv, (int64_t)rt * BM + row_local, j0 + col0 + h, prm.same);
+            if constexpr (EU != 0) cost_transform<EU, 16>(accv, (int64_t)rt * BM + row_local, j0 + col0 + h, prm.same);
             const int vh = valid - col0 - h;
             if constexpr (FIX) {
               if (vh >= 16) lse_chunk_anchored<16, false>(accv, bv, c2k, m, 0, s);
@@ -920,7 +939,7 @@ struct Plan2 {
                               2 * (NG - 1) * 2 * BM * (int)sizeof(float);
 };
 
-template <int KB, bool EU, bool FIX>
+template <int KB, int EU, bool FIX>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     lse_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_phi, const __grid_constant__ CUtensorMap tm_plo,
                        const __grid_constant__ CUtensorMap tm_qhi, const __grid_constant__ CUtensorMap tm_qlo,
@@ -1123,7 +1142,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           float accv[CH], bv[CH];
 #pragma unroll
           for (int i = 0; i < CH; ++i) accv[i] = __uint_as_float(v[i]);
-          if constexpr (EU) eucl_transform<CH>(accv, (int64_t)rt * BM + row_local, j0 + c * CH, prm.same);
+          if constexpr (EU != 0) cost_transform<EU, CH>(accv, (int64_t)rt * BM + row_local, j0 + c * CH, prm.same);
           const float4 *bp = reinterpret_cast<const float4 *>(bias + c * CH);
 #pragma unroll
           for (int i = 0; i < CH / 4; ++i) {
@@ -1275,7 +1294,7 @@ static int emu_pairs(int v) {
   return 0;  // measured: the split-column epilogue is no longer MUFU-bound at d = 64
 }
 
-template <int V, bool A_RES, int NS, int ABUF, int EP, int NG, bool EU = false, bool FIX = false>
+template <int V, bool A_RES, int NS, int ABUF, int EP, int NG, int EU = 0, bool FIX = false>
 static int launch_one(const CUtensorMap (&maps)[7], const Params &prm, cudaStream_t st) {
   using L = Plan<V, A_RES, NS, ABUF, NG>;
   const int smem = L::smem_bytes(prm.kb);
@@ -1303,18 +1322,22 @@ static int epi_groups() {
 }
 
 template <int V, bool A_RES, int NS, int ABUF>
-static int launch_variant(const CUtensorMap (&maps)[7], const Params &prm, bool eucl, bool fix,
+static int launch_variant(const CUtensorMap (&maps)[7], const Params &prm, int eu, bool fix,
                           cudaStream_t st) {
-  if (eucl) return launch_one<V, A_RES, NS, ABUF, 0, 4, true>(maps, prm, st);  // default knobs only
+  if (eu == 1) return launch_one<V, A_RES, NS, ABUF, 0, 4, 1>(maps, prm, st);  // default knobs only
+  if (eu == 2) {  // identical point sets: exact-zero diagonal, default knobs only
+    return fix ? launch_one<V, A_RES, NS, ABUF, 0, 4, 2, true>(maps, prm, st)
+               : launch_one<V, A_RES, NS, ABUF, 0, 4, 2>(maps, prm, st);
+  }
   if (fix) {
     if constexpr (V == 1) {
       switch (emu_pairs(V)) {
-        case 1: return launch_one<V, A_RES, NS, ABUF, 1, 4, false, true>(maps, prm, st);
-        case 2: return launch_one<V, A_RES, NS, ABUF, 2, 4, false, true>(maps, prm, st);
+        case 1: return launch_one<V, A_RES, NS, ABUF, 1, 4, 0, true>(maps, prm, st);
+        case 2: return launch_one<V, A_RES, NS, ABUF, 2, 4, 0, true>(maps, prm, st);
         default: break;
       }
     }
-    return launch_one<V, A_RES, NS, ABUF, 0, 4, false, true>(maps, prm, st);
+    return launch_one<V, A_RES, NS, ABUF, 0, 4, 0, true>(maps, prm, st);
   }
   if constexpr (V == 4) {  // the V4 slice-release epilogue is written for 4 groups
     return launch_one<V, A_RES, NS, ABUF, 0, 4>(maps, prm, st);
@@ -1341,7 +1364,7 @@ static bool use_pair_kernel(int kb) {
   return kb == 2;
 }
 
-template <int KB, bool EU, bool FIX = false>
+template <int KB, int EU, bool FIX = false>
 static int launch_pair(const CUtensorMap (&maps)[7], const Params &prm, cudaStream_t st) {
   using L = pair::Plan2<KB>;
   auto kern = pair::lse_tc_pair_kernel<KB, EU, FIX>;
@@ -1433,12 +1456,12 @@ int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_
   prm.tps = (prm.ntiles + nsplit - 1) / nsplit;
   prm.num_units = prm.row_tiles * nsplit;
   prm.c2k = two_kappa_scaled;
-  prm.same = same;  // used by the eucl epilogue only (see the file header)
+  prm.same = same;  // eucl epilogue; sqeucl selects the exact-diagonal instantiation
   prm.partial = partial;
   prm.probe = getenv("OTK_TC_PROBE") ? atoi(getenv("OTK_TC_PROBE")) : 0;
-  const bool eu = eucl != 0;
+  const int eu = eucl != 0 ? 1 : (same ? 2 : 0);
   const bool fix = anchor != nullptr && !repair;
-  if (fix && eu) {
+  if (fix && eu == 1) {
     set_error("lse_tc: anchored launch needs the sqeucl epilogue");
     return OTK_EINVAL;
   }
@@ -1451,9 +1474,13 @@ int lse_tc_launch(const uint16_t *p_hi, const uint16_t *p_lo, const uint16_t *p_
   prm.nflags = prm.row_tiles + 1;
   prm.tile_mask = repair ? repair_ws + 1 : nullptr;
   if (use_pair) {
-    if (eu) return kb == 1 ? launch_pair<1, true>(maps, prm, st) : launch_pair<2, true>(maps, prm, st);
-    if (fix) return kb == 1 ? launch_pair<1, false, true>(maps, prm, st) : launch_pair<2, false, true>(maps, prm, st);
-    return kb == 1 ? launch_pair<1, false>(maps, prm, st) : launch_pair<2, false>(maps, prm, st);
+    if (eu == 1) return kb == 1 ? launch_pair<1, 1>(maps, prm, st) : launch_pair<2, 1>(maps, prm, st);
+    if (eu == 2) {
+      if (fix) return kb == 1 ? launch_pair<1, 2, true>(maps, prm, st) : launch_pair<2, 2, true>(maps, prm, st);
+      return kb == 1 ? launch_pair<1, 2>(maps, prm, st) : launch_pair<2, 2>(maps, prm, st);
+    }
+    if (fix) return kb == 1 ? launch_pair<1, 0, true>(maps, prm, st) : launch_pair<2, 0, true>(maps, prm, st);
+    return kb == 1 ? launch_pair<1, 0>(maps, prm, st) : launch_pair<2, 0>(maps, prm, st);
   }
   if (v == 1) {
     if (kb == 1) return launch_variant<1, true, 2, 2>(maps, prm, eu, fix, st);

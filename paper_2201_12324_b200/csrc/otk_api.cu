@@ -86,6 +86,40 @@ __global__ void prep_kernel(const float *__restrict__ pts, int64_t n, int d,
   }
 }
 
+// ---------------------------------------------------------------- translation
+// C is translation-invariant, so both point sets are shifted by one common
+// centre (the column mean of q, float64) before any kernel forms
+// |p|^2 + |q|^2 - 2<p,q> in float32: the cancellation error then scales with
+// the spread of the points, not with their distance from the origin.
+constexpr int kCenterRows = 256;
+
+__global__ void colsum_partial_kernel(const float *__restrict__ q, int64_t m, int d,
+                                      double *__restrict__ part) {
+  const int64_t r0 = (int64_t)blockIdx.x * kCenterRows;
+  const int64_t r1 = r0 + kCenterRows < m ? r0 + kCenterRows : m;
+  for (int k = threadIdx.x; k < d; k += blockDim.x) {
+    double acc = 0.0;
+    for (int64_t r = r0; r < r1; ++r) acc += (double)q[r * d + k];
+    part[(int64_t)blockIdx.x * d + k] = acc;
+  }
+}
+
+__global__ void colmean_final_kernel(const double *__restrict__ part, int nblk, int d, int64_t m,
+                                     double *__restrict__ mean) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= d) return;
+  double acc = 0.0;
+  for (int b = 0; b < nblk; ++b) acc += part[(int64_t)b * d + k];  // fixed order
+  mean[k] = acc / (double)m;
+}
+
+__global__ void shift_kernel(const float *__restrict__ p, int64_t count, int d,
+                             const double *__restrict__ c, float *__restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (float)((double)p[i] - c[i % d]);
+}
+
 __global__ void absmax_kernel(const float *__restrict__ p, int64_t count, unsigned *__restrict__ out) {
   float m = 0.f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
@@ -109,7 +143,8 @@ __global__ void bias_kernel(const float *__restrict__ pot, int64_t m, float kapp
 __device__ __forceinline__ void push_row(const FinArgs &F, int64_t i, float L) {
   const XLayout X(F.xworld, F.np);
   char *const *peers = reinterpret_cast<char *const *>(F.xlocal + X.table);
-  const int64_t off = ((int64_t)(F.xepoch & 1u) * F.xworld + F.xrank) * X.m_pad + i;
+  const unsigned epoch = exchange_epoch(F.xlocal, F.xepoch);
+  const int64_t off = ((int64_t)(epoch & 1u) * F.xworld + F.xrank) * X.m_pad + i;
   for (int s = 0; s < F.xworld; ++s) reinterpret_cast<float *>(peers[s] + X.data)[off] = L;
 }
 // After every thread of the block has pushed its rows: one release per peer
@@ -119,10 +154,11 @@ __device__ __forceinline__ void signal_block(const FinArgs &F) {
   if (threadIdx.x == 0) {
     const XLayout X(F.xworld, F.np);
     char *const *peers = reinterpret_cast<char *const *>(F.xlocal + X.table);
+    const unsigned epoch = exchange_epoch(F.xlocal, F.xepoch);
     __threadfence_system();
     for (int s = 0; s < F.xworld; ++s) {
       unsigned *flag = reinterpret_cast<unsigned *>(peers[s] + X.flags) + (size_t)F.xrank * X.nblk + blockIdx.x;
-      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(F.xepoch) : "memory");
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
     }
   }
 }
@@ -292,6 +328,36 @@ int otk_prep_points(const float *pts, int64_t n, int32_t d, float *sqnorm, uint1
   prep_kernel<<<(unsigned)blocks, warps * 32, 0, as_stream(stream)>>>(
       pts, n, d, sqnorm, reinterpret_cast<__half *>(hi), reinterpret_cast<__half *>(lo),
       reinterpret_cast<__half *>(ext_a), reinterpret_cast<__half *>(ext_b), dpad, split_scale);
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}
+
+size_t otk_center_workspace_bytes(int64_t m, int32_t d) {
+  if (m < 1 || d < 1) return 0;
+  return (size_t)((m + kCenterRows - 1) / kCenterRows) * d * sizeof(double);
+}
+
+int otk_column_mean(const float *q, int64_t m, int32_t d, double *mean, void *ws, void *stream) {
+  OTK_CHECK_ARG(q && mean && ws && m > 0 && d > 0, "otk_column_mean: bad arguments");
+  const int64_t nblk = (m + kCenterRows - 1) / kCenterRows;
+  OTK_CHECK_ARG(nblk <= INT32_MAX, "otk_column_mean: too many points");
+  cudaStream_t st = as_stream(stream);
+  const int thr = d >= 128 ? 128 : 32;
+  colsum_partial_kernel<<<(unsigned)nblk, thr, 0, st>>>(q, m, d, reinterpret_cast<double *>(ws));
+  OTK_LAUNCH_CHECK();
+  colmean_final_kernel<<<(d + 127) / 128, 128, 0, st>>>(reinterpret_cast<const double *>(ws),
+                                                        (int)nblk, d, m, mean);
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}
+
+int otk_shift_points(const float *p, int64_t n, int32_t d, const double *center, float *out,
+                     void *stream) {
+  OTK_CHECK_ARG(p && center && out && n > 0 && d > 0, "otk_shift_points: bad arguments");
+  const int64_t count = n * (int64_t)d;
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
+  shift_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(p, count, d, center, out);
   OTK_LAUNCH_CHECK();
   return OTK_OK;
 }

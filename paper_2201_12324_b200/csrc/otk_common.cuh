@@ -122,15 +122,20 @@ struct FinArgs {
   // of every peer's exchange buffer, then flag this block on every peer
   char *xlocal;   // this rank's exchange buffer (NULL = no push)
   int xworld, xrank;
-  unsigned xepoch;
+  unsigned xepoch;  // 0 = the buffer's device epoch counter (exchange_epoch)
 };
 
-// Exchange-buffer layout (p2p.cu, include/otk.h otk_exchange_*): header with
-// the error word, the peer pointer table, the partials [2][world][m_pad]
-// float, and the per-block flags [world][nblk] uint32 (nblk = ceil(m / 256),
-// the finalize kernels' block size).
+// Exchange-buffer layout (p2p.cu, include/otk.h otk_exchange_*): a header
+// (error word, device epoch counters), the peer pointer table, the partials
+// [2][world][m_pad] float, the per-block flags [world][nblk] uint32 (nblk =
+// ceil(m / 256), the finalize kernels' block size), and the check exchange:
+// slots [2][world][kChkSlot] double + flags [world] uint32.
+constexpr int kChkSlot = 16;
 struct XLayout {
-  size_t table, data, flags, total;
+  // header words (uint32): error, completed g exchanges, combine-block ticket,
+  // completed check exchanges
+  static constexpr size_t ERR = 0, EPOCH = 4, TICKET = 8, CHK_EPOCH = 12;
+  size_t table, data, flags, chk, chkflags, total;
   int64_t m_pad;
   int nblk;
   __host__ __device__ XLayout(int world, int64_t m) {
@@ -139,9 +144,20 @@ struct XLayout {
     table = 256;
     data = table + (((size_t)world * 8 + 255) / 256) * 256;
     flags = data + (((size_t)2 * world * m_pad * 4 + 255) / 256) * 256;
-    total = flags + (((size_t)world * nblk * 4 + 255) / 256) * 256;
+    chk = flags + (((size_t)world * nblk * 4 + 255) / 256) * 256;
+    chkflags = chk + (((size_t)2 * world * kChkSlot * 8 + 255) / 256) * 256;
+    total = chkflags + (((size_t)world * 4 + 255) / 256) * 256;
   }
 };
+__device__ __forceinline__ unsigned ld_cg_u32(const void *p) {
+  return __ldcg(reinterpret_cast<const unsigned *>(p));
+}
+// Epoch of the g exchange in flight: explicit (>= 1) or, with 0, one past the
+// buffer's count of completed combines (advanced by the combine kernel's last
+// block), so the same launches replay correctly inside a CUDA graph.
+__device__ __forceinline__ unsigned exchange_epoch(const char *local, unsigned explicit_epoch) {
+  return explicit_epoch ? explicit_epoch : ld_cg_u32(local + XLayout::EPOCH) + 1u;
+}
 // kind 0 = plain, 1 = after an anchored launch, 2 = after the repair launch
 int finalize_launch(int kind, const FinArgs &F, cudaStream_t st);
 

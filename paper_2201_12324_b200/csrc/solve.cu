@@ -258,6 +258,8 @@ struct Carver {
 
 struct Layout {
   float *fA, *fB, *g, *xsq, *ysq, *bias_x, *bias_y, *part;
+  float *lcol;                // sharded solve: this shard's log2 column partials
+  double *chk_tot;            // sharded solve: rank-order check totals (10 values)
   float *anc_x, *anc_y;       // anchors of the rows / cols half-steps (otk_lse_step)
   int *rep_x, *rep_y;         // their repair workspaces
   uint16_t *xhi, *xlo, *yhi, *ylo, *xea, *xeb, *yea, *yeb;
@@ -298,6 +300,8 @@ Layout plan(const otk_solve_args *A, void *ws) {
   L.bias_x = c.take<float>(A->n);
   L.bias_y = c.take<float>(A->m);
   L.part = c.take<float>(std::max((size_t)L.nsr * A->n, (size_t)L.nsc * A->m));
+  L.lcol = c.take<float>(A->m);
+  L.chk_tot = c.take<double>(16);
   L.anc_x = c.take<float>(A->n);
   L.anc_y = c.take<float>(A->m);
   L.rep_x = reinterpret_cast<int *>(c.take<char>(otk_lse_step_workspace_bytes(A->n)));
@@ -347,6 +351,15 @@ extern "C" size_t otk_solve_workspace_bytes(const otk_solve_args *A) {
     if (_r != OTK_OK) return _r; \
   } while (0)
 
+// Row-sharded solve (otk_solve_pointcloud_sharded): this rank holds rows
+// [lo, lo + n) of x; the g half-step's column partials go to every rank
+// through the peer-memory exchange (p2p.cu) and the check sums likewise.
+struct ShardCtx {
+  otk_exchange x;       // epoch 0: device-counted (graph-replayable)
+  int64_t m;
+  uint32_t timeout_ms;
+};
+
 // Half-steps go through otk_lse_step: the first of each role runs the
 // running-max kernel and records the per-row anchors, every later one is
 // anchored (TC sqeucl path; OTK_IMPL_NOANCHOR disables it).
@@ -357,6 +370,7 @@ struct HalfStep {
   float sinv;  // 1/s^2 for the TC operand scaling (one common scale s)
   int kflags;
   bool anchored;  // anchored path available for this problem
+  const ShardCtx *sh = nullptr;
   int launches = 0;
   bool have_x = false, have_y = false;
 
@@ -375,17 +389,67 @@ struct HalfStep {
     const int fl = kflags | (have_y ? 0 : OTK_ANCHOR_INIT);
     launches += (anchored && have_y) ? 4 : 2;
     have_y = true;
-    return otk_lse_step(A->y, L->ysq, L->yhi, L->ylo, L->yea, A->m, A->x, L->xsq, L->xhi, L->xlo,
-                        L->xeb, A->n, A->d, L->dpad, sinv, L->bias_x, kappa, fl, L->nsc, L->part,
-                        A->log_b, OTK_FIN_SOLVER, eps, kappa_next, L->g, L->bias_y, L->first_bad,
-                        step, anchored ? L->anc_y : nullptr, L->rep_y, nullptr, st);
+    if (sh == nullptr)
+      return otk_lse_step(A->y, L->ysq, L->yhi, L->ylo, L->yea, A->m, A->x, L->xsq, L->xhi, L->xlo,
+                          L->xeb, A->n, A->d, L->dpad, sinv, L->bias_x, kappa, fl, L->nsc, L->part,
+                          A->log_b, OTK_FIN_SOLVER, eps, kappa_next, L->g, L->bias_y, L->first_bad,
+                          step, anchored ? L->anc_y : nullptr, L->rep_y, nullptr, st);
+    // this shard's log2 partial per column (anchored on the shard's own previous
+    // partials), pushed to every rank by the half-step's last kernel; then the W
+    // partials of every column combined in rank order into g
+    int rc = otk_lse_step(A->y, L->ysq, L->yhi, L->ylo, L->yea, A->m, A->x, L->xsq, L->xhi, L->xlo,
+                          L->xeb, A->n, A->d, L->dpad, sinv, L->bias_x, kappa, fl, L->nsc, L->part,
+                          nullptr, OTK_FIN_LOG2, 0.f, 0.f, L->lcol, nullptr, nullptr, 0,
+                          anchored ? L->anc_y : nullptr, L->rep_y, &sh->x, st);
+    if (rc != OTK_OK) return rc;
+    launches += 1;
+    NvtxRange rx("otk g exchange combine");
+    return otk_exchange_finalize(sh->x.local, sh->x.world, A->m, 0u, A->log_b, OTK_FIN_SOLVER, eps,
+                                 kappa_next, L->g, L->bias_y, L->first_bad, step, sh->timeout_ms, st);
   }
+
+  // The fused check of this rank's rows; sharded: + the rank-order exchange
+  // of the sums.  The host reads `out` (8 sums; sharded: [8] = first bad
+  // step of any rank, [9] = exchange error) after one stream sync.
+  int check(const float *f, const float *fn, double eps) {
+    NvtxRange r("otk check");
+    int rc = otk_check(f, fn, A->a, A->n, L->g, A->b, A->m, eps, L->chk, L->chk_ws, st);
+    if (rc != OTK_OK || sh == nullptr) return rc;
+    launches += 1;
+    return otk_exchange_check(sh->x.local, sh->x.world, sh->x.rank, A->m, L->chk, L->first_bad,
+                              L->chk_tot, sh->timeout_ms, st);
+  }
+  const double *check_result() const { return sh ? L->chk_tot : L->chk; }
 };
 
 
-static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st);
+static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st, const ShardCtx *sh = nullptr,
+                           float split_scale = 0.f);
 
-extern "C" int otk_solve_pointcloud(otk_solve_args *A) {
+static int solve_entry(otk_solve_args *A, const ShardCtx *sh, float split_scale);
+
+extern "C" int otk_solve_pointcloud(otk_solve_args *A) { return solve_entry(A, nullptr, 0.f); }
+
+// Row-sharded whole solve: A describes THIS rank's rows (x, n, a, log_a are
+// the shard's; y, b, log_b, g_init are replicated).  Same loop and outputs as
+// otk_solve_pointcloud, with the g half-step's column partials and the check
+// sums exchanged over peer memory (p2p.cu) -- no host collective; one host
+// sync per check; constant-eps check periods replayed as CUDA graphs (the
+// exchange epochs are device-counted).  g_out and the check trace are
+// identical on every rank; a world-1 exchange is bitwise equal to
+// otk_solve_pointcloud's general loop.
+extern "C" int otk_solve_pointcloud_sharded(otk_solve_args *A, const otk_exchange *xchg,
+                                            float split_scale, uint32_t timeout_ms) {
+  OTK_CHECK_ARG(xchg && xchg->local && xchg->world >= 1 && xchg->rank >= 0 &&
+                    xchg->rank < xchg->world && xchg->epoch == 0u,
+                "otk_solve_pointcloud_sharded: bad exchange (epoch must be 0: device-counted)");
+  OTK_CHECK_ARG(A && (A->flags & OTK_IMPL_NOPERSIST) && A->same_points == 0,
+                "otk_solve_pointcloud_sharded: needs OTK_IMPL_NOPERSIST and distinct point sets");
+  ShardCtx sh{*xchg, A->m, timeout_ms};
+  return solve_entry(A, &sh, split_scale);
+}
+
+static int solve_entry(otk_solve_args *A, const ShardCtx *sh, float split_scale) {
   OTK_CHECK_ARG(A && A->x && A->y && A->a && A->b && A->log_a && A->log_b && A->f_out && A->g_out,
                 "otk_solve_pointcloud: missing pointers");
   OTK_CHECK_ARG(A->n > 0 && A->m > 0 && A->d > 0, "otk_solve_pointcloud: bad shape");
@@ -406,7 +470,7 @@ extern "C" int otk_solve_pointcloud(otk_solve_args *A) {
   OTK_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
   OTK_CUDA(cudaEventRecord(ev_in, caller));
   OTK_CUDA(cudaStreamWaitEvent(st, ev_in, 0));
-  int rc = solve_on_stream(A, L, st);
+  int rc = solve_on_stream(A, L, st, sh, split_scale);
   cudaEventRecord(ev_out, st);
   cudaStreamWaitEvent(caller, ev_out, 0);
   cudaStreamSynchronize(st);
@@ -482,8 +546,33 @@ static int solve_small(otk_solve_args *A, Layout &L, cudaStream_t st) {
   return state[3];
 }
 
-static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st) {
-  NvtxRange range("otk_solve_pointcloud");
+// Host view of one check: the 8 sums of sinkhorn.py:183-186 + the first bad
+// step; sharded: the rank-order totals, any rank's first bad step and the
+// exchange error word, all from one D2H read after one stream sync.
+struct CheckRead {
+  double v[10];
+  int fb;
+};
+static int read_check(const HalfStep &H, Layout &L, cudaStream_t st, CheckRead *cr) {
+  if (H.sh) {
+    OTK_CUDA(cudaMemcpyAsync(cr->v, L.chk_tot, sizeof(cr->v), cudaMemcpyDeviceToHost, st));
+    OTK_CUDA(cudaStreamSynchronize(st));
+    cr->fb = (int)cr->v[8];
+    if (cr->v[9] != 0.0) {
+      set_error("peer-memory exchange timed out waiting for another rank");
+      return OTK_ENCCL;
+    }
+    return OTK_OK;
+  }
+  OTK_CUDA(cudaMemcpyAsync(cr->v, L.chk, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  OTK_CUDA(cudaMemcpyAsync(&cr->fb, L.first_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  OTK_CUDA(cudaStreamSynchronize(st));
+  return OTK_OK;
+}
+
+static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st, const ShardCtx *sh,
+                           float split_scale) {
+  NvtxRange range(sh ? "otk_solve_pointcloud_sharded" : "otk_solve_pointcloud");
   A->n_checks = 0;
   A->iterations = 0;
   A->converged = 0;
@@ -492,7 +581,9 @@ static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st) {
 
   // ---- prep (K0)
   float s = 1.f;  // one common power-of-two operand scale for x and y
-  if (L.tc) {
+  if (L.tc && split_scale > 0.f) {
+    s = split_scale;  // sharded: common to every rank (from the global |coordinate| max)
+  } else if (L.tc) {
     float amax[2];
     OTK_TRY(otk_absmax(A->x, A->n * (int64_t)A->d, L.absmax, st));
     OTK_TRY(otk_absmax(A->y, A->m * (int64_t)A->d, L.absmax + 1, st));
@@ -509,6 +600,7 @@ static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st) {
              (A->flags & (OTK_IMPL_SIMT | OTK_IMPL_TC | OTK_COST_EUCL)) | OTK_CLAMP |
                  (A->same_points ? OTK_SAME_POINTS : 0)};
   H.anchored = L.tc && !(A->flags & OTK_IMPL_NOANCHOR) && otk_lse_step_anchored(A->n, A->m, A->d, H.kflags);
+  H.sh = sh;
 
   // ---- initial g (zeros or warm start) and its bias for h = 1
   const double e0 = eps_at(A, 0);
@@ -551,7 +643,7 @@ static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st) {
           if (rc == OTK_OK) rc = H.cols(kap, (float)e, kap, k + 1 == A->inner_iters ? 3 : 2);
         }
         if (rc == OTK_OK) rc = H.rows(kap, (float)e, kap, fn, 4);
-        if (rc == OTK_OK) rc = otk_check(f, fn, A->a, A->n, L.g, A->b, A->m, e, L.chk, L.chk_ws, st);
+        if (rc == OTK_OK) rc = H.check(f, fn, e);
         cudaError_t ce = cudaStreamEndCapture(st, &graph);
         graph_launches = H.launches - before + 1;
         H.launches = before;
@@ -567,11 +659,10 @@ static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st) {
       OTK_CUDA(cudaGraphLaunch(period_exec[which], st));
       extra_launches += graph_launches;
       t = t_end;
-      double out[8];
-      int fb;
-      OTK_CUDA(cudaMemcpyAsync(out, L.chk, sizeof(out), cudaMemcpyDeviceToHost, st));
-      OTK_CUDA(cudaMemcpyAsync(&fb, L.first_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-      OTK_CUDA(cudaStreamSynchronize(st));
+      CheckRead cr;
+      if ((status = read_check(H, L, st, &cr)) != OTK_OK) break;
+      const double *out = cr.v;
+      const int fb = cr.fb;
       if (fb <= 2) { status = OTK_BAD_POTENTIAL; A->fail_iter = t; break; }
       if (out[4] > 0 || out[5] > 0) { status = OTK_DIVERGED; A->fail_iter = t; break; }
       if (out[7] > 0) { status = OTK_BAD_POTENTIAL; A->fail_iter = t; break; }
@@ -601,15 +692,12 @@ static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st) {
       if (measure) {
         if ((status = H.rows(kap, (float)e, kap, fn, 2 * t + 2)) != OTK_OK) break;
       }
-      if ((status = otk_check(f, measure ? fn : nullptr, A->a, A->n, L.g, A->b, A->m, e, L.chk,
-                              L.chk_ws, st)) != OTK_OK)
-        break;
+      if ((status = H.check(f, measure ? fn : nullptr, e)) != OTK_OK) break;
       extra_launches += 1;
-      double out[8];
-      int fb;
-      OTK_CUDA(cudaMemcpyAsync(out, L.chk, sizeof(out), cudaMemcpyDeviceToHost, st));
-      OTK_CUDA(cudaMemcpyAsync(&fb, L.first_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-      OTK_CUDA(cudaStreamSynchronize(st));
+      CheckRead cr;
+      if ((status = read_check(H, L, st, &cr)) != OTK_OK) break;
+      const double *out = cr.v;
+      const int fb = cr.fb;
       if (fb <= 2 * t) { status = OTK_BAD_POTENTIAL; A->fail_iter = (fb + 1) / 2; break; }
       if (out[4] > 0 || out[5] > 0) { status = OTK_DIVERGED; A->fail_iter = t; break; }
       if (!measure) continue;

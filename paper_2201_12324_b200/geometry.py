@@ -230,6 +230,35 @@ def kernel_points(p, cost_fn: str):
     return q / np.linalg.norm(q, axis=1, keepdims=True) / np.sqrt(2.0)
 
 
+def centered_points(px, py, cost_fn: str, same: bool = False):
+    """The kernel points of both sets, shifted by one common centre (the float64
+    column mean of y; otk_column_mean / otk_shift_points).  sqeucl and eucl
+    costs are translation-invariant (geometry.py:268-275), and the float32
+    norm form |x|^2 + |y|^2 - 2<x,y> the kernels use then loses precision only
+    with the spread of the points, not with their offset from the origin.  y is
+    replicated on every rank of a sharded solve, so every rank derives the same
+    centre.  cosine points are normalised instead (kernel_points)."""
+    import torch
+    kx = as_device_f32(kernel_points(px, cost_fn)).contiguous()
+    ky = kx if same else as_device_f32(kernel_points(py, cost_fn)).contiguous()
+    if cost_fn == "cosine":
+        return kx, ky
+    lib = N.lib()
+    m, d = ky.shape
+    dev = ky.device
+    center = torch.empty(d, dtype=torch.float64, device=dev)
+    ws = torch.empty(lib.otk_center_workspace_bytes(m, d), dtype=torch.uint8, device=dev)
+    st = stream()
+    N.check(lib.otk_column_mean(N.ptr(ky), m, d, N.ptr(center), N.ptr(ws), st), "column mean")
+    cy = torch.empty_like(ky)
+    N.check(lib.otk_shift_points(N.ptr(ky), m, d, N.ptr(center), N.ptr(cy), st), "shift y")
+    if same:
+        return cy, cy
+    cx = torch.empty_like(kx)
+    N.check(lib.otk_shift_points(N.ptr(kx), kx.shape[0], d, N.ptr(center), N.ptr(cx), st), "shift x")
+    return cx, cy
+
+
 def cost_fn_flags(cost_fn: str) -> int:
     if cost_fn not in COST_FNS:
         raise ValueError(f"cost_fn must be one of {COST_FNS}, got {cost_fn!r}")
@@ -301,14 +330,13 @@ class PointCloudGeometry(Geometry):
         return kernel_points(p, self.cost_fn)
 
     def _points(self):
-        """fp32 device points the kernels see (cosine: normalised), cached; the
-        whole-solve entry needs only these (it prepares norms / planes itself)."""
+        """fp32 device points the kernels see (cosine: normalised; sqeucl / eucl:
+        centred on the mean of y, centered_points), cached; the whole-solve
+        entry needs only these (it prepares norms / planes itself)."""
         if self._kpts is None:
             device()
             px, py = self._dev_pts if self._dev_pts is not None else (self.x, self.y)
-            kx = as_device_f32(self._kernel_points(px)).contiguous()
-            ky = kx if self._same_points else as_device_f32(self._kernel_points(py)).contiguous()
-            self._kpts = (kx, ky)
+            self._kpts = centered_points(px, py, self.cost_fn, same=self._same_points)
         return self._kpts
 
     def _clouds(self):

@@ -175,6 +175,19 @@ class PeerExchange:
     a GPU (``ThreadComm``) must not run kernels that wait on each other.
     """
 
+    _CACHE: dict = {}
+
+    @classmethod
+    def shared(cls, comm, m: int) -> "PeerExchange":
+        """One exchange buffer per (process group, m): built (IPC handles
+        exported, opened and exchanged) on first use, reused by every later
+        ShardedProblem on the same group -- the epoch sequence continues."""
+        key = (id(getattr(comm, "group", None)), comm.world, comm.rank, int(m))
+        px = cls._CACHE.get(key)
+        if px is None or px.local is None:
+            px = cls._CACHE[key] = cls(comm, m)
+        return px
+
     def __init__(self, comm, m: int):
         import ctypes
         lib = N.lib()
@@ -486,7 +499,7 @@ class ShardedProblem:
     def __init__(self, x, y, a=None, b=None, *, comm=None, x_is_local: bool = False,
                  n_total: int | None = None, impl: str = "auto", cost_fn: str = "sqeucl",
                  exchange: str = "auto"):
-        from .geometry import cost_fn_flags, kernel_points
+        from .geometry import centered_points, cost_fn_flags
         from .sinkhorn import _impl_flags
         cflags = cost_fn_flags(cost_fn)
         self.cost_fn = cost_fn
@@ -515,8 +528,8 @@ class ShardedProblem:
         def amax_reduce(v):  # one common split scale on every rank
             return float(comm.all_gather_host(np.array([v]), dev)[:, 0].max())
 
-        self.engine = CudaShardEngine(kernel_points(x_local, cost_fn), kernel_points(y, cost_fn),
-                                      a_loc, b_w, flags=_impl_flags(impl) | cflags,
+        kx, ky = centered_points(x_local, y, cost_fn)  # common centre: the replicated y's mean
+        self.engine = CudaShardEngine(kx, ky, a_loc, b_w, flags=_impl_flags(impl) | cflags,
                                       amax_reduce=amax_reduce)
         self.lo, self.hi, self.n_total, self.m = lo, hi, n_total, m
         # g half-step exchange: "p2p" = pushed over NVLink peer memory by the
@@ -534,7 +547,7 @@ class ShardedProblem:
                 raise ValueError("peer-memory exchange needs one process per GPU of one host "
                                  "(TorchComm over NCCL) with peer access between all GPUs")
             if ok:
-                self.p2p = PeerExchange(comm, m)
+                self.p2p = PeerExchange.shared(comm, m)
         self.exchange = "p2p" if self.p2p is not None else "collective"
 
     def solve(self, eps, *, threshold: float = 1e-3, max_iters: int = 2000,
@@ -598,10 +611,10 @@ def reg_ot_cost_sharded(out: ShardedSinkhornOutput, x_local, y, a_local, b, comm
                         cost_fn: str = "sqeucl"):
     """reg_ot_cost (sinkhorn.py:210-216) over row shards: online local sums + rank-order total."""
     import torch
-    from .geometry import _Cloud, cost_fn_flags, kernel_points
+    from .geometry import _Cloud, centered_points, cost_fn_flags
     comm = comm or TorchComm()
     cflags = cost_fn_flags(cost_fn)
-    cx, cy = _Cloud(kernel_points(x_local, cost_fn)), _Cloud(kernel_points(y, cost_fn))
+    cx, cy = (_Cloud(p) for p in centered_points(x_local, y, cost_fn))
     cx.prepare(1.0, False)
     cy.prepare(1.0, False)
     lib = N.lib()

@@ -33,6 +33,8 @@ class Workload:
     max_iters: int
     inner_iters: int = 10
     materialised: bool = False
+    eps_scale: float = 0.05              # eps = eps_scale x mean cost ...
+    eps_subsample_seed: int | None = None  # ... over a seeded SUBSAMPLE x SUBSAMPLE block (else exact)
 
     @property
     def shape(self):
@@ -52,12 +54,34 @@ def exact_mean_sqeucl(x: np.ndarray, y: np.ndarray) -> float:
                  - 2.0 * x.mean(axis=0) @ y.mean(axis=0))
 
 
+def subsample_rows(n: int, m: int, seed: int, edge: int = SUBSAMPLE):
+    """The seeded subsample rows of the eps estimate (drawn without replacement)."""
+    rng = np.random.default_rng(seed + 1000)
+    ix = rng.choice(n, size=min(edge, n), replace=False)
+    iy = rng.choice(m, size=min(edge, m), replace=False)
+    return ix, iy
+
+
 def subsample_mean_sqeucl(x: np.ndarray, y: np.ndarray, seed: int, edge: int = SUBSAMPLE) -> float:
     """Exact mean cost over a seeded edge x edge subsample (rows drawn without replacement)."""
-    rng = np.random.default_rng(seed + 1000)
-    ix = rng.choice(x.shape[0], size=min(edge, x.shape[0]), replace=False)
-    iy = rng.choice(y.shape[0], size=min(edge, y.shape[0]), replace=False)
+    ix, iy = subsample_rows(x.shape[0], y.shape[0], seed, edge)
     return exact_mean_sqeucl(x[ix], y[iy])
+
+
+def estimate_eps_device(wl: Workload, xd, yd) -> float:
+    """The workload's eps rule evaluated on device-resident points (torch, float64):
+    the time-to-tolerance measurement includes it.  Same
+    formula and subsample as the host value, so it agrees to float64 rounding."""
+    import torch
+    if wl.eps_subsample_seed is not None:
+        ix, iy = subsample_rows(xd.shape[0], yd.shape[0], wl.eps_subsample_seed)
+        xd = xd[torch.as_tensor(ix, device=xd.device)]
+        yd = yd[torch.as_tensor(iy, device=yd.device)]
+    x = xd.double()
+    y = yd.double()
+    mean = ((x * x).sum() / x.shape[0] + (y * y).sum() / y.shape[0]
+            - 2.0 * torch.dot(x.mean(dim=0), y.mean(dim=0)))
+    return wl.eps_scale * float(mean.item())
 
 
 def _f32(a):
@@ -79,7 +103,8 @@ def cfg2(n: int = 65536, m: int = 65536, d: int = 64, seed: int = 2) -> Workload
     x = _f32(rng.standard_normal((n, d)))
     y = _f32(1.5 * rng.standard_normal((m, d)))
     eps = 0.05 * subsample_mean_sqeucl(x, y, seed)
-    return Workload("cfg2_online_65536_d64", x, y, None, None, eps, 1e-3, 1000)
+    return Workload("cfg2_online_65536_d64", x, y, None, None, eps, 1e-3, 1000,
+                    eps_subsample_seed=seed)
 
 
 def cfg3(batch: int = 512, n: int = 512, m: int = 512, d: int = 16, seed: int = 3) -> Workload:
@@ -112,7 +137,8 @@ def cfg4(n: int = 262144, m: int = 131072, d: int = 128, seed: int = 4) -> Workl
     b = rng.uniform(0.5, 1.5, size=m)
     b /= b.sum()
     eps = 0.05 * subsample_mean_sqeucl(x, y, seed)
-    return Workload("cfg4_unbalanced_262144x131072_d128", x, y, a, b, eps, 1e-3, 1000)
+    return Workload("cfg4_unbalanced_262144x131072_d128", x, y, a, b, eps, 1e-3, 1000,
+                    eps_subsample_seed=seed)
 
 
 def cfg5(n: int = 32768, m: int = 32768, d: int = 1024, seed: int = 5) -> Workload:
@@ -125,7 +151,7 @@ def cfg5(n: int = 32768, m: int = 32768, d: int = 1024, seed: int = 5) -> Worklo
     y /= np.linalg.norm(y, axis=1, keepdims=True)
     x, y = _f32(x), _f32(y)
     eps = 0.01 * exact_mean_sqeucl(x, y)
-    return Workload("cfg5_highdim_32768_d1024", x, y, None, None, eps, 1e-4, 3000)
+    return Workload("cfg5_highdim_32768_d1024", x, y, None, None, eps, 1e-4, 3000, eps_scale=0.01)
 
 
 CONFIGS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5}
