@@ -490,9 +490,11 @@ def run_ours(args, wl, rank, world):
 
         def cells_of(out):
             return float(n) * m * out.iterations
-        parallelism = (f"row-sharded x{world} (g half-step partials pushed over NVLink peer memory "
-                       "by the half-step's last kernel)" if sprob.exchange == "p2p" else
-                       f"row-sharded x{world} (all-gather per g half-step)")
+        parallelism = (f"row-sharded x{world} (native loop: g half-step partials pushed over NVLink "
+                       "peer memory by the half-step's last kernel, check sums exchanged on the "
+                       "device, CUDA-graph check periods)" if sprob.loop == "native" else
+                       f"row-sharded x{world} ({sprob.exchange} exchange per g half-step, "
+                       "Python loop)")
     else:
         xd = torch.from_numpy(wl.x).to(dev)
         yd = torch.from_numpy(wl.y).to(dev)
@@ -654,7 +656,11 @@ def count_launches(otk, wl, args, solve, world):
             S.N.lib = saved
         return calls["n"]
     if world > 1:
-        eng = solve.sharded_problem.engine
+        sp = solve.sharded_problem
+        if sp.loop == "native":  # otk_solve_pointcloud_sharded reports its count (graph nodes incl.)
+            solve()
+            return int(sp.launches_last)
+        eng = sp.engine
         before = eng.launches
         solve()
         return int(eng.launches - before)

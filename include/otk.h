@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define OTK_ABI_VERSION 5
+#define OTK_ABI_VERSION 6
 
 enum otk_status {
   OTK_OK = 0,
@@ -335,6 +335,9 @@ typedef struct otk_solve_args {
   void *workspace;
   size_t workspace_bytes;
   void *stream;
+  /* nullable PINNED host buffers [n], [m]: the solver copies f and g there
+   * before its one final synchronisation (saves the caller a second D2H sync) */
+  float *f_host, *g_host;
 } otk_solve_args;
 
 /* Bytes of device workspace otk_solve_pointcloud needs for these args. */

@@ -23,7 +23,7 @@ OTK_IMPL_NOPERSIST = 0x40
 OTK_ANCHOR_INIT, OTK_IMPL_NOANCHOR = 0x80, 0x100
 OTK_COST_EUCL = 0x4
 OTK_FIN_SOLVER, OTK_FIN_APPLY, OTK_FIN_LOG2 = 0, 1, 2
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 P = C.c_void_p
 I64, I32, F32, F64, SZ = C.c_int64, C.c_int32, C.c_float, C.c_double, C.c_size_t
@@ -41,6 +41,7 @@ class SolveArgs(C.Structure):
         ("f_out", P), ("g_out", P), ("errors", P), ("duals", P), ("max_checks", I32),
         ("n_checks", I32), ("iterations", I32), ("converged", I32), ("fail_iter", I32),
         ("launches", I32), ("workspace", P), ("workspace_bytes", SZ), ("stream", P),
+        ("f_host", P), ("g_host", P),
     ]
 
 

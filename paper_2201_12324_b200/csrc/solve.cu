@@ -206,7 +206,7 @@ extern "C" int otk_lse_step(const float *p, const float *p_sq, const uint16_t *p
                             int32_t *repair_ws, const otk_exchange *xchg, void *stream) {
   OTK_CHECK_ARG(partial && out_pot && np > 0 && nq > 0 && nsplit >= 1, "otk_lse_step: bad arguments");
   OTK_CHECK_ARG(!xchg || (xchg->local && xchg->world >= 1 && xchg->rank >= 0 &&
-                          xchg->rank < xchg->world && xchg->epoch >= 1 && mode == OTK_FIN_LOG2),
+                          xchg->rank < xchg->world && mode == OTK_FIN_LOG2),
                 "otk_lse_step: the exchange needs OTK_FIN_LOG2 and a valid otk_exchange");
   OTK_CHECK_ARG(mode == OTK_FIN_SOLVER || mode == OTK_FIN_APPLY || mode == OTK_FIN_LOG2,
                 "otk_lse_step: bad mode");
@@ -461,22 +461,36 @@ static int solve_entry(otk_solve_args *A, const ShardCtx *sh, float split_scale)
   OTK_CHECK_ARG(A->workspace && A->workspace_bytes >= L.bytes,
                 "otk_solve_pointcloud: workspace too small (%zu < %zu)", A->workspace_bytes, L.bytes);
   // Work runs on a private non-blocking stream ordered after the caller's
-  // stream (graph capture is not allowed on the legacy default stream).
+  // stream (graph capture is not allowed on the legacy default stream); the
+  // stream and its two events are created once per host thread and device.
+  struct Priv {
+    int dev = -1;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  };
+  static thread_local Priv priv;
+  int dev = 0;
+  OTK_CUDA(cudaGetDevice(&dev));
+  if (priv.dev != dev) {
+    if (priv.st) {
+      cudaEventDestroy(priv.ev_in);
+      cudaEventDestroy(priv.ev_out);
+      cudaStreamDestroy(priv.st);
+      priv.st = nullptr;
+    }
+    OTK_CUDA(cudaStreamCreateWithFlags(&priv.st, cudaStreamNonBlocking));
+    OTK_CUDA(cudaEventCreateWithFlags(&priv.ev_in, cudaEventDisableTiming));
+    OTK_CUDA(cudaEventCreateWithFlags(&priv.ev_out, cudaEventDisableTiming));
+    priv.dev = dev;
+  }
   cudaStream_t caller = as_stream(A->stream);
-  cudaStream_t st;
-  cudaEvent_t ev_in, ev_out;
-  OTK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  OTK_CUDA(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
-  OTK_CUDA(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
-  OTK_CUDA(cudaEventRecord(ev_in, caller));
-  OTK_CUDA(cudaStreamWaitEvent(st, ev_in, 0));
+  cudaStream_t st = priv.st;
+  OTK_CUDA(cudaEventRecord(priv.ev_in, caller));
+  OTK_CUDA(cudaStreamWaitEvent(st, priv.ev_in, 0));
   int rc = solve_on_stream(A, L, st, sh, split_scale);
-  cudaEventRecord(ev_out, st);
-  cudaStreamWaitEvent(caller, ev_out, 0);
+  cudaEventRecord(priv.ev_out, st);
+  cudaStreamWaitEvent(caller, priv.ev_out, 0);
   cudaStreamSynchronize(st);
-  cudaEventDestroy(ev_in);
-  cudaEventDestroy(ev_out);
-  cudaStreamDestroy(st);
   return rc;
 }
 
@@ -529,15 +543,15 @@ static int solve_small(otk_solve_args *A, Layout &L, cudaStream_t st) {
       fclose(fp);
     }
   }
+  // one synchronisation: state, the whole check trace and (optionally) f, g
   int state[8];
   OTK_CUDA(cudaMemcpyAsync(state, L.state, 5 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  OTK_CUDA(cudaMemcpyAsync(A->errors, L.d_errors, A->max_checks * sizeof(double), cudaMemcpyDeviceToHost, st));
+  OTK_CUDA(cudaMemcpyAsync(A->duals, L.d_duals, A->max_checks * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (A->f_host) OTK_CUDA(cudaMemcpyAsync(A->f_host, A->f_out, A->n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (A->g_host) OTK_CUDA(cudaMemcpyAsync(A->g_host, A->g_out, A->m * sizeof(float), cudaMemcpyDeviceToHost, st));
   OTK_CUDA(cudaStreamSynchronize(st));
   const int nc = std::min(state[0], A->max_checks);
-  if (nc > 0) {
-    OTK_CUDA(cudaMemcpyAsync(A->errors, L.d_errors, nc * sizeof(double), cudaMemcpyDeviceToHost, st));
-    OTK_CUDA(cudaMemcpyAsync(A->duals, L.d_duals, nc * sizeof(double), cudaMemcpyDeviceToHost, st));
-    OTK_CUDA(cudaStreamSynchronize(st));
-  }
   A->n_checks = nc;
   A->iterations = state[1];
   A->converged = state[2];
@@ -723,6 +737,8 @@ static int solve_on_stream(otk_solve_args *A, Layout &L, cudaStream_t st, const 
   if (status < 0) return status;
   OTK_CUDA(cudaMemcpyAsync(A->f_out, f, A->n * sizeof(float), cudaMemcpyDeviceToDevice, st));
   OTK_CUDA(cudaMemcpyAsync(A->g_out, L.g, A->m * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  if (A->f_host) OTK_CUDA(cudaMemcpyAsync(A->f_host, f, A->n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (A->g_host) OTK_CUDA(cudaMemcpyAsync(A->g_host, L.g, A->m * sizeof(float), cudaMemcpyDeviceToHost, st));
   OTK_CUDA(cudaStreamSynchronize(st));
   return status;
 }

@@ -26,6 +26,7 @@ drive the same loop with a float64 numpy engine over ``gloo``.
 from __future__ import annotations
 
 import dataclasses
+import os
 import threading
 
 import numpy as np
@@ -220,9 +221,16 @@ class PeerExchange:
         self.epoch = 0
 
     def next(self):
-        """Arguments of the next exchange (epochs 1, 2, ... on every rank alike)."""
+        """Arguments of the next exchange.  Epoch 0 = device-counted: the buffer
+        itself numbers the exchanges (the combine kernel advances the count), so
+        the Python loop and the native solver (and its CUDA graphs) share one
+        epoch sequence; ``epoch`` here only counts this object's exchanges."""
         self.epoch += 1
-        return N.Exchange(self.local, self.world, self.rank, self.epoch)
+        return N.Exchange(self.local, self.world, self.rank, 0)
+
+    def args(self):
+        """otk_exchange for the native sharded solver (device-counted epochs)."""
+        return N.Exchange(self.local, self.world, self.rank, 0)
 
     def status(self) -> int:
         import ctypes
@@ -528,15 +536,18 @@ class ShardedProblem:
         def amax_reduce(v):  # one common split scale on every rank
             return float(comm.all_gather_host(np.array([v]), dev)[:, 0].max())
 
+        self._amax_reduce = amax_reduce
         kx, ky = centered_points(x_local, y, cost_fn)  # common centre: the replicated y's mean
-        self.engine = CudaShardEngine(kx, ky, a_loc, b_w, flags=_impl_flags(impl) | cflags,
-                                      amax_reduce=amax_reduce)
+        self.kx, self.ky = kx, ky
+        self.a_loc, self.b_w = a_loc, b_w
+        self.flags = _impl_flags(impl) | cflags
+        self._engine = None
+        self._native = None
         self.lo, self.hi, self.n_total, self.m = lo, hi, n_total, m
         # g half-step exchange: "p2p" = pushed over NVLink peer memory by the
         # half-step's last kernel (csrc/p2p.cu); "collective" = comm all-gather
         # (NCCL) + combine; "auto" = p2p whenever every rank is its own process
         # on its own peer-accessible GPU of one host (OTK_EXCHANGE overrides)
-        import os
         exchange = os.environ.get("OTK_EXCHANGE", exchange)
         if exchange not in ("auto", "p2p", "collective"):
             raise ValueError("exchange must be 'auto', 'p2p' or 'collective'")
@@ -549,6 +560,84 @@ class ShardedProblem:
             if ok:
                 self.p2p = PeerExchange.shared(comm, m)
         self.exchange = "p2p" if self.p2p is not None else "collective"
+        # the loop: native C++ (otk_solve_pointcloud_sharded: graph-captured check
+        # periods, check sums exchanged on the device, one host sync per check)
+        # whenever the exchange is peer memory; the Python loop otherwise
+        # (collective / ThreadComm / gloo) or with OTK_SHARDED_LOOP=python
+        self.loop = "native" if (self.p2p is not None and
+                                 os.environ.get("OTK_SHARDED_LOOP", "native") != "python") else "python"
+
+    @property
+    def engine(self) -> "CudaShardEngine":
+        """Device half-steps for the Python loop (built on first use)."""
+        if self._engine is None:
+            self._engine = CudaShardEngine(self.kx, self.ky, self.a_loc, self.b_w, flags=self.flags,
+                                           amax_reduce=self._amax_reduce)
+        return self._engine
+
+    def _native_state(self):
+        """Per-problem state of the native loop, built once: device weights,
+        the common operand scale and the solver workspace (reused by every solve)."""
+        if self._native is None:
+            import torch
+            lib = N.lib()
+            n, d = self.kx.shape
+            m = self.m
+            scale = 0.0
+            if lib.otk_lse_uses_tc(d, self.flags):
+                amax = max(float(_absmax(self.kx)), float(_absmax(self.ky)))
+                scale = float(lib.otk_split_scale(self._amax_reduce(amax), d))
+            with np.errstate(divide="ignore"):
+                la, lb = np.log(self.a_loc), np.log(self.b_w)
+            st = dict(a=as_device_f32(self.a_loc), b=as_device_f32(self.b_w), la=as_device_f32(la),
+                      lb=as_device_f32(lb), scale=scale, ws=None, ws_key=None)
+            n_pad = (n + 63) // 64 * 64
+            st["fg"] = torch.empty(n_pad + m, dtype=torch.float32, device=self.kx.device)
+            st["n_pad"] = n_pad
+            self._native = st
+        return self._native
+
+    def _solve_native(self, sched, threshold, max_iters, inner_iters, g_init):
+        import ctypes
+        import torch
+        from .sinkhorn import _raise_status
+        st = self._native_state()
+        n, d = self.kx.shape
+        m = self.m
+        max_checks = max_iters // inner_iters + 2
+        errs, duals = np.zeros(max_checks), np.zeros(max_checks)
+        gi = None
+        if g_init is not None:
+            gi = as_device_f32(g_init)
+            if tuple(gi.shape) != (m,):
+                raise ValueError(f"g_init must have shape ({m},)")
+        fg, n_pad = st["fg"], st["n_pad"]
+        A = N.SolveArgs()
+        A.x, A.y, A.n, A.m, A.d = N.ptr(self.kx), N.ptr(self.ky), n, m, d
+        A.a, A.b, A.log_a, A.log_b = N.ptr(st["a"]), N.ptr(st["b"]), N.ptr(st["la"]), N.ptr(st["lb"])
+        A.same_points = 0
+        A.eps_target, A.eps_init_scale, A.eps_decay = sched.target, sched.init_scale, sched.decay
+        A.threshold, A.max_iters, A.inner_iters = float(threshold), int(max_iters), int(inner_iters)
+        A.g_init = N.ptr(gi)
+        A.flags = self.flags | N.OTK_IMPL_NOPERSIST
+        A.use_graphs = 1
+        A.f_out, A.g_out = N.ptr(fg[:n]), N.ptr(fg[n_pad:])
+        A.errors = errs.ctypes.data_as(ctypes.c_void_p)
+        A.duals = duals.ctypes.data_as(ctypes.c_void_p)
+        A.max_checks = max_checks
+        lib = N.lib()
+        nbytes = lib.otk_solve_workspace_bytes(ctypes.byref(A))
+        if st["ws"] is None or st["ws"].numel() < nbytes:
+            st["ws"] = torch.empty(nbytes, dtype=torch.uint8, device=self.kx.device)
+        A.workspace, A.workspace_bytes, A.stream = N.ptr(st["ws"]), st["ws"].numel(), stream()
+        X = self.p2p.args()
+        rc = lib.otk_solve_pointcloud_sharded(ctypes.byref(A), ctypes.byref(X), st["scale"], 0)
+        self.launches_last = int(A.launches)
+        if rc != N.OTK_OK:
+            _raise_status(rc, A.fail_iter)
+        k = A.n_checks
+        return (fg[:n].clone(), fg[n_pad:].clone(), int(A.iterations), bool(A.converged),
+                errs[:k].copy(), duals[:k].copy())
 
     def solve(self, eps, *, threshold: float = 1e-3, max_iters: int = 2000,
               inner_iters: int = 10, g_init=None, gather_f: bool = False) -> ShardedSinkhornOutput:
@@ -561,11 +650,16 @@ class ShardedProblem:
             raise ValueError("threshold must be positive")
         sched = eps if isinstance(eps, EpsilonSchedule) else EpsilonSchedule(float(eps))
         _fp32_guard(sched, inner_iters, max_iters)
-        comm, eng = self.comm, self.engine
-        eng.reset_first_bad()
-        which, iters, conv, errs, duals = sharded_loop(eng, comm, sched, threshold, max_iters,
-                                                       inner_iters, g_init, p2p=self.p2p)
-        f_dev, g_dev = eng.f_result(which).clone(), eng.g_result().clone()
+        comm = self.comm
+        if self.loop == "native":
+            f_dev, g_dev, iters, conv, errs, duals = self._solve_native(
+                sched, threshold, max_iters, inner_iters, g_init)
+        else:
+            eng = self.engine
+            eng.reset_first_bad()
+            which, iters, conv, errs, duals = sharded_loop(eng, comm, sched, threshold, max_iters,
+                                                           inner_iters, g_init, p2p=self.p2p)
+            f_dev, g_dev = eng.f_result(which).clone(), eng.g_result().clone()
         f_full = None
         if gather_f:
             import torch
@@ -598,6 +692,13 @@ def solve_sinkhorn_sharded(x, y, eps, a=None, b=None, *, threshold: float = 1e-3
                           impl=impl, cost_fn=cost_fn, exchange=exchange)
     return prob.solve(eps, threshold=threshold, max_iters=max_iters, inner_iters=inner_iters,
                       g_init=g_init, gather_f=gather_f)
+
+
+def _absmax(p) -> float:
+    import torch
+    amax = torch.empty(1, dtype=torch.float32, device=p.device)
+    N.check(N.lib().otk_absmax(N.ptr(p), p.numel(), N.ptr(amax), stream()), "absmax")
+    return float(amax.item())
 
 
 def _dev_of(x):

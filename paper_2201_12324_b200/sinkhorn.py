@@ -19,6 +19,7 @@ reference; ``f_device``/``g_device`` hold the float32 CUDA tensors.
 from __future__ import annotations
 
 import dataclasses
+import threading
 import logging
 from typing import NamedTuple
 
@@ -276,6 +277,25 @@ def _raise_status(rc: int, iteration: int):
     N.check(rc, "solve_sinkhorn")
 
 
+_GEOM_LOCK = threading.Lock()
+
+
+def _host_buffers(geom, n_pad: int, m: int, nbytes: int, dev):
+    """Per-geometry reusable buffers of the whole-solve entry: the device
+    workspace and a pinned host staging buffer for f | g (the solver copies
+    the potentials there before its single final sync).  Reused by every
+    solve on the geometry -- a solve's outputs are copied out of them."""
+    import torch
+    cache = getattr(geom, "_solve_bufs", None)
+    if cache is None or cache["ws"].numel() < nbytes or cache["host"].numel() < n_pad + m \
+            or cache["ws"].device != dev:
+        cache = {"ws": torch.empty(nbytes, dtype=torch.uint8, device=dev),
+                 "host": torch.empty(n_pad + m, dtype=torch.float32).pin_memory(),
+                 "lock": cache["lock"] if cache else threading.Lock()}
+        geom._solve_bufs = cache
+    return cache
+
+
 def _solve_pointcloud(prob, sched, threshold, max_iters, inner_iters, g_init, impl, use_graphs):
     import torch
     geom: PointCloudGeometry = prob.geom
@@ -284,8 +304,8 @@ def _solve_pointcloud(prob, sched, threshold, max_iters, inner_iters, g_init, im
     n, m = geom.shape
     d = int(px.shape[1])
     dev = px.device
-    # f and g in one buffer (one device->host read at the end); g starts on a
-    # 256-byte boundary, as every separately allocated potential does
+    # f and g in one device buffer (the outputs' f_device / g_device); g starts
+    # on a 256-byte boundary, as every separately allocated potential does
     n_pad = (n + 63) // 64 * 64
     fg = torch.empty(n_pad + m, dtype=torch.float32, device=dev)
     f_out, g_out = fg[:n], fg[n_pad:]
@@ -312,20 +332,26 @@ def _solve_pointcloud(prob, sched, threshold, max_iters, inner_iters, g_init, im
     A.max_checks = max_checks
     lib = N.lib()
     nbytes = lib.otk_solve_workspace_bytes(ctypes.byref(A))
-    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    A.workspace, A.workspace_bytes, A.stream = N.ptr(ws), nbytes, stream()
-    rc = lib.otk_solve_pointcloud(ctypes.byref(A))
-    if rc != N.OTK_OK:
-        _raise_status(rc, A.fail_iter)
+    with _GEOM_LOCK:
+        bufs = _host_buffers(geom, n_pad, m, nbytes, dev)
+    with bufs["lock"]:  # instances may be shared between threads (reference SPEC.md:94)
+        host = bufs["host"]
+        A.workspace, A.workspace_bytes, A.stream = N.ptr(bufs["ws"]), bufs["ws"].numel(), stream()
+        A.f_host, A.g_host = host.data_ptr(), host.data_ptr() + 4 * n_pad
+        rc = lib.otk_solve_pointcloud(ctypes.byref(A))
+        if rc != N.OTK_OK:
+            _raise_status(rc, A.fail_iter)
+        fg_host = host.numpy()  # filled by the solver before its final sync
+        f_h = fg_host[:n].astype(np.float64)
+        g_h = fg_host[n_pad:n_pad + m].astype(np.float64)
     k = A.n_checks
     if not A.converged:
         logger.info("sinkhorn: no convergence after %d iterations (last error %s)", A.iterations,
                     errs[k - 1] if k else None)
-    fg_host = fg.cpu().numpy().astype(np.float64)
     return SinkhornOutput(
-        f=fg_host[:n], g=fg_host[n_pad:],
-        errors=errs[:k].copy(), dual_trace=duals[:k].copy(), iterations=int(A.iterations),
-        converged=bool(A.converged), eps=sched.target, f_device=f_out, g_device=g_out)
+        f=f_h, g=g_h, errors=errs[:k].copy(), dual_trace=duals[:k].copy(),
+        iterations=int(A.iterations), converged=bool(A.converged), eps=sched.target,
+        f_device=f_out, g_device=g_out)
 
 
 # ---------------------------------------------------------------- dense / batched

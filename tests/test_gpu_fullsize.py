@@ -13,9 +13,11 @@ at d = 1024 -- i.e. the kernels bench.py times.
 Tolerances (north_star): f, g 1e-4 relative (inf-norm); transport cost and
 dual 1e-5 relative; identical iteration count and converged flag.  The
 marginal errors and the dual trace are the reference's check values
-(sinkhorn.py:183-186) evaluated by the fused check kernel in float32 with
-float64 sums: errors within 1e-3 relative (the float32 floor ~ulp(f)/eps per
-row is ~1e-6 absolute), dual trace within 1e-5 relative.
+(sinkhorn.py:183-186) evaluated by the fused check kernel from float32
+potentials with float64 sums: errors within 1e-3 relative plus twice the
+float32 floor ulp(max|f|)/eps (each row's r_i = a_i exp((f_i - f'_i)/eps)
+carries a relative rounding of that size; ~6e-6 for cfg5),
+dual trace within 1e-5 relative.
 """
 
 import os
@@ -31,7 +33,11 @@ pytestmark = pytest.mark.gpu
 POT_TOL = 1e-4
 COST_TOL = 1e-5
 ERR_RTOL = 1e-3
-ERR_ATOL = 2e-6
+
+
+def err_floor(f, eps):
+    """float32 floor of the marginal error: ulp(max|f|) / eps."""
+    return float(np.spacing(np.float32(np.max(np.abs(f))))) / float(eps)
 
 
 @pytest.fixture(scope="module")
@@ -67,7 +73,8 @@ def _check_against(otk, fx, out, prob):
     assert len(out.errors) == len(fx["errors"]) and len(out.dual_trace) == len(fx["dual_trace"])
     ef, eg = rel_inf(out.f, fx["f"]), rel_inf(out.g, fx["g"])
     assert ef <= POT_TOL and eg <= POT_TOL, (ef, eg)
-    np.testing.assert_allclose(out.errors, fx["errors"], rtol=ERR_RTOL, atol=ERR_ATOL)
+    np.testing.assert_allclose(out.errors, fx["errors"], rtol=ERR_RTOL,
+                               atol=2.0 * err_floor(fx["f"], fx["eps"]))
     np.testing.assert_allclose(out.dual_trace, fx["dual_trace"], rtol=COST_TOL)
     cost = otk.reg_ot_cost(out, prob)
     rt = abs(cost.transport_cost / float(fx["transport"]) - 1.0)
@@ -113,7 +120,8 @@ def test_cfg3_all_512_problems_match_reference(otk):
     np.testing.assert_allclose(costs[:, 1], fx["dual"], rtol=COST_TOL)
     for k in range(0, 512, 37):  # the per-problem check traces
         nk = int(fx["n_checks"][k])
-        np.testing.assert_allclose(outs[k].errors, fx["errors"][k, :nk], rtol=ERR_RTOL, atol=ERR_ATOL)
+        np.testing.assert_allclose(outs[k].errors, fx["errors"][k, :nk], rtol=ERR_RTOL,
+                                   atol=2.0 * err_floor(fx["f"][k], fx["eps"][k]))
         np.testing.assert_allclose(outs[k].dual_trace, fx["dual_trace"][k, :nk], rtol=COST_TOL)
 
 
@@ -131,4 +139,5 @@ def test_converged_flag_pinned_by_float64_check(otk, name):
     assert out.converged and out.iterations == int(fx["iterations"])
     assert rel_inf(out.f, fx["f"]) <= 1e-5 and rel_inf(out.g, fx["g"]) <= 1e-5
     assert float(fx["ref_error"]) <= wl.threshold
-    np.testing.assert_allclose(out.errors[-1], float(fx["ref_error"]), rtol=ERR_RTOL, atol=ERR_ATOL)
+    np.testing.assert_allclose(out.errors[-1], float(fx["ref_error"]), rtol=ERR_RTOL,
+                               atol=2.0 * err_floor(fx["f"], fx["eps"]))

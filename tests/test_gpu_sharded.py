@@ -156,7 +156,75 @@ def test_world1_peer_exchange_is_bitwise_the_collective(otk, nccl_world1, d, gen
         assert np.array_equal(a.g, b.g)
         np.testing.assert_array_equal(a.errors, b.errors)
     assert p2p.p2p.status() == 0
-    assert p2p.p2p.epoch > 0
+    assert p2p.loop == "native" and col.loop == "python"
+
+
+@pytest.mark.parametrize("d,gen", [(3, "cfg1"), (64, "cfg2"), (128, "cfg4")])
+def test_world1_native_sharded_loop_matches_python_loop_and_single_gpu(otk, nccl_world1, d, gen,
+                                                                       monkeypatch):
+    """otk_solve_pointcloud_sharded (C++ loop, graph-captured check periods,
+    device-counted exchange epochs, check sums exchanged on the device) vs the
+    Python loop over the same peer exchange and vs the single-GPU general loop:
+    bitwise equal f, g, errors, dual trace, iterations -- over repeated solves
+    (the epoch sequence continues across solves and across the two loops)."""
+    from paper_2201_12324_b200 import _native as N
+    from paper_2201_12324_b200.sharded import ShardedProblem
+    kw = dict(n=700, m=515) if gen != "cfg2" else dict(n=700, m=515, d=d)
+    wl = getattr(workloads, gen)(**kw)
+    sp = ShardedProblem(wl.x, wl.y, wl.a, wl.b, exchange="p2p")
+    assert sp.loop == "native"
+    geom = otk.PointCloudGeometry(wl.x, wl.y)
+    geom.impl_flags = N.OTK_IMPL_NOPERSIST
+    prob = otk.LinearProblem(geom, wl.a, wl.b)
+    for rep in range(2):
+        for thr, its in ((wl.threshold, 60), (1e-300, 23), (1e-300, 41)):
+            single = otk.solve_sinkhorn(prob, wl.eps, threshold=thr, max_iters=its)
+            sp.loop = "native"
+            nat = sp.solve(wl.eps, threshold=thr, max_iters=its)
+            sp.loop = "python"
+            py = sp.solve(wl.eps, threshold=thr, max_iters=its)
+            for o in (nat, py):
+                assert o.iterations == single.iterations and o.converged == single.converged
+                assert np.array_equal(o.f_local, single.f) and np.array_equal(o.g, single.g)
+                np.testing.assert_array_equal(o.errors, single.errors)
+                np.testing.assert_array_equal(o.dual_trace, single.dual_trace)
+    sp.loop = "native"
+    assert sp.p2p.status() == 0
+    sp.solve(wl.eps, threshold=1e-300, max_iters=30)
+    assert sp.launches_last > 0
+
+
+def test_world1_native_sharded_loop_failure_paths(otk, nccl_world1):
+    """Same exceptions at the same iteration as the single-GPU solver: a warm
+    start with NaN (ValueError, geometry.py:65-72) and divergence
+    (DivergedError, sinkhorn.py:176-180)."""
+    from paper_2201_12324_b200 import _native as N
+    from paper_2201_12324_b200.sharded import ShardedProblem
+    wl = workloads.cfg2(n=600, m=400, d=64)
+    sp = ShardedProblem(wl.x, wl.y, exchange="p2p")
+    geom = otk.PointCloudGeometry(wl.x, wl.y)
+    geom.impl_flags = N.OTK_IMPL_NOPERSIST
+    prob = otk.LinearProblem(geom)
+    g0 = np.zeros(400)
+    g0[5] = np.nan
+    for call in (lambda: sp.solve(wl.eps, g_init=g0), lambda: otk.solve_sinkhorn(prob, wl.eps, g_init=g0)):
+        with pytest.raises(ValueError):
+            call()
+    outcomes = []
+    for call in (lambda: sp.solve(1e-30, inner_iters=1, max_iters=20),
+                 lambda: otk.solve_sinkhorn(prob, 1e-30, inner_iters=1, max_iters=20)):
+        try:
+            o = call()
+            outcomes.append(("ok", o.iterations))
+        except otk.DivergedError as e:
+            outcomes.append(("diverged", e.iteration))
+        except ValueError as e:
+            outcomes.append(("value", str(e)))
+    assert outcomes[0] == outcomes[1], outcomes
+    # the exchange is still consistent after the failures
+    a = sp.solve(wl.eps, threshold=1e-300, max_iters=12)
+    b = otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=12)
+    assert np.array_equal(a.g, b.g)
 
 
 def test_peer_exchange_wait_times_out_instead_of_hanging(otk, nccl_world1):

@@ -350,3 +350,91 @@ def test_exchange_protocol_model_never_reads_a_stale_or_overwritten_slot():
     for t in ts:
         t.join(120)
     assert not errors, errors[:3]
+
+
+def test_device_counted_epoch_protocol_model():
+    """Host model of the device-counted epochs of csrc/p2p.cu, which let the
+    native sharded loop replay the same launches inside CUDA graphs: the push
+    (finalize) and every block of the combine use E = done + 1 read from the
+    rank's own buffer; each combine block takes a ticket after reading E and
+    the last one sets done = E.  Blocks run as threads in any order (as if not
+    co-resident); every 10th epoch a single-block check exchange with its own
+    counter runs in the same stream order.  No block may see a wrong epoch,
+    a stale slot, or a wrong rank-order total."""
+    import random
+    import threading as th
+    W, E, B = 3, 120, 3
+    slots = [[[None] * W for _ in range(2)] for _ in range(W)]   # [owner][slot][writer]
+    flags = [[0] * W for _ in range(W)]
+    chk_slots = [[[None] * W for _ in range(2)] for _ in range(W)]
+    chk_flags = [[0] * W for _ in range(W)]
+    done = [0] * W          # header EPOCH word per rank
+    ticket = [0] * W        # header TICKET word per rank
+    chk_done = [0] * W      # header CHK_EPOCH word per rank
+    lock = th.Lock()
+    cv = th.Condition()
+    errors = []
+
+    def combine_block(r, e_expected, rng):
+        ep = done[r] + 1                                # exchange_epoch(local, 0)
+        if ep != e_expected:
+            errors.append(("epoch", r, ep, e_expected))
+        if rng.random() < 0.5:
+            th.Event().wait(0.0001)
+        with cv:
+            cv.wait_for(lambda: all(flags[r][w] >= ep for w in range(W)))
+        got = [slots[r][ep & 1][w] for w in range(W)]
+        if got != [(w, ep) for w in range(W)]:
+            errors.append(("slot", r, ep, got))
+        with lock:                                      # atomicAdd(ticket) == gridDim - 1
+            ticket[r] += 1
+            last = ticket[r] == B
+            if last:
+                ticket[r] = 0
+        if last:
+            done[r] = ep
+
+    def rank(r):
+        rng = random.Random(100 + r)
+        for e in range(1, E + 1):
+            ep = done[r] + 1                            # push kernel: same formula
+            for s in rng.sample(range(W), W):
+                slots[s][ep & 1][r] = (r, ep)
+            with cv:
+                for s in range(W):
+                    flags[s][r] = ep
+                cv.notify_all()
+            blocks = [th.Thread(target=combine_block, args=(r, e, random.Random(e * 7 + r + b)))
+                      for b in range(B)]
+            for b in rng.sample(blocks, B):
+                b.start()
+            for b in blocks:                            # stream order: the combine completes
+                b.join()
+            if done[r] != e:
+                errors.append(("done", r, done[r], e))
+            if e % 10 == 0:                             # check exchange (one block)
+                ce = chk_done[r] + 1
+                for s in range(W):
+                    chk_slots[s][ce & 1][r] = (r, ce, float(r + 1))
+                with cv:
+                    for s in range(W):
+                        chk_flags[s][r] = ce
+                    cv.notify_all()
+                    cv.wait_for(lambda: all(chk_flags[r][w] >= ce for w in range(W)))
+                vals = [chk_slots[r][ce & 1][w] for w in range(W)]
+                if [v[:2] for v in vals] != [(w, ce) for w in range(W)]:
+                    errors.append(("chk", r, ce, vals))
+                tot = 0.0
+                for w in range(W):                      # fixed rank order
+                    tot += vals[w][2]
+                if tot != W * (W + 1) / 2:
+                    errors.append(("tot", r, tot))
+                chk_done[r] = ce
+
+    ts = [th.Thread(target=rank, args=(r,)) for r in range(W)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(300)
+    assert not errors, errors[:3]
+    assert done == [E] * W and chk_done == [E // 10] * W
