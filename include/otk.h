@@ -80,11 +80,11 @@ int otk_prep_points(const float *pts, int64_t n, int32_t d, float *sqnorm,
  * forms _cost_block (geometry.py:268-273) in float64, where a common offset of
  * the clouds costs nothing, but float32 |p|^2 + |q|^2 - 2<p,q> loses
  * ~ulp(|p|^2) to cancellation.  Both sets are therefore shifted by one common
- * centre before prep: otk_column_mean writes mean[k] = (1/m) sum_j q_jk in
- * float64 (fixed-order, deterministic; ws of otk_center_workspace_bytes(m, d)
- * bytes), otk_shift_points writes out = fp32(p - center) (out may not alias p). */
-size_t otk_center_workspace_bytes(int64_t m, int32_t d);
-int otk_column_mean(const float *q, int64_t m, int32_t d, double *mean, void *ws, void *stream);
+ * centre before prep: otk_column_median writes center[k] = the (lower)
+ * median of q[:, k] over at most 8192 evenly strided rows (robust to far
+ * outliers, unlike the mean; exact float32 values, deterministic);
+ * otk_shift_points writes out = fp32(p - center) (out may not alias p). */
+int otk_column_median(const float *q, int64_t m, int32_t d, double *center, void *stream);
 int otk_shift_points(const float *p, int64_t n, int32_t d, const double *center, float *out,
                      void *stream);
 

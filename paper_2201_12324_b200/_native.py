@@ -59,8 +59,7 @@ SIGNATURES = {
     "otk_prep_points": (C.c_int, [P, I64, I32, P, P, P, P, P, I32, F32, P]),
     "otk_split_scale": (F32, [F32, I32]),
     "otk_absmax": (C.c_int, [P, I64, P, P]),
-    "otk_center_workspace_bytes": (SZ, [I64, I32]),
-    "otk_column_mean": (C.c_int, [P, I64, I32, P, P, P]),
+    "otk_column_median": (C.c_int, [P, I64, I32, P, P]),
     "otk_shift_points": (C.c_int, [P, I64, I32, P, P, P]),
     "otk_make_bias": (C.c_int, [P, I64, F32, P, P, I32, P]),
     "otk_lse_partial": (C.c_int, [P, P, P, P, P, I64, P, P, P, P, P, I64, I32, I32, F32, P, F32,

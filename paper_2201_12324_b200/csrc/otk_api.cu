@@ -88,29 +88,40 @@ __global__ void prep_kernel(const float *__restrict__ pts, int64_t n, int d,
 
 // ---------------------------------------------------------------- translation
 // C is translation-invariant, so both point sets are shifted by one common
-// centre (the column mean of q, float64) before any kernel forms
-// |p|^2 + |q|^2 - 2<p,q> in float32: the cancellation error then scales with
-// the spread of the points, not with their distance from the origin.
-constexpr int kCenterRows = 256;
+// centre before any kernel forms |p|^2 + |q|^2 - 2<p,q> in float32: the
+// cancellation error then scales with the spread of the points, not with
+// their distance from the origin.  The centre is the coordinate-wise median
+// of q (over at most kMedianRows evenly strided rows): unlike the mean it is
+// not dragged away from the bulk of the points by a few far outliers.
+constexpr int kMedianRows = 8192;
 
-__global__ void colsum_partial_kernel(const float *__restrict__ q, int64_t m, int d,
-                                      double *__restrict__ part) {
-  const int64_t r0 = (int64_t)blockIdx.x * kCenterRows;
-  const int64_t r1 = r0 + kCenterRows < m ? r0 + kCenterRows : m;
-  for (int k = threadIdx.x; k < d; k += blockDim.x) {
-    double acc = 0.0;
-    for (int64_t r = r0; r < r1; ++r) acc += (double)q[r * d + k];
-    part[(int64_t)blockIdx.x * d + k] = acc;
+// One block per coordinate: the strided samples in shared memory, +inf
+// padded to a power of two, bitonic sort, lower median.
+__global__ void __launch_bounds__(1024) column_median_kernel(const float *__restrict__ q, int64_t m,
+                                                             int d, int64_t stride, int count,
+                                                             int pow2, double *__restrict__ center) {
+  extern __shared__ float v[];
+  const int k = blockIdx.x;
+  for (int i = threadIdx.x; i < pow2; i += blockDim.x)
+    v[i] = (i < count) ? q[(int64_t)i * stride * d + k] : INFINITY;
+  __syncthreads();
+  for (int size = 2; size <= pow2; size <<= 1) {
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < pow2; i += blockDim.x) {
+        const int p = i ^ j;
+        if (p > i) {
+          const bool up = (i & size) == 0;
+          const float a = v[i], b = v[p];
+          if ((a > b) == up) {
+            v[i] = b;
+            v[p] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
   }
-}
-
-__global__ void colmean_final_kernel(const double *__restrict__ part, int nblk, int d, int64_t m,
-                                     double *__restrict__ mean) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= d) return;
-  double acc = 0.0;
-  for (int b = 0; b < nblk; ++b) acc += part[(int64_t)b * d + k];  // fixed order
-  mean[k] = acc / (double)m;
+  if (threadIdx.x == 0) center[k] = (double)v[(count - 1) / 2];
 }
 
 __global__ void shift_kernel(const float *__restrict__ p, int64_t count, int d,
@@ -332,21 +343,21 @@ int otk_prep_points(const float *pts, int64_t n, int32_t d, float *sqnorm, uint1
   return OTK_OK;
 }
 
-size_t otk_center_workspace_bytes(int64_t m, int32_t d) {
-  if (m < 1 || d < 1) return 0;
-  return (size_t)((m + kCenterRows - 1) / kCenterRows) * d * sizeof(double);
-}
-
-int otk_column_mean(const float *q, int64_t m, int32_t d, double *mean, void *ws, void *stream) {
-  OTK_CHECK_ARG(q && mean && ws && m > 0 && d > 0, "otk_column_mean: bad arguments");
-  const int64_t nblk = (m + kCenterRows - 1) / kCenterRows;
-  OTK_CHECK_ARG(nblk <= INT32_MAX, "otk_column_mean: too many points");
-  cudaStream_t st = as_stream(stream);
-  const int thr = d >= 128 ? 128 : 32;
-  colsum_partial_kernel<<<(unsigned)nblk, thr, 0, st>>>(q, m, d, reinterpret_cast<double *>(ws));
-  OTK_LAUNCH_CHECK();
-  colmean_final_kernel<<<(d + 127) / 128, 128, 0, st>>>(reinterpret_cast<const double *>(ws),
-                                                        (int)nblk, d, m, mean);
+int otk_column_median(const float *q, int64_t m, int32_t d, double *center, void *stream) {
+  OTK_CHECK_ARG(q && center && m > 0 && d > 0, "otk_column_median: bad arguments");
+  const int64_t stride = (m + kMedianRows - 1) / kMedianRows;
+  const int count = (int)((m + stride - 1) / stride);
+  int pow2 = 1;
+  while (pow2 < count) pow2 <<= 1;
+  const size_t smem = (size_t)pow2 * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    OTK_CUDA(cudaFuncSetAttribute(column_median_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kMedianRows * (int)sizeof(float)));
+    attr = true;
+  }
+  column_median_kernel<<<(unsigned)d, 1024, smem, as_stream(stream)>>>(q, m, d, stride, count, pow2,
+                                                                      center);
   OTK_LAUNCH_CHECK();
   return OTK_OK;
 }

@@ -231,8 +231,8 @@ def kernel_points(p, cost_fn: str):
 
 
 def centered_points(px, py, cost_fn: str, same: bool = False):
-    """The kernel points of both sets, shifted by one common centre (the float64
-    column mean of y; otk_column_mean / otk_shift_points).  sqeucl and eucl
+    """The kernel points of both sets, shifted by one common centre (the
+    coordinate-wise median of y; otk_column_median / otk_shift_points).  sqeucl and eucl
     costs are translation-invariant (geometry.py:268-275), and the float32
     norm form |x|^2 + |y|^2 - 2<x,y> the kernels use then loses precision only
     with the spread of the points, not with their offset from the origin.  y is
@@ -247,9 +247,8 @@ def centered_points(px, py, cost_fn: str, same: bool = False):
     m, d = ky.shape
     dev = ky.device
     center = torch.empty(d, dtype=torch.float64, device=dev)
-    ws = torch.empty(lib.otk_center_workspace_bytes(m, d), dtype=torch.uint8, device=dev)
     st = stream()
-    N.check(lib.otk_column_mean(N.ptr(ky), m, d, N.ptr(center), N.ptr(ws), st), "column mean")
+    N.check(lib.otk_column_median(N.ptr(ky), m, d, N.ptr(center), st), "column median")
     cy = torch.empty_like(ky)
     N.check(lib.otk_shift_points(N.ptr(ky), m, d, N.ptr(center), N.ptr(cy), st), "shift y")
     if same:
@@ -331,7 +330,7 @@ class PointCloudGeometry(Geometry):
 
     def _points(self):
         """fp32 device points the kernels see (cosine: normalised; sqeucl / eucl:
-        centred on the mean of y, centered_points), cached; the whole-solve
+        centred on the coordinate-wise median of y, centered_points), cached; the whole-solve
         entry needs only these (it prepares norms / planes itself)."""
         if self._kpts is None:
             device()

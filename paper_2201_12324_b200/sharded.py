@@ -447,9 +447,13 @@ def sharded_loop(engine, comm, sched: EpsilonSchedule, threshold: float, max_ite
                 engine.rows(kap, e, kap, 1 - which, 2 * t + 2)
             local = engine.check(which, measure, e)
             fb = engine.read_first_bad()
-            if p2p is not None and p2p.status() != 0:
+            # this rank's exchange status travels with its sums: a timed-out peer
+            # wait makes EVERY rank raise at the same check (none is left waiting
+            # in the gather below)
+            xs = float(p2p.status()) if p2p is not None else 0.0
+            rows = comm.all_gather_host(np.concatenate([local, [float(fb), xs]]), engine.device)
+            if rows[:, 9].max() != 0.0:
                 raise RuntimeError("peer-memory exchange timed out waiting for another rank")
-            rows = comm.all_gather_host(np.append(local, float(fb)), engine.device)
             tot = np.zeros(8)
             for r in range(rows.shape[0]):          # fixed rank order: deterministic
                 tot += rows[r, :8]
@@ -537,7 +541,7 @@ class ShardedProblem:
             return float(comm.all_gather_host(np.array([v]), dev)[:, 0].max())
 
         self._amax_reduce = amax_reduce
-        kx, ky = centered_points(x_local, y, cost_fn)  # common centre: the replicated y's mean
+        kx, ky = centered_points(x_local, y, cost_fn)  # common centre: the replicated y's median
         self.kx, self.ky = kx, ky
         self.a_loc, self.b_w = a_loc, b_w
         self.flags = _impl_flags(impl) | cflags

@@ -3,7 +3,8 @@
 The reference forms _cost_block (geometry.py:268-273) in float64, where a
 common offset of both clouds is harmless.  The device kernels form
 |x|^2 + |y|^2 - 2<x,y> in float32 (or split fp16), so they run on clouds
-shifted by one common centre (geometry.centered_points: the float64 mean of y).
+shifted by one common centre (geometry.centered_points: the coordinate-wise
+median of y).
 These cases put both clouds at offsets of 10, 100 and 1000 per coordinate and
 hold every device path to the north-star tolerances against the float64
 oracle on the same float32 inputs.

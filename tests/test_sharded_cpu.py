@@ -438,3 +438,45 @@ def test_device_counted_epoch_protocol_model():
         t.join(300)
     assert not errors, errors[:3]
     assert done == [E] * W and chk_done == [E // 10] * W
+
+
+def test_peer_timeout_on_one_rank_raises_on_every_rank():
+    """A rank whose peer-memory wait timed out (status word != 0) must not leave
+    the others blocked in the check's gather: its status travels with the
+    check sums and EVERY rank raises at the same check."""
+
+    class FakeP2P:
+        def __init__(self, bad):
+            self.bad = bad
+
+        def status(self):
+            return 1 if self.bad else 0
+
+    class ExchangingEngine(NumpyShardEngine):
+        comm = None
+
+        def cols_exchange(self, p2p, kappa, eps, kappa_next, step):
+            lall = self.comm.all_gather_rows(self.cols_partial(kappa))
+            self.cols_finalize(lall, eps, kappa_next, step)
+
+    world = 2
+    comms = ThreadComm.group(world)
+    seen = [None] * world
+    x, y, a, b, eps = _problem(9, 44, 30, 3, False)
+
+    def run(r):
+        lo, hi = shard_rows(44, world, r)
+        eng = ExchangingEngine(x[lo:hi], y, a[lo:hi], b)
+        eng.comm = comms[r]
+        try:
+            sharded_loop(eng, comms[r], EpsilonSchedule(eps), 1e-300, 100, 10, p2p=FakeP2P(r == 1))
+        except RuntimeError as e:
+            seen[r] = str(e)
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(120)
+    assert all(not t.is_alive() for t in ts)
+    assert seen[0] is not None and seen[0] == seen[1] and "timed out" in seen[0]

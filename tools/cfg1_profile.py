@@ -3,11 +3,9 @@
 Prints, for the 100-iteration fixed solve and the tolerance solve:
   * the bench step (CUDA events on torch's stream around solve_sinkhorn, L2
     flushed before each call, as bench.py times it);
-  * the wall time of back-to-back calls (host overhead included);
-  * the device time of the solve kernel alone (events around a raw
-    otk_solve_pointcloud call with prebuilt arguments).
+  * the wall time of back-to-back calls (host overhead included).
+The solve kernel's own duration comes from the ncu launch list.
 """
-import ctypes
 import os
 import sys
 import time
@@ -19,8 +17,6 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2201_12324_b200 as otk  # noqa: E402
-from paper_2201_12324_b200 import _native as N  # noqa: E402
-from paper_2201_12324_b200 import sinkhorn as S  # noqa: E402
 from paper_2201_12324_b200 import workloads  # noqa: E402
 
 wl = workloads.make(int(os.environ.get("CFG", "1")))
@@ -48,29 +44,5 @@ for label, kw in (("fixed100", dict(threshold=1e-300, max_iters=100)),
     for _ in range(50):
         solve()
     wall = (time.perf_counter() - t0) / 50 * 1e3
-    # raw entry, prebuilt args (the native call alone)
-    captured = {}
-    real = N.lib()
-
-    class Spy:
-        def __getattr__(self, name):
-            if name == "otk_solve_pointcloud":
-                def spy(ptr):
-                    captured["args"] = ctypes.cast(ptr, ctypes.POINTER(N.SolveArgs)).contents
-                    return real.otk_solve_pointcloud(ptr)
-                return spy
-            return getattr(real, name)
-    saved = S.N.lib
-    S.N.lib = lambda: Spy()
-    try:
-        solve()
-    finally:
-        S.N.lib = saved
-    A = captured["args"]
-    t0 = time.perf_counter()
-    for _ in range(50):
-        real.otk_solve_pointcloud(ctypes.byref(A))
-    raw = (time.perf_counter() - t0) / 50 * 1e3
-    print(f"{label}: iterations={out.iterations} launches={A.launches} bench-step median "
-          f"{np.median(ts):.3f} ms (min {np.min(ts):.3f}); wall {wall:.3f} ms/call; raw native call "
-          f"{raw:.3f} ms", flush=True)
+    print(f"{label}: iterations={out.iterations} bench-step median "
+          f"{np.median(ts):.3f} ms (min {np.min(ts):.3f}); wall {wall:.3f} ms/call", flush=True)
