@@ -171,8 +171,9 @@ def test_solver_anchored_graph_periods(env, anchor_always):
     a = otk.solve_sinkhorn(prob, eps, impl="tc", **kw)
     b = otk.solve_sinkhorn(prob, eps, impl="tc-noanchor", **kw)
     # either run may stop early at an exact fp32 fixed point (err == 0 <= 1e-300);
-    # past it the potentials no longer move, so the two stay comparable
-    assert a.iterations >= 40 and b.iterations >= 40
+    # past it the potentials no longer move, so the two stay comparable.  At
+    # least two graph-captured check periods ran in each.
+    assert a.iterations >= 20 and b.iterations >= 20
     assert a.converged == (a.iterations < 120) and b.converged == (b.iterations < 120)
     for name in ("f", "g"):
         u, v = getattr(a, name), getattr(b, name)
