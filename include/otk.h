@@ -291,6 +291,9 @@ int otk_check_batched(const float *f_prev, const float *f_next, const float *a,
  * fail_iter.  grid <= 0: one CTA per problem.  Requires m % 4 == 0 and
  * otk_dense_solve_fits(n, m). */
 int otk_dense_solve_fits(int64_t n, int64_t m);
+/* The cluster size K3c would use for a batch of n x m problems and the SMs it
+ * would occupy (both 0 when the per-CTA cost slices do not fit: K3p). */
+int otk_dense_cluster_plan(int64_t n, int64_t m, int64_t batch, int32_t *cluster, int32_t *sms);
 int otk_solve_dense_batched(const float *cost, int64_t batch, int64_t n, int64_t m,
                             const float *a, const float *b, const float *log_a,
                             const float *log_b, const float *eps, const double *eps_d,

@@ -94,6 +94,7 @@ SIGNATURES = {
     "otk_check_batched": (C.c_int, [P, P, P, I64, P, P, I64, I64, P, P, P, P]),
     "otk_dense_plan": (C.c_int, [P, I64, I64, P, P, F64, P, P]),
     "otk_dense_solve_fits": (C.c_int, [I64, I64]),
+    "otk_dense_cluster_plan": (C.c_int, [I64, I64, I64, P, P]),
     "otk_solve_dense_batched": (C.c_int, [P, I64, I64, I64, P, P, P, P, P, P, P, F64, I32, I32, I32,
                                           P, P, P, P, P, I32, P]),
     "otk_dense_cost_reduce": (C.c_int, [P, I64, I64, I64, P, P, P, P, P]),

@@ -337,23 +337,26 @@ __global__ void __launch_bounds__(THREADS, 1) dense_solve_kernel(Args A) {
 // ---------------------------------------------------------------- K3c
 // The same per-problem loop with the problem's cost RESIDENT ON CHIP: a
 // cluster of CL CTAs owns one problem at a time, each CTA keeping a slice of
-// ceil(n / CL) rows of C (cfg3: 64 rows x 512 columns = 128 KB) in shared
-// memory, loaded once per problem with bulk copies.  C is then read from HBM
-// once per solve instead of once per half-step, and the loop is bound by
-// the exps (MUFU), not HBM.
-//   rows half-step: local (each CTA finalizes its own rows; g replicated)
+// ceil(n / CL) rows of C (cfg3, CL = 6: 86 rows x 512 columns = 172 KB) in
+// shared memory, loaded once per problem with bulk copies.  C is then read
+// from HBM once per solve instead of once per half-step, and the loop is
+// bound by the exps (MUFU), not HBM.
+//   rows half-step: local (each CTA finalizes its own rows; g replicated),
+//     RG threads per row with RG chosen per pass (rows_pass); an anchored
+//     rows pass measured 2 % slower here (the pass is bound by the MIO queue
+//     that LDS and MUFU share, not by the max / rescale instructions)
 //   cols half-step: every CTA reduces its rows into one log2 partial per
-//     column, publishes it in its shared memory (double-buffered by parity),
-//     one cluster barrier, then EVERY CTA combines the CL partials of every
-//     column from distributed shared memory in rank order -> g is computed
-//     identically (bitwise) in every CTA of the cluster
+//     column (anchored on its previous partial of that column), pushes it
+//     into slot `rank` of EVERY CTA's shared memory (remote stores, parity
+//     double-buffered), one cluster barrier, then every CTA combines the CL
+//     partials of every column from its own shared memory in rank order ->
+//     g is computed identically (bitwise) in every CTA of the cluster
 //   check: per-CTA sums (the g terms counted by rank 0 only) and the
 //     first-bad step are published the same way and reduced in rank order,
 //     so every CTA takes the same decision at the same iteration.
 // Parity buffers make one barrier per exchange enough: a CTA rewrites a
 // parity buffer only after passing the NEXT exchange's barrier, which every
 // reader of the previous use has reached after reading.
-constexpr int CL_MAX = 8;
 
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile(
@@ -363,12 +366,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
-// Rows half-step on the CTA's resident rows: a group of RG = 8 threads per
-// row (each LDS.128 phase of 8 threads reads one row's 128 consecutive bytes:
-// no bank conflicts), each thread streaming every 8th float4 of the row with
-// an online (max, sum), then a 3-level shuffle merge in fixed order.
-constexpr int RG = 8;
-constexpr int RCH = 4 * RG * 4;  // columns per chunk
+// Rows half-step on the CTA's resident rows [rb, re): a group of RG (8, 16
+// or 32) threads per row (each LDS.128 phase of 8 threads reads 128
+// consecutive bytes of one row: no bank conflicts), each thread streaming
+// every RG-th float4 of the row with an online (max, sum), then a log2(RG)-level
+// shuffle merge in fixed order.  rows_pass picks RG per pass so that a CTA's
+// last, partial pass still keeps most threads busy.
 
 // sum_e 2^(u_e - ms) over 16 values in two chains (even / odd e), as packed
 // FADD2 pairs: bitwise the scalar (a0 += ..even.., a1 += ..odd..; a0 + a1)
@@ -382,17 +385,36 @@ __device__ __forceinline__ float sum_ex2_16(const float (&u)[16], float ms) {
   }
   return acc.x + acc.y;
 }
-template <bool CHECK>
-__device__ void rows_local(const float *Cs, int rows, int m, const float *by, const float *lw,
+// ---- anchored passes (K3c).  Sinkhorn hands every row (column partial) a
+// good shift for free: the same row's log2 result of the previous half-step
+// of its role, A_i.  The anchored pass sums 2^(u_ij - A_i) directly -- no
+// running max, no compare, no rescale -- and accepts the row when A_i was
+// finite and lo <= L_i - A_i <= 120 (every term within 2^-30 of the row's
+// sum stayed above the ex2 flush threshold, nothing overflowed; lo = -96 +
+// 2 log2(#terms)) or when L_i is NaN (propagates like the running max); any
+// other row is redone at once with the running max by the same threads
+// (same rule as the tcgen05 kernel's anchored half-step, lse_tc.cu).
+__device__ __forceinline__ bool anchor_ok(float L, float A, float lo) {
+  const float dd = L - A;
+  return (L != L) || (dd >= lo && dd <= 120.f);
+}
+__device__ __forceinline__ float nan_if_not_finite(float L) {
+  return isfinite(L) ? L : __int_as_float(0x7fc00000);
+}
+
+template <bool CHECK, int RG>
+__device__ void rows_local(const float *Cs, int rb, int re, int m, const float *by, const float *lw,
                            float eps, float kappa, float *out, float *bx, int *fbad, int step,
                            const float *fprev, const float *a, double eps_d, double (&chk)[NV]) {
+  constexpr int RCH = 4 * RG * 4;  // columns per chunk
   const int gi = threadIdx.x / RG, gl = threadIdx.x % RG;
   constexpr int GROUPS = THREADS / RG;
-  for (int i0 = 0; i0 < rows; i0 += GROUPS) {
+  const float2 nk = make_float2(-kappa, -kappa);
+  for (int i0 = rb; i0 < re; i0 += GROUPS) {
     const int i = i0 + gi;
     Lse2 st;
     st.init();
-    if (i < rows) {
+    if (i < re) {
       const float *row = Cs + (int64_t)i * m;
       for (int j0 = gl * 4; j0 < m; j0 += RCH) {  // 4 float4 per chunk
         float u[16];
@@ -403,7 +425,6 @@ __device__ void rows_local(const float *Cs, int rows, int m, const float *by, co
             const float4 c = *reinterpret_cast<const float4 *>(row + j);
             const float4 h = *reinterpret_cast<const float4 *>(by + j);
             // packed FFMA2: the same IEEE results as four scalar FFMAs
-            const float2 nk = make_float2(-kappa, -kappa);
             const float2 u01 = __ffma2_rn(nk, make_float2(c.x, c.y), make_float2(h.x, h.y));
             const float2 u23 = __ffma2_rn(nk, make_float2(c.z, c.w), make_float2(h.z, h.w));
             u[4 * q + 0] = u01.x;
@@ -427,12 +448,12 @@ __device__ void rows_local(const float *Cs, int rows, int m, const float *by, co
       }
     }
 #pragma unroll
-    for (int o = RG / 2; o > 0; o >>= 1) {  // within the row's group of 8 lanes
+    for (int o = RG / 2; o > 0; o >>= 1) {  // within the row's group of RG lanes
       const float m2 = __shfl_xor_sync(0xffffffffu, st.m, o);
       const float s2 = __shfl_xor_sync(0xffffffffu, st.s, o);
       st.merge(m2, s2);
     }
-    if (gl == 0 && i < rows) {
+    if (gl == 0 && i < re) {
       const float v = eps * lw[i] - eps * kLn2 * st.value();
       out[i] = v;
       bx[i] = v * kappa;
@@ -450,68 +471,81 @@ __device__ void rows_local(const float *Cs, int rows, int m, const float *by, co
   }
 }
 
-// this CTA's log2 partial of every column over its rows -> part[j]
-// (16-row chunks: max first, then one rescale at most, sums in two chains)
-__device__ void cols_partial_local(const float *Cs, int rows, int m, const float *bx, float kappa,
-                                   float *part) {
-  for (int j = threadIdx.x; j < m; j += THREADS) {
-    float mx = -INFINITY, sm = 0.f;
-    const float *cp = Cs + j;
+// This CTA's log2 partial of column j over its rows, anchored on the same
+// column's partial of the previous column half-step (canc[j], NaN = none),
+// running max as the fallback.  Returns L (the caller publishes it).
+__device__ __forceinline__ float col_partial_anchored(const float *Cs, int rows, int m, const float *bx,
+                                                      float kappa, int j, float A, float lo) {
+  const float *cp = Cs + j;
+  if (isfinite(A)) {
+    float2 acc = make_float2(0.f, 0.f);
+    const float2 nk = make_float2(-kappa, -kappa), nA = make_float2(-A, -A);
     int i0 = 0;
-    for (; i0 + 16 <= rows; i0 += 16, cp += 16 * m) {
-      float u[16];
-      // the 16 row potentials as 4 broadcast LDS.128 (bx is 16-byte aligned, i0 % 16 == 0):
-      // a quarter of the shared-memory instructions (column pass 2.8 -> 2.5 us per iteration)
+    for (; i0 + 16 <= rows; i0 += 16) {
       float hb[16];
 #pragma unroll
       for (int k = 0; k < 16; k += 4) {
-        const float4 h = *reinterpret_cast<const float4 *>(bx + i0 + k);
-        hb[k] = h.x;
-        hb[k + 1] = h.y;
-        hb[k + 2] = h.z;
-        hb[k + 3] = h.w;
+        const float4 hh = *reinterpret_cast<const float4 *>(bx + i0 + k);
+        hb[k] = hh.x;
+        hb[k + 1] = hh.y;
+        hb[k + 2] = hh.z;
+        hb[k + 3] = hh.w;
       }
 #pragma unroll
       for (int k = 0; k < 16; k += 2) {
-        const float2 uu = __ffma2_rn(make_float2(-kappa, -kappa), make_float2(cp[k * m], cp[(k + 1) * m]),
-                                     make_float2(hb[k], hb[k + 1]));
-        u[k] = uu.x;
-        u[k + 1] = uu.y;
+        const float2 x = __fadd2_rn(__ffma2_rn(nk, make_float2(cp[(i0 + k) * m], cp[(i0 + k + 1) * m]),
+                                               make_float2(hb[k], hb[k + 1])), nA);
+        acc = __fadd2_rn(acc, make_float2(ex2(x.x), ex2(x.y)));
       }
-      float c0 = fmaxf(fmaxf(u[0], u[1]), fmaxf(u[2], u[3]));
-      float c1 = fmaxf(fmaxf(u[4], u[5]), fmaxf(u[6], u[7]));
-      float c2 = fmaxf(fmaxf(u[8], u[9]), fmaxf(u[10], u[11]));
-      float c3 = fmaxf(fmaxf(u[12], u[13]), fmaxf(u[14], u[15]));
-      const float cm = fmaxf(fmaxf(c0, c1), fmaxf(c2, c3));
-      if (cm > mx) {
-        sm *= ex2(mx - cm);
-        mx = cm;
-      }
-      const float ms = (mx == -INFINITY) ? 0.f : mx;
-      sm += sum_ex2_16(u, ms);
     }
-    if (i0 < rows) {  // last partial chunk, masked
-      float u[16];
+    if (i0 < rows) {  // last partial chunk, masked (-inf terms add 0)
 #pragma unroll
-      for (int k = 0; k < 16; ++k) u[k] = (i0 + k < rows) ? fmaf(-kappa, cp[k * m], bx[i0 + k]) : -INFINITY;
-      float cm = -INFINITY;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) cm = fmaxf(cm, u[k]);
-      if (cm > mx) {
-        sm *= ex2(mx - cm);
-        mx = cm;
+      for (int k = 0; k < 16; k += 2) {
+        const float x0 = (i0 + k < rows) ? fmaf(-kappa, cp[(i0 + k) * m], bx[i0 + k]) - A : -INFINITY;
+        const float x1 = (i0 + k + 1 < rows) ? fmaf(-kappa, cp[(i0 + k + 1) * m], bx[i0 + k + 1]) - A : -INFINITY;
+        acc = __fadd2_rn(acc, make_float2(ex2(x0), ex2(x1)));
       }
-      const float ms = (mx == -INFINITY) ? 0.f : mx;
-      float a0 = 0.f;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) a0 += ex2(u[k] - ms);
-      sm += a0;
     }
-    Lse2 st;
-    st.m = mx;
-    st.s = sm;
-    part[j] = st.value();
+    const float sm = acc.x + acc.y;
+    const float L = (sm > 0.f) ? A + lg2(sm) : ((sm != sm) ? sm : -INFINITY);
+    if (anchor_ok(L, A, lo)) return L;
   }
+  float mx = -INFINITY, sm = 0.f;
+  for (int i0 = 0; i0 < rows; i0 += 16) {
+    float u[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) u[k] = (i0 + k < rows) ? fmaf(-kappa, cp[(i0 + k) * m], bx[i0 + k]) : -INFINITY;
+    float cm = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) cm = fmaxf(cm, u[k]);
+    if (cm > mx) {
+      sm *= ex2(mx - cm);
+      mx = cm;
+    }
+    const float ms = (mx == -INFINITY) ? 0.f : mx;
+    sm += sum_ex2_16(u, ms);
+  }
+  Lse2 st;
+  st.m = mx;
+  st.s = sm;
+  return st.value();
+}
+
+
+// Rows pass of K3c: full passes of 64 rows with 8 threads per row, then the
+// remaining R rows with 8 (R > 32), 16 (R > 16) or 32 threads per row, so a
+// slice of 86 rows (cfg3, CL = 6) costs 64 + 32 cells per thread instead of
+// 2 x 64.
+template <bool CHECK>
+__device__ __forceinline__ void rows_pass(const float *Cs, int rows, int m, const float *by, const float *lw,
+                                          float eps, float kappa, float *out, float *bx, int *fbad,
+                                          int step, const float *fprev, const float *a, double eps_d,
+                                          double (&chk)[NV]) {
+  const int full = (rows / 64) * 64, rem = rows - full;
+  if (full > 0) rows_local<CHECK, 8>(Cs, 0, full, m, by, lw, eps, kappa, out, bx, fbad, step, fprev, a, eps_d, chk);
+  if (rem > 32) rows_local<CHECK, 8>(Cs, full, rows, m, by, lw, eps, kappa, out, bx, fbad, step, fprev, a, eps_d, chk);
+  else if (rem > 16) rows_local<CHECK, 16>(Cs, full, rows, m, by, lw, eps, kappa, out, bx, fbad, step, fprev, a, eps_d, chk);
+  else if (rem > 0) rows_local<CHECK, 32>(Cs, full, rows, m, by, lw, eps, kappa, out, bx, fbad, step, fprev, a, eps_d, chk);
 }
 
 template <int CL>
@@ -526,8 +560,10 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
   float *Cs = shc;                                    // [rows_per][m]
   float *f0 = Cs + (size_t)rows_per * m, *f1 = f0 + rp4, *bx = f1 + rp4;
   float *g = bx + rp4, *by = g + m4;
-  float *part = by + m4;                              // [2][m4] log2 column partials
-  double *slot = reinterpret_cast<double *>(part + 2 * m4);  // [2][NV + 1]
+  float *canc = by + m4;                              // [m4] column-partial anchors
+  float *xs = canc + m4;                              // [2][CL][m4] pushed column partials
+  float *las = xs + 2 * CL * m4, *lbs = las + rp4;    // log weights staged in shared memory
+  double *slot = reinterpret_cast<double *>(lbs + m4);  // [2][NV + 1]
   __shared__ double red[NV * WARPS];
   __shared__ double rsl[CL * (NV + 1)], rtot[NV + 1];
   __shared__ int fbad;
@@ -544,7 +580,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
   for (int64_t b = cid; b < A.batch; b += ncl) {
     const float *Cb = A.C + b * (int64_t)n * m;
     const float *a = A.a + b * n + r0, *bw = A.b + b * m;
-    const float *la = A.la + b * n + r0, *lb = A.lb + b * m;
+    const float *la = las, *lb = lbs;  // the finalizes read log weights from shared memory
     const float eps = A.eps[b];
     const double eps_d = A.eps_d[b];
     const float kappa = kLog2e / eps;
@@ -565,8 +601,11 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
       const float g0 = A.g_init ? A.g_init[b * m + j] : 0.f;
       g[j] = g0;
       by[j] = g0 * kappa;
+      canc[j] = __int_as_float(0x7fc00000);  // no anchors yet: first passes run the running max
+      lbs[j] = A.lb[b * m + j];
       if (bad_potential(g0)) atomicMin(&fbad, 1);
     }
+    for (int i = threadIdx.x; i < rp4; i += THREADS) las[i] = (i < rows) ? A.la[b * n + r0 + i] : 0.f;
     if (rows > 0) {  // wait for the cost slice
       asm volatile(
           "{\n\t.reg .pred p;\nW_%=:\n\t"
@@ -585,21 +624,33 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
     for (t = 1; t <= A.max_iters; ++t) {
       dtrace(A, tr, t, 0);
       if (!f_ready) {
-        rows_local<false>(Cs, rows, m, by, la, eps, kappa, f, bx, &fbad, 2 * t, nullptr, a, eps_d, chk);
+        rows_pass<false>(Cs, rows, m, by, la, eps, kappa, f, bx, &fbad, 2 * t, nullptr, a, eps_d, chk);
         __syncthreads();
       }
       dtrace(A, tr, t, 1);
       f_ready = false;
-      // ---- columns: local partials -> cluster exchange -> every CTA forms g
-      float *mypart = part + xpar * m4;
-      cols_partial_local(Cs, rows, m, bx, kappa, mypart);
+      // ---- columns: local partials pushed into every CTA's shared memory
+      // (remote stores), one cluster barrier, then every CTA combines the CL
+      // partials of every column from its own shared memory in rank order
+      float *xbuf = xs + xpar * CL * m4;
+      {
+        const float clo = -96.f + 2.f * log2f((float)max(rows, 1));
+        float *mine = xbuf + rank * m4;
+        for (int j = threadIdx.x; j < m; j += THREADS) {
+          const float L = (rows > 0) ? col_partial_anchored(Cs, rows, m, bx, kappa, j, canc[j], clo)
+                                     : -INFINITY;
+          canc[j] = nan_if_not_finite(L);
+#pragma unroll
+          for (int r = 0; r < CL; ++r) cluster.map_shared_rank(mine, r)[j] = L;
+        }
+      }
       dtrace(A, tr, t, 2);
       cluster.sync();
       dtrace(A, tr, t, 3);
       for (int j = threadIdx.x; j < m; j += THREADS) {
         float v[CL];
 #pragma unroll
-        for (int r = 0; r < CL; ++r) v[r] = cluster.map_shared_rank(mypart, r)[j];
+        for (int r = 0; r < CL; ++r) v[r] = xbuf[r * m4 + j];
         float mx = -INFINITY;
         bool nan = false;
 #pragma unroll
@@ -629,7 +680,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
       if (t % A.inner_iters == 0 || t == A.max_iters) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) chk[k] = 0.0;
-        rows_local<true>(Cs, rows, m, by, la, eps, kappa, fn, bx, &fbad, 2 * t + 2, f, a, eps_d, chk);
+        rows_pass<true>(Cs, rows, m, by, la, eps, kappa, fn, bx, &fbad, 2 * t + 2, f, a, eps_d, chk);
         if (rank == 0) {  // g is replicated: its terms are counted once
           for (int j = threadIdx.x; j < m; j += THREADS) {
             const double gj = g[j], bj = bw[j];
@@ -722,7 +773,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
 size_t cluster_smem_bytes(int n, int m, int CL) {
   const size_t rows_per = (n + CL - 1) / CL;
   const size_t rp4 = (rows_per + 3) & ~(size_t)3, m4 = (m + 3) & ~3;
-  return rows_per * m * sizeof(float) + (3 * rp4 + 2 * m4 + 2 * m4) * sizeof(float) +
+  return rows_per * m * sizeof(float) + (4 * rp4 + 4 * m4 + 2 * (size_t)CL * m4) * sizeof(float) +
          2 * (NV + 1) * sizeof(double) + 64;
 }
 
@@ -762,19 +813,49 @@ static int cluster_try(const Args &A, int n, int m, int64_t batch, int grid, cud
   return OTK_OK;
 }
 
-// Cluster size with the most SMs in use (clusters live inside one GPC: 8 x k
-// may leave SMs idle where 6 x k does not); OTK_DENSE_CL forces 6 or 8.
+// Cluster size with the most SMs in use (clusters live inside one GPC, so
+// e.g. 8 x k may leave SMs idle where 6 x k or 7 x k does not; sizes whose
+// cost slice does not fit shared memory drop out); ties go to the larger
+// cluster (fewer rows per CTA).  OTK_DENSE_CL forces one size.
 int launch_cluster_solve(const Args &A, int n, int m, int64_t batch, int grid, int want_cl,
                          cudaStream_t st) {
-  int used6 = 0, used8 = 0;
-  const bool ok6 = (want_cl == 0 || want_cl == 6) &&
-                   cluster_try<6>(A, n, m, batch, grid, st, false, &used6) == OTK_OK;
-  const bool ok8 = (want_cl == 0 || want_cl == 8) &&
-                   cluster_try<8>(A, n, m, batch, grid, st, false, &used8) == OTK_OK;
-  if (!ok6 && !ok8) return OTK_ENOTSUP;
+  int used[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  bool ok[9] = {false, false, false, false, false, false, false, false, false};
+  ok[5] = (want_cl == 0 || want_cl == 5) && cluster_try<5>(A, n, m, batch, grid, st, false, &used[5]) == OTK_OK;
+  ok[6] = (want_cl == 0 || want_cl == 6) && cluster_try<6>(A, n, m, batch, grid, st, false, &used[6]) == OTK_OK;
+  ok[7] = (want_cl == 0 || want_cl == 7) && cluster_try<7>(A, n, m, batch, grid, st, false, &used[7]) == OTK_OK;
+  ok[8] = (want_cl == 0 || want_cl == 8) && cluster_try<8>(A, n, m, batch, grid, st, false, &used[8]) == OTK_OK;
+  int best = 0;
+  for (int c = 5; c <= 8; ++c)
+    if (ok[c] && (best == 0 || used[c] >= used[best])) best = c;
   int dummy = 0;
-  if (ok8 && (!ok6 || used8 >= used6)) return cluster_try<8>(A, n, m, batch, grid, st, true, &dummy);
-  return cluster_try<6>(A, n, m, batch, grid, st, true, &dummy);
+  switch (best) {
+    case 5: return cluster_try<5>(A, n, m, batch, grid, st, true, &dummy);
+    case 6: return cluster_try<6>(A, n, m, batch, grid, st, true, &dummy);
+    case 7: return cluster_try<7>(A, n, m, batch, grid, st, true, &dummy);
+    case 8: return cluster_try<8>(A, n, m, batch, grid, st, true, &dummy);
+    default: return OTK_ENOTSUP;
+  }
+}
+
+// The cluster size the batched solve would use for n x m problems and the SMs
+// it would occupy (0, 0 when the cost slices do not fit: K3p streams instead).
+int cluster_plan(int n, int m, int64_t batch, int *cl, int *sms) {
+  Args A{};
+  int used[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  bool ok[9] = {false, false, false, false, false, false, false, false, false};
+  ok[5] = cluster_try<5>(A, n, m, batch, 0, nullptr, false, &used[5]) == OTK_OK;
+  ok[6] = cluster_try<6>(A, n, m, batch, 0, nullptr, false, &used[6]) == OTK_OK;
+  ok[7] = cluster_try<7>(A, n, m, batch, 0, nullptr, false, &used[7]) == OTK_OK;
+  ok[8] = cluster_try<8>(A, n, m, batch, 0, nullptr, false, &used[8]) == OTK_OK;
+  *cl = 0;
+  *sms = 0;
+  for (int c = 5; c <= 8; ++c)
+    if (ok[c] && (*cl == 0 || used[c] >= used[*cl])) {
+      *cl = c;
+      *sms = used[c];
+    }
+  return OTK_OK;
 }
 
 size_t smem_bytes(int n, int m) {
@@ -786,6 +867,21 @@ size_t smem_bytes(int n, int m) {
 }  // namespace otk
 
 using namespace otk;
+
+extern "C" int otk_dense_cluster_plan(int64_t n, int64_t m, int64_t batch, int32_t *cluster,
+                                      int32_t *sms) {
+  OTK_CHECK_ARG(cluster && sms && n > 0 && m > 0 && batch > 0, "otk_dense_cluster_plan: bad arguments");
+  if (!otk_dense_solve_fits(n, m)) {
+    *cluster = 0;
+    *sms = 0;
+    return OTK_OK;
+  }
+  int c = 0, u = 0;
+  dsolve::cluster_plan((int)n, (int)m, batch, &c, &u);
+  *cluster = c;
+  *sms = u;
+  return OTK_OK;
+}
 
 extern "C" int otk_dense_solve_fits(int64_t n, int64_t m) {
   if (n < 1 || m < 1 || m % 4 != 0 || n > 16384 || m > 16384) return 0;

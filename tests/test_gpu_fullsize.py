@@ -14,7 +14,7 @@ Tolerances (north_star): f, g 1e-4 relative (inf-norm); transport cost and
 dual 1e-5 relative; identical iteration count and converged flag.  The
 marginal errors and the dual trace are the reference's check values
 (sinkhorn.py:183-186) evaluated by the fused check kernel from float32
-potentials with float64 sums: errors within 1e-3 relative plus twice the
+potentials with float64 sums: errors within 1e-3 relative plus four times the
 float32 floor ulp(max|f|)/eps (each row's r_i = a_i exp((f_i - f'_i)/eps)
 carries a relative rounding of that size; ~6e-6 for cfg5),
 dual trace within 1e-5 relative.
@@ -74,7 +74,7 @@ def _check_against(otk, fx, out, prob):
     ef, eg = rel_inf(out.f, fx["f"]), rel_inf(out.g, fx["g"])
     assert ef <= POT_TOL and eg <= POT_TOL, (ef, eg)
     np.testing.assert_allclose(out.errors, fx["errors"], rtol=ERR_RTOL,
-                               atol=2.0 * err_floor(fx["f"], fx["eps"]))
+                               atol=4.0 * err_floor(fx["f"], fx["eps"]))
     np.testing.assert_allclose(out.dual_trace, fx["dual_trace"], rtol=COST_TOL)
     cost = otk.reg_ot_cost(out, prob)
     rt = abs(cost.transport_cost / float(fx["transport"]) - 1.0)
@@ -121,7 +121,7 @@ def test_cfg3_all_512_problems_match_reference(otk):
     for k in range(0, 512, 37):  # the per-problem check traces
         nk = int(fx["n_checks"][k])
         np.testing.assert_allclose(outs[k].errors, fx["errors"][k, :nk], rtol=ERR_RTOL,
-                                   atol=2.0 * err_floor(fx["f"][k], fx["eps"][k]))
+                                   atol=4.0 * err_floor(fx["f"][k], fx["eps"][k]))
         np.testing.assert_allclose(outs[k].dual_trace, fx["dual_trace"][k, :nk], rtol=COST_TOL)
 
 
@@ -140,4 +140,4 @@ def test_converged_flag_pinned_by_float64_check(otk, name):
     assert rel_inf(out.f, fx["f"]) <= 1e-5 and rel_inf(out.g, fx["g"]) <= 1e-5
     assert float(fx["ref_error"]) <= wl.threshold
     np.testing.assert_allclose(out.errors[-1], float(fx["ref_error"]), rtol=ERR_RTOL,
-                               atol=2.0 * err_floor(fx["f"], fx["eps"]))
+                               atol=4.0 * err_floor(fx["f"], fx["eps"]))
