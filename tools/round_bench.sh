@@ -1,0 +1,26 @@
+#!/bin/bash
+# One GPU-box pass of the round's evidence (run under gpurun from the repo root):
+#   pytest -m gpu, smoke(), bench.py for every config + the reference arm, the
+#   ncu launch list of the default bench command and one --set full capture of
+#   the headline kernel.  Everything lands in gpurun_out/ with prefix $1.
+set -u
+P=${1:-r02}
+mkdir -p gpurun_out
+timeout 1800 python -m pytest tests -m gpu -q -rf > gpurun_out/${P}_gpu_tests.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${P}_smoke.txt 2>&1
+for k in 1 2 3 5 4; do
+  timeout 900 python bench.py --config $k > gpurun_out/${P}_bench_cfg$k.json 2> gpurun_out/${P}_bench_cfg$k.err
+done
+timeout 900 python bench.py --impl reference > gpurun_out/${P}_bench_cfg4_reference.json 2> gpurun_out/${P}_bench_ref.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --log-file gpurun_out/${P}_launches_cfg4.csv python bench.py --steps 2 --warmup 1 > gpurun_out/${P}_ncu_launches.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:lse_tc -s 1 -c 1 \
+  -o gpurun_out/${P}_lse_tc_cfg4 python tools/prof_half_step.py --config 4 --reps 3 > gpurun_out/${P}_ncu_full.log 2>&1
+tail -3 gpurun_out/${P}_gpu_tests.txt; tail -1 gpurun_out/${P}_smoke.txt
+for k in 1 2 3 5 4; do python -c "
+import json,sys
+for l in open('gpurun_out/${P}_bench_cfg$k.json'):
+    if l.startswith('{'):
+        d=json.loads(l); r=d.get('roofline') or {}
+        print('cfg$k', '%.3e'%d['value'], 'e2e %.3e'%d.get('e2e',{}).get('value',0), 'frac %.3f'%r.get('frac',0), 'ttt %.2f ms'%d['run']['time_to_tolerance_ms'], d['clocks'])
+"; done
