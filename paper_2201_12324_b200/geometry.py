@@ -184,7 +184,7 @@ def _all_finite(p) -> bool:
 
 
 class _Cloud:
-    """Device-resident point set: fp32 points, squared norms and, for d >= 32,
+    """Device-resident point set: fp32 points, squared norms and, on the tcgen05 path (every d),
     the split-fp16 operand planes (hi, lo) and norm planes (ext_a, ext_b) of
     the tcgen05 kernel, all scaled by the geometry's common power-of-two s."""
 
