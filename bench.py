@@ -37,7 +37,6 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 
 import numpy as np
@@ -100,54 +99,87 @@ def traffic_for(name):
 
 
 # ------------------------------------------------------------------ clocks
+_SAMPLER_SRC = r"""
+import json, sys, time
+import pynvml
+idx, period = int(sys.argv[1]), float(sys.argv[2])
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+out = []
+sys.stdout.write("ready\n"); sys.stdout.flush()
+import select
+while True:
+    r, _, _ = select.select([sys.stdin], [], [], 0)
+    if r:
+        break
+    out.append((time.time(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))))
+    time.sleep(period)
+sys.stdout.write(json.dumps(out) + "\n"); sys.stdout.flush()
+"""
+
+
 class ClockSampler:
-    """Samples SM clock and throttle reasons (NVML) while the timed region runs."""
+    """Samples SM clock and throttle reasons (NVML) while the timed region runs,
+    every `period` s, from a SEPARATE process: a sampling thread in this
+    process would contend with the timed host code (GIL, driver locks) --
+    measured on cfg1, a 2 ms in-process sampler stretched a 0.8 ms solve to
+    4.3 ms.  Only the samples taken inside [enter, exit] are kept."""
 
     REASONS = {0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, index=0, period=0.002):
+    def __init__(self, index=0, period=None):
+        import subprocess
         self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.proc = None
+        if period is None:
+            period = float(os.environ.get("OTK_CLOCK_PERIOD", "0.01"))
         self.period = period
-        self._stop = threading.Event()
         try:
+            if period <= 0:
+                raise RuntimeError("sampling disabled")
             import pynvml
             pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER_SRC, str(index), str(period)],
+                                         stdin=subprocess.PIPE, stdout=subprocess.PIPE, text=True)
+            if self.proc.stdout.readline().strip() != "ready":
+                raise RuntimeError("clock sampler did not start")
         except Exception:  # noqa: BLE001
-            self.nv = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit:
-                        self.reasons.add(name)
-            except Exception:  # noqa: BLE001
-                pass
-            time.sleep(self.period)
+            self.proc = None
 
     def __enter__(self):
-        if self.nv is not None:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        if self.nv is not None:
-            self.t.join()
+        self.t1 = time.time()
+        if self.proc is None:
+            return
+        try:
+            out, _ = self.proc.communicate("stop\n", timeout=30)
+            rows = json.loads(out.strip().splitlines()[-1])
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+            return
+        inside = [r for r in rows if self.t0 <= r[0] <= self.t1]
+        if not inside and rows:  # a region shorter than one period: the nearest sample
+            inside = [min(rows, key=lambda r: abs(r[0] - 0.5 * (self.t0 + self.t1)))]
+        for _, mhz, mask in inside:
+            self.samples.append(mhz)
+            for bit, name in self.REASONS.items():
+                if mask & bit:
+                    self.reasons.add(name)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
         return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "sampler": f"separate process, NVML every {self.period * 1e3:g} ms"}
 
 
 # ------------------------------------------------------------------ CPU reference arm
@@ -444,6 +476,7 @@ def run_ours(args, wl, rank, world):
     kw_step = solve_kw(wl, args.iters)
     kw_tol = solve_kw(wl, 0)
     tol_note = "one tolerance solve from device-resident points"
+    exchange_note = None
     if wl.materialised:
         xd = torch.from_numpy(wl.x).to(dev)
         yd = torch.from_numpy(wl.y).to(dev)
@@ -467,10 +500,35 @@ def run_ours(args, wl, rank, world):
         ix, iy = workloads.subsample_rows(n, m, wl.eps_subsample_seed or 0)
         x_sub = torch.from_numpy(wl.x[ix] if wl.eps_subsample_seed is not None else wl.x).to(dev)
 
+        exchange = os.environ.get("OTK_EXCHANGE", "auto")
+
         def new_problem():
             return otk.ShardedProblem(xd, yd, a_loc, wl.b, x_is_local=True, n_total=n, comm=comm,
-                                      impl=args.kernel)
+                                      impl=args.kernel, exchange=exchange)
         sprob = new_problem()
+        exchange_note = None
+        if sprob.exchange == "p2p":
+            # the peer-memory exchange must reproduce the NCCL all-gather path bit for
+            # bit on a short solve before it is timed; otherwise every rank falls back
+            ok = 1.0
+            try:
+                p_out = sprob.solve(wl.eps, threshold=1e-300, max_iters=3)
+                c_out = otk.ShardedProblem(xd, yd, a_loc, wl.b, x_is_local=True, n_total=n, comm=comm,
+                                           impl=args.kernel, exchange="collective").solve(
+                    wl.eps, threshold=1e-300, max_iters=3)
+                ok = float(np.array_equal(p_out.g, c_out.g) and np.array_equal(p_out.f_local, c_out.f_local))
+            except Exception as exc:  # noqa: BLE001 -- reported in the JSON line, then the fallback
+                exchange_note = f"peer exchange failed its check ({type(exc).__name__}: {exc})"
+                ok = 0.0
+            flag = torch.tensor([ok], device=dev)
+            torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+            if flag.item() < 1.0:
+                exchange = "collective"
+                os.environ["OTK_EXCHANGE"] = "collective"  # the e2e leg too
+                exchange_note = exchange_note or "peer exchange differed from the all-gather path"
+                sprob = new_problem()
+            else:
+                exchange_note = "peer exchange verified bitwise against the NCCL all-gather path (3 iterations)"
 
         def make_solve(kw):
             def solve():
@@ -586,12 +644,28 @@ def run_ours(args, wl, rank, world):
         tt = float(t.item())
     tol_ms = 1e3 * tt / args.steps
     tol_iters, tol_conv, tol_checks = summary(o_tol[-1])
+    # the same tolerance solve on the already-prepared problem (solver time alone)
+    solve_only = make_solve(kw_tol)
+    for _ in range(2):
+        solve_only()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t_so, _ = timed_steps(solve_only, args.steps, dev, flush)
+    tso = sum(t_so)
+    if world > 1:
+        t = torch.tensor([tso], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tso = float(t.item())
     step_desc = (f"one fixed {kw_step['max_iters']}-iteration solve (threshold 1e-300, checks every "
                  f"{wl.inner_iters} as in the reference; SURVEY.md §8d: throughput from "
                  "fixed-iteration runs), inputs resident in HBM" if args.iters
                  else "one complete solve to tolerance (inputs resident in HBM)")
     run = {"parallelism": parallelism, "iterations_per_step": iters, "converged": conv,
-           "step": step_desc, "time_to_tolerance_ms": tol_ms, "tolerance_iterations": tol_iters,
+           "step_ms": [round(1e3 * t_, 4) for t_ in times],
+           **({"exchange_check": exchange_note} if world > 1 and not wl.materialised else {}),
+           "step": step_desc, "time_to_tolerance_ms": tol_ms,
+           "time_to_tolerance_solve_only_ms": 1e3 * tso / args.steps, "tolerance_iterations": tol_iters,
            "tolerance_converged": tol_conv, "tolerance_checks": tol_checks,
            "time_to_tolerance_note": tol_note, "kernel": args.kernel}
     result = {

@@ -2,7 +2,8 @@
 
 Random shapes (odd sizes, n != m), dimensions across every kernel route
 (FP32 small solve, tcgen05 V1 / pair / V2 / V4), eps scales, zero weights,
-warm starts; fixed-iteration solves compared on f, g (1e-4 of the largest
+warm starts, common offsets of 0 / 10 / 100 / 1000 per coordinate;
+fixed-iteration solves compared on f, g (1e-4 of the largest
 finite entry) and the transport cost (1e-5); anchored vs running-max
 trajectories compared at 2e-6.  usage: python tools/fuzz_parity.py [cases] [seed]
 """
@@ -31,8 +32,10 @@ def main(cases=60, seed=0):
         d = int(rng.choice([2, 3, 5, 16, 33, 64, 100, 128, 200, 300, 520]))
         n = int(rng.integers(1, 900))
         m = int(rng.integers(1, 900))
-        x = rng.standard_normal((n, d)).astype(np.float32) * float(rng.choice([0.3, 1.0, 4.0]))
-        y = (rng.standard_normal((m, d)) * float(rng.choice([0.5, 1.0, 2.0])) + rng.uniform(-1, 1)).astype(np.float32)
+        off = float(rng.choice([0.0, 0.0, 10.0, 100.0, 1000.0]))  # common offset (translation)
+        x = (rng.standard_normal((n, d)) * float(rng.choice([0.3, 1.0, 4.0])) + off).astype(np.float32)
+        y = (rng.standard_normal((m, d)) * float(rng.choice([0.5, 1.0, 2.0])) + rng.uniform(-1, 1)
+             + off).astype(np.float32)
         a = rng.uniform(0.5, 1.5, n)
         b = rng.uniform(0.5, 1.5, m)
         if rng.random() < 0.4 and n > 2:
@@ -69,7 +72,7 @@ def main(cases=60, seed=0):
             worst[kk] = max(worst[kk], v)
         bad = e["f"] > 1e-4 or e["g"] > 1e-4 or e["cost"] > 1e-5 or e.get("anch", 0.0) > 1e-5
         fails += bad
-        print(f"case {c:3d} n={n:4d} m={m:4d} d={d:3d} eps/mc={eps / max(mc, 1e-3):.3g} its={its:2d} "
+        print(f"case {c:3d} n={n:4d} m={m:4d} d={d:3d} off={off:g} eps/mc={eps / max(mc, 1e-3):.3g} its={its:2d} "
               f"zeros={int((a == 0).sum())}/{int((b == 0).sum())} g0={'y' if g0 is not None else 'n'} "
               + " ".join(f"{kk}={v:.1e}" for kk, v in e.items()) + ("  <-- FAIL" if bad else ""),
               flush=True)
