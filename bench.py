@@ -391,9 +391,10 @@ def small_roofline(value, step_s, wl):
 def dense_roofline(C, wl, reps=3):
     """Dominant kernel of the batched materialised path: the one-launch batched
     solve (otk_solve_dense_batched: K3c by default, K3p with OTK_DENSE_KERNEL=cta),
-    timed with CUDA events on its stream.
-    Algorithmic bytes: 4 B of C per cell per half-step, 2*iters + 1 half-steps
-    per problem (the fused check's extra row pass included)."""
+    timed with CUDA events on its stream.  K3c's roof is MUFU: one ex2 per cell
+    per half-step, 2*iters + 1 half-steps per problem (the fused check's extra
+    row pass included); the streaming-equivalent byte rate (4 B of C per cell
+    per half-step) is reported beside it.  K3p's roof is HBM."""
     import ctypes
     import torch
     from paper_2201_12324_b200 import _native as N
@@ -429,19 +430,27 @@ def dense_roofline(C, wl, reps=3):
     cluster = os.environ.get("OTK_DENSE_KERNEL", "cluster") != "cta"
     ex2, _ = pipes()
     exps = float(n) * m * float(np.sum(2 * iters + 1))
-    return {"bound": "hbm", "achieved": gbs, "peak": float(pk["hbm_gbs"]), "unit": "GB/s",
-            "frac": gbs / float(pk["hbm_gbs"]), "traffic": traffic_for(wl.name),
-            "kernel": ("otk_solve_dense_batched (K3c: cost resident in a cluster's shared memory, "
-                       "one launch)" if cluster else
-                       "otk_solve_dense_batched (K3p: one CTA per problem streaming C, one launch)"),
-            "kernel_ms": sec * 1e3, "algorithmic_bytes_per_launch": nbytes, "peak_note": pk_kind,
-            "read_only_gbs": read_gbs.value, "read_only_frac": gbs / read_gbs.value,
-            "mufu": {"ex2_per_s": exps / sec, "peak_ex2_per_s": ex2, "frac": exps / sec / ex2},
-            "note": ("achieved = the streaming formulation's algorithmic bytes (4 B of C per cell per "
-                     "half-step) / time: K3c reads each cost from HBM ONCE per solve (traffic) and "
-                     "is bound by the exps and cluster synchronisation, so frac may exceed what a "
-                     "streaming kernel could reach" if cluster else
-                     "one CTA per problem re-reads its 1 MiB cost from L2/HBM every half-step")}
+    if not cluster:  # K3p streams C from L2/HBM every half-step: the byte roof binds
+        return {"bound": "hbm", "achieved": gbs, "peak": float(pk["hbm_gbs"]), "unit": "GB/s",
+                "frac": gbs / float(pk["hbm_gbs"]), "traffic": traffic_for(wl.name),
+                "kernel": "otk_solve_dense_batched (K3p: one CTA per problem streaming C, one launch)",
+                "kernel_ms": sec * 1e3, "algorithmic_bytes_per_launch": nbytes, "peak_note": pk_kind,
+                "read_only_gbs": read_gbs.value, "read_only_frac": gbs / read_gbs.value,
+                "mufu": {"ex2_per_s": exps / sec, "peak_ex2_per_s": ex2, "frac": exps / sec / ex2}}
+    # K3c keeps each problem's cost resident in its cluster's shared memory and
+    # reads it from HBM ONCE per solve (traffic), so HBM is not its roof: the
+    # exps are (one MUFU ex2 per cell per half-step)
+    return {"bound": "mufu", "achieved": exps / sec / 1e9, "peak": ex2 / 1e9, "unit": "Gex2/s",
+            "frac": exps / sec / ex2, "traffic": traffic_for(wl.name),
+            "kernel": "otk_solve_dense_batched (K3c: cost resident in a cluster's shared memory, one launch)",
+            "kernel_ms": sec * 1e3, "exps_per_launch": exps,
+            "peak_note": "MUFU ex2 rate measured on this GPU (csrc/pipes.cu)",
+            "streaming_equivalent": {
+                "gbs": gbs, "hbm_peak_gbs": float(pk["hbm_gbs"]), "frac": gbs / float(pk["hbm_gbs"]),
+                "read_only_gbs": read_gbs.value,
+                "note": "what a kernel streaming 4 B of C per cell per half-step would have to move "
+                        "(2*iters + 1 half-steps per problem) / time -- above 1 because K3c does not "
+                        "stream C at all"}}
 
 
 # ------------------------------------------------------------------ our arm
