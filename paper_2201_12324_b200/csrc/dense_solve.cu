@@ -373,15 +373,43 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // shuffle merge in fixed order.  rows_pass picks RG per pass so that a CTA's
 // last, partial pass still keeps most threads busy.
 
+// 2^x for x <= 0 on the FMA pipe (two values per packed op): round-to-nearest
+// split x = n + f, |f| <= 1/2, degree-5 minimax polynomial for 2^f (relative
+// error 2.3e-7 in float32, the class of ex2.approx), 2^n added to the exponent
+// bits; x < -125 flushes to 0 like ex2.approx.ftz.  Relieves the MIO queue
+// that MUFU shares with the shared-memory loads (K3c's rows pass).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 p = make_float2(0.001327647129073739f, 0.001327647129073739f);
+  p = __ffma2_rn(p, f, make_float2(0.009675540961325169f, 0.009675540961325169f));
+  p = __ffma2_rn(p, f, make_float2(0.05550713092088699f, 0.05550713092088699f));
+  p = __ffma2_rn(p, f, make_float2(0.24022120237350464f, 0.24022120237350464f));
+  p = __ffma2_rn(p, f, make_float2(0.6931469440460205f, 0.6931469440460205f));
+  p = __ffma2_rn(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
+  const int nx = __float_as_int(t.x) - 0x4B400000, ny = __float_as_int(t.y) - 0x4B400000;
+  const float vx = __int_as_float(__float_as_int(p.x) + (nx << 23));
+  const float vy = __int_as_float(__float_as_int(p.y) + (ny << 23));
+  return make_float2(x.x < -125.f ? 0.f : vx, x.y < -125.f ? 0.f : vy);
+}
+
+#ifndef OTK_K3C_NPOLY
+#define OTK_K3C_NPOLY 0  // value pairs per 16 that take the FMA-pipe exp2 (A/B knob)
+#endif
+
 // sum_e 2^(u_e - ms) over 16 values in two chains (even / odd e), as packed
 // FADD2 pairs: bitwise the scalar (a0 += ..even.., a1 += ..odd..; a0 + a1)
+template <int NPOLY = 0>
 __device__ __forceinline__ float sum_ex2_16(const float (&u)[16], float ms) {
   float2 acc = make_float2(0.f, 0.f);
   const float2 nms = make_float2(-ms, -ms);
 #pragma unroll
   for (int e = 0; e < 16; e += 2) {
     const float2 t = __fadd2_rn(make_float2(u[e], u[e + 1]), nms);
-    acc = __fadd2_rn(acc, make_float2(ex2(t.x), ex2(t.y)));
+    if (e / 2 < NPOLY) acc = __fadd2_rn(acc, ex2_poly2(t));
+    else acc = __fadd2_rn(acc, make_float2(ex2(t.x), ex2(t.y)));
   }
   return acc.x + acc.y;
 }
@@ -444,7 +472,7 @@ __device__ void rows_local(const float *Cs, int rb, int re, int m, const float *
           st.m = cm;
         }
         const float ms = (st.m == -INFINITY) ? 0.f : st.m;
-        st.s += sum_ex2_16(u, ms);
+        st.s += sum_ex2_16<OTK_K3C_NPOLY>(u, ms);
       }
     }
 #pragma unroll
