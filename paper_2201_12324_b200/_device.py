@@ -71,3 +71,26 @@ def validate_potential(p, size, name):
     if np.isnan(p).any() or np.any(p == np.inf):
         raise ValueError(f"{name} contains NaN or +inf entries")
     return as_device_f32(p)
+
+
+class nvtx_range:
+    """NVTX range around host-driven device work (the C++ loops carry their own,
+    csrc/solve.cu); a no-op where NVTX is unavailable."""
+
+    def __init__(self, name: str):
+        self.name = name
+        self.on = False
+
+    def __enter__(self):
+        try:
+            import torch
+            torch.cuda.nvtx.range_push(self.name)
+            self.on = True
+        except Exception:  # noqa: BLE001 -- profiling aid only
+            pass
+        return self
+
+    def __exit__(self, *exc):
+        if self.on:
+            import torch
+            torch.cuda.nvtx.range_pop()

@@ -32,7 +32,7 @@ import threading
 import numpy as np
 
 from . import _native as N
-from ._device import as_device_f32, device, stream
+from ._device import as_device_f32, device, nvtx_range, stream
 from .errors import DivergedError
 from .geometry import EpsilonSchedule
 
@@ -434,18 +434,21 @@ def sharded_loop(engine, comm, sched: EpsilonSchedule, threshold: float, max_ite
         kap = float(np.float32(_LOG2E / e))
         kap_next = float(np.float32(_LOG2E / sched.at(t)))
         if not f_ready:
-            engine.rows(kap, e, kap, which, 2 * t)
+            with nvtx_range("otk sharded f half-step"):
+                engine.rows(kap, e, kap, which, 2 * t)
         f_ready = False
-        if p2p is not None:  # fused push (last kernel of the half-step) + combine
-            engine.cols_exchange(p2p, kap, e, kap_next, 2 * t + 1)
-        else:
-            lall = comm.all_gather_rows(engine.cols_partial(kap))
-            engine.cols_finalize(lall, e, kap_next, 2 * t + 1)
+        with nvtx_range("otk sharded g half-step + exchange"):
+            if p2p is not None:  # fused push (last kernel of the half-step) + combine
+                engine.cols_exchange(p2p, kap, e, kap_next, 2 * t + 1)
+            else:
+                lall = comm.all_gather_rows(engine.cols_partial(kap))
+                engine.cols_finalize(lall, e, kap_next, 2 * t + 1)
         if t % inner_iters == 0 or t == max_iters:
             measure = not (e > target)
-            if measure:
-                engine.rows(kap, e, kap, 1 - which, 2 * t + 2)
-            local = engine.check(which, measure, e)
+            with nvtx_range("otk sharded check"):
+                if measure:
+                    engine.rows(kap, e, kap, 1 - which, 2 * t + 2)
+                local = engine.check(which, measure, e)
             fb = engine.read_first_bad()
             # this rank's exchange status travels with its sums: a timed-out peer
             # wait makes EVERY rank raise at the same check (none is left waiting

@@ -30,7 +30,7 @@ from collections.abc import Sequence
 import numpy as np
 
 from . import _native as N
-from ._device import as_device_f32, device, is_torch, stream, to_output
+from ._device import as_device_f32, device, is_torch, nvtx_range, stream, to_output
 from .errors import DivergedError
 from .geometry import DenseGeometry, EpsilonSchedule, Geometry, PointCloudGeometry
 
@@ -596,13 +596,14 @@ def solve_sinkhorn_batched(x, y, eps, a=None, b=None, *, threshold: float = 1e-3
     CT = None if persistent else torch.empty((B, m, n), dtype=torch.float32, device=dev)
     N.check(N.lib().otk_dense_cost(N.ptr(xd), N.ptr(yd), B, n, m, d, 0, N.ptr(C), N.ptr(CT),
                                    stream()), "dense_cost")
-    if persistent:
-        outs = _dense_persistent(C, (a_d, b_d, la_d, lb_d), np.asarray(eps, dtype=float), threshold,
-                                 max_iters, inner_iters, g_init)
-    else:
-        scheds = [EpsilonSchedule(float(e)) for e in eps]
-        outs = _dense_loop(C, CT, (a_d, b_d, la_d, lb_d), scheds, threshold, max_iters,
-                           inner_iters, g_init=g_init)
+    with nvtx_range("otk batched solve"):
+        if persistent:
+            outs = _dense_persistent(C, (a_d, b_d, la_d, lb_d), np.asarray(eps, dtype=float), threshold,
+                                     max_iters, inner_iters, g_init)
+        else:
+            scheds = [EpsilonSchedule(float(e)) for e in eps]
+            outs = _dense_loop(C, CT, (a_d, b_d, la_d, lb_d), scheds, threshold, max_iters,
+                               inner_iters, g_init=g_init)
     if not return_cost:
         return outs
     costs = _dense_costs(C, outs, aw, bw)
