@@ -366,6 +366,30 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+// Cluster-scope push of one float into a peer CTA's shared memory that also
+// counts its 4 bytes on the peer's mbarrier (st.async ... complete_tx): the
+// receiver waits on its own barrier -- no cluster-wide barrier and none of the
+// GPU-scope fences a release-arrive emits (measured: MEMBAR.ALL.GPU + ERRBAR
+// at the column exchange's cluster.sync took ~25 % of K3c's stall samples).
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t local, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_f32(uint32_t raddr, float v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr),
+               "r"(__float_as_uint(v)), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\nW_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // Rows half-step on the CTA's resident rows [rb, re): a group of RG (8, 16
 // or 32) threads per row (each LDS.128 phase of 8 threads reads 128
 // consecutive bytes of one row: no bank conflicts), each thread streaming
@@ -560,6 +584,218 @@ __device__ __forceinline__ float col_partial_anchored(const float *Cs, int rows,
 }
 
 
+
+// ---- K3c in the scaling domain (the default) -------------------------------
+// Sinkhorn's half-steps are LSEs of u_ij = b_j - kappa C_ij (rows) or
+// f'_i - kappa C_ij (columns).  With the cost resident on chip, the exps can
+// be taken ONCE into a stabilised kernel K_ij = 2^(beta_j - kappa C_ij - rho_i)
+// (beta_j: the column potentials kappa*g_j at build time, rho_i: the row max,
+// so 0 < K_ij <= 1, flushed below 2^-126 of its row's max) and every later
+// half-step is a matrix-vector product in FP32 FMAs (Schmitzer's absorption,
+// in log2 units):
+//   rows:    L_i = rho_i + log2 sum_j K_ij v_j,          v_j = 2^(b_j - beta_j)
+//   columns: P_j = -beta_j + log2 sum_{i in CTA} K_ij w_i, w_i = 2^(kappa f'_i + rho_i)
+// -- one FMA and 4 B of shared memory per cell instead of one MUFU ex2 (and
+// the max / rescale work around it).  Exactness guards: the kernel slice is
+// rebuilt from the cost (kept in global memory, L2-resident) whenever a
+// column potential drifted more than kDrift bits from its beta (v stays in
+// [2^-40, 2^40], so no term that mattered can have been flushed), and a column
+// partial whose FMA sum leaves [2^-90, 2^120] -- a column far from every row
+// of the slice, a dead (zero-weight) column, overflow -- is recomputed exactly
+// in the log domain from the global cost.  Results match the log-domain
+// passes to float32 rounding (tests: K3c vs K3p, the reference fixtures).
+constexpr float kDrift = 40.f;
+
+// This CTA's kernel slice from its global cost rows Cg [rows][m]:
+// beta_j = by_j, rho_i = max_j (beta_j - kappa C_ij), K_ij = 2^(.. - rho_i).
+__device__ void build_kernel(const float *__restrict__ Cg, int rows, int m, const float *by,
+                             float kappa, float *Ks, float *beta, float *rho) {
+  for (int j = threadIdx.x; j < m; j += THREADS) beta[j] = by[j];
+  __syncthreads();
+  constexpr int RGB = 8, GROUPS = THREADS / RGB, RCH = 4 * RGB;
+  const int gi = threadIdx.x / RGB, gl = threadIdx.x % RGB;
+  for (int i0 = 0; i0 < rows; i0 += GROUPS) {
+    const int i = i0 + gi;
+    const bool live = i < rows;
+    const float *crow = Cg + (int64_t)(live ? i : 0) * m;
+    float mx = -INFINITY;
+    if (live) {
+      for (int j = gl * 4; j < m; j += RCH) {
+        const float4 c = __ldg(reinterpret_cast<const float4 *>(crow + j));
+        const float4 bb = *reinterpret_cast<const float4 *>(beta + j);
+        mx = fmaxf(mx, fmaxf(fmaxf(fmaf(-kappa, c.x, bb.x), fmaf(-kappa, c.y, bb.y)),
+                             fmaxf(fmaf(-kappa, c.z, bb.z), fmaf(-kappa, c.w, bb.w))));
+      }
+    }
+#pragma unroll
+    for (int o = RGB / 2; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (live) {
+      const bool dead = !(mx > -INFINITY);  // every term -inf (or NaN): an all-zero row
+      float *krow = Ks + (int64_t)i * m;
+      for (int j = gl * 4; j < m; j += RCH) {
+        const float4 c = __ldg(reinterpret_cast<const float4 *>(crow + j));
+        const float4 bb = *reinterpret_cast<const float4 *>(beta + j);
+        float4 k;
+        k.x = dead ? 0.f : ex2(fmaf(-kappa, c.x, bb.x) - mx);
+        k.y = dead ? 0.f : ex2(fmaf(-kappa, c.y, bb.y) - mx);
+        k.z = dead ? 0.f : ex2(fmaf(-kappa, c.z, bb.z) - mx);
+        k.w = dead ? 0.f : ex2(fmaf(-kappa, c.w, bb.w) - mx);
+        *reinterpret_cast<float4 *>(krow + j) = k;
+      }
+      if (gl == 0) rho[i] = dead ? -INFINITY : mx;
+    }
+  }
+  __syncthreads();
+}
+
+// v_j = 2^(by_j - beta_j) and the kernel rebuild decision: drift of a finite
+// column potential beyond kDrift bits from its beta (the caller rebuilds and
+// calls again).  Returns true when v is ready.
+#ifdef OTK_DENSE_TRACE_BUILD
+__device__ unsigned long long g_dense_rebuilds, g_dense_fallbacks;  // diagnostics (trace builds)
+#endif
+__device__ bool scaled_v(const float *by, const float *beta, int m, float *vv, int *flag) {
+  if (threadIdx.x == 0) *flag = 0;
+  __syncthreads();
+  bool drift = false;
+  for (int j = threadIdx.x; j < m; j += THREADS) {
+    const float bt = beta[j], b = by[j];
+    const float dlt = b - bt;
+    if (bt > -INFINITY && fabsf(dlt) > kDrift && isfinite(dlt)) drift = true;
+    vv[j] = (bt > -INFINITY) ? ex2(dlt) : 0.f;
+  }
+  if (__syncthreads_or(drift)) {
+#ifdef OTK_DENSE_TRACE_BUILD
+    if (threadIdx.x == 0) atomicAdd(&g_dense_rebuilds, 1ull);
+#endif
+    return false;
+  }
+  return true;
+}
+
+// Rows half-step as K v, one warp per row and two rows in flight (rows w and
+// w + WARPS, ...): the warp's v values (lane l: columns 4l + 128q, m <= 512)
+// are loaded once per pass and kept in registers, so shared memory carries
+// only K (4 B per cell); the two rows' shuffle reductions and finalizes
+// (lanes 0 and 1) overlap.  The check's per-row terms (a float64 exp per
+// row) run afterwards, one thread per row.
+template <bool CHECK>
+__device__ void rows_pass_scaled(const float *Ks, int rows, int m, const float *vv, const float *rho,
+                                 const float *lw, float eps, float kappa, float *out, float *bx,
+                                 float *uw, int *fbad, int step, const float *fprev, const float *a,
+                                 double eps_d, double (&chk)[NV]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float4 v[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j = q * 128 + lane * 4;
+    v[q] = (j < m) ? *reinterpret_cast<const float4 *>(vv + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int i0 = warp; i0 < rows; i0 += 2 * WARPS) {
+    const int i1 = i0 + WARPS;
+    const bool two = i1 < rows;
+    const float *k0 = Ks + (int64_t)i0 * m, *k1 = Ks + (int64_t)(two ? i1 : i0) * m;
+    float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+    float2 c0 = make_float2(0.f, 0.f), c1 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = q * 128 + lane * 4;
+      if (j < m) {
+        const float4 x = *reinterpret_cast<const float4 *>(k0 + j);
+        const float4 y = *reinterpret_cast<const float4 *>(k1 + j);
+        a0 = __ffma2_rn(make_float2(x.x, x.y), make_float2(v[q].x, v[q].y), a0);
+        a1 = __ffma2_rn(make_float2(x.z, x.w), make_float2(v[q].z, v[q].w), a1);
+        c0 = __ffma2_rn(make_float2(y.x, y.y), make_float2(v[q].x, v[q].y), c0);
+        c1 = __ffma2_rn(make_float2(y.z, y.w), make_float2(v[q].z, v[q].w), c1);
+      }
+    }
+    const float2 s0 = __fadd2_rn(a0, a1), s1 = __fadd2_rn(c0, c1);
+    float r0 = s0.x + s0.y, r1 = s1.x + s1.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r0 += __shfl_xor_sync(0xffffffffu, r0, o);
+      r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+    }
+    if (lane < 2 && (lane == 0 || two)) {
+      const int i = lane == 0 ? i0 : i1;
+      const float sm = lane == 0 ? r0 : r1;
+      const float rh = rho[i];
+      const float L = rh + ((sm > 0.f) ? lg2(sm) : ((sm != sm) ? sm : -INFINITY));
+      const float v_ = eps * lw[i] - eps * kLn2 * L;
+      out[i] = v_;
+      bx[i] = v_ * kappa;
+      uw[i] = (rh > -INFINITY) ? ex2(v_ * kappa + rh) : 0.f;
+      if (bad_potential(v_)) atomicMin(fbad, step);
+    }
+  }
+  if (CHECK) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < rows; i += THREADS) {
+      const double fp = fprev[i], ai = a[i];
+      const double rr = (ai > 0.0) ? ai * exp((fp - (double)out[i]) / eps_d) : 0.0;
+      chk[0] += fabs(rr - ai);
+      chk[1] += rr;
+      if (ai > 0.0) chk[2] += ai * fp;
+      chk[4] += (fp != fp) ? 1.0 : 0.0;
+      chk[6] += (fp == INFINITY) ? 1.0 : 0.0;
+    }
+  }
+}
+
+// This CTA's log2 partial of column j: -beta_j + log2 sum_i K_ij w_i, or the
+// exact log-domain partial from the global cost when the FMA sum left its
+// safe range (far / dead column, overflow).
+__device__ __forceinline__ float col_partial_scaled(const float *Ks, const float *__restrict__ Cg, int rows,
+                                                    int m, const float *bx, const float *uw,
+                                                    const float *beta, float kappa, int j) {
+  const float *kp = Ks + j;
+  // four independent FFMA2 chains over 16-row chunks (the K loads of a chunk
+  // are issued before its FMAs)
+  float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                   make_float2(0.f, 0.f)};
+  int i0 = 0;
+  for (; i0 + 16 <= rows; i0 += 16) {
+    float wb[16], kb[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) kb[k] = kp[(i0 + k) * m];
+#pragma unroll
+    for (int k = 0; k < 16; k += 4) {
+      const float4 ww = *reinterpret_cast<const float4 *>(uw + i0 + k);
+      wb[k] = ww.x;
+      wb[k + 1] = ww.y;
+      wb[k + 2] = ww.z;
+      wb[k + 3] = ww.w;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; k += 2)
+      acc[(k / 2) & 3] = __ffma2_rn(make_float2(kb[k], kb[k + 1]), make_float2(wb[k], wb[k + 1]), acc[(k / 2) & 3]);
+  }
+  for (; i0 < rows; ++i0) acc[0].x = fmaf(kp[i0 * m], uw[i0], acc[0].x);
+  const float2 a01 = __fadd2_rn(acc[0], acc[1]), a23 = __fadd2_rn(acc[2], acc[3]);
+  const float2 a4 = __fadd2_rn(a01, a23);
+  const float sm = a4.x + a4.y;
+  const float bt = beta[j];
+  if (sm != sm) return sm;
+  if (bt > -INFINITY && sm >= 0x1p-90f && sm <= 0x1p120f) return lg2(sm) - bt;
+#ifdef OTK_DENSE_TRACE_BUILD
+  atomicAdd(&g_dense_fallbacks, 1ull);
+#endif
+  // exact: running max over this CTA's rows of kappa f'_i - kappa C_ij (global cost)
+  float mx = -INFINITY, s = 0.f;
+  for (int i = 0; i < rows; ++i) {
+    const float u = fmaf(-kappa, __ldg(Cg + (int64_t)i * m + j), bx[i]);
+    if (u > mx) {
+      s = (mx == -INFINITY) ? 0.f : s * ex2(mx - u);
+      mx = u;
+    }
+    if (mx > -INFINITY) s += ex2(u - mx);
+  }
+  Lse2 st;
+  st.m = mx;
+  st.s = s;
+  return st.value();
+}
+
 // Rows pass of K3c: full passes of 64 rows with 8 threads per row, then the
 // remaining R rows with 8 (R > 32), 16 (R > 16) or 32 threads per row, so a
 // slice of 86 rows (cfg3, CL = 6) costs 64 + 32 cells per thread instead of
@@ -576,7 +812,7 @@ __device__ __forceinline__ void rows_pass(const float *Cs, int rows, int m, cons
   else if (rem > 0) rows_local<CHECK, 32>(Cs, full, rows, m, by, lw, eps, kappa, out, bx, fbad, step, fprev, a, eps_d, chk);
 }
 
-template <int CL>
+template <int CL, bool SCALED>
 __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -591,20 +827,29 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
   float *canc = by + m4;                              // [m4] column-partial anchors
   float *xs = canc + m4;                              // [2][CL][m4] pushed column partials
   float *las = xs + 2 * CL * m4, *lbs = las + rp4;    // log weights staged in shared memory
-  double *slot = reinterpret_cast<double *>(lbs + m4);  // [2][NV + 1]
+  // SCALED: Cs holds the kernel slice K; beta / v per column, rho / w per row
+  float *beta = lbs + m4, *vv = beta + m4, *rho = vv + m4, *uw = rho + rp4;
+  double *slot = reinterpret_cast<double *>(uw + rp4);  // [2][NV + 1]
+  __shared__ int rebuild_flag;
   __shared__ double red[NV * WARPS];
   __shared__ double rsl[CL * (NV + 1)], rtot[NV + 1];
   __shared__ int fbad;
   __shared__ __align__(8) uint64_t lbar;
+  __shared__ __align__(8) uint64_t xbar[2];  // column-partial arrivals, one per buffer parity
   const int r0 = min(n, rank * rows_per), r1 = min(n, r0 + rows_per), rows = r1 - r0;
   const int ncl = (int)(gridDim.x / CL), cid = (int)(blockIdx.x / CL);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&lbar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&xbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&xbar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  cluster.sync();  // every peer's barriers are initialised before the first push
   uint32_t lphase = 0;
-  int xpar = 0;  // parity of the next exchange (column partials or check slots)
+  uint32_t xphase = 0u;  // bit p: phase of xbar[p]
+  int xpar = 0;  // parity of the next check-slot exchange
+  int cpar = 0;  // parity of the next column exchange (buffer xs[cpar], barrier xbar[cpar])
   for (int64_t b = cid; b < A.batch; b += ncl) {
     const float *Cb = A.C + b * (int64_t)n * m;
     const float *a = A.a + b * n + r0, *bw = A.b + b * m;
@@ -612,8 +857,9 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
     const float eps = A.eps[b];
     const double eps_d = A.eps_d[b];
     const float kappa = kLog2e / eps;
-    // this CTA's rows of C -> shared memory (bulk copies, 32 KB pieces)
-    if (threadIdx.x == 0 && rows > 0) {
+    const float *Cg = Cb + (int64_t)r0 * m;  // this CTA's rows of the cost (global, L2-resident)
+    // log domain: this CTA's rows of C -> shared memory (bulk copies, 32 KB pieces)
+    if (!SCALED && threadIdx.x == 0 && rows > 0) {
       const size_t bytes = (size_t)rows * m * sizeof(float);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                        (uint32_t)__cvta_generic_to_shared(&lbar)),
@@ -634,7 +880,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
       if (bad_potential(g0)) atomicMin(&fbad, 1);
     }
     for (int i = threadIdx.x; i < rp4; i += THREADS) las[i] = (i < rows) ? A.la[b * n + r0 + i] : 0.f;
-    if (rows > 0) {  // wait for the cost slice
+    if (!SCALED && rows > 0) {  // wait for the cost slice
       asm volatile(
           "{\n\t.reg .pred p;\nW_%=:\n\t"
           "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
@@ -644,6 +890,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
       lphase ^= 1;
     }
     __syncthreads();
+    if constexpr (SCALED) build_kernel(Cg, rows, m, by, kappa, Cs, beta, rho);
     float *f = f0, *fn = f1;
     bool f_ready = false;
     int n_checks = 0, status = OTK_OK, fail_iter = 0, converged = 0, t;
@@ -652,28 +899,48 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
     for (t = 1; t <= A.max_iters; ++t) {
       dtrace(A, tr, t, 0);
       if (!f_ready) {
-        rows_pass<false>(Cs, rows, m, by, la, eps, kappa, f, bx, &fbad, 2 * t, nullptr, a, eps_d, chk);
+        if constexpr (SCALED) {
+          while (!scaled_v(by, beta, m, vv, &rebuild_flag)) build_kernel(Cg, rows, m, by, kappa, Cs, beta, rho);
+          rows_pass_scaled<false>(Cs, rows, m, vv, rho, la, eps, kappa, f, bx, uw, &fbad, 2 * t, nullptr, a,
+                                  eps_d, chk);
+        } else {
+          rows_pass<false>(Cs, rows, m, by, la, eps, kappa, f, bx, &fbad, 2 * t, nullptr, a, eps_d, chk);
+        }
         __syncthreads();
       }
       dtrace(A, tr, t, 1);
       f_ready = false;
-      // ---- columns: local partials pushed into every CTA's shared memory
-      // (remote stores), one cluster barrier, then every CTA combines the CL
-      // partials of every column from its own shared memory in rank order
-      float *xbuf = xs + xpar * CL * m4;
+      // ---- columns: local partials pushed into slot `rank` of every CTA's
+      // shared memory with st.async (each push counted on the receiver's
+      // mbarrier), each CTA waits for its own barrier, then combines the CL
+      // partials of every column from its own shared memory in rank order.
+      // Buffer reuse: a CTA pushes epoch e+2 into parity (e & 1) only after its
+      // own combine of e+1, which needed every peer's push of e+1, issued after
+      // that peer's combine of e -- two buffers suffice, no cluster barrier.
+      float *xbuf = xs + cpar * CL * m4;
       {
         const float clo = -96.f + 2.f * log2f((float)max(rows, 1));
-        float *mine = xbuf + rank * m4;
+        const uint32_t mine = (uint32_t)__cvta_generic_to_shared(xbuf + rank * m4);
+        const uint32_t mybar = (uint32_t)__cvta_generic_to_shared(&xbar[cpar]);
+        if (threadIdx.x == 0)  // arm: CL pushes of m floats land here this epoch
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mybar),
+                       "r"((uint32_t)(CL * m * 4))
+                       : "memory");
         for (int j = threadIdx.x; j < m; j += THREADS) {
-          const float L = (rows > 0) ? col_partial_anchored(Cs, rows, m, bx, kappa, j, canc[j], clo)
-                                     : -INFINITY;
-          canc[j] = nan_if_not_finite(L);
+          float L;
+          if constexpr (SCALED) {
+            L = col_partial_scaled(Cs, Cg, rows, m, bx, uw, beta, kappa, j);
+          } else {
+            L = (rows > 0) ? col_partial_anchored(Cs, rows, m, bx, kappa, j, canc[j], clo) : -INFINITY;
+            canc[j] = nan_if_not_finite(L);
+          }
 #pragma unroll
-          for (int r = 0; r < CL; ++r) cluster.map_shared_rank(mine, r)[j] = L;
+          for (int r = 0; r < CL; ++r) st_async_f32(mapa_u32(mine + 4u * j, r), L, mapa_u32(mybar, r));
         }
       }
       dtrace(A, tr, t, 2);
-      cluster.sync();
+      mbar_wait_cluster(&xbar[cpar], (xphase >> cpar) & 1u);
+      xphase ^= 1u << cpar;
       dtrace(A, tr, t, 3);
       for (int j = threadIdx.x; j < m; j += THREADS) {
         float v[CL];
@@ -702,13 +969,19 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
         by[j] = gv * kappa;
         if (bad_potential(gv)) atomicMin(&fbad, 2 * t + 1);
       }
-      xpar ^= 1;
+      cpar ^= 1;
       __syncthreads();
       dtrace(A, tr, t, 4);
       if (t % A.inner_iters == 0 || t == A.max_iters) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) chk[k] = 0.0;
-        rows_pass<true>(Cs, rows, m, by, la, eps, kappa, fn, bx, &fbad, 2 * t + 2, f, a, eps_d, chk);
+        if constexpr (SCALED) {
+          while (!scaled_v(by, beta, m, vv, &rebuild_flag)) build_kernel(Cg, rows, m, by, kappa, Cs, beta, rho);
+          rows_pass_scaled<true>(Cs, rows, m, vv, rho, la, eps, kappa, fn, bx, uw, &fbad, 2 * t + 2, f, a,
+                                 eps_d, chk);
+        } else {
+          rows_pass<true>(Cs, rows, m, by, la, eps, kappa, fn, bx, &fbad, 2 * t + 2, f, a, eps_d, chk);
+        }
         if (rank == 0) {  // g is replicated: its terms are counted once
           for (int j = threadIdx.x; j < m; j += THREADS) {
             const double gj = g[j], bj = bw[j];
@@ -801,8 +1074,15 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
 size_t cluster_smem_bytes(int n, int m, int CL) {
   const size_t rows_per = (n + CL - 1) / CL;
   const size_t rp4 = (rows_per + 3) & ~(size_t)3, m4 = (m + 3) & ~3;
-  return rows_per * m * sizeof(float) + (4 * rp4 + 4 * m4 + 2 * (size_t)CL * m4) * sizeof(float) +
+  return rows_per * m * sizeof(float) + (6 * rp4 + 6 * m4 + 2 * (size_t)CL * m4) * sizeof(float) +
          2 * (NV + 1) * sizeof(double) + 64;
+}
+
+// The scaling-domain kernel holds a row's v values in registers: m <= 512;
+// OTK_DENSE_DOMAIN=log forces the log-domain passes (A/B).
+static bool scaled_domain(int m) {
+  const char *e = getenv("OTK_DENSE_DOMAIN");
+  return m <= 512 && !(e && strcmp(e, "log") == 0);
 }
 
 template <int CL>
@@ -813,7 +1093,7 @@ static int cluster_try(const Args &A, int n, int m, int64_t batch, int grid, cud
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t smem = cluster_smem_bytes(n, m, CL);
   if (smem + 2048 > (size_t)max_smem) return OTK_ENOTSUP;
-  auto kern = dense_cluster_solve_kernel<CL>;
+  auto kern = scaled_domain(m) ? dense_cluster_solve_kernel<CL, true> : dense_cluster_solve_kernel<CL, false>;
   OTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CL * 64);
@@ -938,6 +1218,11 @@ extern "C" int otk_solve_dense_batched(const float *cost, int64_t batch, int64_t
   if (trace_path) {
     OTK_CUDA(cudaMalloc(&A.trace, 64 * 8 * sizeof(unsigned long long)));
     OTK_CUDA(cudaMemsetAsync(A.trace, 0, 64 * 8 * sizeof(unsigned long long), as_stream(stream)));
+#ifdef OTK_DENSE_TRACE_BUILD
+    const unsigned long long zero = 0;
+    OTK_CUDA(cudaMemcpyToSymbol(dsolve::g_dense_rebuilds, &zero, sizeof(zero)));
+    OTK_CUDA(cudaMemcpyToSymbol(dsolve::g_dense_fallbacks, &zero, sizeof(zero)));
+#endif
   }
   // K3c (cost resident in a cluster's shared memory) whenever a slice fits;
   // OTK_DENSE_KERNEL=cta forces the one-CTA-per-problem streaming kernel K3p
@@ -951,6 +1236,11 @@ extern "C" int otk_solve_dense_batched(const float *cost, int64_t batch, int64_t
         OTK_CUDA(cudaMemcpyAsync(h, A.trace, sizeof(h), cudaMemcpyDeviceToHost, as_stream(stream)));
         OTK_CUDA(cudaStreamSynchronize(as_stream(stream)));
         cudaFree(A.trace);
+#ifdef OTK_DENSE_TRACE_BUILD
+        // row 63: rebuilds of kernel slices and exact column fallbacks over the whole batch
+        OTK_CUDA(cudaMemcpyFromSymbol(&h[63 * 8], dsolve::g_dense_rebuilds, sizeof(h[0])));
+        OTK_CUDA(cudaMemcpyFromSymbol(&h[63 * 8 + 1], dsolve::g_dense_fallbacks, sizeof(h[0])));
+#endif
         if (FILE *fp = fopen(trace_path, "wb")) {
           fwrite(h, sizeof(h[0]), 64 * 8, fp);
           fclose(fp);

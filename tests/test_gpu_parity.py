@@ -497,7 +497,10 @@ def test_apply_kernel_matches_dense_gibbs_product(otk, cost_fn):
 def test_batched_cluster_solver_matches_streaming_solver(otk, monkeypatch, n, m, cl):
     """K3c vs K3p on ragged shapes (rows not a multiple of the cluster, CTAs with no
     rows, several column chunks), warm start, fixed iterations and tolerance runs:
-    same iteration counts and convergence, potentials within fp32 rounding."""
+    same iteration counts and convergence, potentials within float32 rounding.
+    K3c runs in the scaling domain (a stored stabilised kernel, FMA half-steps)
+    and K3p in the log domain: each lands within ~3.5e-6 of the float64 oracle
+    on these shapes (tools/k3_accuracy.py), so they agree to 5e-6."""
     rng = np.random.default_rng(n + m)
     B, d = 20, 5
     x = rng.standard_normal((B, n, d)).astype(np.float32)
@@ -515,8 +518,8 @@ def test_batched_cluster_solver_matches_streaming_solver(otk, monkeypatch, n, m,
         assert np.array_equal(a.iterations, b.iterations)
         assert np.array_equal(a.converged, b.converged)
         for k in range(B):
-            assert rel_inf(a.f[k], b.f[k]) <= 2e-6
-            assert rel_inf(a.g[k], b.g[k]) <= 2e-6
+            assert rel_inf(a.f[k], b.f[k]) <= 5e-6
+            assert rel_inf(a.g[k], b.g[k]) <= 5e-6
 
 
 def _small_vs_general(otk, x, y, a, b, eps, **kw):
@@ -587,3 +590,36 @@ def test_persistent_small_solve_shapes_and_zero_weights(otk, n, m):
         assert out.iterations == ref["iterations"] and out.converged == ref["converged"]
         assert rel_inf(out.f, ref["f"]) <= POT_TOL
         assert rel_inf(out.g, ref["g"]) <= POT_TOL
+
+
+@pytest.mark.parametrize("domain", ["scaled", "log"])
+def test_batched_cluster_solver_edge_cases_match_oracle(otk, monkeypatch, domain):
+    """K3c in both domains on the cases the scaling domain must fall back on:
+    zero weights (dead columns and rows, -inf potentials), a far outlier
+    column (its FMA partial underflows -> exact log-domain partial), a far-off
+    warm start (kernel rebuilds) and a tight eps -- against the float64 oracle."""
+    if domain == "log":
+        monkeypatch.setenv("OTK_DENSE_DOMAIN", "log")
+    rng = np.random.default_rng(77)
+    B, n, m, d = 4, 300, 260, 4
+    x = rng.standard_normal((B, n, d)).astype(np.float32)
+    y = (rng.standard_normal((B, m, d)) + 0.3).astype(np.float32)
+    y[1, 5] = 25.0  # far from every x: an underflowing column
+    a = rng.uniform(0.5, 1.5, (B, n))
+    b = rng.uniform(0.5, 1.5, (B, m))
+    a[2, ::11] = 0.0
+    b[2, ::7] = 0.0
+    a /= a.sum(axis=1, keepdims=True)
+    b /= b.sum(axis=1, keepdims=True)
+    Cs = [((x[k].astype(np.float64)[:, None] - y[k].astype(np.float64)[None]) ** 2).sum(-1) for k in range(B)]
+    eps = np.array([0.05 * C.mean() for C in Cs])
+    eps[3] *= 0.2
+    g0 = np.zeros((B, m), np.float32)
+    g0[0] = (rng.standard_normal(m) * 60 * eps[0]).astype(np.float32)  # drifts far: rebuilds
+    outs = otk.solve_sinkhorn_batched(x, y, eps, a, b, threshold=1e-300, max_iters=40, g_init=g0)
+    for k in range(B):
+        ref = oracle.sinkhorn(oracle.DenseOracle(Cs[k].astype(np.float32).astype(np.float64)), a[k], b[k],
+                              float(eps[k]), threshold=1e-300, max_iters=40, g_init=g0[k].astype(np.float64))
+        assert outs.iterations[k] == ref["iterations"]
+        assert rel_inf(outs.f[k], ref["f"]) <= POT_TOL, (k, rel_inf(outs.f[k], ref["f"]))
+        assert rel_inf(outs.g[k], ref["g"]) <= POT_TOL, (k, rel_inf(outs.g[k], ref["g"]))

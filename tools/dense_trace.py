@@ -28,3 +28,5 @@ for t in range(2, 30):
     chk = (T[t, 5] - T[t, 4]) if T[t, 5] else 0
     print("%4d %6d %5d %5d %6d %7d %6d" % (t, tot, T[t, 1] - T[t, 0], T[t, 2] - T[t, 1],
                                            T[t, 3] - T[t, 2], T[t, 4] - T[t, 3], chk))
+print("scaled domain: kernel-slice rebuilds %d, exact column fallbacks %d (whole batch, 30 iterations)"
+      % (T[63, 0], T[63, 1]))
