@@ -673,12 +673,14 @@ __device__ bool scaled_v(const float *by, const float *beta, int m, float *vv, i
   return true;
 }
 
-// Rows half-step as K v, one warp per row and two rows in flight (rows w and
-// w + WARPS, ...): the warp's v values (lane l: columns 4l + 128q, m <= 512)
-// are loaded once per pass and kept in registers, so shared memory carries
-// only K (4 B per cell); the two rows' shuffle reductions and finalizes
-// (lanes 0 and 1) overlap.  The check's per-row terms (a float64 exp per
-// row) run afterwards, one thread per row.
+// Rows half-step as K v: one warp per row, FOUR rows in flight (rows w,
+// w + WARPS, w + 2 WARPS, w + 3 WARPS, then the next four): the warp's v values
+// (lane l: columns 4l + 128q, m <= 512) are loaded once per pass and kept in
+// registers, so shared memory carries only K (4 B per cell); the four rows'
+// partial sums leave the warp through a reduce-scatter (6 shuffles for the
+// four rows instead of 20: xor 16 and xor 8 halve the rows per lane, then a
+// 3-level sum) and lanes 0, 8, 16, 24 finalize one row each.  The check's
+// per-row terms (a float64 exp per row) run afterwards, one thread per row.
 template <bool CHECK>
 __device__ void rows_pass_scaled(const float *Ks, int rows, int m, const float *vv, const float *rho,
                                  const float *lw, float eps, float kappa, float *out, float *bx,
@@ -691,36 +693,41 @@ __device__ void rows_pass_scaled(const float *Ks, int rows, int m, const float *
     const int j = q * 128 + lane * 4;
     v[q] = (j < m) ? *reinterpret_cast<const float4 *>(vv + j) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  for (int i0 = warp; i0 < rows; i0 += 2 * WARPS) {
-    const int i1 = i0 + WARPS;
-    const bool two = i1 < rows;
-    const float *k0 = Ks + (int64_t)i0 * m, *k1 = Ks + (int64_t)(two ? i1 : i0) * m;
-    float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
-    float2 c0 = make_float2(0.f, 0.f), c1 = make_float2(0.f, 0.f);
+  for (int i0 = warp; i0 < rows; i0 += 4 * WARPS) {
+    float r[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = q * 128 + lane * 4;
-      if (j < m) {
-        const float4 x = *reinterpret_cast<const float4 *>(k0 + j);
-        const float4 y = *reinterpret_cast<const float4 *>(k1 + j);
-        a0 = __ffma2_rn(make_float2(x.x, x.y), make_float2(v[q].x, v[q].y), a0);
-        a1 = __ffma2_rn(make_float2(x.z, x.w), make_float2(v[q].z, v[q].w), a1);
-        c0 = __ffma2_rn(make_float2(y.x, y.y), make_float2(v[q].x, v[q].y), c0);
-        c1 = __ffma2_rn(make_float2(y.z, y.w), make_float2(v[q].z, v[q].w), c1);
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + k * WARPS;
+      const float *kr = Ks + (int64_t)(i < rows ? i : i0) * m;
+      float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = q * 128 + lane * 4;
+        if (j < m) {
+          const float4 x = *reinterpret_cast<const float4 *>(kr + j);
+          a0 = __ffma2_rn(make_float2(x.x, x.y), make_float2(v[q].x, v[q].y), a0);
+          a1 = __ffma2_rn(make_float2(x.z, x.w), make_float2(v[q].z, v[q].w), a1);
+        }
       }
+      const float2 s2 = __fadd2_rn(a0, a1);
+      r[k] = s2.x + s2.y;
     }
-    const float2 s0 = __fadd2_rn(a0, a1), s1 = __fadd2_rn(c0, c1);
-    float r0 = s0.x + s0.y, r1 = s1.x + s1.y;
+    // reduce-scatter: after xor 16 lane bit 4 selects rows {0,1} / {2,3}, after
+    // xor 8 lane bit 3 selects the row within the pair (fixed tree, deterministic)
+    const bool hi16 = lane & 16, hi8 = lane & 8;
+    float p0 = hi16 ? r[2] : r[0], p1 = hi16 ? r[3] : r[1];
+    const float q0 = hi16 ? r[0] : r[2], q1 = hi16 ? r[1] : r[3];
+    p0 += __shfl_xor_sync(0xffffffffu, q0, 16);
+    p1 += __shfl_xor_sync(0xffffffffu, q1, 16);
+    float t = hi8 ? p1 : p0;
+    t += __shfl_xor_sync(0xffffffffu, hi8 ? p0 : p1, 8);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      r0 += __shfl_xor_sync(0xffffffffu, r0, o);
-      r1 += __shfl_xor_sync(0xffffffffu, r1, o);
-    }
-    if (lane < 2 && (lane == 0 || two)) {
-      const int i = lane == 0 ? i0 : i1;
-      const float sm = lane == 0 ? r0 : r1;
+    for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    const int k = (hi16 ? 2 : 0) + (hi8 ? 1 : 0);
+    const int i = i0 + k * WARPS;
+    if ((lane & 7) == 0 && i < rows) {
       const float rh = rho[i];
-      const float L = rh + ((sm > 0.f) ? lg2(sm) : ((sm != sm) ? sm : -INFINITY));
+      const float L = rh + ((t > 0.f) ? lg2(t) : ((t != t) ? t : -INFINITY));
       const float v_ = eps * lw[i] - eps * kLn2 * L;
       out[i] = v_;
       bx[i] = v_ * kappa;
@@ -901,6 +908,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
       if (!f_ready) {
         if constexpr (SCALED) {
           while (!scaled_v(by, beta, m, vv, &rebuild_flag)) build_kernel(Cg, rows, m, by, kappa, Cs, beta, rho);
+          dtrace(A, tr, t, 6);
           rows_pass_scaled<false>(Cs, rows, m, vv, rho, la, eps, kappa, f, bx, uw, &fbad, 2 * t, nullptr, a,
                                   eps_d, chk);
         } else {

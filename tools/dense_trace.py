@@ -20,13 +20,14 @@ path = os.path.join(tempfile.mkdtemp(), "trace.bin")
 os.environ["OTK_DENSE_TRACE"] = path
 otk.solve_sinkhorn_batched(wl.x, wl.y, wl.eps, threshold=1e-300, max_iters=30)
 T = np.fromfile(path, dtype=np.uint64).reshape(64, 8).astype(np.int64)
-print("iter  total  rows  cols  csync  combine  check")
+print("iter  total  rows  cols  csync  combine  check  (rows: v/drift part)")
 for t in range(2, 30):
     if T[t + 1, 0] == 0:
         break
     tot = T[t + 1, 0] - T[t, 0]
     chk = (T[t, 5] - T[t, 4]) if T[t, 5] else 0
-    print("%4d %6d %5d %5d %6d %7d %6d" % (t, tot, T[t, 1] - T[t, 0], T[t, 2] - T[t, 1],
-                                           T[t, 3] - T[t, 2], T[t, 4] - T[t, 3], chk))
+    vpart = (T[t, 6] - T[t, 0]) if T[t, 6] else 0
+    print("%4d %6d %5d %5d %6d %7d %6d %6d" % (t, tot, T[t, 1] - T[t, 0], T[t, 2] - T[t, 1],
+                                               T[t, 3] - T[t, 2], T[t, 4] - T[t, 3], chk, vpart))
 print("scaled domain: kernel-slice rebuilds %d, exact column fallbacks %d (whole batch, 30 iterations)"
       % (T[63, 0], T[63, 1]))
