@@ -391,10 +391,10 @@ def small_roofline(value, step_s, wl):
 def dense_roofline(C, wl, reps=3):
     """Dominant kernel of the batched materialised path: the one-launch batched
     solve (otk_solve_dense_batched: K3c by default, K3p with OTK_DENSE_KERNEL=cta),
-    timed with CUDA events on its stream.  K3c's roof is MUFU: one ex2 per cell
-    per half-step, 2*iters + 1 half-steps per problem (the fused check's extra
-    row pass included); the streaming-equivalent byte rate (4 B of C per cell
-    per half-step) is reported beside it.  K3p's roof is HBM."""
+    timed with CUDA events on its stream.  K3c's roof is the shared-memory read
+    rate: 4 B of its stored kernel per cell per half-step, 2*iters + 1
+    half-steps per problem (the fused check's extra row pass included); the
+    HBM streaming-equivalent rate is reported beside it.  K3p's roof is HBM."""
     import ctypes
     import torch
     from paper_2201_12324_b200 import _native as N
@@ -437,20 +437,29 @@ def dense_roofline(C, wl, reps=3):
                 "kernel_ms": sec * 1e3, "algorithmic_bytes_per_launch": nbytes, "peak_note": pk_kind,
                 "read_only_gbs": read_gbs.value, "read_only_frac": gbs / read_gbs.value,
                 "mufu": {"ex2_per_s": exps / sec, "peak_ex2_per_s": ex2, "frac": exps / sec / ex2}}
-    # K3c keeps each problem's cost resident in its cluster's shared memory and
-    # reads it from HBM ONCE per solve (traffic), so HBM is not its roof: the
-    # exps are (one MUFU ex2 per cell per half-step)
-    return {"bound": "mufu", "achieved": exps / sec / 1e9, "peak": ex2 / 1e9, "unit": "Gex2/s",
-            "frac": exps / sec / ex2, "traffic": traffic_for(wl.name),
-            "kernel": "otk_solve_dense_batched (K3c: cost resident in a cluster's shared memory, one launch)",
-            "kernel_ms": sec * 1e3, "exps_per_launch": exps,
-            "peak_note": "MUFU ex2 rate measured on this GPU (csrc/pipes.cu)",
-            "streaming_equivalent": {
+    # K3c keeps each problem's stabilised kernel resident in its cluster's shared
+    # memory (built from C, read from HBM ONCE per solve: traffic) and runs every
+    # half-step as an FP32 matrix-vector product over it: its roof is the
+    # shared-memory read rate, 4 B of kernel per cell per half-step
+    smem = ctypes.c_double()
+    N.check(lib.otk_bench_smem(ctypes.byref(smem), stream()))
+    sbytes = 4.0 * n * m * float(np.sum(2 * iters + 1))
+    return {"bound": "smem", "achieved": sbytes / sec / 1e9, "peak": smem.value / 1e9, "unit": "GB/s",
+            "frac": sbytes / sec / smem.value, "traffic": traffic_for(wl.name),
+            "kernel": ("otk_solve_dense_batched (K3c: stabilised kernel resident in a cluster's shared "
+                       "memory, FP32 matrix-vector half-steps, one launch)"),
+            "kernel_ms": sec * 1e3, "algorithmic_bytes_per_launch": sbytes,
+            "peak_note": "shared-memory LDS.128 read rate measured on this GPU (csrc/pipes.cu otk_bench_smem)",
+            "achieved_note": "4 B of the stored kernel per cell per half-step (2*iters + 1 half-steps per "
+                             "problem) / kernel time",
+            "hbm_streaming_equivalent": {
                 "gbs": gbs, "hbm_peak_gbs": float(pk["hbm_gbs"]), "frac": gbs / float(pk["hbm_gbs"]),
                 "read_only_gbs": read_gbs.value,
-                "note": "what a kernel streaming 4 B of C per cell per half-step would have to move "
-                        "(2*iters + 1 half-steps per problem) / time -- above 1 because K3c does not "
-                        "stream C at all"}}
+                "note": "what a kernel streaming 4 B of C per cell per half-step from HBM would have to "
+                        "move / time"},
+            "mufu": {"ex2_per_s_log_domain_equivalent": exps / sec, "peak_ex2_per_s": ex2,
+                     "note": "the log-domain formulation's one ex2 per cell per half-step / time; the "
+                             "scaling domain takes the exps once per kernel build"}}
 
 
 # ------------------------------------------------------------------ our arm

@@ -378,6 +378,11 @@ int otk_bench_pipes(double *ex2_per_s, double *ffma_per_s, void *stream);
  * of `buf` -- the achievable bound of the materialised-cost half-steps. */
 int otk_bench_read(const float *buf, int64_t bytes, double *gbs, void *stream);
 
+/* Shared-memory read microbenchmark: best-of-3 full-chip LDS.128 bytes/s --
+ * the roof of the scaling-domain batched solve (4 B of kernel per cell per
+ * half-step from shared memory). */
+int otk_bench_smem(double *bytes_per_s, void *stream);
+
 /* Whole solve_sinkhorn (sinkhorn.py:122-200) on device.  Returns OTK_OK,
  * OTK_DIVERGED (fail_iter = t) or OTK_BAD_POTENTIAL (fail_iter = t).
  * Small FP32-path problems with a constant eps (both point sets fit in one

@@ -100,6 +100,7 @@ SIGNATURES = {
     "otk_dense_cost_reduce": (C.c_int, [P, I64, I64, I64, P, P, P, P, P]),
     "otk_bench_pipes": (C.c_int, [P, P, P]),
     "otk_bench_read": (C.c_int, [P, I64, P, P]),
+    "otk_bench_smem": (C.c_int, [P, P]),
     "otk_barycenter_ld": (I64, [I64]),
     "otk_barycenter_part_len": (I64, [I64, I32]),
     "otk_barycenter_pad": (C.c_int, [P, I64, I64, P, P, P]),

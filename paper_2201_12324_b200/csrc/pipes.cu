@@ -57,9 +57,59 @@ __global__ void __launch_bounds__(256) read_bw_kernel(const float4 *__restrict__
   if (acc == 12345.f) out[0] = acc;
 }
 
+// Shared-memory read bandwidth: every thread streams LDS.128 over a 32 KB
+// tile (conflict-free, 8 loads in flight) -- the roof of the scaling-domain
+// batched solve, which reads 4 B of its stored kernel per cell per half-step.
+__global__ void __launch_bounds__(512) smem_read_kernel(float *out, int iters) {
+  __shared__ float4 tile[2048];  // 32 KB
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+    tile[i] = make_float4((float)i, 1.f, 2.f, 3.f);
+  __syncthreads();
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 v = tile[(threadIdx.x + k * 512 + it) & 2047];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+  }
+  if (acc.x + acc.y + acc.z + acc.w == 12345.f) out[threadIdx.x] = acc.x;
+}
+
 }  // namespace otk
 
 using namespace otk;
+
+extern "C" int otk_bench_smem(double *bytes_per_s, void *stream) {
+  OTK_CHECK_ARG(bytes_per_s, "otk_bench_smem: null output");
+  cudaStream_t st = as_stream(stream);
+  float *scratch = nullptr;
+  OTK_CUDA(cudaMallocAsync(&scratch, 512 * sizeof(float), st));
+  cudaEvent_t e0, e1;
+  OTK_CUDA(cudaEventCreate(&e0));
+  OTK_CUDA(cudaEventCreate(&e1));
+  const int blocks = num_sms() * 2, threads = 512, iters = 2048;
+  const double bytes = (double)blocks * threads * iters * 8 * 16;
+  double best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0, st);
+    smem_read_kernel<<<blocks, threads, 0, st>>>(scratch, iters);
+    cudaEventRecord(e1, st);
+    OTK_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0) best = std::max(best, bytes / (ms * 1e-3));
+  }
+  *bytes_per_s = best;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  OTK_CUDA(cudaFreeAsync(scratch, st));
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}
 
 extern "C" int otk_bench_read(const float *buf, int64_t bytes, double *gbs, void *stream) {
   OTK_CHECK_ARG(buf && gbs && bytes >= 16, "otk_bench_read: bad arguments");
