@@ -22,7 +22,7 @@ OBJ = os.path.join(PKG, "build_obj")
 LIB = os.path.join(PKG, "libotk_sm100.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "--split-compile", "0",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
 

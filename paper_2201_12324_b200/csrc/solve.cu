@@ -47,6 +47,7 @@ struct Args {  // solve_small.cu
   double eps_d, threshold;
   int max_iters, inner_iters, max_checks;
   float *f0, *f1, *g, *f_out, *g_out;
+  float *f_host, *g_host;
   double *slots;
   double *errors, *duals;
   int *state;
@@ -56,7 +57,7 @@ struct Args {  // solve_small.cu
   unsigned long long *trace;
   int trace_steps;
 };
-constexpr int SLOT = 10;
+constexpr int SLOT = 20;
 }  // namespace small
 bool small_solve_fits(int64_t n, int64_t m, int d);
 int small_solve_launch(const small::Args &A, bool same, bool eucl, cudaStream_t st);
@@ -323,7 +324,7 @@ Layout plan(const otk_solve_args *A, void *ws) {
   L.chk_ws = c.take<char>(otk_check_workspace_bytes());
   L.first_bad = c.take<int>(1);
   if (L.small) {
-    L.slots = c.take<double>((size_t)2 * num_sms() * small::SLOT);
+    L.slots = c.take<double>((size_t)2 * num_sms() * small::SLOT + 2);  // + 2 decision words
     L.d_errors = c.take<double>(A->max_checks);
     L.d_duals = c.take<double>(A->max_checks);
     L.state = c.take<int>(8);
@@ -519,9 +520,36 @@ static int solve_small(otk_solve_args *A, Layout &L, cudaStream_t st) {
   S.f_out = A->f_out;
   S.g_out = A->g_out;
   S.slots = L.slots;
-  S.errors = L.d_errors;
-  S.duals = L.d_duals;
-  S.state = L.state;
+  // results block in pinned host memory (per host thread, grown on demand):
+  // [8 ints of state | errors | duals], written by the kernel itself
+  struct HostRes {
+    char *p = nullptr;
+    size_t bytes = 0;
+  };
+  static thread_local HostRes hres;
+  const size_t need = 64 + 2 * (size_t)A->max_checks * sizeof(double);
+  if (hres.bytes < need) {
+    if (hres.p) cudaFreeHost(hres.p);
+    hres.p = nullptr;
+    hres.bytes = 0;
+    OTK_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&hres.p), need, cudaHostAllocDefault));
+    hres.bytes = need;
+  }
+  double *h_err = reinterpret_cast<double *>(hres.p + 64);
+  double *h_dual = h_err + A->max_checks;
+  S.errors = h_err;
+  S.duals = h_dual;
+  S.state = reinterpret_cast<int *>(hres.p);
+  auto pinned = [](const void *p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  S.f_host = (A->f_host && pinned(A->f_host)) ? A->f_host : nullptr;
+  S.g_host = (A->g_host && pinned(A->g_host)) ? A->g_host : nullptr;
   S.probe = getenv("OTK_SMALL_PROBE") ? atoi(getenv("OTK_SMALL_PROBE")) : 0;
   S.xch_x = L.xch;
   S.xch_y = L.xch + 2 * A->n;
@@ -543,15 +571,19 @@ static int solve_small(otk_solve_args *A, Layout &L, cudaStream_t st) {
       fclose(fp);
     }
   }
-  // one synchronisation: state, the whole check trace and (optionally) f, g
-  int state[8];
-  OTK_CUDA(cudaMemcpyAsync(state, L.state, 5 * sizeof(int), cudaMemcpyDeviceToHost, st));
-  OTK_CUDA(cudaMemcpyAsync(A->errors, L.d_errors, A->max_checks * sizeof(double), cudaMemcpyDeviceToHost, st));
-  OTK_CUDA(cudaMemcpyAsync(A->duals, L.d_duals, A->max_checks * sizeof(double), cudaMemcpyDeviceToHost, st));
-  if (A->f_host) OTK_CUDA(cudaMemcpyAsync(A->f_host, A->f_out, A->n * sizeof(float), cudaMemcpyDeviceToHost, st));
-  if (A->g_host) OTK_CUDA(cudaMemcpyAsync(A->g_host, A->g_out, A->m * sizeof(float), cudaMemcpyDeviceToHost, st));
+  // one synchronisation and no copy calls: the kernel wrote its state, the
+  // check trace and (when the caller's buffers are pinned) f, g straight into
+  // host memory
   OTK_CUDA(cudaStreamSynchronize(st));
+  if (A->f_host && !S.f_host)
+    OTK_CUDA(cudaMemcpyAsync(A->f_host, A->f_out, A->n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (A->g_host && !S.g_host)
+    OTK_CUDA(cudaMemcpyAsync(A->g_host, A->g_out, A->m * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if ((A->f_host && !S.f_host) || (A->g_host && !S.g_host)) OTK_CUDA(cudaStreamSynchronize(st));
+  const int *state = reinterpret_cast<const int *>(hres.p);
   const int nc = std::min(state[0], A->max_checks);
+  std::memcpy(A->errors, h_err, (size_t)nc * sizeof(double));
+  std::memcpy(A->duals, h_dual, (size_t)nc * sizeof(double));
   A->n_checks = nc;
   A->iterations = state[1];
   A->converged = state[2];

@@ -36,7 +36,7 @@ namespace small {
 constexpr int THREADS = 512;
 constexpr int WARPS = THREADS / 32;
 constexpr int NVALS = 8;
-constexpr int SLOT = 10;  // doubles per CTA check slot: 8 sums, first bad half-step, pad
+constexpr int SLOT = 20;  // 64-bit words per CTA check slot: 8 sums as two tagged halves each, first bad half-step, pad
 constexpr int MAX_GRID = 160;  // CTAs (one per SM)
 
 struct Args {
@@ -46,7 +46,8 @@ struct Args {
   double eps_d, threshold;
   int max_iters, inner_iters, max_checks;
   float *f0, *f1, *g, *f_out, *g_out;
-  double *slots;             // [2][gridDim][SLOT] check slots (by check parity)
+  float *f_host, *g_host;    // nullable: device-visible pinned host copies of the results (zero-copy)
+  double *slots;             // [2][gridDim][SLOT] tagged check words (by check parity) + 2 decision words
   double *errors, *duals;    // [max_checks]
   int *state;                // n_checks, iterations, converged, status, fail_iter
   int probe;                 // timing probe (OTK_SMALL_PROBE): skip the passes over the cells;
@@ -128,6 +129,8 @@ constexpr int KMAX = 8;   // chunks per CTA per role (n <= 8 * 16 * #SMs)
 
 typedef unsigned long long xword;
 
+extern __shared__ float4 sh4[];  // dynamic shared memory: resident points, or the stored y-role terms
+
 __device__ __forceinline__ xword ld_relaxed(const xword *p) {
   xword v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -173,14 +176,23 @@ struct RoleRows {
   float2 p2[KMAX * RC / 2][4 * NV];
   float cp[KMAX * RC];
   float an[KMAX * RC];
+  float elw[KMAX * RC];  // eps * log weight of the row (read from global memory once, not per half-step)
+  int rc, n_chunks;      // rows per chunk, chunks of the role
+  float lo;              // lower end of the anchored acceptance window
 };
 
 template <int NV>
-__device__ __forceinline__ void init_role_rows(const Args &A, const float4 *P, int np, RoleRows<NV> &S) {
+__device__ __forceinline__ void init_role_rows(const Args &A, const float4 *P, int np, int nq, const float *logw,
+                                               RoleRows<NV> &S) {
   const int G = gridDim.x;
   const int rc = min(RC, (np + G - 1) / G);
   const int n_chunks = (np + rc - 1) / rc;
   const float two_k = 2.f * A.kappa;
+  if (threadIdx.x == 0) {
+    S.rc = rc;
+    S.n_chunks = n_chunks;
+    S.lo = -96.f + 2.f * log2f((float)nq);
+  }
   for (int idx = threadIdx.x; idx < KMAX * RC; idx += blockDim.x) {
     const int k = idx / RC, r = idx % RC;
     const int ch = blockIdx.x + k * G;
@@ -192,6 +204,34 @@ __device__ __forceinline__ void init_role_rows(const Args &A, const float4 *P, i
     for (int kk = 0; kk < 4 * NV; ++kk) dst[2 * kk] = (kk < A.d) ? two_k * pv[kk] : (kk == A.d ? 1.f : 0.f);
     S.cp[idx] = -pv[A.d];
     S.an[idx] = -INFINITY;
+    S.elw[idx] = A.eps * logw[i];
+  }
+}
+
+// Per-thread row-pair partials -> the CTA's total of row r in tot[r]: shuffle
+// reduce-scatter inside a warp, then the warps' values folded in warp order.
+template <bool MAXP>
+__device__ __forceinline__ void fold_rows(const float2 (&acc)[RC / 2], int rc, float (*red)[RC], float *tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float v16[RC];
+#pragma unroll
+  for (int h = 0; h < RC / 2; ++h) {
+    v16[2 * h] = acc[h].x;
+    v16[2 * h + 1] = acc[h].y;
+  }
+  const float v = rs16<MAXP>(v16, lane);
+  if (!(lane & 1)) red[warp][rs16_row(lane)] = v;
+  __syncthreads();
+  if (threadIdx.x < rc) {  // fixed pairwise tree over the warps (short dependent chain)
+    float t[WARPS];
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) t[w] = red[w][threadIdx.x];
+#pragma unroll
+    for (int s = 1; s < WARPS; s *= 2)
+#pragma unroll
+      for (int w = 0; w + s < WARPS; w += 2 * s) t[w] = rs_op<MAXP>(t[w], t[w + s]);
+    tot[threadIdx.x] = t[0];  // read back by this same thread only: no barrier here (the
+                              // callers' next barrier comes before `red` is written again)
   }
 }
 
@@ -208,7 +248,6 @@ __device__ __forceinline__ void chunk_pass(const Args &A, const float4 *Q, int n
                                            float *tot) {
   constexpr int CPT = Cols<NV>::CPT;
   static_assert(CPT == 2 || CPT == 4, "column groups of 2 or 4");
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float sk = sqrtf(A.kappa);
   float2 acc[RC / 2];
 #pragma unroll
@@ -306,41 +345,220 @@ __device__ __forceinline__ void chunk_pass(const Args &A, const float4 *Q, int n
     }
   }
   if (!MAXP) trace_mark(A, need + 1, 2);
-  float v16[RC];
-#pragma unroll
-  for (int h = 0; h < RC / 2; ++h) {
-    v16[2 * h] = acc[h].x;
-    v16[2 * h + 1] = acc[h].y;
-  }
-  const float v = rs16<MAXP>(v16, lane);
-  if (!(lane & 1)) red[warp][rs16_row(lane)] = v;
-  __syncthreads();
-  if (threadIdx.x < rc) {
-    float t = red[0][threadIdx.x];
-#pragma unroll
-    for (int w = 1; w < WARPS; ++w) t = rs_op<MAXP>(t, red[w][threadIdx.x]);
-    tot[threadIdx.x] = t;
-  }
-  __syncthreads();
+  fold_rows<MAXP>(acc, rc, red, tot);
   if (!MAXP) trace_mark(A, need + 1, 3);
+}
+
+// ---- stored-kernel half-steps (ST instantiations) ----
+//
+// When a role's chunk is the CTA's only one and its columns fit one register
+// group (nq <= SC * THREADS), the exps of a half-step are taken ONCE: the exact
+// pass that follows the row maxima keeps E_rj = 2^(beta_j - kappa C_rj - rho_r)
+// (beta_j: the column's kappa * potential at that moment, rho_r: the row max,
+// so 0 <= E <= 1 and every row holds a 1) -- the x role in registers (SC
+// columns x RC rows per thread), the y role in shared memory -- and the
+// following half-steps of the role are FP32 matrix-vector products
+//   L_r = rho_r + log2 sum_j E_rj v_j,   v_j = 2^(kappa g_j - beta_j)
+// (Schmitzer's absorption in log2 units; the same scheme as the batched
+// cluster kernel, dense_solve.cu).  A column whose potential drifted more than
+// DRIFT bits from its beta, or turned NaN / +inf, sends the CTA back to the
+// exact passes, which rebuild E around the current potentials: terms flushed
+// to zero at build time were below 2^-126 of their row's largest, so after a
+// drift of DRIFT bits either way they are still below 2^(-126 + 2 DRIFT) of
+// the row sum.  The decision is local to the CTA.
+constexpr int SC = 4;            // columns per thread of a stored role
+#ifndef OTK_ER_PAIRS
+#define OTK_ER_PAIRS 8
+#endif
+#ifndef OTK_ST_HB
+#define OTK_ST_HB 4
+#endif
+constexpr int ER_PAIRS = OTK_ER_PAIRS;  // row pairs of the x role kept in registers (the others in shared memory)
+constexpr float DRIFT = 40.f;
+
+// Predicated 64-bit shared-memory load (zeros when !p), no branch.
+__device__ __forceinline__ float2 lds_f2_pred(uint32_t addr, bool p) {
+  float2 r;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\tmov.f32 %0, 0f00000000;\n\tmov.f32 %1, 0f00000000;\n\t"
+      "@p ld.shared.v2.f32 {%0, %1}, [%2];\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "r"(addr), "r"((unsigned)p));
+  return r;
+}
+
+__device__ __forceinline__ void wait_words(const xword *qx, int nq, int need, xword (&w)[SC], int (&jj)[SC]) {
+#pragma unroll
+  for (int c = 0; c < SC; ++c) {
+    jj[c] = threadIdx.x + c * THREADS;
+    w[c] = (jj[c] < nq) ? ld_relaxed(qx + jj[c]) : xpack(-INFINITY, need);
+  }
+  for (int spins = 0;; ++spins) {
+    bool ready = true;
+#pragma unroll
+    for (int c = 0; c < SC; ++c) ready &= (int)(w[c] >> 32) == need;
+    if (ready) break;
+    if (spins > (1 << 23)) __trap();
+#pragma unroll
+    for (int c = 0; c < SC; ++c)
+      if ((int)(w[c] >> 32) != need) w[c] = ld_relaxed(qx + jj[c]);
+  }
+}
+
+// The matrix-vector half-step.  The first NREG row pairs of E live in
+// registers (er), the others in shared memory: pair h at byte offset
+// es_off + (h - NREG) * nq * 8, one float2 per column.  Sets *redo when a
+// column left the drift window.
+template <int NREG>
+__device__ __forceinline__ void stored_pass(const Args &A, int nq, const xword *qx, int need, int rc,
+                                            const float2 (&er)[ER_PAIRS > 0 ? ER_PAIRS : 1][SC], uint32_t es_off,
+                                            const float (&beta)[SC], int *redo, float (*red)[RC], float *tot) {
+  xword w[SC];
+  int jj[SC];
+  wait_words(qx, nq, need, w, jj);
+  trace_mark(A, need + 1, 1);
+  float2 v[SC];
+  bool drift = false;
+#pragma unroll
+  for (int c = 0; c < SC; ++c) {
+    const float dl = __uint_as_float((unsigned)w[c]) - beta[c];
+    const float e = (jj[c] < nq) ? ex2(dl) : 0.f;
+    v[c] = make_float2(e, e);
+    drift |= (jj[c] < nq) && !(fabsf(dl) <= DRIFT) && dl != -INFINITY;
+  }
+  if (drift) *redo = 1;
+  float2 acc[RC / 2];
+  // shared-memory pairs first (their loads in flight while the register pairs run):
+  // predicated ld.shared from 32-bit shared addresses, HB row pairs per batch
+  const uint32_t es0 = (uint32_t)__cvta_generic_to_shared(sh4) + es_off;
+  constexpr int NS = RC / 2 - NREG;
+  constexpr int HB = NS < OTK_ST_HB ? (NS > 0 ? NS : 1) : OTK_ST_HB;
+#pragma unroll
+  for (int h0 = 0; h0 < NS; h0 += HB) {
+    float2 e[HB][SC];
+#pragma unroll
+    for (int h = 0; h < HB; ++h)
+#pragma unroll
+      for (int c = 0; c < SC; ++c)
+        e[h][c] = lds_f2_pred(es0 + (uint32_t)(((h0 + h) * nq + jj[c]) * (int)sizeof(float2)),
+                              2 * (NREG + h0 + h) < rc && jj[c] < nq);
+#pragma unroll
+    for (int h = 0; h < HB; ++h) {
+      float2 a2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < SC; ++c) a2 = __ffma2_rn(e[h][c], v[c], a2);
+      acc[NREG + h0 + h] = a2;
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < NREG; ++h) {
+    float2 a2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < SC; ++c) a2 = __ffma2_rn(er[h][c], v[c], a2);  // pairs past rc hold zeros
+    acc[h] = a2;
+  }
+  trace_mark(A, need + 1, 2);
+  fold_rows<false>(acc, rc, red, tot);  // its barrier also publishes *redo
+  trace_mark(A, need + 1, 3);
+}
+
+// The exact sum pass against the row maxima sh[], keeping every term as E and
+// the columns' kappa * potential as beta.  One column at a time (the x role
+// holds NREG x SC pairs of its terms in registers next to this pass).
+template <int NV, bool SAME, bool EU, int NREG>
+__device__ __forceinline__ void build_pass(const Args &A, const float4 *Q, int nq, const xword *qx, int need,
+                                           int r0, int rc, const float2 (*p2)[4 * NV], const float *cp,
+                                           const float *sh, float2 (&er)[ER_PAIRS > 0 ? ER_PAIRS : 1][SC], uint32_t es_off,
+                                           float (&beta)[SC], float (*red)[RC], float *tot) {
+  const float sk = sqrtf(A.kappa);
+  float2 *es = reinterpret_cast<float2 *>(reinterpret_cast<char *>(sh4) + es_off);
+  xword w[SC];
+  int jj[SC];
+  wait_words(qx, nq, need, w, jj);
+  float2 acc[RC / 2];
+#pragma unroll
+  for (int h = 0; h < RC / 2; ++h) acc[h] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < SC; ++c) {
+    const bool ok = jj[c] < nq;
+    float q[4 * NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const float4 qv = ok ? Q[jj[c] * NV + v] : make_float4(0.f, 0.f, 0.f, 0.f);
+      q[4 * v] = qv.x;
+      q[4 * v + 1] = qv.y;
+      q[4 * v + 2] = qv.z;
+      q[4 * v + 3] = qv.w;
+    }
+    const float bj = __uint_as_float((unsigned)w[c]);
+    beta[c] = (bj == -INFINITY) ? 0.f : bj;  // a -inf column stays at E = 0, v = 0
+    if (!EU) {
+#pragma unroll
+      for (int k = 0; k < 4 * NV; ++k) q[k] = q[k] + (k == A.d ? bj : 0.f);
+    }
+#pragma unroll
+    for (int h = 0; h < RC / 2; ++h) {
+      float2 e = make_float2(0.f, 0.f);
+      if (2 * h < rc) {
+        float2 pk[4 * NV];
+#pragma unroll
+        for (int k = 0; k < 4 * NV; ++k) pk[k] = p2[h][k];
+        const float2 cp2 = *reinterpret_cast<const float2 *>(cp + 2 * h);
+        const float2 ns2 = make_float2(-sh[2 * h], -sh[2 * h + 1]);
+        float2 u;
+        if (EU) {
+          const float2 bs = __fadd2_rn(ns2, make_float2(bj, bj));
+          float2 dt = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int k = 0; k < 4 * NV; ++k) dt = __ffma2_rn(pk[k], make_float2(q[k], q[k]), dt);
+          float v0 = -sk * sqrt_approx(fmaxf(cp2.x - dt.x, 0.f));
+          float v1 = -sk * sqrt_approx(fmaxf(cp2.y - dt.y, 0.f));
+          if (SAME && jj[c] == r0 + 2 * h) v0 = 0.f;
+          if (SAME && jj[c] == r0 + 2 * h + 1) v1 = 0.f;
+          u = __fadd2_rn(make_float2(v0, v1), bs);
+        } else {
+          float2 dt = ns2;
+#pragma unroll
+          for (int k = 0; k < 4 * NV; ++k) dt = __ffma2_rn(pk[k], make_float2(q[k], q[k]), dt);
+          const float2 lim = __fadd2_rn(__fadd2_rn(cp2, ns2), make_float2(bj, bj));
+          u = make_float2(fminf(dt.x, lim.x), fminf(dt.y, lim.y));
+          if (SAME && jj[c] == r0 + 2 * h) u.x = lim.x;
+          if (SAME && jj[c] == r0 + 2 * h + 1) u.y = lim.y;
+        }
+        e = make_float2(ex2(u.x), ex2(u.y));
+        if (!ok) e = make_float2(0.f, 0.f);
+        acc[h] = __fadd2_rn(acc[h], e);
+        if (h >= NREG && ok) es[(h - NREG) * nq + jj[c]] = e;
+      }
+      if (h < NREG) er[h][c] = e;
+    }
+  }
+  fold_rows<false>(acc, rc, red, tot);
 }
 
 // One half-step of a role: rows P (np) against the columns' exchange words
 // qx (tag step - 1).  Publishes {kappa * out_pot, step} into px and writes
 // out_pot (own rows).  CHECK: the f-side check sums (f_prev = previous f,
 // weights A.a); CHECKG: the g-side sums (weights A.b) of this g half-step.
-template <int NV, bool SAME, bool CHECK, bool CHECKG, bool EU>
+// Stored-kernel state of one role (STR = 1: E in registers, 2: in shared memory).
+struct StoredRole {
+  float2 er[ER_PAIRS > 0 ? ER_PAIRS : 1][SC];
+  float beta[SC];
+  uint32_t es_off;  // byte offset of the role's shared-memory terms in the dynamic array
+  bool have;
+};
+
+template <int NV, bool SAME, bool CHECK, bool CHECKG, bool EU, int STR>
 __device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, int np, const float4 *Q, int nq,
                                const xword *qx, xword *px, const float *logw, float *out_pot,
                                RoleRows<NV> &S, bool anchored, int step, const float *f_prev,
-                               double (&chk)[NVALS], int *bad_s) {
+                               double (*chk_s)[NVALS], int *bad_s, StoredRole &SR, int *drift_pp) {
   __shared__ float red[WARPS][RC];
   __shared__ float tot[RC];
   __shared__ int redo;
   const int G = gridDim.x;
-  const int rc = min(RC, (np + G - 1) / G);
-  const int n_chunks = (np + rc - 1) / rc;
-  const float lo = -96.f + 2.f * log2f((float)nq);
+  const int rc = S.rc, n_chunks = S.n_chunks;
+  const float lo = S.lo;
   const int need = step - 1;
   for (int ch = blockIdx.x, k = 0; ch < n_chunks; ch += G, ++k) {
     const int r0 = ch * rc, rn = min(rc, np - r0);
@@ -348,13 +566,40 @@ __device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, i
     const float2 (*p2)[4 * NV] = S.p2 + k * (RC / 2);
     const float *cp = S.cp + k * RC;
     float *an = S.an + k * RC;
-    if (threadIdx.x == 0) redo = 0;
-    __syncthreads();
-    if (threadIdx.x < rn && !(anchored && fabsf(an[threadIdx.x]) <= 3.0e38f)) redo = 1;
-    __syncthreads();
+    if (STR == 0) {
+      if (threadIdx.x == 0) redo = 0;
+      __syncthreads();
+      if (threadIdx.x < rn && !(anchored && fabsf(an[threadIdx.x]) <= 3.0e38f)) redo = 1;
+      __syncthreads();
+    }
     float L = 0.f;  // log2 sum (before the -kappa|p|^2 shift), row threadIdx.x
     if (A.probe != 0) {  // timing probe: everything but the passes over the cells
       if (threadIdx.x < rn) L = cp[threadIdx.x];
+    } else if (STR != 0) {  // stored kernel: an[] holds the row maxima rho of the last build
+      // drift flags ping-pong by half-step parity: this step's flag was cleared
+      // during the previous step (after every reader of its last use had passed
+      // that step's closing barrier), so no barrier is spent on the reset
+      bool rebuild = !SR.have;
+      if (threadIdx.x == 0) drift_pp[(step + 1) & 1] = 0;
+      if (SR.have) {
+        stored_pass<STR == 1 ? ER_PAIRS : 0>(A, nq, qx, need, rn, SR.er, SR.es_off, SR.beta, &drift_pp[step & 1],
+                                             red, tot);
+        rebuild = drift_pp[step & 1] != 0;
+        if (threadIdx.x < rn) L = an[threadIdx.x] + lg2(tot[threadIdx.x]);
+      }
+      if (rebuild) {
+        __syncthreads();
+        chunk_pass<NV, SAME, EU, true>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
+        if (threadIdx.x < rn) {
+          const float mx = tot[threadIdx.x];
+          an[threadIdx.x] = (mx == -INFINITY) ? 0.f : mx;
+        }
+        __syncthreads();
+        build_pass<NV, SAME, EU, STR == 1 ? ER_PAIRS : 0>(A, Q, nq, qx, need, r0, rn, p2, cp, an, SR.er,
+                                                          SR.es_off, SR.beta, red, tot);
+        SR.have = true;
+        if (threadIdx.x < rn) L = an[threadIdx.x] + lg2(tot[threadIdx.x]);
+      }
     } else if (!redo) {
       chunk_pass<NV, SAME, EU, false>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
       if (threadIdx.x < rn) {
@@ -365,7 +610,7 @@ __device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, i
       }
       __syncthreads();
     }
-    if (redo && A.probe == 0) {  // exact: row maxima, then the sum against them
+    if (STR == 0 && redo && A.probe == 0) {  // exact: row maxima, then the sum against them
       chunk_pass<NV, SAME, EU, true>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
       if (threadIdx.x < rn) {
         const float mx = tot[threadIdx.x];
@@ -378,11 +623,12 @@ __device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, i
     if (threadIdx.x < rn) {
       const int i = r0 + threadIdx.x;
       const float Lf = L - (EU ? 0.f : cp[threadIdx.x]);
-      an[threadIdx.x] = L;
-      const float v = A.eps * logw[i] - A.eps * kLn2 * Lf;
+      if (STR == 0) an[threadIdx.x] = L;
+      const float v = S.elw[k * RC + threadIdx.x] - A.eps * kLn2 * Lf;
       st_relaxed(px + i, xpack(v * A.kappa, step));
       out_pot[i] = v;
       if (bad_potential(v)) atomicMin(bad_s, step);
+      double *chk = chk_s[threadIdx.x];  // this row thread's check terms (shared memory: no registers held)
       if (CHECK) {
         const double fp = f_prev[i], ai = A.a[i];
         const double rr = (ai > 0.0) ? ai * exp((fp - (double)v) / A.eps_d) : 0.0;
@@ -404,23 +650,30 @@ __device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, i
   }
 }
 
-template <int NV, bool SAME, bool EU>
+template <int NV, bool SAME, bool EU, bool ST>
 __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ float4 sh4[];
   __shared__ RoleRows<NV> rows_x, rows_y;
-  __shared__ double red[NVALS][WARPS];
   __shared__ double tot_s[NVALS];
   __shared__ int bad_s, bad_all;
-  __shared__ double slot_s[MAX_GRID][NVALS + 1];
+  __shared__ int drift_pp[2];
+  __shared__ unsigned dec_s;
+  __shared__ double chk_s[RC][NVALS];
   const int G = gridDim.x;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = G * blockDim.x;
 
-  if (threadIdx.x == 0) bad_s = INT_MAX;
+  if (threadIdx.x == 0) {
+    bad_s = INT_MAX;
+    drift_pp[0] = drift_pp[1] = 0;
+  }
   // d <= 7: both point sets resident in every CTA's shared memory; d >= 8:
   // staged once in global memory (L2-resident), each CTA writing a share
   float4 *xs, *ys;
-  if constexpr (NV <= 2) {
+  StoredRole sx, sy;  // ST: the x role's terms in registers, the y role's in shared memory
+  sx.have = sy.have = false;
+  sy.es_off = 0;  // y role: RC / 2 pairs x n columns; then the x role's RC / 2 - ER_PAIRS pairs x m columns
+  sx.es_off = (uint32_t)((RC / 2) * A.n * (int)sizeof(float2));
+  if constexpr (NV <= 2 && !ST) {
     xs = sh4;
     ys = xs + A.n * NV;
     load_points<NV>(A.x, A.n, A.d, A.kappa, xs, threadIdx.x, blockDim.x);
@@ -442,10 +695,11 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
     if (bad_potential(g0)) atomicMin(&bad_s, 1);  // a bad warm start
   }
   for (int i = gtid; i < 2 * A.n; i += gstride) A.xch_x[i] = xpack(0.f, -1);
+  for (int i = gtid; i < 2 * G * SLOT + 2; i += gstride) reinterpret_cast<xword *>(A.slots)[i] = 0;  // tag 0: no check
   __syncthreads();
   grid.sync();
-  init_role_rows<NV>(A, xs, A.n, rows_x);  // after the barrier: global points are complete
-  init_role_rows<NV>(A, ys, A.m, rows_y);
+  init_role_rows<NV>(A, xs, A.n, A.m, A.la, rows_x);  // after the barrier: global points are complete
+  init_role_rows<NV>(A, ys, A.m, A.n, A.lb, rows_y);
   __syncthreads();
 
   // exchange buffer of the words tagged T: (T >> 1) & 1
@@ -453,62 +707,102 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
   float *f = A.f0, *fn = A.f1;
   bool f_ready = false;
   int n_checks = 0, status = OTK_OK, fail_iter = 0, converged = 0, t;
-  double chk[NVALS];
   for (t = 1; t <= A.max_iters; ++t) {
     const bool check = (t % A.inner_iters == 0 || t == A.max_iters);
+    if (check && threadIdx.x < RC) {  // each row thread's own terms: same-thread ordering, no barrier
 #pragma unroll
-    for (int k = 0; k < NVALS; ++k) chk[k] = 0.0;
+      for (int k = 0; k < NVALS; ++k) chk_s[threadIdx.x][k] = 0.0;
+    }
     if (!f_ready)
-      half_step_rows<NV, SAME, false, false, EU>(A, xs, A.n, ys, A.m, xb(A.xch_y, A.m, 2 * t - 1),
-                                                 xb(A.xch_x, A.n, 2 * t), A.la, f, rows_x, t > 1, 2 * t,
-                                                 nullptr, chk, &bad_s);
+      half_step_rows<NV, SAME, false, false, EU, ST ? 1 : 0>(A, xs, A.n, ys, A.m, xb(A.xch_y, A.m, 2 * t - 1),
+                                                             xb(A.xch_x, A.n, 2 * t), A.la, f, rows_x, t > 1,
+                                                             2 * t, nullptr, chk_s, &bad_s, sx, drift_pp);
     f_ready = false;
     if (check)
-      half_step_rows<NV, SAME, false, true, EU>(A, ys, A.m, xs, A.n, xb(A.xch_x, A.n, 2 * t),
-                                                xb(A.xch_y, A.m, 2 * t + 1), A.lb, A.g, rows_y, t > 1,
-                                                2 * t + 1, nullptr, chk, &bad_s);
+      half_step_rows<NV, SAME, false, true, EU, ST ? 2 : 0>(A, ys, A.m, xs, A.n, xb(A.xch_x, A.n, 2 * t),
+                                                            xb(A.xch_y, A.m, 2 * t + 1), A.lb, A.g, rows_y,
+                                                            t > 1, 2 * t + 1, nullptr, chk_s, &bad_s, sy, drift_pp);
     else
-      half_step_rows<NV, SAME, false, false, EU>(A, ys, A.m, xs, A.n, xb(A.xch_x, A.n, 2 * t),
-                                                 xb(A.xch_y, A.m, 2 * t + 1), A.lb, A.g, rows_y, t > 1,
-                                                 2 * t + 1, nullptr, chk, &bad_s);
+      half_step_rows<NV, SAME, false, false, EU, ST ? 2 : 0>(A, ys, A.m, xs, A.n, xb(A.xch_x, A.n, 2 * t),
+                                                             xb(A.xch_y, A.m, 2 * t + 1), A.lb, A.g, rows_y,
+                                                             t > 1, 2 * t + 1, nullptr, chk_s, &bad_s, sy, drift_pp);
     if (!check) continue;
     // f_{t+1} into fn, with the check of (f_t, g_t) fused in
-    half_step_rows<NV, SAME, true, false, EU>(A, xs, A.n, ys, A.m, xb(A.xch_y, A.m, 2 * t + 1),
-                                              xb(A.xch_x, A.n, 2 * t + 2), A.la, fn, rows_x, true,
-                                              2 * t + 2, f, chk, &bad_s);
-    // fixed-order block reduction -> this CTA's slot
+    half_step_rows<NV, SAME, true, false, EU, ST ? 1 : 0>(A, xs, A.n, ys, A.m, xb(A.xch_y, A.m, 2 * t + 1),
+                                                          xb(A.xch_x, A.n, 2 * t + 2), A.la, fn, rows_x, true,
+                                                          2 * t + 2, f, chk_s, &bad_s, sx, drift_pp);
+    // The check's global sums without a grid barrier.  Only the row threads
+    // (threadIdx.x < RC, all in warp 0) accumulated terms, so a fixed shuffle
+    // tree over warp 0 is the whole block reduction.  Each CTA publishes its 8
+    // sums and its first bad half-step as tagged 64-bit words {32 bits of the
+    // value, check index} (same single-copy-atomic trick as the exchange
+    // words: no fence), double-buffered by check parity.  CTA 0 alone gathers
+    // them -- one reader, so no L2 line is hammered by 148 SMs -- totals them in
+    // a fixed order, records the error / dual and publishes ONE decision word
+    // that every CTA spins on.
+    const int ctag = n_checks + 1;
+    xword *sw = reinterpret_cast<xword *>(A.slots) + (size_t)(n_checks & 1) * G * SLOT;
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      unsigned bits = (unsigned)bad_s;  // word 2 * NVALS
 #pragma unroll
-    for (int k = 0; k < NVALS; ++k) {
-      double v = chk[k];
+      for (int k = 0; k < NVALS; ++k) {
+        double v = lane < RC ? chk_s[lane][k] : 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = v;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+        if (lane == 2 * k) bits = (unsigned)(b >> 32);
+        if (lane == 2 * k + 1) bits = (unsigned)b;
+      }
+      if (lane <= 2 * NVALS)
+        st_relaxed(sw + (size_t)lane * G + blockIdx.x, ((xword)(unsigned)ctag << 32) | bits);  // word-major
     }
-    __syncthreads();
-    // slots double-buffered by check parity: a CTA may write the next check's
-    // slot while a slower one still reads this check's
-    double *slots = A.slots + (size_t)(n_checks & 1) * G * SLOT;
-    if (threadIdx.x < NVALS) {
-      double v = 0.0;
-      for (int w = 0; w < WARPS; ++w) v += red[threadIdx.x][w];
-      slots[blockIdx.x * SLOT + threadIdx.x] = v;
-    } else if (threadIdx.x == NVALS) {
-      slots[blockIdx.x * SLOT + NVALS] = (double)bad_s;
-    }
-    grid.sync();
-    // every CTA gathers all slots (one round trip) and reduces them in the
-    // same order -> identical decisions everywhere
-    for (int k = threadIdx.x; k < G; k += blockDim.x) {
-#pragma unroll
-      for (int v = 0; v <= NVALS; ++v) slot_s[k][v] = __ldcg(slots + k * SLOT + v);
-    }
-    __syncthreads();
-    {  // warp v folds value v: lanes stride the slots, then a fixed shuffle tree
+    trace_mark(A, 2 * t + 2, 5);
+    xword *dec_w = reinterpret_cast<xword *>(A.slots) + (size_t)2 * G * SLOT;
+    if (blockIdx.x == 0) {
+      // warp v totals value v: lanes stride the CTAs (independent loads), then a fixed shuffle tree
       const int wv = threadIdx.x >> 5, lane = threadIdx.x & 31;
       if (wv <= NVALS) {
-        const bool mn = wv == NVALS;  // the first bad half-step: a minimum
+        const bool mn = wv == NVALS;  // the first bad half-step: a minimum of ints
+        constexpr int QN = (MAX_GRID + 31) / 32;
+        unsigned ph[QN], pl[QN];  // 32-bit payloads (high / low half of the double)
+        unsigned pending = 0;     // bit 2q: high word of CTA lane + 32 q outstanding, bit 2q + 1: low word
+#pragma unroll
+        for (int q = 0; q < QN; ++q) {
+          ph[q] = pl[q] = 0u;
+          if (lane + 32 * q < G) pending |= (mn ? 1u : 3u) << (2 * q);
+        }
+        const xword *src = sw + (size_t)(2 * wv) * G + lane;  // word-major: lanes read consecutive words
+        for (int spins = 0; pending; ++spins) {
+          if (spins > (1 << 23)) __trap();
+          xword wh[QN], wl[QN];  // every outstanding word requested before any is tested
+#pragma unroll
+          for (int q = 0; q < QN; ++q) {
+            wh[q] = wl[q] = 0;
+            if (pending & (1u << (2 * q))) wh[q] = ld_relaxed(src + 32 * q);
+            if (pending & (2u << (2 * q))) wl[q] = ld_relaxed(src + G + 32 * q);
+          }
+#pragma unroll
+          for (int q = 0; q < QN; ++q) {
+            if ((pending & (1u << (2 * q))) && (int)(wh[q] >> 32) == ctag) {
+              ph[q] = (unsigned)wh[q];
+              pending &= ~(1u << (2 * q));
+            }
+            if ((pending & (2u << (2 * q))) && (int)(wl[q] >> 32) == ctag) {
+              pl[q] = (unsigned)wl[q];
+              pending &= ~(2u << (2 * q));
+            }
+          }
+        }
         double v = mn ? (double)INT_MAX : 0.0;
-        for (int bk = lane; bk < G; bk += 32) v = mn ? fmin(v, slot_s[bk][wv]) : v + slot_s[bk][wv];
+#pragma unroll
+        for (int q = 0; q < QN; ++q) {
+          if (lane + 32 * q < G) {
+            const double u = mn ? (double)(int)ph[q]
+                                : __longlong_as_double((long long)(((xword)ph[q] << 32) | (xword)pl[q]));
+            v = mn ? fmin(v, u) : v + u;
+          }
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           const double u = __shfl_xor_sync(0xffffffffu, v, o);
@@ -519,31 +813,47 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
           else tot_s[wv] = v;
         }
       }
+      __syncthreads();
+      trace_mark(A, 2 * t + 2, 6);
+      if (threadIdx.x == 0) {
+        // decision code: converged | status << 1 | fail_iter << 4
+        const int fb = bad_all;
+        const double err = tot_s[0];
+        unsigned code = 0;
+        bool record = false;
+        if (fb <= 2 * t) code = (1u << 1) | ((unsigned)((fb + 1) / 2) << 4);
+        else if (tot_s[4] > 0 || tot_s[5] > 0) code = (2u << 1) | ((unsigned)t << 4);
+        else if (fb == 2 * t + 1) code = (1u << 1) | ((unsigned)t << 4);
+        else {
+          record = n_checks < A.max_checks;
+          if (err <= A.threshold && A.probe == 0) code = 1u;
+        }
+        // the decision leaves first; the trace entries (host memory) follow
+        st_relaxed(dec_w + (n_checks & 1), ((xword)(unsigned)ctag << 32) | code);
+        dec_s = code;
+        if (record) {
+          A.errors[n_checks] = err;
+          A.duals[n_checks] = tot_s[2] + tot_s[3] - A.eps_d * (tot_s[1] - 1.0);
+        }
+      }
+    } else if (threadIdx.x == 0) {
+      xword w = ld_relaxed(dec_w + (n_checks & 1));
+      for (int spins = 0; (int)(w >> 32) != ctag; ++spins) {
+        if (spins > (1 << 23)) __trap();
+        w = ld_relaxed(dec_w + (n_checks & 1));
+      }
+      dec_s = (unsigned)w;
     }
     __syncthreads();
-    const int fb = bad_all;
-    const double err = tot_s[0];
-    if (fb <= 2 * t) {
-      status = OTK_BAD_POTENTIAL;
-      fail_iter = (fb + 1) / 2;
+    trace_mark(A, 2 * t + 2, 7);
+    const unsigned code = dec_s;
+    if ((code >> 1) & 7u) {
+      status = ((code >> 1) & 7u) == 1u ? OTK_BAD_POTENTIAL : OTK_DIVERGED;
+      fail_iter = (int)(code >> 4);
       break;
-    }
-    if (tot_s[4] > 0 || tot_s[5] > 0) {
-      status = OTK_DIVERGED;
-      fail_iter = t;
-      break;
-    }
-    if (fb == 2 * t + 1) {
-      status = OTK_BAD_POTENTIAL;
-      fail_iter = t;
-      break;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0 && n_checks < A.max_checks) {
-      A.errors[n_checks] = err;
-      A.duals[n_checks] = tot_s[2] + tot_s[3] - A.eps_d * (tot_s[1] - 1.0);
     }
     ++n_checks;
-    if (err <= A.threshold && A.probe == 0) {
+    if (code & 1u) {
       converged = 1;
       break;
     }
@@ -556,8 +866,16 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
   }
   grid.sync();  // every CTA's rows of f and g written
   // results (f = f_t of the last completed iteration, g = g_t)
-  for (int i = gtid; i < A.n; i += gstride) A.f_out[i] = f[i];
-  for (int j = gtid; j < A.m; j += gstride) A.g_out[j] = A.g[j];
+  for (int i = gtid; i < A.n; i += gstride) {
+    const float v = f[i];
+    A.f_out[i] = v;
+    if (A.f_host) A.f_host[i] = v;
+  }
+  for (int j = gtid; j < A.m; j += gstride) {
+    const float v = A.g[j];
+    A.g_out[j] = v;
+    if (A.g_host) A.g_host[j] = v;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.state[0] = min(n_checks, A.max_checks);
     A.state[1] = min(t, A.max_iters);
@@ -573,6 +891,31 @@ inline int nv_of(int d) {
   const int nv = (d + 1 + 3) / 4;
   return nv <= 3 ? nv : 5;  // instantiated: 1, 2, 3, 5 float4 per point
 }
+// current device, its cooperative-launch support and opt-in shared memory (cached per host thread)
+inline void device_limits(int *dev, int *coop, int *max_smem) {
+  static thread_local int c_dev = -1, c_coop = 0, c_smem = 0;
+  cudaGetDevice(dev);
+  if (*dev != c_dev) {
+    cudaDeviceGetAttribute(&c_coop, cudaDevAttrCooperativeLaunch, *dev);
+    cudaDeviceGetAttribute(&c_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, *dev);
+    c_dev = *dev;
+  }
+  *coop = c_coop;
+  *max_smem = c_smem;
+}
+// stored-kernel instantiation: dynamic shared memory = the y role's terms,
+// one float2 per (row pair, x column); the points are read from global memory
+// (only the rare exact passes touch them)
+inline int role_rows(int np, int grid) { return std::min(RC, (np + grid - 1) / grid); }
+size_t stored_smem_bytes(int n, int m) {
+  return ((size_t)(RC / 2) * n + (size_t)(RC / 2 - ER_PAIRS) * m) * sizeof(float2);
+}
+// Both roles: one chunk per CTA and every column in one register group.
+bool stored_fits(int n, int m, int grid, size_t max_smem) {
+  if (n > SC * THREADS || m > SC * THREADS) return false;
+  if ((n + grid - 1) / grid > RC || (m + grid - 1) / grid > RC) return false;
+  return stored_smem_bytes(n, m) + 30720 <= max_smem;  // static: the per-role row state (<= 29 KB at NV = 5)
+}
 
 }  // namespace small
 
@@ -585,9 +928,7 @@ bool small_solve_fits(int64_t n, int64_t m, int d) {
   // 2048^2 d = 16 17.4 vs 24.7 us per iteration; 512^2 d = 16 6.5 vs 24.7)
   if (nv >= 3 && (double)n * (double)m * (d + 1) > (double)(1 << 27)) return false;
   int dev = 0, coop = 0, max_smem = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  small::device_limits(&dev, &coop, &max_smem);
   const int64_t per_cta = (int64_t)small::RC * num_sms() * small::KMAX;  // chunks per CTA per role
   if (n > per_cta || m > per_cta) return false;
   if (num_sms() > small::MAX_GRID) return false;
@@ -598,21 +939,38 @@ bool small_solve_fits(int64_t n, int64_t m, int d) {
 int small_solve_launch(const small::Args &A, bool same, bool eucl, cudaStream_t st) {
   using namespace small;
   const int nv = nv_of(A.d);
-  const size_t smem = smem_bytes(A.n, A.m, nv);
-#define OTK_SMALL_K(NV_, SA_, EU_) (void *)solve_small_kernel<NV_, SA_, EU_>
-#define OTK_SMALL_K4(NV_) OTK_SMALL_K(NV_, false, false), OTK_SMALL_K(NV_, false, true), \
-                          OTK_SMALL_K(NV_, true, false), OTK_SMALL_K(NV_, true, true)
-  void *const table[16] = {OTK_SMALL_K4(1), OTK_SMALL_K4(2), OTK_SMALL_K4(3), OTK_SMALL_K4(5)};
+  int dev = 0, coop = 0, max_smem = 0;
+  device_limits(&dev, &coop, &max_smem);
+  const char *env = getenv("OTK_SMALL_STORED");  // A/B: 0 keeps the exps in every half-step
+  const bool stored = !(env && atoi(env) == 0) && stored_fits(A.n, A.m, num_sms(), (size_t)max_smem);
+  const size_t smem = stored ? stored_smem_bytes(A.n, A.m) : smem_bytes(A.n, A.m, nv);
+#define OTK_SMALL_K(NV_, SA_, EU_, ST_) (void *)solve_small_kernel<NV_, SA_, EU_, ST_>
+#define OTK_SMALL_K4(NV_, ST_) OTK_SMALL_K(NV_, false, false, ST_), OTK_SMALL_K(NV_, false, true, ST_), \
+                               OTK_SMALL_K(NV_, true, false, ST_), OTK_SMALL_K(NV_, true, true, ST_)
+  void *const table[32] = {OTK_SMALL_K4(1, false), OTK_SMALL_K4(2, false), OTK_SMALL_K4(3, false),
+                           OTK_SMALL_K4(5, false), OTK_SMALL_K4(1, true),  OTK_SMALL_K4(2, true),
+                           OTK_SMALL_K4(3, true),  OTK_SMALL_K4(5, true)};
 #undef OTK_SMALL_K4
 #undef OTK_SMALL_K
   const int slot = nv == 5 ? 3 : nv - 1;
-  void *kern = table[slot * 4 + same * 2 + eucl];
-  OTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  OTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
-  if (per_sm < 1) {
-    set_error("solve_small: kernel does not fit on an SM");
-    return OTK_ENOTSUP;
+  const int ki = stored * 16 + slot * 4 + same * 2 + eucl;
+  void *kern = table[ki];
+  // attribute + occupancy check once per (device, kernel, shared-memory size), not per solve
+  static thread_local int ok_dev = -1;
+  static thread_local size_t ok_smem[32];
+  if (ok_dev != dev) {
+    for (size_t &v : ok_smem) v = (size_t)-1;
+    ok_dev = dev;
+  }
+  if (ok_smem[ki] != smem) {
+    OTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    OTK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
+    if (per_sm < 1) {
+      set_error("solve_small: kernel does not fit on an SM");
+      return OTK_ENOTSUP;
+    }
+    ok_smem[ki] = smem;
   }
   Args args = A;
   void *params[] = {&args};

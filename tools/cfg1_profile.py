@@ -24,6 +24,10 @@ dev = torch.device("cuda", 0)
 xd, yd = torch.from_numpy(wl.x).to(dev), torch.from_numpy(wl.y).to(dev)
 prob = otk.LinearProblem(otk.PointCloudGeometry(xd, yd), wl.a, wl.b)
 flush = torch.empty(512 * 2 ** 20 // 4, dtype=torch.float32, device=dev)
+t_w = time.perf_counter()  # bring the clocks up before anything is timed
+while time.perf_counter() - t_w < 1.5:
+    flush.fill_(0.0)
+torch.cuda.synchronize()
 for label, kw in (("fixed100", dict(threshold=1e-300, max_iters=100)),
                   ("tolerance", dict(threshold=wl.threshold, max_iters=wl.max_iters))):
     def solve():
@@ -46,3 +50,40 @@ for label, kw in (("fixed100", dict(threshold=1e-300, max_iters=100)),
     wall = (time.perf_counter() - t0) / 50 * 1e3
     print(f"{label}: iterations={out.iterations} bench-step median "
           f"{np.median(ts):.3f} ms (min {np.min(ts):.3f}); wall {wall:.3f} ms/call", flush=True)
+# fixed overhead vs per-iteration cost: wall time of back-to-back solves at several iteration counts
+pts = []
+for its in (10, 50, 100, 200, 400):
+    for _ in range(5):
+        otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=its)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(40):
+        otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=its)
+    pts.append((its, (time.perf_counter() - t0) / 40 * 1e6))
+slope, icpt = np.polyfit([p[0] for p in pts], [p[1] for p in pts], 1)
+print("wall us by iterations:", " ".join(f"{i}:{t:.0f}" for i, t in pts),
+      f"-> {slope:.2f} us per iteration + {icpt:.0f} us per call", flush=True)
+# where the per-call time goes: the native call alone vs the whole Python entry (10-iteration solves)
+from paper_2201_12324_b200 import _native as N  # noqa: E402
+lib = N.lib()
+real = lib.otk_solve_pointcloud
+spent = []
+
+
+def timed(arg):
+    t0 = time.perf_counter()
+    rc = real(arg)
+    spent.append(time.perf_counter() - t0)
+    return rc
+
+
+lib.otk_solve_pointcloud = timed
+try:
+    t0 = time.perf_counter()
+    for _ in range(200):
+        otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=10)
+    whole = (time.perf_counter() - t0) / 200 * 1e6
+finally:
+    lib.otk_solve_pointcloud = real
+print(f"10-iteration solve: {whole:.1f} us per call, of which the native call {np.median(spent) * 1e6:.1f} us "
+      f"(Python around it {whole - np.median(spent) * 1e6:.1f} us)", flush=True)
