@@ -623,3 +623,43 @@ def test_batched_cluster_solver_edge_cases_match_oracle(otk, monkeypatch, domain
         assert outs.iterations[k] == ref["iterations"]
         assert rel_inf(outs.f[k], ref["f"]) <= POT_TOL, (k, rel_inf(outs.f[k], ref["f"]))
         assert rel_inf(outs.g[k], ref["g"]) <= POT_TOL, (k, rel_inf(outs.g[k], ref["g"]))
+
+
+@pytest.mark.parametrize("d,cost_fn", [(3, "sqeucl"), (6, "sqeucl"), (12, "sqeucl"), (3, "eucl")])
+def test_persistent_small_solve_stored_kernel_edge_cases(otk, monkeypatch, d, cost_fn):
+    """The stored-kernel half-steps of the persistent small solve (exps taken
+    once, FP32 matrix-vector half-steps, csrc/solve_small.cu) on the cases that
+    send a CTA back to its exact passes or sit at the edge of the scaling
+    window: a far-off warm start (columns drift > 40 bits -> rebuilds), a tight
+    eps, zero weights on both sides (-inf potentials), one far outlier point --
+    against the float64 oracle and against the same kernel with the stored
+    path switched off (OTK_SMALL_STORED=0)."""
+    rng = np.random.default_rng(300 + d)
+    n, m = 1500, 1333
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    y = (rng.standard_normal((m, d)) + 0.3).astype(np.float32)
+    y[5] = 4.0
+    a = rng.uniform(0.5, 1.5, n)
+    b = rng.uniform(0.5, 1.5, m)
+    a[::11] = 0.0
+    b[::7] = 0.0
+    a /= a.sum()
+    b /= b.sum()
+    geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64), cost_fn=cost_fn)
+    eps = 0.02 * float(np.mean(geom64.cost_matrix()))
+    g0 = (rng.standard_normal(m) * 60 * eps).astype(np.float32)
+    ref = oracle.sinkhorn(geom64, a, b, eps, threshold=1e-300, max_iters=40, g_init=g0.astype(np.float64))
+
+    def run():
+        prob = otk.LinearProblem(otk.PointCloudGeometry(x, y, cost_fn=cost_fn), a, b)
+        return otk.solve_sinkhorn(prob, eps, threshold=1e-300, max_iters=40, g_init=g0)
+    stored, stored2 = run(), run()
+    monkeypatch.setenv("OTK_SMALL_STORED", "0")
+    plain = run()
+    for out in (stored, plain):
+        assert out.iterations == ref["iterations"] and len(out.errors) == len(ref["errors"])
+        assert rel_inf(out.f, ref["f"]) <= POT_TOL, rel_inf(out.f, ref["f"])
+        assert rel_inf(out.g, ref["g"]) <= POT_TOL, rel_inf(out.g, ref["g"])
+        np.testing.assert_allclose(out.dual_trace, ref["dual_trace"], rtol=1e-5)
+    assert np.array_equal(stored.f, stored2.f) and np.array_equal(stored.g, stored2.g)
+    assert rel_inf(stored.f, plain.f) <= 1e-5 and rel_inf(stored.g, plain.g) <= 1e-5
