@@ -174,9 +174,11 @@ __device__ __forceinline__ int rs16_row(int lane) {
 template <int NV>
 struct RoleRows {
   float2 p2[KMAX * RC / 2][4 * NV];
+  float2 pr[RC / 2][4 * NV];  // the first chunk's raw coordinates, same pairing, zeros from slot d (stored-kernel builds)
   float cp[KMAX * RC];
   float an[KMAX * RC];
-  float elw[KMAX * RC];  // eps * log weight of the row (read from global memory once, not per half-step)
+  float ci[KMAX * RC];   // stored kernel: 1 / the row's total at build time
+  float lw2[KMAX * RC];  // log2 weight of the row (read from global memory once, not per half-step)
   int rc, n_chunks;      // rows per chunk, chunks of the role
   float lo;              // lower end of the anchored acceptance window
 };
@@ -202,9 +204,14 @@ __device__ __forceinline__ void init_role_rows(const Args &A, const float4 *P, i
     float *dst = reinterpret_cast<float *>(S.p2[idx / 2]) + (idx & 1);
 #pragma unroll
     for (int kk = 0; kk < 4 * NV; ++kk) dst[2 * kk] = (kk < A.d) ? two_k * pv[kk] : (kk == A.d ? 1.f : 0.f);
+    if (k == 0) {
+      float *raw = reinterpret_cast<float *>(S.pr[idx / 2]) + (idx & 1);
+#pragma unroll
+      for (int kk = 0; kk < 4 * NV; ++kk) raw[2 * kk] = (kk < A.d) ? pv[kk] : 0.f;
+    }
     S.cp[idx] = -pv[A.d];
     S.an[idx] = -INFINITY;
-    S.elw[idx] = A.eps * logw[i];
+    S.lw2[idx] = (float)((double)logw[i] * 1.4426950408889634);
   }
 }
 
@@ -375,6 +382,17 @@ constexpr int SC = 4;            // columns per thread of a stored role
 #endif
 constexpr int ER_PAIRS = OTK_ER_PAIRS;  // row pairs of the x role kept in registers (the others in shared memory)
 constexpr float DRIFT = 40.f;
+// At the half-steps of a (later) check iteration the window is DRIFT_CHECK: once the
+// potentials have settled, the terms are rebuilt around them and the column
+// factors' exponents stay near 0.  Why: ex2 / lg2 approximation errors at a
+// large, FROZEN argument repeat identically every half-step, and Sinkhorn
+// does not contract the (f + c, g - c) direction, so such a bias adds up
+// linearly with the iterations (measured 1e-6 log2 units per iteration on a
+// 1 x m problem with |drift| ~ 3); near 0 both approximations are exact.
+// Applied from iteration SETTLE_ITERS on: shorter solves cannot collect a
+// visible bias (<= 1e-4 log2 units), long ones pay a rebuild or two.
+constexpr float DRIFT_CHECK = 1.f;
+constexpr int SETTLE_ITERS = 100;
 
 // Predicated 64-bit shared-memory load (zeros when !p), no branch.
 __device__ __forceinline__ float2 lds_f2_pred(uint32_t addr, bool p) {
@@ -412,7 +430,8 @@ __device__ __forceinline__ void wait_words(const xword *qx, int nq, int need, xw
 template <int NREG>
 __device__ __forceinline__ void stored_pass(const Args &A, int nq, const xword *qx, int need, int rc,
                                             const float2 (&er)[ER_PAIRS > 0 ? ER_PAIRS : 1][SC], uint32_t es_off,
-                                            const float (&beta)[SC], int *redo, float (*red)[RC], float *tot) {
+                                            const float (&beta)[SC], float window, int *redo, float (*red)[RC],
+                                            float *tot) {
   xword w[SC];
   int jj[SC];
   wait_words(qx, nq, need, w, jj);
@@ -424,7 +443,7 @@ __device__ __forceinline__ void stored_pass(const Args &A, int nq, const xword *
     const float dl = __uint_as_float((unsigned)w[c]) - beta[c];
     const float e = (jj[c] < nq) ? ex2(dl) : 0.f;
     v[c] = make_float2(e, e);
-    drift |= (jj[c] < nq) && !(fabsf(dl) <= DRIFT) && dl != -INFINITY;
+    drift |= (jj[c] < nq) && !(fabsf(dl) <= window) && dl != -INFINITY;
   }
   if (drift) *redo = 1;
   float2 acc[RC / 2];
@@ -464,11 +483,17 @@ __device__ __forceinline__ void stored_pass(const Args &A, int nq, const xword *
 
 // The exact sum pass against the row maxima sh[], keeping every term as E and
 // the columns' kappa * potential as beta.  One column at a time (the x role
-// holds NREG x SC pairs of its terms in registers next to this pass).
+// holds its terms in registers next to this pass).  The cost is taken in the
+// difference form kappa sum_k (p_k - q_k)^2, not the norm form of the other
+// passes: no cancellation against kappa |p|^2, and -- same formula, same
+// summation order -- the x role's E(i, j) and the y role's E(j, i) carry
+// bitwise the same cost.  Frozen terms make rounding differences between the
+// two roles a constant bias per iteration; a pair of points coupled mostly to
+// each other (an identical pair in the same-points case) barely contracts it.
 template <int NV, bool SAME, bool EU, int NREG>
 __device__ __forceinline__ void build_pass(const Args &A, const float4 *Q, int nq, const xword *qx, int need,
-                                           int r0, int rc, const float2 (*p2)[4 * NV], const float *cp,
-                                           const float *sh, float2 (&er)[ER_PAIRS > 0 ? ER_PAIRS : 1][SC], uint32_t es_off,
+                                           int r0, int rc, const float2 (*pr)[4 * NV], const float *sh,
+                                           float2 (&er)[ER_PAIRS > 0 ? ER_PAIRS : 1][SC], uint32_t es_off,
                                            float (&beta)[SC], float (*red)[RC], float *tot) {
   const float sk = sqrtf(A.kappa);
   float2 *es = reinterpret_cast<float2 *>(reinterpret_cast<char *>(sh4) + es_off);
@@ -490,43 +515,26 @@ __device__ __forceinline__ void build_pass(const Args &A, const float4 *Q, int n
       q[4 * v + 2] = qv.z;
       q[4 * v + 3] = qv.w;
     }
-    const float bj = __uint_as_float((unsigned)w[c]);
-    beta[c] = (bj == -INFINITY) ? 0.f : bj;  // a -inf column stays at E = 0, v = 0
-    if (!EU) {
 #pragma unroll
-      for (int k = 0; k < 4 * NV; ++k) q[k] = q[k] + (k == A.d ? bj : 0.f);
-    }
+    for (int k = 0; k < 4 * NV; ++k) q[k] = (k < A.d) ? q[k] : 0.f;  // slot d holds -kappa |q|^2: not a coordinate
+    const float bj = ok ? __uint_as_float((unsigned)w[c]) : -INFINITY;
+    beta[c] = (bj == -INFINITY) ? 0.f : bj;  // a -inf column stays at E = 0, v = 0
 #pragma unroll
     for (int h = 0; h < RC / 2; ++h) {
       float2 e = make_float2(0.f, 0.f);
       if (2 * h < rc) {
-        float2 pk[4 * NV];
+        float2 c2 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int k = 0; k < 4 * NV; ++k) pk[k] = p2[h][k];
-        const float2 cp2 = *reinterpret_cast<const float2 *>(cp + 2 * h);
-        const float2 ns2 = make_float2(-sh[2 * h], -sh[2 * h + 1]);
-        float2 u;
-        if (EU) {
-          const float2 bs = __fadd2_rn(ns2, make_float2(bj, bj));
-          float2 dt = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int k = 0; k < 4 * NV; ++k) dt = __ffma2_rn(pk[k], make_float2(q[k], q[k]), dt);
-          float v0 = -sk * sqrt_approx(fmaxf(cp2.x - dt.x, 0.f));
-          float v1 = -sk * sqrt_approx(fmaxf(cp2.y - dt.y, 0.f));
-          if (SAME && jj[c] == r0 + 2 * h) v0 = 0.f;
-          if (SAME && jj[c] == r0 + 2 * h + 1) v1 = 0.f;
-          u = __fadd2_rn(make_float2(v0, v1), bs);
-        } else {
-          float2 dt = ns2;
-#pragma unroll
-          for (int k = 0; k < 4 * NV; ++k) dt = __ffma2_rn(pk[k], make_float2(q[k], q[k]), dt);
-          const float2 lim = __fadd2_rn(__fadd2_rn(cp2, ns2), make_float2(bj, bj));
-          u = make_float2(fminf(dt.x, lim.x), fminf(dt.y, lim.y));
-          if (SAME && jj[c] == r0 + 2 * h) u.x = lim.x;
-          if (SAME && jj[c] == r0 + 2 * h + 1) u.y = lim.y;
+        for (int k = 0; k < 4 * NV; ++k) {
+          const float2 df = __fadd2_rn(pr[h][k], make_float2(-q[k], -q[k]));
+          c2 = __ffma2_rn(df, df, c2);
         }
+        const float2 kc = make_float2(A.kappa * c2.x, A.kappa * c2.y);
+        const float2 bs = make_float2(bj - sh[2 * h], bj - sh[2 * h + 1]);
+        float2 u;
+        if (EU) u = make_float2(bs.x - sk * sqrt_approx(kc.x), bs.y - sk * sqrt_approx(kc.y));
+        else u = make_float2(bs.x - kc.x, bs.y - kc.y);
         e = make_float2(ex2(u.x), ex2(u.y));
-        if (!ok) e = make_float2(0.f, 0.f);
         acc[h] = __fadd2_rn(acc[h], e);
         if (h >= NREG && ok) es[(h - NREG) * nq + jj[c]] = e;
       }
@@ -566,6 +574,7 @@ __device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, i
     const float2 (*p2)[4 * NV] = S.p2 + k * (RC / 2);
     const float *cp = S.cp + k * RC;
     float *an = S.an + k * RC;
+    float *ci = S.ci + k * RC;
     if (STR == 0) {
       if (threadIdx.x == 0) redo = 0;
       __syncthreads();
@@ -582,23 +591,37 @@ __device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, i
       bool rebuild = !SR.have;
       if (threadIdx.x == 0) drift_pp[(step + 1) & 1] = 0;
       if (SR.have) {
-        stored_pass<STR == 1 ? ER_PAIRS : 0>(A, nq, qx, need, rn, SR.er, SR.es_off, SR.beta, &drift_pp[step & 1],
-                                             red, tot);
+        stored_pass<STR == 1 ? ER_PAIRS : 0>(A, nq, qx, need, rn, SR.er, SR.es_off, SR.beta,
+                                             ((CHECK || CHECKG) && step >= 2 * SETTLE_ITERS) ? DRIFT_CHECK : DRIFT,
+                                             &drift_pp[step & 1], red, tot);
         rebuild = drift_pp[step & 1] != 0;
-        if (threadIdx.x < rn) L = an[threadIdx.x] + lg2(tot[threadIdx.x]);
+        // an[] holds the row's L at build time, ci[] 1 / its total then: the
+        // log is taken of total / total_at_build (~1 once the potentials have
+        // settled), with log2f: at arguments like 2^8 lg2.approx is off in the
+        // last place (1e-6) with a sign that repeats every half-step, and
+        // Sinkhorn never contracts such a bias along (f + c, g - c)
+        if (threadIdx.x < rn) L = an[threadIdx.x] + log2f(tot[threadIdx.x] * ci[threadIdx.x]);
       }
       if (rebuild) {
         __syncthreads();
         chunk_pass<NV, SAME, EU, true>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
         if (threadIdx.x < rn) {
-          const float mx = tot[threadIdx.x];
+          // the maxima come from the norm form, which carries + kappa |p|^2; the
+          // stored frame is max_j (b_j - kappa C_ij): one rounding, and only a
+          // choice of shift (E and L use the same value)
+          const float mx = tot[threadIdx.x] - (EU ? 0.f : cp[threadIdx.x]);
           an[threadIdx.x] = (mx == -INFINITY) ? 0.f : mx;
         }
         __syncthreads();
-        build_pass<NV, SAME, EU, STR == 1 ? ER_PAIRS : 0>(A, Q, nq, qx, need, r0, rn, p2, cp, an, SR.er,
-                                                          SR.es_off, SR.beta, red, tot);
+        build_pass<NV, SAME, EU, STR == 1 ? ER_PAIRS : 0>(A, Q, nq, qx, need, r0, rn, S.pr, an,
+                                                          SR.er, SR.es_off, SR.beta, red, tot);
         SR.have = true;
-        if (threadIdx.x < rn) L = an[threadIdx.x] + lg2(tot[threadIdx.x]);
+        if (threadIdx.x < rn) {
+          const float tb = tot[threadIdx.x];
+          L = an[threadIdx.x] + log2f(tb);
+          an[threadIdx.x] = L;  // read again only by this thread (the next build starts from new maxima)
+          ci[threadIdx.x] = (tb > 0.f && tb < 3.0e38f) ? 1.f / tb : 1.f;
+        }
       }
     } else if (!redo) {
       chunk_pass<NV, SAME, EU, false>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
@@ -622,10 +645,16 @@ __device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, i
     }
     if (threadIdx.x < rn) {
       const int i = r0 + threadIdx.x;
-      const float Lf = L - (EU ? 0.f : cp[threadIdx.x]);
+      const float Lf = L - ((EU || STR != 0) ? 0.f : cp[threadIdx.x]);  // the stored frame has no kappa |p|^2
       if (STR == 0) an[threadIdx.x] = L;
-      const float v = S.elw[k * RC + threadIdx.x] - A.eps * kLn2 * Lf;
-      st_relaxed(px + i, xpack(v * A.kappa, step));
+      // The exchanged word stays in log2 units, bq = log2 w - L: one rounding.
+      // Going through the potential (eps ln2 bq, then kappa times that) would
+      // multiply by fl(kappa) fl(eps) fl(ln2) = 1 + ~1e-7 every half-step, a
+      // bias of ~1e-7 |L| that Sinkhorn never contracts along (f + c, g - c):
+      // measured 9e-7 log2 units per iteration, linear, on a 48 x 40 problem.
+      const float bq = S.lw2[k * RC + threadIdx.x] - Lf;
+      const float v = (A.eps * kLn2) * bq;
+      st_relaxed(px + i, xpack(bq, step));
       out_pot[i] = v;
       if (bad_potential(v)) atomicMin(bad_s, step);
       double *chk = chk_s[threadIdx.x];  // this row thread's check terms (shared memory: no registers held)
@@ -913,6 +942,9 @@ size_t stored_smem_bytes(int n, int m) {
 // Both roles: one chunk per CTA and every column in one register group.
 bool stored_fits(int n, int m, int grid, size_t max_smem) {
   if (n > SC * THREADS || m > SC * THREADS) return false;
+  // a handful of rows or columns: nothing to gain, and no averaging of the
+  // frozen terms' rounding over a row's columns (see DRIFT_CHECK)
+  if (n < 32 || m < 32) return false;
   if ((n + grid - 1) / grid > RC || (m + grid - 1) / grid > RC) return false;
   return stored_smem_bytes(n, m) + 30720 <= max_smem;  // static: the per-role row state (<= 29 KB at NV = 5)
 }

@@ -141,12 +141,17 @@ def test_fixed_iteration_runs(otk, name):
     wl = getattr(workloads, str(fx["gen"]))(**json.loads(str(fx["kw"])))
     prob = otk.LinearProblem(otk.PointCloudGeometry(wl.x, wl.y), wl.a, wl.b)
     out = otk.solve_sinkhorn(prob, float(fx["eps"]), threshold=1e-300, max_iters=int(fx["iters"]))
-    # float32 iterates can reach an exact fixed point (marginal error 0.0 <= 1e-300)
-    assert out.iterations == int(fx["iters"])
-    assert not out.converged or out.errors[-1] == 0.0
+    # float32 iterates can reach an exact fixed point (f_{t+1} == f_t bitwise: marginal error
+    # 0.0 <= 1e-300, so the loop stops there); every later iterate would be the same
+    # potentials, so they still compare with the reference's at the full count
+    if out.converged:
+        assert out.errors[-1] == 0.0 and out.iterations <= int(fx["iters"])
+    else:
+        assert out.iterations == int(fx["iters"])
     assert rel_inf(out.f, fx["f"]) <= POT_TOL, rel_inf(out.f, fx["f"])
     assert rel_inf(out.g, fx["g"]) <= POT_TOL, rel_inf(out.g, fx["g"])
-    np.testing.assert_allclose(out.dual_trace, fx["dual_trace"], rtol=COST_TOL)
+    k = len(out.dual_trace)
+    np.testing.assert_allclose(out.dual_trace, fx["dual_trace"][:k], rtol=COST_TOL)
     cost = otk.reg_ot_cost(out, prob)
     assert abs(cost.transport_cost / float(fx["transport"]) - 1) <= COST_TOL
     assert abs(cost.dual_objective / float(fx["dual"]) - 1) <= COST_TOL
@@ -663,3 +668,29 @@ def test_persistent_small_solve_stored_kernel_edge_cases(otk, monkeypatch, d, co
         np.testing.assert_allclose(out.dual_trace, ref["dual_trace"], rtol=1e-5)
     assert np.array_equal(stored.f, stored2.f) and np.array_equal(stored.g, stored2.g)
     assert rel_inf(stored.f, plain.f) <= 1e-5 and rel_inf(stored.g, plain.g) <= 1e-5
+
+
+def test_persistent_small_solve_stored_kernel_long_run_has_no_gauge_drift(otk, monkeypatch):
+    """Sinkhorn does not contract the (f + c, g - c) direction, so a bias that
+    repeats identically every half-step adds up linearly with the iterations.
+    The stored-kernel half-steps evaluate ex2 / lg2 at frozen arguments; the
+    tighter drift window at later checks (DRIFT_CHECK, csrc/solve_small.cu)
+    rebuilds the terms once the potentials have settled.  600 forced
+    iterations of a small, large-eps problem (few columns to average over,
+    potentials of a few bits): stored and plain kernels against the oracle."""
+    rng = np.random.default_rng(5)
+    n, m, d = 48, 40, 3
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    y = (rng.standard_normal((m, d)) + 0.5).astype(np.float32)
+    geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64))
+    eps = 0.5 * float(np.mean(geom64.cost_matrix()))
+    ref = oracle.sinkhorn(geom64, None, None, eps, threshold=1e-300, max_iters=600)
+    prob = otk.LinearProblem(otk.PointCloudGeometry(x, y))
+    stored = otk.solve_sinkhorn(prob, eps, threshold=1e-300, max_iters=600)
+    monkeypatch.setenv("OTK_SMALL_STORED", "0")
+    plain = otk.solve_sinkhorn(prob, eps, threshold=1e-300, max_iters=600)
+    for out in (stored, plain):
+        # an exact float32 fixed point (marginal error 0.0) may end the loop early: same potentials
+        assert out.iterations == 600 or (out.converged and out.errors[-1] == 0.0)
+        assert rel_inf(out.f, ref["f"]) <= 2e-5, rel_inf(out.f, ref["f"])
+        assert rel_inf(out.g, ref["g"]) <= 2e-5, rel_inf(out.g, ref["g"])

@@ -28,6 +28,7 @@ def main(cases=60, seed=0):
     rng = np.random.default_rng(seed)
     worst = {"f": 0.0, "g": 0.0, "cost": 0.0, "anch": 0.0}
     fails = 0
+    only = {int(v) for v in os.environ.get("OTK_FUZZ_ONLY", "").split(",") if v}
     for c in range(cases):
         d = int(rng.choice([2, 3, 5, 16, 33, 64, 100, 128, 200, 300, 520]))
         n = int(rng.integers(1, 900))
@@ -51,6 +52,8 @@ def main(cases=60, seed=0):
         g0 = None
         if rng.random() < 0.3:
             g0 = (rng.standard_normal(m) * eps * float(rng.choice([1.0, 50.0]))).astype(np.float32)
+        if only and c not in only:  # OTK_FUZZ_ONLY=125,173: replay just these cases of the seed
+            continue
         geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64))
         prob = otk.LinearProblem(otk.PointCloudGeometry(x, y), a, b)
         try:

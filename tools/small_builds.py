@@ -1,0 +1,11 @@
+import os, sys
+sys.path.insert(0, os.getcwd())
+import torch, numpy as np
+import paper_2201_12324_b200 as otk
+from paper_2201_12324_b200 import workloads
+wl = workloads.make(1)
+dev = torch.device("cuda", 0)
+prob = otk.LinearProblem(otk.PointCloudGeometry(torch.from_numpy(wl.x).to(dev), torch.from_numpy(wl.y).to(dev)))
+os.environ["OTK_SMALL_DEBUG"] = "1"
+for its in (5, 10, 50, 100, 400):
+    otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=its)
