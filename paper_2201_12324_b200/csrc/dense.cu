@@ -173,7 +173,9 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(
     const int64_t o = (int64_t)b * n + i;
     float v = (mode == OTK_FIN_SOLVER) ? eps * base[o] - eps * kLn2 * L : base[o] + eps * kLn2 * L;
     out[o] = v;
-    if (out_bias != nullptr) out_bias[o] = v * kappa_next[b];
+    if (out_bias != nullptr)
+      out_bias[o] = (mode == OTK_FIN_SOLVER) ? next_bias(base[o], L, eps, kappa_next[b])
+                                              : v * kappa_next[b];
     if (first_bad != nullptr && bad_potential(v)) atomicMin(first_bad + b, step);
   }
 }
@@ -265,7 +267,9 @@ __global__ void __launch_bounds__(128 * DCOL_GROUPS) dense_cols_kernel(
       const int64_t o = (int64_t)b * m + j;
       float v = (mode == OTK_FIN_SOLVER) ? eps * base[o] - eps * kLn2 * L : base[o] + eps * kLn2 * L;
       out[o] = v;
-      if (out_bias != nullptr) out_bias[o] = v * kappa_next[b];
+      if (out_bias != nullptr)
+        out_bias[o] = (mode == OTK_FIN_SOLVER) ? next_bias(base[o], L, eps, kappa_next[b])
+                                                : v * kappa_next[b];
       if (first_bad != nullptr && bad_potential(v)) atomicMin(first_bad + b, step);
     }
   }

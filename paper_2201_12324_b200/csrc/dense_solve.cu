@@ -139,7 +139,7 @@ __device__ void rows_half(const float *__restrict__ Cb, int n, int m, const floa
       if (lane == 0 && i < n) {
         const float v = eps * lw[i] - eps * kLn2 * st[r].value();
         out[i] = v;
-        bx[i] = v * kappa;
+        bx[i] = next_bias(lw[i], st[r].value(), eps, kappa);
         if (bad_potential(v)) atomicMin(fbad, step);
         if (CHECK) {
           const double fp = fprev[i], ai = a[i];
@@ -224,7 +224,7 @@ __device__ void cols_half(const float *__restrict__ Cb, int n, int m, const floa
       const int jg = cb0 + jj;
       const float v = eps * lw[jg] - eps * kLn2 * st.value();
       out[jg] = v;
-      by[jg] = v * kappa;
+      by[jg] = next_bias(lw[jg], st.value(), eps, kappa);
       if (bad_potential(v)) atomicMin(fbad, step);
     }
     __syncthreads();
@@ -508,7 +508,7 @@ __device__ void rows_local(const float *Cs, int rb, int re, int m, const float *
     if (gl == 0 && i < re) {
       const float v = eps * lw[i] - eps * kLn2 * st.value();
       out[i] = v;
-      bx[i] = v * kappa;
+      bx[i] = next_bias(lw[i], st.value(), eps, kappa);
       if (bad_potential(v)) atomicMin(fbad, step);
       if (CHECK) {
         const double fp = fprev[i], ai = a[i];
@@ -729,9 +729,10 @@ __device__ void rows_pass_scaled(const float *Ks, int rows, int m, const float *
       const float rh = rho[i];
       const float L = rh + ((t > 0.f) ? lg2(t) : ((t != t) ? t : -INFINITY));
       const float v_ = eps * lw[i] - eps * kLn2 * L;
+      const float bq = next_bias(lw[i], L, eps, kappa);
       out[i] = v_;
-      bx[i] = v_ * kappa;
-      uw[i] = (rh > -INFINITY) ? ex2(v_ * kappa + rh) : 0.f;
+      bx[i] = bq;
+      uw[i] = (rh > -INFINITY) ? ex2(bq + rh) : 0.f;
       if (bad_potential(v_)) atomicMin(fbad, step);
     }
   }
@@ -974,7 +975,7 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
         }
         const float gv = eps * lb[j] - eps * kLn2 * L;
         g[j] = gv;
-        by[j] = gv * kappa;
+        by[j] = next_bias(lb[j], L, eps, kappa);
         if (bad_potential(gv)) atomicMin(&fbad, 2 * t + 1);
       }
       cpar ^= 1;

@@ -184,7 +184,8 @@ __device__ __forceinline__ void finalize_row(const FinArgs &F, int64_t i, float 
   const float c = F.eps * kLn2;
   const float v = (F.mode == OTK_FIN_SOLVER) ? F.eps * F.base[i] - c * L : F.base[i] + c * L;
   F.out[i] = v;
-  if (F.out_bias != nullptr) F.out_bias[i] = v * F.kappa_next;
+  if (F.out_bias != nullptr)
+    F.out_bias[i] = (F.mode == OTK_FIN_SOLVER) ? next_bias(F.base[i], L, F.eps, F.kappa_next) : v * F.kappa_next;
   if (F.first_bad != nullptr && bad_potential(v)) atomicMin(F.first_bad, F.step);
 }
 

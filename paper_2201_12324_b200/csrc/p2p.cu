@@ -121,7 +121,8 @@ __global__ void exchange_combine_kernel(char *local, int world, int64_t m, unsig
   const float c = eps * kLn2;
   const float v = (mode == OTK_FIN_SOLVER) ? eps * base[i] - c * L : base[i] + c * L;
   out[i] = v;
-  if (out_bias != nullptr) out_bias[i] = v * kappa_next;
+  if (out_bias != nullptr)
+    out_bias[i] = (mode == OTK_FIN_SOLVER) ? next_bias(base[i], L, eps, kappa_next) : v * kappa_next;
   if (first_bad != nullptr && bad_potential(v)) atomicMin(first_bad, step);
 }
 
