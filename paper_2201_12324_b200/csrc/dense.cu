@@ -171,10 +171,11 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(
   if (lane == 0) {
     const float L = st.value();
     const int64_t o = (int64_t)b * n + i;
-    float v = (mode == OTK_FIN_SOLVER) ? eps * base[o] - eps * kLn2 * L : base[o] + eps * kLn2 * L;
+    const float bo = base[o];
+    float v = (mode == OTK_FIN_SOLVER) ? eps * bo - eps * kLn2 * L : bo + eps * kLn2 * L;
     out[o] = v;
     if (out_bias != nullptr)
-      out_bias[o] = (mode == OTK_FIN_SOLVER) ? next_bias(base[o], L, eps, kappa_next[b])
+      out_bias[o] = (mode == OTK_FIN_SOLVER) ? next_bias(bo, L, eps, kappa_next[b])
                                               : v * kappa_next[b];
     if (first_bad != nullptr && bad_potential(v)) atomicMin(first_bad + b, step);
   }
@@ -265,10 +266,11 @@ __global__ void __launch_bounds__(128 * DCOL_GROUPS) dense_cols_kernel(
     if (j < m) {
       const float L = st.value();
       const int64_t o = (int64_t)b * m + j;
-      float v = (mode == OTK_FIN_SOLVER) ? eps * base[o] - eps * kLn2 * L : base[o] + eps * kLn2 * L;
+      const float bo = base[o];
+      float v = (mode == OTK_FIN_SOLVER) ? eps * bo - eps * kLn2 * L : bo + eps * kLn2 * L;
       out[o] = v;
       if (out_bias != nullptr)
-        out_bias[o] = (mode == OTK_FIN_SOLVER) ? next_bias(base[o], L, eps, kappa_next[b])
+        out_bias[o] = (mode == OTK_FIN_SOLVER) ? next_bias(bo, L, eps, kappa_next[b])
                                                 : v * kappa_next[b];
       if (first_bad != nullptr && bad_potential(v)) atomicMin(first_bad + b, step);
     }

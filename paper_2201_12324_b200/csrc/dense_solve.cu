@@ -137,9 +137,10 @@ __device__ void rows_half(const float *__restrict__ Cb, int n, int m, const floa
       }
       const int i = i0 + r;
       if (lane == 0 && i < n) {
-        const float v = eps * lw[i] - eps * kLn2 * st[r].value();
+        const float lwi = lw[i], Lr = st[r].value();
+        const float v = eps * lwi - eps * kLn2 * Lr;
         out[i] = v;
-        bx[i] = next_bias(lw[i], st[r].value(), eps, kappa);
+        bx[i] = next_bias(lwi, Lr, eps, kappa);
         if (bad_potential(v)) atomicMin(fbad, step);
         if (CHECK) {
           const double fp = fprev[i], ai = a[i];
@@ -222,9 +223,10 @@ __device__ void cols_half(const float *__restrict__ Cb, int n, int m, const floa
       for (int g = 1; g < groups; ++g)
         st.merge(part[(g * pstride + jj) * 2], part[(g * pstride + jj) * 2 + 1]);
       const int jg = cb0 + jj;
-      const float v = eps * lw[jg] - eps * kLn2 * st.value();
+      const float lwj = lw[jg], Lc = st.value();
+      const float v = eps * lwj - eps * kLn2 * Lc;
       out[jg] = v;
-      by[jg] = next_bias(lw[jg], st.value(), eps, kappa);
+      by[jg] = next_bias(lwj, Lc, eps, kappa);
       if (bad_potential(v)) atomicMin(fbad, step);
     }
     __syncthreads();
@@ -506,9 +508,10 @@ __device__ void rows_local(const float *Cs, int rb, int re, int m, const float *
       st.merge(m2, s2);
     }
     if (gl == 0 && i < re) {
-      const float v = eps * lw[i] - eps * kLn2 * st.value();
+      const float lwi = lw[i], Lr = st.value();
+      const float v = eps * lwi - eps * kLn2 * Lr;
       out[i] = v;
-      bx[i] = next_bias(lw[i], st.value(), eps, kappa);
+      bx[i] = next_bias(lwi, Lr, eps, kappa);
       if (bad_potential(v)) atomicMin(fbad, step);
       if (CHECK) {
         const double fp = fprev[i], ai = a[i];
@@ -728,8 +731,9 @@ __device__ void rows_pass_scaled(const float *Ks, int rows, int m, const float *
     if ((lane & 7) == 0 && i < rows) {
       const float rh = rho[i];
       const float L = rh + ((t > 0.f) ? lg2(t) : ((t != t) ? t : -INFINITY));
-      const float v_ = eps * lw[i] - eps * kLn2 * L;
-      const float bq = next_bias(lw[i], L, eps, kappa);
+      const float lwi = lw[i];
+      const float v_ = eps * lwi - eps * kLn2 * L;
+      const float bq = next_bias(lwi, L, eps, kappa);
       out[i] = v_;
       bx[i] = bq;
       uw[i] = (rh > -INFINITY) ? ex2(bq + rh) : 0.f;
@@ -973,9 +977,10 @@ __global__ void __launch_bounds__(THREADS, 1) dense_cluster_solve_kernel(Args A)
           for (int r = 0; r < CL; ++r) acc += ex2(v[r] - mx);
           L = mx + lg2(acc);
         }
-        const float gv = eps * lb[j] - eps * kLn2 * L;
+        const float lbj = lb[j];  // one read (a second one after the store to g would be a global round trip)
+        const float gv = eps * lbj - eps * kLn2 * L;
         g[j] = gv;
-        by[j] = next_bias(lb[j], L, eps, kappa);
+        by[j] = next_bias(lbj, L, eps, kappa);
         if (bad_potential(gv)) atomicMin(&fbad, 2 * t + 1);
       }
       cpar ^= 1;

@@ -181,11 +181,11 @@ __device__ __forceinline__ void finalize_row(const FinArgs &F, int64_t i, float 
     F.out[i] = L;
     return;
   }
-  const float c = F.eps * kLn2;
-  const float v = (F.mode == OTK_FIN_SOLVER) ? F.eps * F.base[i] - c * L : F.base[i] + c * L;
+  const float c = F.eps * kLn2, bi = F.base[i];
+  const float v = (F.mode == OTK_FIN_SOLVER) ? F.eps * bi - c * L : bi + c * L;
   F.out[i] = v;
   if (F.out_bias != nullptr)
-    F.out_bias[i] = (F.mode == OTK_FIN_SOLVER) ? next_bias(F.base[i], L, F.eps, F.kappa_next) : v * F.kappa_next;
+    F.out_bias[i] = (F.mode == OTK_FIN_SOLVER) ? next_bias(bi, L, F.eps, F.kappa_next) : v * F.kappa_next;
   if (F.first_bad != nullptr && bad_potential(v)) atomicMin(F.first_bad, F.step);
 }
 

@@ -118,11 +118,11 @@ __global__ void exchange_combine_kernel(char *local, int world, int64_t m, unsig
     out[i] = L;
     return;
   }
-  const float c = eps * kLn2;
-  const float v = (mode == OTK_FIN_SOLVER) ? eps * base[i] - c * L : base[i] + c * L;
+  const float c = eps * kLn2, bi = base[i];
+  const float v = (mode == OTK_FIN_SOLVER) ? eps * bi - c * L : bi + c * L;
   out[i] = v;
   if (out_bias != nullptr)
-    out_bias[i] = (mode == OTK_FIN_SOLVER) ? next_bias(base[i], L, eps, kappa_next) : v * kappa_next;
+    out_bias[i] = (mode == OTK_FIN_SOLVER) ? next_bias(bi, L, eps, kappa_next) : v * kappa_next;
   if (first_bad != nullptr && bad_potential(v)) atomicMin(first_bad, step);
 }
 
