@@ -16,6 +16,15 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file gpurun_out/${P}_launches_cfg4.csv python bench.py --steps 2 --warmup 1 > gpurun_out/${P}_ncu_launches.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:lse_tc -s 1 -c 1 \
   -o gpurun_out/${P}_lse_tc_cfg4 python tools/prof_half_step.py --config 4 --reps 3 > gpurun_out/${P}_ncu_full.log 2>&1
+# cfg1 (persistent small solve) and cfg3 (K3c): launch list of the bench command + one full capture each
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --log-file gpurun_out/${P}_launches_cfg1.csv python bench.py --config 1 --steps 2 --warmup 1 > gpurun_out/${P}_ncu_launches_cfg1.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:solve_small -s 2 -c 1 \
+  -o gpurun_out/${P}_solve_small_cfg1 python tools/small_builds.py > gpurun_out/${P}_ncu_full_cfg1.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:dense_cluster -s 1 -c 1 \
+  -o gpurun_out/${P}_dense_cluster_cfg3 python tools/dense_prof.py > gpurun_out/${P}_ncu_full_cfg3.log 2>&1
+timeout 300 python tools/small_trace.py > gpurun_out/${P}_small_trace_cfg1.txt 2>&1
+timeout 300 python tools/cfg1_profile.py > gpurun_out/${P}_cfg1_profile.txt 2>&1
 tail -3 gpurun_out/${P}_gpu_tests.txt; tail -1 gpurun_out/${P}_smoke.txt
 for k in 1 2 3 5 4; do python -c "
 import json,sys

@@ -1,3 +1,5 @@
+"""cfg1 solves of several lengths through the public API (OTK_SMALL_DEBUG prints the stored-kernel build counts;
+also the short command behind the ncu capture of solve_small_kernel)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch, numpy as np
