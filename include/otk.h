@@ -323,7 +323,7 @@ typedef struct otk_solve_args {
   int32_t same_points;
   /* epsilon schedule (geometry.py:75-97): eps_t = max(target, target*init*decay^t) */
   double eps_target, eps_init_scale, eps_decay;
-  double threshold;
+  double threshold;          /* > 0 (sinkhorn.py:187); < 0: never stop early (fixed-iteration measurement runs) */
   int32_t max_iters, inner_iters;
   const float *g_init;       /* nullable warm start (sinkhorn.py:166)         */
   int32_t flags;             /* OTK_IMPL_* / OTK_CLAMP / OTK_COST_EUCL        */
@@ -338,8 +338,13 @@ typedef struct otk_solve_args {
   void *workspace;
   size_t workspace_bytes;
   void *stream;
-  /* nullable PINNED host buffers [n], [m]: the solver copies f and g there
-   * before its one final synchronisation (saves the caller a second D2H sync) */
+  /* nullable PINNED host buffers [n], [m]: f and g are there after the call's one
+   * final synchronisation (saves the caller a second D2H sync).  The persistent
+   * small-problem kernel writes them directly (zero-copy) when they are pinned
+   * (cudaHostAlloc / cudaHostRegister memory); pageable buffers get a copy.
+   * Note: with threshold so small that only an exact float32 fixed point
+   * satisfies it (f_{t+1} == f_t bitwise, marginal error 0.0), the loop stops at
+   * that iteration with converged = 1 -- every later iterate would be the same. */
   float *f_host, *g_host;
 } otk_solve_args;
 

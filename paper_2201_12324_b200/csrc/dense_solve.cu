@@ -1224,7 +1224,7 @@ extern "C" int otk_solve_dense_batched(const float *cost, int64_t batch, int64_t
                     duals && state && batch > 0,
                 "otk_solve_dense_batched: bad arguments");
   OTK_CHECK_ARG(otk_dense_solve_fits(n, m), "otk_solve_dense_batched: n, m unsupported (m %% 4, smem)");
-  OTK_CHECK_ARG(max_iters >= 1 && inner_iters >= 1 && max_checks >= 1 && threshold > 0,
+  OTK_CHECK_ARG(max_iters >= 1 && inner_iters >= 1 && max_checks >= 1 && (threshold > 0 || threshold < 0),
                 "otk_solve_dense_batched: bad loop parameters");
   dsolve::Args A{cost, batch, (int)n, (int)m, a, b, log_a, log_b, eps, g_init, eps_d, threshold,
                  max_iters, inner_iters, max_checks, f_out, g_out, errors, duals, state, nullptr};

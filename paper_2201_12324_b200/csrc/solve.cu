@@ -455,7 +455,8 @@ static int solve_entry(otk_solve_args *A, const ShardCtx *sh, float split_scale)
                 "otk_solve_pointcloud: missing pointers");
   OTK_CHECK_ARG(A->n > 0 && A->m > 0 && A->d > 0, "otk_solve_pointcloud: bad shape");
   OTK_CHECK_ARG(A->max_iters >= 1 && A->inner_iters >= 1, "max_iters and inner_iters must be >= 1");
-  OTK_CHECK_ARG(A->threshold > 0, "threshold must be positive");
+  // a negative threshold never stops the loop early (fixed-iteration measurement runs)
+  OTK_CHECK_ARG(A->threshold > 0 || A->threshold < 0, "threshold must be positive (or negative: never stop early)");
   OTK_CHECK_ARG(A->eps_target > 0, "eps must be positive");
   OTK_CHECK_ARG(A->errors && A->duals && A->max_checks >= 1, "otk_solve_pointcloud: no trace buffers");
   Layout L = plan(A, A->workspace);

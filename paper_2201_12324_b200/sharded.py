@@ -647,14 +647,18 @@ class ShardedProblem:
                 errs[:k].copy(), duals[:k].copy())
 
     def solve(self, eps, *, threshold: float = 1e-3, max_iters: int = 2000,
-              inner_iters: int = 10, g_init=None, gather_f: bool = False) -> ShardedSinkhornOutput:
+              inner_iters: int = 10, g_init=None, gather_f: bool = False,
+              fixed_iters: bool = False) -> ShardedSinkhornOutput:
         """The reference loop (sinkhorn.py:151-200) over the shards; same
-        validation and errors as ``solve_sinkhorn``."""
+        validation and errors as ``solve_sinkhorn`` (``fixed_iters``: its
+        measurement knob -- the checks never stop the loop)."""
         from .sinkhorn import _fp32_guard
         if max_iters < 1 or inner_iters < 1:
             raise ValueError("max_iters and inner_iters must be >= 1")
         if not (threshold > 0):
             raise ValueError("threshold must be positive")
+        if fixed_iters:
+            threshold = -1.0
         sched = eps if isinstance(eps, EpsilonSchedule) else EpsilonSchedule(float(eps))
         _fp32_guard(sched, inner_iters, max_iters)
         comm = self.comm
@@ -688,7 +692,8 @@ def solve_sinkhorn_sharded(x, y, eps, a=None, b=None, *, threshold: float = 1e-3
                            max_iters: int = 2000, inner_iters: int = 10, g_init=None,
                            comm=None, x_is_local: bool = False, n_total: int | None = None,
                            impl: str = "auto", gather_f: bool = False,
-                           cost_fn: str = "sqeucl", exchange: str = "auto") -> ShardedSinkhornOutput:
+                           cost_fn: str = "sqeucl", exchange: str = "auto",
+                           fixed_iters: bool = False) -> ShardedSinkhornOutput:
     """Row-sharded ``solve_sinkhorn`` on a point cloud (one rank per GPU):
     ``ShardedProblem(x, y, a, b, ...).solve(eps, ...)``."""
     if max_iters < 1 or inner_iters < 1:
@@ -698,7 +703,7 @@ def solve_sinkhorn_sharded(x, y, eps, a=None, b=None, *, threshold: float = 1e-3
     prob = ShardedProblem(x, y, a, b, comm=comm, x_is_local=x_is_local, n_total=n_total,
                           impl=impl, cost_fn=cost_fn, exchange=exchange)
     return prob.solve(eps, threshold=threshold, max_iters=max_iters, inner_iters=inner_iters,
-                      g_init=g_init, gather_f=gather_f)
+                      g_init=g_init, gather_f=gather_f, fixed_iters=fixed_iters)
 
 
 def _absmax(p) -> float:

@@ -16,6 +16,16 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file gpurun_out/${P}_launches_cfg4.csv python bench.py --steps 2 --warmup 1 > gpurun_out/${P}_ncu_launches.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:lse_tc -s 1 -c 1 \
   -o gpurun_out/${P}_lse_tc_cfg4 python tools/prof_half_step.py --config 4 --reps 3 > gpurun_out/${P}_ncu_full.log 2>&1
+# summaries are made on the box and the reports dropped (gpurun_out/ is capped at 64 MiB)
+summarize() {  # $1 = report stem, $2 = summary name
+  if [ -f gpurun_out/$1.ncu-rep ]; then
+    python profiles/summarize_ncu.py gpurun_out/$1.ncu-rep > gpurun_out/$2.txt 2>&1
+    ncu -i gpurun_out/$1.ncu-rep --page source --csv --print-source sass > gpurun_out/$1_src.csv 2>/dev/null \
+      && python tools/ncu_stalls.py gpurun_out/$1_src.csv > gpurun_out/$2_stalls.txt 2>&1
+    rm -f gpurun_out/$1.ncu-rep gpurun_out/$1_src.csv
+  fi
+}
+summarize ${P}_lse_tc_cfg4 ${P}_ncu_lse_tc_anchored_cfg4
 # cfg1 (persistent small solve) and cfg3 (K3c): launch list of the bench command + one full capture each
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/${P}_launches_cfg1.csv python bench.py --config 1 --steps 2 --warmup 1 > gpurun_out/${P}_ncu_launches_cfg1.log 2>&1
@@ -23,6 +33,8 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:solv
   -o gpurun_out/${P}_solve_small_cfg1 python tools/small_builds.py > gpurun_out/${P}_ncu_full_cfg1.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:dense_cluster -s 1 -c 1 \
   -o gpurun_out/${P}_dense_cluster_cfg3 python tools/dense_prof.py > gpurun_out/${P}_ncu_full_cfg3.log 2>&1
+summarize ${P}_solve_small_cfg1 ${P}_ncu_solve_small_cfg1
+summarize ${P}_dense_cluster_cfg3 ${P}_ncu_dense_cluster_cfg3
 timeout 300 python tools/small_trace.py > gpurun_out/${P}_small_trace_cfg1.txt 2>&1
 timeout 300 python tools/cfg1_profile.py > gpurun_out/${P}_cfg1_profile.txt 2>&1
 tail -3 gpurun_out/${P}_gpu_tests.txt; tail -1 gpurun_out/${P}_smoke.txt
