@@ -405,6 +405,17 @@ __device__ __forceinline__ float2 lds_f2_pred(uint32_t addr, bool p) {
   return r;
 }
 
+// Predicated 128-bit shared-memory load (zeros when !p), no branch.
+__device__ __forceinline__ float4 lds_f4_pred(uint32_t addr, bool p) {
+  float4 r;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\tmov.f32 %0, 0f00000000;\n\tmov.f32 %1, 0f00000000;\n\t"
+      "mov.f32 %2, 0f00000000;\n\tmov.f32 %3, 0f00000000;\n\t@p ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "r"(addr), "r"((unsigned)p));
+  return r;
+}
+
 #ifndef OTK_SMALL_PREPOLL_NS
 #define OTK_SMALL_PREPOLL_NS 0  // A/B knob: sleep before the first poll of a stored half-step
 #endif
@@ -455,22 +466,33 @@ __device__ __forceinline__ void stored_pass(const Args &A, int nq, const xword *
   // predicated ld.shared from 32-bit shared addresses, HB row pairs per batch
   const uint32_t es0 = (uint32_t)__cvta_generic_to_shared(sh4) + es_off;
   constexpr int NS = RC / 2 - NREG;
-  constexpr int HB = NS < OTK_ST_HB ? (NS > 0 ? NS : 1) : OTK_ST_HB;
+  static_assert(NS % 2 == 0, "shared-memory row pairs travel two at a time (one 128-bit load per column)");
+  // layout: quad q (row pairs NREG + 2q, NREG + 2q + 1) at es0 + q * nq * 16, one float4 per column:
+  // 128-bit loads run at twice the bytes per clock of 64-bit ones (csrc/pipes.cu otk_bench_smem)
+  constexpr int QB = 2;  // quads per batch of loads
 #pragma unroll
-  for (int h0 = 0; h0 < NS; h0 += HB) {
-    float2 e[HB][SC];
+  for (int q0 = 0; q0 < NS / 2; q0 += QB) {
+    float4 e[QB][SC];
 #pragma unroll
-    for (int h = 0; h < HB; ++h)
+    for (int q = 0; q < QB; ++q)
 #pragma unroll
       for (int c = 0; c < SC; ++c)
-        e[h][c] = lds_f2_pred(es0 + (uint32_t)(((h0 + h) * nq + jj[c]) * (int)sizeof(float2)),
-                              2 * (NREG + h0 + h) < rc && jj[c] < nq);
+        e[q][c] = (q0 + q < NS / 2)
+                      ? lds_f4_pred(es0 + (uint32_t)(((q0 + q) * nq + jj[c]) * (int)sizeof(float4)),
+                                    2 * (NREG + 2 * (q0 + q)) < rc && jj[c] < nq)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int h = 0; h < HB; ++h) {
-      float2 a2 = make_float2(0.f, 0.f);
+    for (int q = 0; q < QB; ++q) {
+      if (q0 + q < NS / 2) {
+        float2 a2 = make_float2(0.f, 0.f), b2 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int c = 0; c < SC; ++c) a2 = __ffma2_rn(e[h][c], v[c], a2);
-      acc[NREG + h0 + h] = a2;
+        for (int c = 0; c < SC; ++c) {
+          a2 = __ffma2_rn(make_float2(e[q][c].x, e[q][c].y), v[c], a2);
+          b2 = __ffma2_rn(make_float2(e[q][c].z, e[q][c].w), v[c], b2);
+        }
+        acc[NREG + 2 * (q0 + q)] = a2;
+        acc[NREG + 2 * (q0 + q) + 1] = b2;
+      }
     }
   }
 #pragma unroll
@@ -540,7 +562,7 @@ __device__ __forceinline__ void build_pass(const Args &A, const float4 *Q, int n
         else u = make_float2(bs.x - kc.x, bs.y - kc.y);
         e = make_float2(ex2(u.x), ex2(u.y));
         acc[h] = __fadd2_rn(acc[h], e);
-        if (h >= NREG && ok) es[(h - NREG) * nq + jj[c]] = e;
+        if (h >= NREG && ok) es[(((h - NREG) >> 1) * nq + jj[c]) * 2 + ((h - NREG) & 1)] = e;  // quad layout
       }
       if (h < NREG) er[h][c] = e;
     }

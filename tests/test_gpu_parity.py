@@ -694,3 +694,32 @@ def test_persistent_small_solve_stored_kernel_long_run_has_no_gauge_drift(otk, m
         assert out.iterations == 600 or (out.converged and out.errors[-1] == 0.0)
         assert rel_inf(out.f, ref["f"]) <= 2e-5, rel_inf(out.f, ref["f"])
         assert rel_inf(out.g, ref["g"]) <= 2e-5, rel_inf(out.g, ref["g"])
+
+
+@pytest.mark.parametrize("route", ["small", "general", "batched"])
+def test_fixed_iters_runs_every_iteration_past_an_exact_fixed_point(otk, route):
+    """float32 iterates can reach an exact fixed point (f_{t+1} == f_t bitwise, marginal
+    error 0.0), which satisfies any positive threshold and ends the loop as the
+    reference's test `err <= threshold` (sinkhorn.py:187) says.  The measurement knob
+    `fixed_iters` keeps iterating: same potentials, every check recorded, converged False."""
+    from paper_2201_12324_b200 import _native as N
+    wl = workloads.cfg1(n=300, m=260)
+    iters = 400
+    if route == "batched":
+        x, y = wl.x[None], wl.y[None]
+        stop = otk.solve_sinkhorn_batched(x, y, wl.eps, threshold=1e-300, max_iters=iters)[0]
+        full = otk.solve_sinkhorn_batched(x, y, wl.eps, threshold=1e-300, max_iters=iters, fixed_iters=True)[0]
+    else:
+        geom = otk.PointCloudGeometry(wl.x, wl.y)
+        if route == "general":
+            geom.impl_flags = N.OTK_IMPL_NOPERSIST
+        prob = otk.LinearProblem(geom)
+        stop = otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=iters)
+        full = otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=iters, fixed_iters=True)
+    assert full.iterations == iters and not full.converged and len(full.errors) == iters // 10
+    if stop.converged:  # an exact fixed point: nothing moves afterwards
+        assert stop.errors[-1] == 0.0 and stop.iterations < iters
+        assert np.array_equal(stop.f, full.f) and np.array_equal(stop.g, full.g)
+        assert full.errors[-1] == 0.0
+    else:
+        assert stop.iterations == iters
