@@ -416,11 +416,7 @@ __device__ __forceinline__ float4 lds_f4_pred(uint32_t addr, bool p) {
   return r;
 }
 
-#ifndef OTK_SMALL_PREPOLL_NS
-#define OTK_SMALL_PREPOLL_NS 0  // A/B knob: sleep before the first poll of a stored half-step
-#endif
 __device__ __forceinline__ void wait_words(const xword *qx, int nq, int need, xword (&w)[SC], int (&jj)[SC]) {
-  if (OTK_SMALL_PREPOLL_NS > 0) __nanosleep(OTK_SMALL_PREPOLL_NS);
 #pragma unroll
   for (int c = 0; c < SC; ++c) {
     jj[c] = threadIdx.x + c * THREADS;
