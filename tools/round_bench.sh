@@ -8,8 +8,10 @@ P=${1:-r02}
 mkdir -p gpurun_out
 timeout 1800 python -m pytest tests -m gpu -q -rf > gpurun_out/${P}_gpu_tests.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${P}_smoke.txt 2>&1
+# the ms-scale steps of cfg1 / cfg3 get more steps: one NVML sample landing in a 0.6 ms step costs it ~1 ms
 for k in 1 2 3 5 4; do
-  timeout 900 python bench.py --config $k > gpurun_out/${P}_bench_cfg$k.json 2> gpurun_out/${P}_bench_cfg$k.err
+  case $k in 1) S="--steps 50";; 3) S="--steps 20";; *) S="";; esac
+  timeout 900 python bench.py --config $k $S > gpurun_out/${P}_bench_cfg$k.json 2> gpurun_out/${P}_bench_cfg$k.err
 done
 timeout 900 python bench.py --impl reference > gpurun_out/${P}_bench_cfg4_reference.json 2> gpurun_out/${P}_bench_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
@@ -26,6 +28,11 @@ summarize() {  # $1 = report stem, $2 = summary name
   fi
 }
 summarize ${P}_lse_tc_cfg4 ${P}_ncu_lse_tc_anchored_cfg4
+for k in 2 5; do
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:lse_tc -s 1 -c 1 \
+    -o gpurun_out/${P}_lse_tc_cfg$k python tools/prof_half_step.py --config $k --reps 3 > gpurun_out/${P}_ncu_full_cfg$k.log 2>&1
+  summarize ${P}_lse_tc_cfg$k ${P}_ncu_lse_tc_anchored_cfg$k
+done
 # cfg1 (persistent small solve) and cfg3 (K3c): launch list of the bench command + one full capture each
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/${P}_launches_cfg1.csv python bench.py --config 1 --steps 2 --warmup 1 > gpurun_out/${P}_ncu_launches_cfg1.log 2>&1
