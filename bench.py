@@ -383,8 +383,10 @@ def small_roofline(value, step_s, wl):
             "kernel": "solve_small_kernel (whole solve, one launch)", "kernel_ms": step_s * 1e3,
             "cells_per_launch": float(wl.x.shape[0]) * wl.y.shape[0],
             "peak_note": "MUFU ex2 rate measured on this GPU (csrc/pipes.cu)",
-            "achieved_note": "2 ex2 per cell-update x cell-updates/s of the timed steps; the "
-                             "kernel is latency-bound (the half-step exchange and reductions, "
+            "achieved_note": "the log-domain formulation's 2 ex2 per cell-update x cell-updates/s of "
+                             "the timed steps (SURVEY.md 8d's unit of work); the stored-kernel "
+                             "half-steps take the exps once per build and then do one FFMA per cell, "
+                             "and the kernel is latency-bound (half-step exchange, reductions: "
                              "tools/small_trace.py), not MUFU-bound",
             "pipes": {"ex2_per_s": ex2, "ffma_per_s": ffma}}
 
