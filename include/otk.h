@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define OTK_ABI_VERSION 6
+#define OTK_ABI_VERSION 7
 
 enum otk_status {
   OTK_OK = 0,
@@ -90,6 +90,19 @@ int otk_shift_points(const float *p, int64_t n, int32_t d, const double *center,
 
 /* max |p_ik| over the array (for choosing split_scale); out is one float. */
 int otk_absmax(const float *pts, int64_t count, float *out, void *stream);
+
+/* PointCloudGeometry.__init__ (geometry.py:247-261) in one launch: flags[0] / [1] = 1
+ * when x / y holds a non-finite coordinate, flags[2] = 1 when compare != 0 and the
+ * sets differ anywhere (compare only with nx == ny).  flags: device int32[3]. */
+int otk_points_flags(const float *x, int64_t nx, const float *y, int64_t ny, int32_t d,
+                     int32_t compare, int32_t *flags, void *stream);
+
+/* mean_cost's sampled estimate (geometry.py:294-312): the mean over `count` pairs
+ * (ii[s], jj[s]) of the cost between kernel points x[ii] and y[jj] (float64
+ * difference form; flags: OTK_COST_EUCL, OTK_SAME_POINTS -> exact zero for i == j).
+ * ii, jj: device int64[count]; mean: device double[1]. */
+int otk_mean_cost_pairs(const float *x, const float *y, const int64_t *ii, const int64_t *jj,
+                        int64_t count, int32_t d, int32_t flags, double *mean, void *stream);
 
 /* The power-of-two operand scale for point sets of dimension d whose largest
  * |coordinate| is amax (one common scale for both sets of a geometry). */

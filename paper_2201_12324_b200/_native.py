@@ -23,7 +23,7 @@ OTK_IMPL_NOPERSIST = 0x40
 OTK_ANCHOR_INIT, OTK_IMPL_NOANCHOR = 0x80, 0x100
 OTK_COST_EUCL = 0x4
 OTK_FIN_SOLVER, OTK_FIN_APPLY, OTK_FIN_LOG2 = 0, 1, 2
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 P = C.c_void_p
 I64, I32, F32, F64, SZ = C.c_int64, C.c_int32, C.c_float, C.c_double, C.c_size_t
@@ -59,6 +59,8 @@ SIGNATURES = {
     "otk_prep_points": (C.c_int, [P, I64, I32, P, P, P, P, P, I32, F32, P]),
     "otk_split_scale": (F32, [F32, I32]),
     "otk_absmax": (C.c_int, [P, I64, P, P]),
+    "otk_points_flags": (C.c_int, [P, I64, P, I64, I32, I32, P, P]),
+    "otk_mean_cost_pairs": (C.c_int, [P, P, P, P, I64, I32, I32, P, P]),
     "otk_column_median": (C.c_int, [P, I64, I32, P, P]),
     "otk_shift_points": (C.c_int, [P, I64, I32, P, P, P]),
     "otk_make_bias": (C.c_int, [P, I64, F32, P, P, I32, P]),

@@ -239,6 +239,55 @@ int finalize_launch(int kind, const FinArgs &F, cudaStream_t st) {
   return OTK_OK;
 }
 
+// ---------------------------------------------------------------- geometry construction helpers
+// One launch for the constructor's three questions (geometry.py:247-261): any
+// non-finite coordinate in x, in y, and -- equal shapes only -- any x != y.
+__global__ void points_flags_kernel(const float *__restrict__ x, int64_t cx, const float *__restrict__ y,
+                                    int64_t cy, int compare, int *__restrict__ flags) {
+  bool bx = false, by = false, df = false;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t top = cx > cy ? cx : cy;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < top; k += stride) {
+    const float a = k < cx ? x[k] : 0.f, b = k < cy ? y[k] : 0.f;
+    bx |= !isfinite(a);
+    by |= !isfinite(b);
+    df |= compare && !(a == b);
+  }
+  if (__syncthreads_or(bx) && threadIdx.x == 0) flags[0] = 1;
+  if (__syncthreads_or(by) && threadIdx.x == 0) flags[1] = 1;
+  if (__syncthreads_or(df) && threadIdx.x == 0) flags[2] = 1;
+}
+
+// Mean cost over `count` sampled pairs (geometry.py:294-312: the eps estimate),
+// float64 difference form on the kernel points, fixed-order block reduction.
+__global__ void __launch_bounds__(1024) mean_cost_pairs_kernel(const float *__restrict__ x,
+                                                               const float *__restrict__ y,
+                                                               const int64_t *__restrict__ ii,
+                                                               const int64_t *__restrict__ jj, int64_t count,
+                                                               int d, int eucl, int same,
+                                                               double *__restrict__ out) {
+  __shared__ double red[1024];
+  double acc = 0.0;
+  for (int64_t s = threadIdx.x; s < count; s += blockDim.x) {
+    const int64_t i = ii[s], j = jj[s];
+    double c = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double df = (double)x[i * d + k] - (double)y[j * d + k];
+      c = fma(df, df, c);
+    }
+    if (eucl) c = sqrt(c);
+    if (same && i == j) c = 0.0;
+    acc += c;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0] / (double)count;
+}
+
 // ---------------------------------------------------------------- K5 check
 constexpr int kCheckBlocks = 148;
 constexpr int kCheckThreads = 256;
@@ -432,3 +481,25 @@ int otk_check(const float *f_prev, const float *f_next, const float *a, int64_t 
 }
 
 }  // extern "C"
+
+extern "C" int otk_points_flags(const float *x, int64_t nx, const float *y, int64_t ny, int32_t d,
+                                int32_t compare, int32_t *flags, void *stream) {
+  OTK_CHECK_ARG(x && y && flags && nx > 0 && ny > 0 && d > 0, "otk_points_flags: bad arguments");
+  cudaStream_t st = as_stream(stream);
+  OTK_CUDA(cudaMemsetAsync(flags, 0, 3 * sizeof(int32_t), st));
+  const int64_t top = std::max(nx, ny) * d;
+  const unsigned blocks = (unsigned)std::min<int64_t>((top + 255) / 256, 4 * (int64_t)num_sms());
+  points_flags_kernel<<<blocks, 256, 0, st>>>(x, nx * d, y, ny * d, compare && nx == ny, flags);
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}
+
+extern "C" int otk_mean_cost_pairs(const float *x, const float *y, const int64_t *ii, const int64_t *jj,
+                                   int64_t count, int32_t d, int32_t flags, double *mean, void *stream) {
+  OTK_CHECK_ARG(x && y && ii && jj && mean && count > 0 && d > 0, "otk_mean_cost_pairs: bad arguments");
+  mean_cost_pairs_kernel<<<1, 1024, 0, as_stream(stream)>>>(x, y, ii, jj, count, d,
+                                                             (flags & OTK_COST_EUCL) != 0,
+                                                             (flags & OTK_SAME_POINTS) != 0, mean);
+  OTK_LAUNCH_CHECK();
+  return OTK_OK;
+}

@@ -258,6 +258,27 @@ def centered_points(px, py, cost_fn: str, same: bool = False):
     return cx, cy
 
 
+_PAIR_CACHE: dict = {}
+
+
+def _mean_cost_pairs(n: int, m: int, dev):
+    """The reference's seeded sample of index pairs (geometry.py:296-298:
+    default_rng(0), i then j), as device int64 tensors; they depend only on the
+    shape, so they are drawn and uploaded once per (n, m, device)."""
+    import torch
+    key = (n, m, str(dev))
+    hit = _PAIR_CACHE.get(key)
+    if hit is None:
+        rng = np.random.default_rng(0)
+        i = rng.integers(0, n, size=_MEAN_COST_SAMPLES)
+        j = rng.integers(0, m, size=_MEAN_COST_SAMPLES)
+        hit = (torch.as_tensor(i, dtype=torch.int64, device=dev), torch.as_tensor(j, dtype=torch.int64, device=dev))
+        if len(_PAIR_CACHE) > 64:
+            _PAIR_CACHE.clear()
+        _PAIR_CACHE[key] = hit
+    return hit
+
+
 def cost_fn_flags(cost_fn: str) -> int:
     if cost_fn not in COST_FNS:
         raise ValueError(f"cost_fn must be one of {COST_FNS}, got {cost_fn!r}")
@@ -288,14 +309,17 @@ class PointCloudGeometry(Geometry):
         vx, vy = self._dev_pts if self._dev_pts is not None else (x, y)
         same_dev = None
         if self._dev_pts is not None:
-            # one device->host read for both finiteness flags and the same-points test
+            # one launch and one device->host read for both finiteness flags and the
+            # same-points test (otk_points_flags)
             import torch
-            flags = [torch.isfinite(vx).all(), torch.isfinite(vy).all()]
-            if not same_obj and x.shape == y.shape:
-                flags.append((vx == vy).all())
-            got = torch.stack(flags).cpu().tolist()
-            finite = got[0] and (same_obj or got[1])
-            same_dev = bool(got[2]) if len(got) > 2 else False
+            compare = (not same_obj) and tuple(x.shape) == tuple(y.shape)
+            fl = torch.empty(3, dtype=torch.int32, device=vx.device)
+            N.check(N.lib().otk_points_flags(N.ptr(vx), vx.shape[0], N.ptr(vy), vy.shape[0],
+                                             int(vx.shape[1]), 1 if compare else 0, N.ptr(fl), stream()),
+                    "points flags")
+            got = fl.cpu().tolist()
+            finite = got[0] == 0 and got[1] == 0
+            same_dev = compare and got[2] == 0
         else:
             finite = _all_finite(vx) and (same_obj or _all_finite(vy))
         if not finite:
@@ -368,22 +392,17 @@ class PointCloudGeometry(Geometry):
         """0.05 * this is epsilon_default; subsampled like geometry.py:294-312."""
         import torch
         n, m = self.shape
-        cx, cy = self._clouds()
         if n * m <= _MEAN_COST_SAMPLES:
             return float(torch.as_tensor(self.cost_matrix(max_entries=n * m)).mean())
-        rng = np.random.default_rng(0)
-        i = rng.integers(0, n, size=_MEAN_COST_SAMPLES)
-        j = rng.integers(0, m, size=_MEAN_COST_SAMPLES)
-        # cosine: the kernel points are x^/sqrt2, so |x'-y'|^2 = 1 - <x^,y^> (geometry.py:303-306)
-        ii = torch.as_tensor(i, device=cx.p.device)
-        jj = torch.as_tensor(j, device=cx.p.device)
-        diff = cx.p[ii].double() - cy.p[jj].double()
-        vals = torch.clamp((diff * diff).sum(dim=1), min=0.0)
-        if self.cost_fn == "eucl":
-            vals = torch.sqrt(vals)
-        if self._same_points:
-            vals = torch.where(ii == jj, torch.zeros_like(vals), vals)
-        return float(vals.mean().item())
+        # the kernel points are enough (no norms / operand planes); cosine: they are
+        # x^/sqrt2, so |x'-y'|^2 = 1 - <x^,y^> (geometry.py:303-306)
+        kx, ky = self._points()
+        ii, jj = _mean_cost_pairs(n, m, kx.device)
+        out = torch.empty(1, dtype=torch.float64, device=kx.device)
+        N.check(N.lib().otk_mean_cost_pairs(N.ptr(kx), N.ptr(ky), N.ptr(ii), N.ptr(jj), ii.numel(),
+                                            int(kx.shape[1]), self._cost_flags, N.ptr(out), stream()),
+                "mean cost")
+        return float(out.item())
 
     def cost_matrix(self, max_entries: int | None = None):
         """Materialise C on the GPU (difference form); refuses past the cap."""
