@@ -541,6 +541,7 @@ static int solve_small(otk_solve_args *A, Layout &L, cudaStream_t st) {
   S.errors = h_err;
   S.duals = h_dual;
   S.state = reinterpret_cast<int *>(hres.p);
+  std::memset(hres.p, 0, 64);
   auto pinned = [](const void *p) {
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -582,6 +583,9 @@ static int solve_small(otk_solve_args *A, Layout &L, cudaStream_t st) {
     OTK_CUDA(cudaMemcpyAsync(A->g_host, A->g_out, A->m * sizeof(float), cudaMemcpyDeviceToHost, st));
   if ((A->f_host && !S.f_host) || (A->g_host && !S.g_host)) OTK_CUDA(cudaStreamSynchronize(st));
   const int *state = reinterpret_cast<const int *>(hres.p);
+  if (getenv("OTK_SMALL_DEBUG"))  // builds are counted by -DOTK_SMALL_COUNT_BUILDS libraries only (else 0 0)
+    fprintf(stderr, "solve_small: %d iterations, stored-kernel builds of CTA 0: x role %d, y role %d\n", state[1],
+            state[5], state[6]);
   const int nc = std::min(state[0], A->max_checks);
   std::memcpy(A->errors, h_err, (size_t)nc * sizeof(double));
   std::memcpy(A->duals, h_dual, (size_t)nc * sizeof(double));

@@ -576,6 +576,9 @@ struct StoredRole {
   float beta[SC];
   uint32_t es_off;  // byte offset of the role's shared-memory terms in the dynamic array
   bool have;
+#ifdef OTK_SMALL_COUNT_BUILDS
+  int builds;  // exact passes this CTA ran for the role -> state[5] / state[6] (CTA 0)
+#endif
 };
 
 template <int NV, bool SAME, bool CHECK, bool CHECKG, bool EU, int STR>
@@ -638,6 +641,9 @@ __device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, i
         build_pass<NV, SAME, EU, STR == 1 ? ER_PAIRS : 0>(A, Q, nq, qx, need, r0, rn, S.pr, an,
                                                           SR.er, SR.es_off, SR.beta, red, tot);
         SR.have = true;
+#ifdef OTK_SMALL_COUNT_BUILDS  // diagnostics build (tools/variant_small.sh ... -DOTK_SMALL_COUNT_BUILDS)
+        ++SR.builds;
+#endif
         if (threadIdx.x < rn) {
           const float tb = tot[threadIdx.x];
           L = an[threadIdx.x] + log2f(tb);
@@ -722,6 +728,9 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
   float4 *xs, *ys;
   StoredRole sx, sy;  // ST: the x role's terms in registers, the y role's in shared memory
   sx.have = sy.have = false;
+#ifdef OTK_SMALL_COUNT_BUILDS
+  sx.builds = sy.builds = 0;
+#endif
   sy.es_off = 0;  // y role: RC / 2 pairs x n columns; then the x role's RC / 2 - ER_PAIRS pairs x m columns
   sx.es_off = (uint32_t)((RC / 2) * A.n * (int)sizeof(float2));
   if constexpr (NV <= 2 && !ST) {
@@ -933,6 +942,10 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
     A.state[2] = converged;
     A.state[3] = status;
     A.state[4] = fail_iter;
+#ifdef OTK_SMALL_COUNT_BUILDS
+    A.state[5] = sx.builds;
+    A.state[6] = sy.builds;
+#endif
   }
 }
 

@@ -1,5 +1,6 @@
-"""cfg1 solves of several lengths through the public API (OTK_SMALL_DEBUG prints the stored-kernel build counts;
-also the short command behind the ncu capture of solve_small_kernel)."""
+"""cfg1 solves of several lengths through the public API: the short command behind the ncu capture of
+solve_small_kernel.  With a library built by `tools/variant_small.sh abx/count.so -DOTK_SMALL_COUNT_BUILDS`
+(OTK_LIB=abx/count.so) OTK_SMALL_DEBUG prints how often CTA 0 rebuilt its stored terms (cfg1: x role 2, y role 1)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch, numpy as np
