@@ -232,11 +232,14 @@ def cpu_cores():
 def run_reference(args, wl, rank):
     if rank != 0:
         return
+    # each step is a bounded sample; the budget per step keeps the whole K-step run at
+    # about two minutes of CPU samples (15 s per step at the default K = 5)
+    budget = min(15.0, max(3.0, 120.0 / max(args.steps, 1)))
     for _ in range(args.warmup):
-        cpu_sample_rate(wl, budget_s=2.0)
+        cpu_sample_rate(wl, budget_s=min(2.0, budget))
     vals, t_total, desc = [], 0.0, ""
     for _ in range(args.steps):
-        v, dt, desc = cpu_sample_rate(wl, budget_s=15.0)
+        v, dt, desc = cpu_sample_rate(wl, budget_s=budget)
         vals.append(v)
         t_total += dt
     value = float(np.mean(vals))
@@ -821,14 +824,28 @@ def run_e2e(otk, wl, args, dev, world, rank):
             return out.iterations  # out.f / out.g: float64 host arrays (D2H in the region)
         h2d = wl.x.nbytes + wl.y.nbytes + 4 * (n + m) * 2
         d2h = 4 * (n + m)
-    for _ in range(args.warmup):
+    # this leg repeats the whole workload through the public API: with second-long steps
+    # (cfg4: 3.9 s) W warm-ups + K steps would double the run, so both are bounded by
+    # time (>= 1 warm-up, >= 3 timed steps, ~10 s / ~40 s); every rank takes the same counts
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    step()
+    torch.cuda.synchronize()
+    est = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([est], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        est = float(t.item())
+    n_warm = min(max(args.warmup - 1, 0), int(10.0 / max(est, 1e-6)))
+    n_steps = min(args.steps, max(3, int(40.0 / max(est, 1e-6))))
+    for _ in range(n_warm):
         step()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     its = 0
-    for _ in range(args.steps):
+    for _ in range(n_steps):
         its += step()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
@@ -837,7 +854,8 @@ def run_e2e(otk, wl, args, dev, world, rank):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         dt = float(t.item())
     return {"value": float(n) * m * its / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * dt / args.steps,
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * dt / n_steps, "steps": n_steps,
+            "warmup": n_warm + 1,
             "api": "public API on pinned host arrays (H2D + D2H inside the timed region)"}
 
 
