@@ -27,7 +27,10 @@
 namespace otk {
 namespace dsolve {
 
-constexpr int THREADS = 512, WARPS = THREADS / 32, NV = 8;
+#ifndef OTK_DENSE_THREADS
+#define OTK_DENSE_THREADS 512
+#endif
+constexpr int THREADS = OTK_DENSE_THREADS, WARPS = THREADS / 32, NV = 8;
 
 struct Args {
   const float *C;
