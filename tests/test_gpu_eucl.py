@@ -183,3 +183,36 @@ def test_barycenter_eucl_support(otk):
     p, conv, iters, _ = ref_solve(rgeom, h, None, eps)
     assert out.converged and conv
     assert float(np.abs(out.barycenter - p).sum()) <= 1e-4
+
+
+@pytest.mark.gpu
+def test_device_constructor_flags_and_mean_cost_sample(otk):
+    """PointCloudGeometry built from CUDA tensors: the constructor's finiteness
+    and same-points tests run as one native launch (otk_points_flags,
+    geometry.py:247-261) and the eps estimate's seeded 1000-pair sample as
+    another (otk_mean_cost_pairs, geometry.py:294-312) -- same answers as the
+    host path, which follows the reference line by line."""
+    import torch
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal((300, 5)).astype(np.float32)
+    y = (rng.standard_normal((300, 5)) + 0.3).astype(np.float32)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    assert otk.PointCloudGeometry(xd, xd.clone())._same_points          # equal values, different objects
+    assert not otk.PointCloudGeometry(xd, yd)._same_points
+    y1 = x.copy()
+    y1[299, 4] += 1e-3                                                   # one differing coordinate, the last
+    assert not otk.PointCloudGeometry(xd, torch.from_numpy(y1).cuda())._same_points
+    assert not otk.PointCloudGeometry(xd, yd[:200])._same_points        # shapes differ: never compared
+    for bad, which in ((np.nan, "x"), (np.inf, "y"), (-np.inf, "y")):
+        xb, yb = x.copy(), y.copy()
+        (xb if which == "x" else yb)[17, 2] = bad
+        with pytest.raises(ValueError, match="non-finite"):
+            otk.PointCloudGeometry(torch.from_numpy(xb).cuda(), torch.from_numpy(yb).cuda())
+    for cost_fn in ("sqeucl", "eucl", "cosine"):
+        for same in (False, True):
+            host = otk.PointCloudGeometry(x, x if same else y, cost_fn=cost_fn)
+            dev = otk.PointCloudGeometry(xd, xd if same else yd, cost_fn=cost_fn)
+            ref = oracle.PointCloudOracle(x.astype(np.float64), (x if same else y).astype(np.float64),
+                                          cost_fn=cost_fn)
+            assert dev.mean_cost() == pytest.approx(host.mean_cost(), rel=1e-6)
+            assert dev.mean_cost() == pytest.approx(ref.mean_cost(), rel=1e-5)
