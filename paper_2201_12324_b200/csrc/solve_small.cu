@@ -173,8 +173,9 @@ __device__ __forceinline__ int rs16_row(int lane) {
 // kappa |p|^2 and the anchor / shift of every row.
 template <int NV>
 struct RoleRows {
-  float2 p2[KMAX * RC / 2][4 * NV];
-  float2 pr[RC / 2][4 * NV];  // the first chunk's raw coordinates, same pairing, zeros from slot d (stored-kernel builds)
+  static constexpr int W = NV > 0 ? 4 * NV : 1;  // NV = 0: any d, the rows' coordinates live in dynamic shared memory
+  float2 p2[NV > 0 ? KMAX * RC / 2 : 1][W];
+  float2 pr[NV > 0 ? RC / 2 : 1][W];  // the first chunk's raw coordinates, same pairing, zeros from slot d (stored-kernel builds)
   float cp[KMAX * RC];
   float an[KMAX * RC];
   float ci[KMAX * RC];   // stored kernel: 1 / the row's total at build time
@@ -195,6 +196,15 @@ __device__ __forceinline__ void init_role_rows(const Args &A, const float4 *P, i
     S.n_chunks = n_chunks;
     S.lo = -96.f + 2.f * log2f((float)nq);
   }
+  if constexpr (NV == 0) {  // any d (stored kernel only): log weights here, raw rows by init_generic_rows
+    for (int r = threadIdx.x; r < RC; r += blockDim.x) {
+      const int i = min(blockIdx.x * rc + r, np - 1);
+      S.an[r] = -INFINITY;
+      S.ci[r] = 1.f;
+      S.cp[r] = 0.f;
+      S.lw2[r] = (blockIdx.x < n_chunks) ? (float)((double)logw[i] * 1.4426950408889634) : 0.f;
+    }
+  } else {
   for (int idx = threadIdx.x; idx < KMAX * RC; idx += blockDim.x) {
     const int k = idx / RC, r = idx % RC;
     const int ch = blockIdx.x + k * G;
@@ -203,15 +213,16 @@ __device__ __forceinline__ void init_role_rows(const Args &A, const float4 *P, i
     const float *pv = reinterpret_cast<const float *>(P + i * NV);
     float *dst = reinterpret_cast<float *>(S.p2[idx / 2]) + (idx & 1);
 #pragma unroll
-    for (int kk = 0; kk < 4 * NV; ++kk) dst[2 * kk] = (kk < A.d) ? two_k * pv[kk] : (kk == A.d ? 1.f : 0.f);
+    for (int kk = 0; kk < RoleRows<NV>::W; ++kk) dst[2 * kk] = (kk < A.d) ? two_k * pv[kk] : (kk == A.d ? 1.f : 0.f);
     if (k == 0) {
       float *raw = reinterpret_cast<float *>(S.pr[idx / 2]) + (idx & 1);
 #pragma unroll
-      for (int kk = 0; kk < 4 * NV; ++kk) raw[2 * kk] = (kk < A.d) ? pv[kk] : 0.f;
+      for (int kk = 0; kk < RoleRows<NV>::W; ++kk) raw[2 * kk] = (kk < A.d) ? pv[kk] : 0.f;
     }
     S.cp[idx] = -pv[A.d];
     S.an[idx] = -INFINITY;
     S.lw2[idx] = (float)((double)logw[i] * 1.4426950408889634);
+  }
   }
 }
 
@@ -566,6 +577,76 @@ __device__ __forceinline__ void build_pass(const Args &A, const float4 *Q, int n
   fold_rows<false>(acc, rc, red, tot);
 }
 
+// ---- any d (NV = 0 instantiations, stored kernel only) ----
+// The exact passes of a role whose points have more than 19 coordinates: rows
+// from shared memory (raw coordinates, pair h of the chunk at prg + h * d, one
+// float2 per coordinate), columns straight from the caller's row-major points
+// (L1 / L2; these passes run two or three times per solve), cost in the
+// difference form kappa sum_k (p_k - q_k)^2 like build_pass.  MAXP: the row
+// maxima of b_j - kappa C_ij (or - sqrt(kappa) sqrt(kappa C_ij)); otherwise
+// the sum against them, keeping every term as E and the columns' b as beta.
+__device__ __forceinline__ void init_generic_rows(const float *P, int np, int d, float2 *prg) {
+  const int G = gridDim.x;
+  const int rc = min(RC, (np + G - 1) / G), n_chunks = (np + rc - 1) / rc;  // as init_role_rows
+  if ((int)blockIdx.x >= n_chunks) return;
+  for (int idx = threadIdx.x; idx < (RC / 2) * d; idx += blockDim.x) {
+    const int h = idx / d, k = idx - h * d;
+    const int i0 = min((int)blockIdx.x * rc + 2 * h, np - 1), i1 = min((int)blockIdx.x * rc + 2 * h + 1, np - 1);
+    prg[idx] = make_float2(P[(int64_t)i0 * d + k], P[(int64_t)i1 * d + k]);
+  }
+}
+
+template <bool MAXP, bool EU, int NREG>
+__device__ __forceinline__ void generic_pass(const Args &A, const float *Qraw, int nq, const xword *qx, int need,
+                                             int rc, const float2 *prg, const float *sh,
+                                             float2 (&er)[ER_PAIRS > 0 ? ER_PAIRS : 1][SC], uint32_t es_off,
+                                             float (&beta)[SC], float (*red)[RC], float *tot) {
+  const int d = A.d;
+  const float sk = sqrtf(A.kappa);
+  float2 *es = reinterpret_cast<float2 *>(reinterpret_cast<char *>(sh4) + es_off);
+  xword w[SC];
+  int jj[SC];
+  wait_words(qx, nq, need, w, jj);
+  float2 acc[RC / 2];
+#pragma unroll
+  for (int h = 0; h < RC / 2; ++h) acc[h] = MAXP ? make_float2(-INFINITY, -INFINITY) : make_float2(0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < SC; ++c) {
+    const bool ok = jj[c] < nq;
+    const float *qp = Qraw + (int64_t)(ok ? jj[c] : 0) * d;
+    float2 c2[RC / 2];
+#pragma unroll
+    for (int h = 0; h < RC / 2; ++h) c2[h] = make_float2(0.f, 0.f);
+    for (int k = 0; k < d; ++k) {
+      const float q = __ldg(qp + k);
+#pragma unroll
+      for (int h = 0; h < RC / 2; ++h) {
+        const float2 df = __fadd2_rn(prg[h * d + k], make_float2(-q, -q));
+        c2[h] = __ffma2_rn(df, df, c2[h]);
+      }
+    }
+    const float bj = ok ? __uint_as_float((unsigned)w[c]) : -INFINITY;
+    if (!MAXP) beta[c] = (bj == -INFINITY) ? 0.f : bj;
+#pragma unroll
+    for (int h = 0; h < RC / 2; ++h) {
+      float2 kc = make_float2(A.kappa * c2[h].x, A.kappa * c2[h].y);
+      if (EU) kc = make_float2(sk * sqrt_approx(kc.x), sk * sqrt_approx(kc.y));
+      if (MAXP) {
+        acc[h] = make_float2(fmaxf(acc[h].x, bj - kc.x), fmaxf(acc[h].y, bj - kc.y));
+      } else {
+        float2 e = make_float2(0.f, 0.f);
+        if (2 * h < rc) {
+          e = make_float2(ex2((bj - sh[2 * h]) - kc.x), ex2((bj - sh[2 * h + 1]) - kc.y));
+          acc[h] = __fadd2_rn(acc[h], e);
+          if (h >= NREG && ok) es[(((h - NREG) >> 1) * nq + jj[c]) * 2 + ((h - NREG) & 1)] = e;
+        }
+        if (h < NREG) er[h][c] = e;
+      }
+    }
+  }
+  fold_rows<MAXP>(acc, rc, red, tot);
+}
+
 // One half-step of a role: rows P (np) against the columns' exchange words
 // qx (tag step - 1).  Publishes {kappa * out_pot, step} into px and writes
 // out_pot (own rows).  CHECK: the f-side check sums (f_prev = previous f,
@@ -575,6 +656,7 @@ struct StoredRole {
   float2 er[ER_PAIRS > 0 ? ER_PAIRS : 1][SC];
   float beta[SC];
   uint32_t es_off;  // byte offset of the role's shared-memory terms in the dynamic array
+  const float2 *prg;  // NV = 0 (any d): the chunk's raw rows in dynamic shared memory, pair h at prg + h * d
   bool have;
 #ifdef OTK_SMALL_COUNT_BUILDS
   int builds;  // exact passes this CTA ran for the role -> state[5] / state[6] (CTA 0)
@@ -596,7 +678,7 @@ __device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, i
   for (int ch = blockIdx.x, k = 0; ch < n_chunks; ch += G, ++k) {
     const int r0 = ch * rc, rn = min(rc, np - r0);
     trace_mark(A, step, 0);
-    const float2 (*p2)[4 * NV] = S.p2 + k * (RC / 2);
+    const float2 (*p2)[RoleRows<NV>::W] = S.p2 + (NV > 0 ? k * (RC / 2) : 0);
     const float *cp = S.cp + k * RC;
     float *an = S.an + k * RC;
     float *ci = S.ci + k * RC;
@@ -629,6 +711,18 @@ __device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, i
       }
       if (rebuild) {
         __syncthreads();
+        if constexpr (NV == 0) {  // any d: both exact passes in the difference form, columns from global memory
+          const float *Qraw = reinterpret_cast<const float *>(Q);
+          generic_pass<true, EU, STR == 1 ? ER_PAIRS : 0>(A, Qraw, nq, qx, need, rn, SR.prg, an, SR.er, SR.es_off,
+                                                          SR.beta, red, tot);
+          if (threadIdx.x < rn) {
+            const float mx = tot[threadIdx.x];
+            an[threadIdx.x] = (mx == -INFINITY) ? 0.f : mx;
+          }
+          __syncthreads();
+          generic_pass<false, EU, STR == 1 ? ER_PAIRS : 0>(A, Qraw, nq, qx, need, rn, SR.prg, an, SR.er, SR.es_off,
+                                                           SR.beta, red, tot);
+        } else {
         chunk_pass<NV, SAME, EU, true>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
         if (threadIdx.x < rn) {
           // the maxima come from the norm form, which carries + kappa |p|^2; the
@@ -640,6 +734,7 @@ __device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, i
         __syncthreads();
         build_pass<NV, SAME, EU, STR == 1 ? ER_PAIRS : 0>(A, Q, nq, qx, need, r0, rn, S.pr, an,
                                                           SR.er, SR.es_off, SR.beta, red, tot);
+        }
         SR.have = true;
 #ifdef OTK_SMALL_COUNT_BUILDS  // diagnostics build (tools/variant_small.sh ... -DOTK_SMALL_COUNT_BUILDS)
         ++SR.builds;
@@ -652,24 +747,28 @@ __device__ __forceinline__ void half_step_rows(const Args &A, const float4 *P, i
         }
       }
     } else if (!redo) {
-      chunk_pass<NV, SAME, EU, false>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
-      if (threadIdx.x < rn) {
-        const float a0 = an[threadIdx.x];
-        L = a0 + lg2(tot[threadIdx.x]);
-        const float dl = L - a0;
-        if (!(L != L) && !(dl >= lo && dl <= 120.f)) redo = 1;
+      if constexpr (STR == 0 && NV > 0) {
+        chunk_pass<NV, SAME, EU, false>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
+        if (threadIdx.x < rn) {
+          const float a0 = an[threadIdx.x];
+          L = a0 + lg2(tot[threadIdx.x]);
+          const float dl = L - a0;
+          if (!(L != L) && !(dl >= lo && dl <= 120.f)) redo = 1;
+        }
+        __syncthreads();
       }
-      __syncthreads();
     }
-    if (STR == 0 && redo && A.probe == 0) {  // exact: row maxima, then the sum against them
-      chunk_pass<NV, SAME, EU, true>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
-      if (threadIdx.x < rn) {
-        const float mx = tot[threadIdx.x];
-        an[threadIdx.x] = (mx == -INFINITY) ? 0.f : mx;  // all -inf -> sum 0 -> -inf; NaN survives
+    if constexpr (STR == 0 && NV > 0) {
+      if (redo && A.probe == 0) {  // exact: row maxima, then the sum against them
+        chunk_pass<NV, SAME, EU, true>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
+        if (threadIdx.x < rn) {
+          const float mx = tot[threadIdx.x];
+          an[threadIdx.x] = (mx == -INFINITY) ? 0.f : mx;  // all -inf -> sum 0 -> -inf; NaN survives
+        }
+        __syncthreads();
+        chunk_pass<NV, SAME, EU, false>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
+        if (threadIdx.x < rn) L = an[threadIdx.x] + lg2(tot[threadIdx.x]);
       }
-      __syncthreads();
-      chunk_pass<NV, SAME, EU, false>(A, Q, nq, qx, need, r0, rn, p2, cp, an, red, tot);
-      if (threadIdx.x < rn) L = an[threadIdx.x] + lg2(tot[threadIdx.x]);
     }
     if (threadIdx.x < rn) {
       const int i = r0 + threadIdx.x;
@@ -733,7 +832,16 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
 #endif
   sy.es_off = 0;  // y role: RC / 2 pairs x n columns; then the x role's RC / 2 - ER_PAIRS pairs x m columns
   sx.es_off = (uint32_t)((RC / 2) * A.n * (int)sizeof(float2));
-  if constexpr (NV <= 2 && !ST) {
+  sx.prg = sy.prg = nullptr;
+  if constexpr (NV == 0) {  // any d: the exact passes read the caller's points directly
+    static_assert(ST, "more than 19 coordinates: stored kernel only");
+    xs = reinterpret_cast<float4 *>(const_cast<float *>(A.x));
+    ys = reinterpret_cast<float4 *>(const_cast<float *>(A.y));
+    float2 *g0 = reinterpret_cast<float2 *>(reinterpret_cast<char *>(sh4) +
+                                            (size_t)((RC / 2) * A.n + (RC / 2 - ER_PAIRS) * A.m) * sizeof(float2));
+    sx.prg = g0;
+    sy.prg = g0 + (RC / 2) * A.d;
+  } else if constexpr (NV <= 2 && !ST) {
     xs = sh4;
     ys = xs + A.n * NV;
     load_points<NV>(A.x, A.n, A.d, A.kappa, xs, threadIdx.x, blockDim.x);
@@ -760,6 +868,10 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
   grid.sync();
   init_role_rows<NV>(A, xs, A.n, A.m, A.la, rows_x);  // after the barrier: global points are complete
   init_role_rows<NV>(A, ys, A.m, A.n, A.lb, rows_y);
+  if constexpr (NV == 0) {
+    init_generic_rows(A.x, A.n, A.d, const_cast<float2 *>(sx.prg));
+    init_generic_rows(A.y, A.m, A.d, const_cast<float2 *>(sy.prg));
+  }
   __syncthreads();
 
   // exchange buffer of the words tagged T: (T >> 1) & 1
@@ -951,7 +1063,9 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
 
 // dynamic shared memory: the resident point sets (d <= 7 only)
 size_t smem_bytes(int n, int m, int nv) { return nv <= 2 ? (size_t)(n + m) * nv * sizeof(float4) : 0; }
+constexpr int GENERIC_MAX_D = 512;  // NV = 0: both roles' raw rows (2 x 8 pairs x d float2) must fit beside the stored terms
 inline int nv_of(int d) {
+  if (d > 19) return 0;  // any d: stored kernel only
   const int nv = (d + 1 + 3) / 4;
   return nv <= 3 ? nv : 5;  // instantiated: 1, 2, 3, 5 float4 per point
 }
@@ -969,38 +1083,43 @@ inline void device_limits(int *dev, int *coop, int *max_smem) {
 }
 // stored-kernel instantiation: dynamic shared memory = the y role's terms,
 // one float2 per (row pair, x column); the points are read from global memory
-// (only the rare exact passes touch them)
-inline int role_rows(int np, int grid) { return std::min(RC, (np + grid - 1) / grid); }
-size_t stored_smem_bytes(int n, int m) {
-  return ((size_t)(RC / 2) * n + (size_t)(RC / 2 - ER_PAIRS) * m) * sizeof(float2);
+// (only the rare exact passes touch them); any d: plus both roles' raw rows
+size_t stored_smem_bytes(int n, int m, int d) {
+  return ((size_t)(RC / 2) * n + (size_t)(RC / 2 - ER_PAIRS) * m) * sizeof(float2)
+         + (d > 19 ? (size_t)2 * (RC / 2) * d * sizeof(float2) : 0);
 }
 // Both roles: one chunk per CTA and every column in one register group.
-bool stored_fits(int n, int m, int grid, size_t max_smem) {
+bool stored_fits(int n, int m, int d, int grid, size_t max_smem) {
   if (n > SC * THREADS || m > SC * THREADS) return false;
   // a handful of rows or columns: nothing to gain, and no averaging of the
   // frozen terms' rounding over a row's columns (see DRIFT_CHECK)
   if (n < 32 || m < 32) return false;
   if ((n + grid - 1) / grid > RC || (m + grid - 1) / grid > RC) return false;
-  return stored_smem_bytes(n, m) + 30720 <= max_smem;  // static: the per-role row state (<= 29 KB at NV = 5)
+  if (d > GENERIC_MAX_D) return false;
+  return stored_smem_bytes(n, m, d) + 30720 <= max_smem;  // static: the per-role row state (<= 29 KB at NV = 5)
 }
 
 }  // namespace small
 
 // Can this problem run as one persistent kernel on this device?
 bool small_solve_fits(int64_t n, int64_t m, int d) {
-  if (d > 19 || n > (1 << 20) || m > (1 << 20)) return false;
+  if (n > (1 << 20) || m > (1 << 20)) return false;
+  int dev = 0, coop = 0, max_smem = 0;
+  small::device_limits(&dev, &coop, &max_smem);
+  if (num_sms() > small::MAX_GRID || !coop) return false;
+  if (d > 19)  // any d: only with stored terms (one chunk per CTA, <= 2048 points a side)
+    return small::stored_fits((int)n, (int)m, d, num_sms(), (size_t)max_smem);
   const int nv = small::nv_of(d);
   // d >= 8: the FP32 cells grow with d; beyond ~2^27 cell-dimensions per
   // half-step the tcgen05 loop is faster despite its launches (measured:
   // 2048^2 d = 16 17.4 vs 24.7 us per iteration; 512^2 d = 16 6.5 vs 24.7)
-  if (nv >= 3 && (double)n * (double)m * (d + 1) > (double)(1 << 27)) return false;
-  int dev = 0, coop = 0, max_smem = 0;
-  small::device_limits(&dev, &coop, &max_smem);
+  if (nv >= 3 && (double)n * (double)m * (d + 1) > (double)(1 << 27) &&
+      !small::stored_fits((int)n, (int)m, d, num_sms(), (size_t)max_smem))
+    return false;
   const int64_t per_cta = (int64_t)small::RC * num_sms() * small::KMAX;  // chunks per CTA per role
   if (n > per_cta || m > per_cta) return false;
-  if (num_sms() > small::MAX_GRID) return false;
   // static shared memory: the per-role row state (<= 21 KB at NV = 5), the gathered check slots (12.5 KB)
-  return coop && small::smem_bytes((int)n, (int)m, nv) + 40960 <= (size_t)max_smem;
+  return small::smem_bytes((int)n, (int)m, nv) + 40960 <= (size_t)max_smem;
 }
 
 int small_solve_launch(const small::Args &A, bool same, bool eucl, cudaStream_t st) {
@@ -1009,22 +1128,27 @@ int small_solve_launch(const small::Args &A, bool same, bool eucl, cudaStream_t 
   int dev = 0, coop = 0, max_smem = 0;
   device_limits(&dev, &coop, &max_smem);
   const char *env = getenv("OTK_SMALL_STORED");  // A/B: 0 keeps the exps in every half-step
-  const bool stored = !(env && atoi(env) == 0) && stored_fits(A.n, A.m, num_sms(), (size_t)max_smem);
-  const size_t smem = stored ? stored_smem_bytes(A.n, A.m) : smem_bytes(A.n, A.m, nv);
+  const bool stored = (nv == 0 || !(env && atoi(env) == 0)) &&
+                      stored_fits(A.n, A.m, A.d, num_sms(), (size_t)max_smem);
+  if (nv == 0 && !stored) {
+    set_error("solve_small: more than 19 coordinates need the stored-kernel path");
+    return OTK_ENOTSUP;
+  }
+  const size_t smem = stored ? stored_smem_bytes(A.n, A.m, A.d) : smem_bytes(A.n, A.m, nv);
 #define OTK_SMALL_K(NV_, SA_, EU_, ST_) (void *)solve_small_kernel<NV_, SA_, EU_, ST_>
 #define OTK_SMALL_K4(NV_, ST_) OTK_SMALL_K(NV_, false, false, ST_), OTK_SMALL_K(NV_, false, true, ST_), \
                                OTK_SMALL_K(NV_, true, false, ST_), OTK_SMALL_K(NV_, true, true, ST_)
-  void *const table[32] = {OTK_SMALL_K4(1, false), OTK_SMALL_K4(2, false), OTK_SMALL_K4(3, false),
+  void *const table[36] = {OTK_SMALL_K4(1, false), OTK_SMALL_K4(2, false), OTK_SMALL_K4(3, false),
                            OTK_SMALL_K4(5, false), OTK_SMALL_K4(1, true),  OTK_SMALL_K4(2, true),
-                           OTK_SMALL_K4(3, true),  OTK_SMALL_K4(5, true)};
+                           OTK_SMALL_K4(3, true),  OTK_SMALL_K4(5, true),  OTK_SMALL_K4(0, true)};
 #undef OTK_SMALL_K4
 #undef OTK_SMALL_K
   const int slot = nv == 5 ? 3 : nv - 1;
-  const int ki = stored * 16 + slot * 4 + same * 2 + eucl;
+  const int ki = nv == 0 ? 32 + same * 2 + eucl : stored * 16 + slot * 4 + same * 2 + eucl;
   void *kern = table[ki];
   // attribute + occupancy check once per (device, kernel, shared-memory size), not per solve
   static thread_local int ok_dev = -1;
-  static thread_local size_t ok_smem[32];
+  static thread_local size_t ok_smem[36];
   if (ok_dev != dev) {
     for (size_t &v : ok_smem) v = (size_t)-1;
     ok_dev = dev;
