@@ -18,11 +18,11 @@ for n in (1024, 2048, 4096, 8192, 16384):
                                                     torch.from_numpy(wl.y).cuda()))
     for its in (10, 100):
         for _ in range(2):
-            otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=its)
+            otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=its, fixed_iters=True)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(5):
-            otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=its)
+            otk.solve_sinkhorn(prob, wl.eps, threshold=1e-300, max_iters=its, fixed_iters=True)
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / 5
         print(f"n=m={n:6d} its={its:4d}: {dt * 1e3:8.3f} ms per solve, {dt / its * 1e6:8.1f} us per iteration",

@@ -58,7 +58,11 @@ for k in counts:
     row = []
     for st in ("1", "0"):
         os.environ["OTK_SMALL_STORED"] = st
-        prob = otk.LinearProblem(otk.PointCloudGeometry(x, y), a, b)
+        geom_ = otk.PointCloudGeometry(x, y)
+        if st == "0" and x.shape[1] > 19:  # no plain small solve beyond 19 coordinates: the general loop
+            from paper_2201_12324_b200 import _native as N
+            geom_.impl_flags = N.OTK_IMPL_NOPERSIST
+        prob = otk.LinearProblem(geom_, a, b)
         out = otk.solve_sinkhorn(prob, eps, threshold=1e-300, max_iters=k, g_init=g0)
         fin = np.isfinite(ref["g"])
         ff = np.isfinite(ref["f"])
