@@ -340,7 +340,8 @@ def test_reference_loop_drives_the_drop_in_geometry(otk):
 
 @pytest.mark.parametrize("d,same,nonuniform", [(3, False, False), (1, False, True), (5, False, False),
                                                (3, True, False), (7, False, True), (8, False, False),
-                                               (11, True, False), (16, False, True), (19, False, False)])
+                                               (11, True, False), (16, False, True), (19, False, False),
+                                               (33, False, True), (64, False, False), (130, False, False)])
 def test_persistent_small_solve_matches_general_loop_and_oracle(otk, d, same, nonuniform):
     """The one-kernel small-problem solve (csrc/solve_small.cu) against the
     general launch-per-half-step loop (OTK_IMPL_NOPERSIST) and the oracle:
@@ -630,7 +631,8 @@ def test_batched_cluster_solver_edge_cases_match_oracle(otk, monkeypatch, domain
         assert rel_inf(outs.g[k], ref["g"]) <= POT_TOL, (k, rel_inf(outs.g[k], ref["g"]))
 
 
-@pytest.mark.parametrize("d,cost_fn", [(3, "sqeucl"), (6, "sqeucl"), (12, "sqeucl"), (3, "eucl")])
+@pytest.mark.parametrize("d,cost_fn", [(3, "sqeucl"), (6, "sqeucl"), (12, "sqeucl"), (3, "eucl"),
+                                       (21, "eucl"), (48, "sqeucl"), (67, "sqeucl")])
 def test_persistent_small_solve_stored_kernel_edge_cases(otk, monkeypatch, d, cost_fn):
     """The stored-kernel half-steps of the persistent small solve (exps taken
     once, FP32 matrix-vector half-steps, csrc/solve_small.cu) on the cases that
@@ -659,7 +661,16 @@ def test_persistent_small_solve_stored_kernel_edge_cases(otk, monkeypatch, d, co
         prob = otk.LinearProblem(otk.PointCloudGeometry(x, y, cost_fn=cost_fn), a, b)
         return otk.solve_sinkhorn(prob, eps, threshold=1e-300, max_iters=40, g_init=g0)
     stored, stored2 = run(), run()
-    monkeypatch.setenv("OTK_SMALL_STORED", "0")
+    if d > 19:  # no plain small solve beyond 19 coordinates: compare with the general loop instead
+        from paper_2201_12324_b200 import _native as N
+
+        def run():  # noqa: F811
+            geom = otk.PointCloudGeometry(x, y, cost_fn=cost_fn)
+            geom.impl_flags = N.OTK_IMPL_NOPERSIST
+            return otk.solve_sinkhorn(otk.LinearProblem(geom, a, b), eps, threshold=1e-300, max_iters=40,
+                                      g_init=g0)
+    else:
+        monkeypatch.setenv("OTK_SMALL_STORED", "0")
     plain = run()
     for out in (stored, plain):
         assert out.iterations == ref["iterations"] and len(out.errors) == len(ref["errors"])
