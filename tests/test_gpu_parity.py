@@ -114,7 +114,7 @@ def _solve_golden(otk, name, **kw):
 
 @pytest.mark.parametrize("name", ["cfg1_small", "cfg1_full", "cfg2_small", "cfg4_small",
                                   "cfg5_small", "short_nonconv", "nonuniform_small"])
-@pytest.mark.parametrize("impl", ["auto", "simt"])
+@pytest.mark.parametrize("impl", ["auto", "simt", "tc"])  # auto: the one-kernel small solve at these sizes; tc: the tcgen05 loop
 def test_solve_matches_reference(otk, name, impl):
     fx, wl, prob = _solve_golden(otk, "solve_" + name)
     out = otk.solve_sinkhorn(prob, float(fx["eps"]), threshold=float(fx["threshold"]),
