@@ -1135,6 +1135,15 @@ bool stored_fits(int n, int m, int d, int grid, size_t max_smem) {
   if (n < 32 || m < 32) return false;
   if ((n + grid - 1) / grid > RC || (m + grid - 1) / grid > RC) return false;
   if (d > GENERIC_MAX_D) return false;
+  if (d > 19) {
+    // any d: a solve pays for ~12 exact passes (two per role and build, 2-3 builds) of
+    // n m d coordinate differences -- measured 5.8e-14 s each with 128-bit loads (d a
+    // multiple of 4), 2.6e-13 s otherwise -- and then saves ~45 us per iteration against
+    // the launch-per-half-step loop.  Taken when the passes cost about ten iterations'
+    // savings at most (2048^2: d <= 236, or d <= 59 when d is not a multiple of 4).
+    const double work = (double)n * (double)m * (double)d;
+    if (work > (((d & 3) == 0) ? 1.0e9 : 2.5e8)) return false;
+  }
   return stored_smem_bytes(n, m, d) + 30720 <= max_smem;  // static: the per-role row state (<= 29 KB at NV = 5)
 }
 
