@@ -329,7 +329,9 @@ Layout plan(const otk_solve_args *A, void *ws) {
     L.d_duals = c.take<double>(A->max_checks);
     L.state = c.take<int>(8);
     L.xch = c.take<unsigned long long>(2 * (size_t)(A->n + A->m));
-    L.pts = c.take<float4>((size_t)(A->n + A->m) * 5);  // d >= 8: staged points (<= 5 float4 each)
+    // d >= 8: staged points (<= 5 float4 each); d > 19 and not a multiple of 4: both sets with rows
+    // padded to a multiple of 4 coordinates (128-bit loads in the exact passes)
+    L.pts = c.take<float4>((size_t)(A->n + A->m) * std::max(5, (A->d + 3) / 4));
   }
   L.bytes = c.off + 256;
   return L;

@@ -601,7 +601,7 @@ __device__ __forceinline__ void generic_pass(const Args &A, const float *Qraw, i
                                              int rc, const float2 *prg, const float *sh,
                                              float2 (&er)[ER_PAIRS > 0 ? ER_PAIRS : 1][SC], uint32_t es_off,
                                              float (&beta)[SC], float (*red)[RC], float *tot) {
-  const int d = A.d;
+  const int d = (A.d + 3) & ~3;  // row stride of Qraw and prg: padded with zeros to a multiple of 4
   const float sk = sqrtf(A.kappa);
   float2 *es = reinterpret_cast<float2 *>(reinterpret_cast<char *>(sh4) + es_off);
   xword w[SC];
@@ -619,7 +619,6 @@ __device__ __forceinline__ void generic_pass(const Args &A, const float *Qraw, i
   float2 acc[RC / 2];
 #pragma unroll
   for (int h = 0; h < RC / 2; ++h) acc[h] = MAXP ? make_float2(-INFINITY, -INFINITY) : make_float2(0.f, 0.f);
-  const bool vec = (d & 3) == 0;  // rows of Q (and of prg) start on 16-byte boundaries: 128-bit loads
   // One column at a time (the x role's terms occupy half the registers).  Sums
   // in two levels -- blocks of 4 coordinates, then the blocks: a plain float32
   // chain over 300 coordinates is off by 2e-7 of C on average, 1e-6 at worst,
@@ -633,29 +632,23 @@ __device__ __forceinline__ void generic_pass(const Args &A, const float *Qraw, i
     for (int h = 0; h < RC / 2; ++h) c2[h] = make_float2(0.f, 0.f);
     for (int k0 = 0; k0 < d; k0 += 4) {
       float q[4];
-      if (vec) {
+      {
         const float4 v = __ldg(reinterpret_cast<const float4 *>(qp[c] + k0));
         q[0] = v.x;
         q[1] = v.y;
         q[2] = v.z;
         q[3] = v.w;
-      } else {
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) q[kk] = (k0 + kk < d) ? __ldg(qp[c] + k0 + kk) : 0.f;
       }
 #pragma unroll
       for (int h = 0; h < RC / 2; ++h) {
         float2 p[4];
-        if (vec) {  // two coordinates of the pair per 128-bit (broadcast) load
+        {  // two coordinates of the pair per 128-bit (broadcast) load
           const float4 a = *reinterpret_cast<const float4 *>(prg + h * d + k0);
           const float4 b = *reinterpret_cast<const float4 *>(prg + h * d + k0 + 2);
           p[0] = make_float2(a.x, a.y);
           p[1] = make_float2(a.z, a.w);
           p[2] = make_float2(b.x, b.y);
           p[3] = make_float2(b.z, b.w);
-        } else {
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) p[kk] = (k0 + kk < d) ? prg[h * d + k0 + kk] : make_float2(0.f, 0.f);
         }
         float2 blk = make_float2(0.f, 0.f);
 #pragma unroll
@@ -876,10 +869,26 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
     static_assert(ST, "more than 19 coordinates: stored kernel only");
     xs = reinterpret_cast<float4 *>(const_cast<float *>(A.x));
     ys = reinterpret_cast<float4 *>(const_cast<float *>(A.y));
+    if (A.d & 3) {  // rows padded with zeros to a multiple of 4 coordinates (complete at the grid barrier below)
+      const int dp = (A.d + 3) & ~3;
+      float *px = reinterpret_cast<float *>(A.pts), *py = px + (size_t)A.n * dp;
+      for (int64_t e = gtid; e < (int64_t)A.n * dp; e += gstride) {
+        const int64_t i = e / dp;
+        const int k = (int)(e - i * dp);
+        px[e] = k < A.d ? A.x[i * A.d + k] : 0.f;
+      }
+      for (int64_t e = gtid; e < (int64_t)A.m * dp; e += gstride) {
+        const int64_t j = e / dp;
+        const int k = (int)(e - j * dp);
+        py[e] = k < A.d ? A.y[j * A.d + k] : 0.f;
+      }
+      xs = reinterpret_cast<float4 *>(px);
+      ys = reinterpret_cast<float4 *>(py);
+    }
     float2 *g0 = reinterpret_cast<float2 *>(reinterpret_cast<char *>(sh4) +
                                             (size_t)((RC / 2) * A.n + (RC / 2 - ER_PAIRS) * A.m) * sizeof(float2));
     sx.prg = g0;
-    sy.prg = g0 + (RC / 2) * A.d;
+    sy.prg = g0 + (RC / 2) * ((A.d + 3) & ~3);
   } else if constexpr (NV <= 2 && !ST) {
     xs = sh4;
     ys = xs + A.n * NV;
@@ -908,8 +917,9 @@ __global__ void __launch_bounds__(THREADS, 1) solve_small_kernel(Args A) {
   init_role_rows<NV>(A, xs, A.n, A.m, A.la, rows_x);  // after the barrier: global points are complete
   init_role_rows<NV>(A, ys, A.m, A.n, A.lb, rows_y);
   if constexpr (NV == 0) {
-    init_generic_rows(A.x, A.n, A.d, const_cast<float2 *>(sx.prg));
-    init_generic_rows(A.y, A.m, A.d, const_cast<float2 *>(sy.prg));
+    // (after the grid barrier: the padded copies are complete)
+    init_generic_rows(reinterpret_cast<const float *>(xs), A.n, (A.d + 3) & ~3, const_cast<float2 *>(sx.prg));
+    init_generic_rows(reinterpret_cast<const float *>(ys), A.m, (A.d + 3) & ~3, const_cast<float2 *>(sy.prg));
   }
   __syncthreads();
 
@@ -1125,7 +1135,7 @@ inline void device_limits(int *dev, int *coop, int *max_smem) {
 // (only the rare exact passes touch them); any d: plus both roles' raw rows
 size_t stored_smem_bytes(int n, int m, int d) {
   return ((size_t)(RC / 2) * n + (size_t)(RC / 2 - ER_PAIRS) * m) * sizeof(float2)
-         + (d > 19 ? (size_t)2 * (RC / 2) * d * sizeof(float2) : 0);
+         + (d > 19 ? (size_t)2 * (RC / 2) * ((d + 3) & ~3) * sizeof(float2) : 0);
 }
 // Both roles: one chunk per CTA and every column in one register group.
 bool stored_fits(int n, int m, int d, int grid, size_t max_smem) {
@@ -1137,12 +1147,10 @@ bool stored_fits(int n, int m, int d, int grid, size_t max_smem) {
   if (d > GENERIC_MAX_D) return false;
   if (d > 19) {
     // any d: a solve pays for ~12 exact passes (two per role and build, 2-3 builds) of
-    // n m d coordinate differences -- measured 5.8e-14 s each with 128-bit loads (d a
-    // multiple of 4), 2.6e-13 s otherwise -- and then saves ~45 us per iteration against
-    // the launch-per-half-step loop.  Taken when the passes cost about ten iterations'
-    // savings at most (2048^2: d <= 236, or d <= 59 when d is not a multiple of 4).
-    const double work = (double)n * (double)m * (double)d;
-    if (work > (((d & 3) == 0) ? 1.0e9 : 2.5e8)) return false;
+    // n m d coordinate differences, measured 5.8e-14 s each, and then saves ~45 us per
+    // iteration against the launch-per-half-step loop.  Taken when the passes cost about
+    // ten iterations' savings at most (2048^2: d <= 236).
+    if ((double)n * (double)m * (double)d > 1.0e9) return false;
   }
   return stored_smem_bytes(n, m, d) + 30720 <= max_smem;  // static: the per-role row state (<= 29 KB at NV = 5)
 }

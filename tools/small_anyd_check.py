@@ -1,9 +1,11 @@
+"""Any-d small solve vs the tcgen05 loop (OTK_IMPL_NOPERSIST): 30 fixed iterations, time and agreement."""
 import os, sys, time
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
 import paper_2201_12324_b200 as otk
 from paper_2201_12324_b200 import workloads, _native as N
-for d, n, m in ((512, 2048, 2048), (256, 2048, 1500), (20, 2048, 2048), (511, 1000, 2048)):
+for d, n, m in ((512, 2048, 2048), (256, 2048, 1500), (20, 2048, 2048), (511, 1000, 2048), (130, 2048, 2048),
+                (67, 1500, 1333)):
     wl = workloads.cfg2(n=n, m=m, d=d)
     xd, yd = torch.from_numpy(wl.x).cuda(), torch.from_numpy(wl.y).cuda()
     res = {}
