@@ -1,25 +1,32 @@
 // K1p -- the whole Sinkhorn solve of a SMALL point-cloud problem in ONE
 // persistent cooperative kernel (one CTA per SM).  Replaces the reference loop
 // sinkhorn._sinkhorn_iterations (reference sinkhorn.py:151-200) with
-// apply_lse_kernel (geometry.py:336-354) for problems whose points fit in
-// shared memory (BASELINE configs[0]: 2048^2, d = 3), where a launch -- or a
-// grid barrier -- per half-step costs more than the math.  d <= 19: up to
-// d = 7 both point sets live in every CTA's shared memory; beyond, they are
-// staged once in global memory (L2-resident) and read per column group.
+// apply_lse_kernel (geometry.py:336-354) where a launch -- or a grid barrier --
+// per half-step costs more than the math (BASELINE configs[0]: 2048^2, d = 3).
 //
-// Every CTA keeps both point sets resident in shared memory as NV float4 per
-// point: coordinates, then -kappa*|q|^2 in slot d, zeros after.  A row's query
-// vector p' = (2 kappa p, 1, 0..) turns one dot product into
-// 2 kappa <p,q> - kappa |q|^2, clamped at kappa |p|^2 (C >= 0,
-// geometry.py:273) and shifted by the column's kappa * potential.
+// Two kinds of half-step:
+//  * exact (d <= 19): both point sets as NV float4 per point (coordinates, then
+//    -kappa*|q|^2 in slot d; shared memory up to d = 7, L2 beyond).  A row's
+//    query vector p' = (2 kappa p, 1, 0..) turns one dot product into
+//    2 kappa <p,q> - kappa |q|^2, clamped at kappa |p|^2 (C >= 0,
+//    geometry.py:273) and shifted by the column's log2-domain potential; sums
+//    against the row's previous result (anchored), redone exactly when the
+//    window is missed.
+//  * stored (n, m <= 2048, any d <= 512): the exps are taken once per build and
+//    kept -- the x role's terms in registers, the y role's in shared memory --
+//    and a half-step is an FP32 matrix-vector product with 2^(drift of the
+//    column potentials); builds take the cost in the difference form, for
+//    d > 19 straight from the caller's row-major points (see "stored-kernel
+//    half-steps" and "any d" below).
 //
-// Half-steps (below) exchange their outputs through tagged 64-bit words, with
-// no grid barrier.  The fused check (sinkhorn.py:175-189) runs inside the
-// f_{t+1} half-step: r_i = a_i exp((f_t,i - f_{t+1},i)/eps); each CTA
-// writes its 8 partial sums and the first half-step at which it produced a
-// NaN/+inf potential into a slot (double-buffered by check parity), and after
-// ONE grid barrier EVERY CTA adds all CTAs' slots in the same order, so all
-// take the same converged / diverged decision.
+// Half-steps exchange their outputs through tagged 64-bit words
+// {log2 w - L, half-step}, with no grid barrier.  The fused check
+// (sinkhorn.py:175-189) runs inside the f_{t+1} half-step:
+// r_i = a_i exp((f_t,i - f_{t+1},i)/eps); each CTA publishes its 8 partial sums
+// and the first half-step at which it produced a NaN/+inf potential as tagged
+// words, CTA 0 alone totals them in a fixed order and publishes one decision
+// word every CTA spins on.  State, check trace and (pinned buffers) f, g are
+// written straight into host memory.
 // Constant-eps schedules only (the general loop is solve.cu).
 #include <cooperative_groups.h>
 
