@@ -29,7 +29,9 @@ def main(cases=60, seed=0):
     worst = {"f": 0.0, "g": 0.0, "cost": 0.0, "anch": 0.0}
     fails = 0
     only = {int(v) for v in os.environ.get("OTK_FUZZ_ONLY", "").split(",") if v}
+    rng_cost = np.random.default_rng(seed + 1000)  # OTK_FUZZ_EUCL=1: a third of the cases with cost_fn="eucl"
     for c in range(cases):
+        cost_fn = "eucl" if (os.environ.get("OTK_FUZZ_EUCL") and rng_cost.random() < 0.34) else "sqeucl"
         d = int(rng.choice([2, 3, 5, 16, 33, 64, 100, 128, 200, 300, 520]))
         n = int(rng.integers(1, 900))
         m = int(rng.integers(1, 900))
@@ -54,8 +56,10 @@ def main(cases=60, seed=0):
             g0 = (rng.standard_normal(m) * eps * float(rng.choice([1.0, 50.0]))).astype(np.float32)
         if only and c not in only:  # OTK_FUZZ_ONLY=125,173: replay just these cases of the seed
             continue
-        geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64))
-        prob = otk.LinearProblem(otk.PointCloudGeometry(x, y), a, b)
+        geom64 = oracle.PointCloudOracle(x.astype(np.float64), y.astype(np.float64), cost_fn=cost_fn)
+        if cost_fn == "eucl":  # eps relative to the mean Euclidean cost
+            eps = eps / max(mc, 1e-3) * max(float(np.sqrt(mc)), 1e-3)
+        prob = otk.LinearProblem(otk.PointCloudGeometry(x, y, cost_fn=cost_fn), a, b)
         try:
             ref = oracle.sinkhorn(geom64, a, b, eps, threshold=1e-300, max_iters=its,
                                   g_init=None if g0 is None else g0.astype(np.float64))
@@ -75,7 +79,7 @@ def main(cases=60, seed=0):
             worst[kk] = max(worst[kk], v)
         bad = e["f"] > 1e-4 or e["g"] > 1e-4 or e["cost"] > 1e-5 or e.get("anch", 0.0) > 1e-5
         fails += bad
-        print(f"case {c:3d} n={n:4d} m={m:4d} d={d:3d} off={off:g} eps/mc={eps / max(mc, 1e-3):.3g} its={its:2d} "
+        print(f"case {c:3d} {cost_fn[:2]} n={n:4d} m={m:4d} d={d:3d} off={off:g} eps/mc={eps / max(mc, 1e-3):.3g} its={its:2d} "
               f"zeros={int((a == 0).sum())}/{int((b == 0).sum())} g0={'y' if g0 is not None else 'n'} "
               + " ".join(f"{kk}={v:.1e}" for kk, v in e.items()) + ("  <-- FAIL" if bad else ""),
               flush=True)
