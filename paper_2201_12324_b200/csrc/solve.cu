@@ -277,8 +277,9 @@ struct Layout {
   size_t bytes;
 };
 
-// Whole-solve persistent kernel (solve_small.cu): FP32 path, constant eps,
-// points resident in shared memory.  OTK_IMPL_NOPERSIST forces the general loop.
+// Whole-solve persistent kernel (solve_small.cu): FP32 path, constant eps; d <= 19 within
+// its cell budget, or any d <= 512 for up to 2048 points a side while the stored-kernel
+// builds pay off (small_solve_fits).  OTK_IMPL_NOPERSIST / OTK_IMPL_TC force the general loop.
 static bool use_small(const otk_solve_args *A) {
   if (A->flags & (OTK_IMPL_TC | OTK_IMPL_NOPERSIST)) return false;
   if (!(A->eps_init_scale <= 1.0)) return false;  // eps_t == target for every t

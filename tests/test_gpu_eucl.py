@@ -71,7 +71,8 @@ def test_apply_lse_kernel_matches_reference(otk, impl):
 @pytest.mark.parametrize("impl", ["auto", "simt", "nopersist"])
 def test_solve_matches_reference(otk, impl):
     """Full solves: same iterations / converged flag, potentials and costs within tolerance.
-    auto = persistent small solve for d <= 7 and the tcgen05 loop above; simt = FP32 loop."""
+    auto = the one-kernel small solve (any d at these sizes); nopersist = the tcgen05 loop;
+    simt = FP32 loop."""
     from paper_2201_12324_b200 import _native as N
     for name, c in cases():
         geom = _geom(otk, c, "simt" if impl == "simt" else "auto")
